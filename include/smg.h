@@ -1,0 +1,150 @@
+/*
+ * smg.h -- C ABI of libsmg.so, the B200 (sm_100a) hot path of the weighted
+ * additive Schwarz / p-multigrid / MGCG solver (arXiv 1512.02390).
+ *
+ * The reference (/root/reference/pkg/src/schwarzmg) is pure Python/NumPy and
+ * has no FFI; every entry point below replaces one NumPy call site on its
+ * hot path (cited per function).  A maintainer binds it from the reference
+ * with ctypes.
+ *
+ * Conventions
+ *   - Fields are dense (N_y, N_x) float64 arrays in DEVICE memory, row-major,
+ *     y slow / x fast, N_* = p * n_*  (reference mesh.py:1-7, 49-70).
+ *   - Every launch is enqueued on the caller's stream (a cudaStream_t passed
+ *     as void*); nothing synchronizes except where documented.
+ *   - Host arrays (factors, matrices) are copied at create time; handles own
+ *     only immutable per-level constants.  Workspaces are caller-owned.
+ *   - Return value: 0 on success, <0 on error; smg_last_error() explains.
+ *     No CPU fallback exists: without a CUDA device every compute call fails.
+ */
+#ifndef SMG_H
+#define SMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMG_OK 0
+#define SMG_EINVAL -1      /* bad argument (maps to ValueError)          */
+#define SMG_EUNSUPPORTED -2 /* order / window size not compiled in        */
+#define SMG_ECUDA -3       /* CUDA runtime error (maps to RuntimeError)  */
+#define SMG_ENOMEM -4
+
+typedef struct smg_op smg_op_t;             /* one level's operator          */
+typedef struct smg_schwarz smg_schwarz_t;   /* one level's additive smoother */
+typedef struct smg_transfer smg_transfer_t; /* level l-1 <-> l transfers     */
+typedef struct smg_coarse smg_coarse_t;     /* p=1 pseudo-inverse            */
+
+const char* smg_last_error(void);
+int smg_version(void);
+/* 1 if a CUDA device is usable, else 0 (and smg_last_error says why). */
+int smg_device_ok(void);
+
+/* ---- operators (replaces operators.py:30-54 PoissonOperator.apply and
+ *      operators.py:57-92 DiffusionOperator.apply; residual operators.py:101-103)
+ * weights: p+1 GLL weights; mat: (p+1)^2 row-major -- the reference stiffness
+ * basis.stiff for Poisson, the derivative matrix basis.diff for diffusion.
+ * nu (diffusion only): device (N_y, N_x) nodal diffusivity, must outlive h. */
+int smg_op_create(smg_op_t** h, int kind /*0 Poisson, 1 diffusion*/, int p, int n_x, int n_y,
+                  double dx, double dy, const double* weights, const double* mat,
+                  const double* nu_dev);
+int smg_op_destroy(smg_op_t* h);
+/* out = f - A u   (f == NULL: out = A u).  out must not alias u. */
+int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out,
+                    void* stream);
+/* Like smg_op_residual, and also *norm2_out (device double) = ||out||^2
+ * summed deterministically; ws must hold smg_reduce_ws_doubles() doubles. */
+int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
+                          double* norm2_out, double* ws, void* stream);
+
+/* ---- additive Schwarz (replaces schwarz.py:215-222 FastDiagSolver.solve,
+ *      :268-275 AdditiveSchwarz.smooth with mesh.py:124-150 gather/scatter)
+ * S_x, S_y: m x m row-major generalized eigenvectors (reference S_x, S_y);
+ * lam_x, lam_y: m eigenvalues; w_x, w_y: m 1D weights (W = w_y (x) w_x);
+ * inv_nu_dev: device (n_y, n_x) 1/nu_bar per element, or NULL (Poisson). */
+int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y,
+                       const double* S_x, const double* S_y, const double* lam_x,
+                       const double* lam_y, const double* w_x, const double* w_y,
+                       const double* inv_nu_dev);
+int smg_schwarz_destroy(smg_schwarz_t* h);
+/* u += sum_s R_s^T W A_s^-1 R_s r (/ nu_bar): the additive correction of one
+ * sweep given the residual r.  Deterministic (no atomics). */
+int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream);
+/* One or more full sweeps: r = f - A u; u += correction.  work: N_y*N_x.
+ * u_is_zero != 0 lets the first sweep skip A u (u must hold zeros). */
+int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
+                       double* work, int n_it, int u_is_zero, void* stream);
+/* FastDiagSolver.solve on nb independent (m,m) blocks: out = W*(S_y(S_y^T B S_x ./ L)S_x^T).
+ * apply_weight=0 skips W (the multiplicative / kind=None solver). */
+int smg_fd_solve_blocks(const smg_schwarz_t* h, const double* blocks, double* out, int nb,
+                        int apply_weight, void* stream);
+
+/* ---- transfers (replaces multigrid.py:180-193 dense P_y C P_x^T products)
+ * J: (p_f+1) x (p_c+1) row-major reference interpolation matrix. */
+int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, const double* J);
+int smg_transfer_destroy(smg_transfer_t* h);
+/* uf = P uc (accumulate=0) or uf += P uc (accumulate=1). */
+int smg_prolongate(const smg_transfer_t* h, const double* uc, double* uf, int accumulate,
+                   void* stream);
+/* fc = P^T ff (P's rows are assigned, not summed: owner-computes). */
+int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* stream);
+/* fc = P^T (f - A u): residual fused with restriction (multigrid.py:244). */
+int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const double* u,
+                          const double* f, double* fc, double* work, void* stream);
+
+/* ---- p=1 coarse problem (replaces multigrid.py:196-228 coarse CG)
+ * Poisson: exact pseudo-inverse by global fast diagonalization (zero mode
+ * dropped).  ws must hold smg_coarse_ws_doubles(h) doubles. */
+int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy);
+int smg_coarse_destroy(smg_coarse_t* h);
+size_t smg_coarse_ws_doubles(const smg_coarse_t* h);
+/* u0 = A0^+ (f0 - mean f0) */
+int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double* ws,
+                    void* stream);
+
+/* Parity mode: the reference's plain CG (multigrid.py:196-228) on the device:
+ * u0 = mean0(CG(A0, f0 - mean f0)) to ||r|| <= tol ||b||, at most max_iter
+ * iterations.  op must be the p=1 operator.  Blocks the host every 32
+ * iterations to test convergence.  *iters_out = iterations, or -max_iter if
+ * the cap was hit (the reference's coarse_cg_exhausted case). */
+size_t smg_coarse_cg_ws_doubles(int64_t n);
+int smg_coarse_cg(const smg_op_t* op, const double* f0, double* u0, double* ws, double tol,
+                  int max_iter, int* iters_out, void* stream);
+
+/* ---- BLAS-1 with device scalars (krylov.py:56-111, multigrid.py:199-214)
+ * All reductions are deterministic (fixed grid, fixed summation order). */
+size_t smg_reduce_ws_doubles(void);
+int smg_dot(const double* x, const double* y, int64_t n, double* out, double* ws, void* stream);
+/* out[0] = x.(y - z), out[1] = x.y  (one pass; krylov.py:108,110) */
+int smg_dot2(const double* x, const double* y, const double* z, int64_t n, double* out,
+             double* ws, void* stream);
+/* y = alpha*x + beta*y */
+int smg_axpby(double alpha, const double* x, double beta, double* y, int64_t n, void* stream);
+/* MGCG step (krylov.py:95-103): pq = scal[1]; if pq <= 0 set flag[0]=1 and
+ * do nothing; else alpha = scal[0]/pq, u += alpha p, r -= alpha q,
+ * scal[2] = ||r||^2, scal[6] = alpha.  scal holds 8 doubles. */
+int smg_cg_update(double* u, double* r, const double* p, const double* q, int64_t n,
+                  double* scal, int* flag, double* ws, void* stream);
+/* Out-of-place variant: r_out = r_in - alpha q (r_in is kept as r_old). */
+int smg_cg_update2(double* u, const double* r_in, double* r_out, const double* p, const double* q,
+                   int64_t n, double* scal, int* flag, double* ws, void* stream);
+/* Polak-Ribiere bookkeeping (krylov.py:108-110): s1 = z.(r - r_old) (r_old may
+ * be NULL = zeros), s2 = z.r; scal[5] = s1 / scal[0] (beta); scal[0] = s2. */
+int smg_cg_beta(const double* z, const double* r, const double* r_old, int64_t n, double* scal,
+                double* ws, void* stream);
+/* p = z + scal[5] p  (krylov.py:109) */
+int smg_cg_direction(double* p, const double* z, int64_t n, double* scal, void* stream);
+/* f -= mean(f) (operators.py:138-140) */
+int smg_project_mean(double* f, int64_t n, double* ws, void* stream);
+/* out = sum(x) */
+int smg_sum(const double* x, int64_t n, double* out, double* ws, void* stream);
+/* out = sum of nb per-CTA partials (fixed order) */
+int smg_sum_partials(const double* part, int nb, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMG_H */

@@ -1,0 +1,310 @@
+"""Generate the golden fixtures in ``tests/golden/`` by running the UNMODIFIED
+reference package (``/root/reference/pkg/src/schwarzmg``) in this container.
+
+TEST INFRASTRUCTURE ONLY.  The GPU box has no ``/root/reference``; the
+committed ``.npz`` files are what travels.  Re-run with
+
+    python oracle/make_golden.py            # small fixtures (~1 min)
+    python oracle/make_golden.py --large    # + BASELINE-size histories (slow)
+
+Every fixture is produced by a reference call (named in the key comments), on
+seeded inputs, so the oracle restatement in ``oracle/smg_oracle.py`` and the
+CUDA path can both be checked against the reference's own numbers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import schwarzmg  # noqa: F401
+    from schwarzmg import basis, krylov, mesh, multigrid, operators, schwarz
+    return basis, krylov, mesh, multigrid, operators, schwarz
+
+
+def save(name, **arrays):
+    os.makedirs(OUT, exist_ok=True)
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+# FD-factor cases: (p, n_o, dx, dy).  Includes every BASELINE top level at
+# fixed:1 and ceilp8, and the smoother-microbenchmark orders.
+FD_CASES = [
+    (2, 1, 0.25, 0.25), (4, 1, 0.5, 0.5), (4, 1, 1.0, 0.25), (8, 2, 0.25, 0.25),
+    (8, 1, 1 / 8, 1 / 8), (4, 1, 1 / 64, 1 / 64), (8, 1, 1 / 64, 1 / 64),
+    (12, 1, 1 / 64, 1 / 64), (16, 1, 1 / 64, 1 / 64), (24, 1, 1 / 64, 1 / 64),
+    (32, 1, 1 / 64, 1 / 64), (16, 2, 1 / 64, 1 / 64), (32, 1, 1 / 128, 1 / 128),
+    (32, 4, 1 / 128, 1 / 128), (16, 1, 1 / 32, 1 / 256), (16, 2, 1 / 32, 1 / 256),
+    (24, 1, 1 / 512, 1 / 512), (24, 3, 1 / 512, 1 / 512), (12, 1, 1 / 512, 1 / 512),
+    (6, 1, 1 / 512, 1 / 512), (3, 1, 1 / 512, 1 / 512), (2, 1, 1 / 64, 1 / 64),
+]
+
+
+def small():
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    rng = np.random.default_rng(20240601)
+
+    # -- basis.py: gll_basis, interp_matrix
+    out = {}
+    for p in [1, 2, 3, 4, 5, 6, 8, 12, 16, 24, 32]:
+        b = basis.gll_basis(p)
+        out[f"nodes_{p}"] = b.nodes
+        out[f"weights_{p}"] = b.weights
+        out[f"diff_{p}"] = b.diff
+        out[f"stiff_{p}"] = b.stiff
+    for pc, pf in [(1, 2), (2, 4), (4, 8), (8, 16), (16, 32), (1, 3), (3, 6), (6, 12), (12, 24)]:
+        out[f"J_{pc}_{pf}"] = basis.interp_matrix(basis.gll_basis(pc), basis.gll_basis(pf)).matrix
+    save("basis", **out)
+
+    # -- schwarz.py: weights, restricted_1d, jacobi-based FD factors
+    out = {}
+    for kind in schwarz.WeightKind:
+        for p, n_o in [(2, 1), (4, 1), (8, 1), (8, 2), (16, 1), (16, 2), (24, 1), (24, 3), (32, 1), (32, 4)]:
+            b = basis.gll_basis(p)
+            g = schwarz.subdomain_geometry(b, n_o)
+            out[f"w_{kind.value}_{p}_{n_o}"] = schwarz.build_weight_1d(kind, b, g)
+    for i, (p, n_o, dx, dy) in enumerate(FD_CASES):
+        b = basis.gll_basis(p)
+        L, m = schwarz.restricted_1d(b, dx, n_o)
+        fd = schwarz.build_fast_diag(b, dx, dy, n_o, schwarz.WeightKind.QUINTIC)
+        out[f"fd{i}_case"] = np.array([p, n_o, dx, dy])
+        out[f"fd{i}_L"] = L
+        out[f"fd{i}_m"] = m
+        out[f"fd{i}_Sx"] = fd.S_x
+        out[f"fd{i}_Sy"] = fd.S_y
+        out[f"fd{i}_lx"] = fd.lam_x
+        out[f"fd{i}_ly"] = fd.lam_y
+        out[f"fd{i}_W"] = fd.weight
+        r = rng.standard_normal((3, 2, fd.S_x.shape[0], fd.S_x.shape[0]))
+        out[f"fd{i}_r"] = r
+        out[f"fd{i}_solve"] = fd.solve(r)
+    out["n_fd"] = np.array(len(FD_CASES))
+    save("schwarz_setup", **out)
+
+    # -- operators.py: Poisson / diffusion apply, element_mean_nu
+    out = {}
+    cases = [(2, 2, 2.0, 2.0, 1), (3, 2, 3.0, 2.0, 2), (3, 2, 3.0, 2.0, 3), (5, 4, 1.0, 1.0, 4),
+             (4, 6, 8.0, 1.0, 8), (3, 3, 1.0, 1.0, 16), (2, 3, 1.0, 1.0, 32), (4, 3, 2.0, 1.0, 12),
+             (3, 4, 1.0, 1.0, 24), (4, 4, 1.0, 1.0, 6)]
+    for i, (nx, ny, lx, ly, p) in enumerate(cases):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        b = basis.gll_basis(p)
+        N = (p * ny, p * nx)
+        u = rng.standard_normal(N)
+        nu = 1.0 + 0.5 * rng.random(N)
+        out[f"op{i}_case"] = np.array([nx, ny, lx, ly, p])
+        out[f"op{i}_u"] = u
+        out[f"op{i}_nu"] = nu
+        out[f"op{i}_Au"] = operators.PoissonOperator(b, msh).apply(u)
+        dop = operators.DiffusionOperator(b, msh, nu)
+        out[f"op{i}_Bu"] = dop.apply(u)
+        out[f"op{i}_nubar"] = dop.element_mean_nu()
+        out[f"op{i}_nufield"] = operators.diffusivity_field(msh, b, 0.9, 0.0)
+    out["n_op"] = np.array(len(cases))
+    save("operators", **out)
+
+    # -- schwarz.py: AdditiveSchwarz.smooth (Poisson and diffusion)
+    out = {}
+    sweeps = [(4, 4, 2.0, 2.0, 4, 1, "w5", None), (6, 5, 2.0, 2.0, 4, 1, "wa", None),
+              (5, 6, 3.0, 1.0, 8, 2, "w5", None), (4, 4, 1.0, 1.0, 16, 1, "w5", None),
+              (3, 3, 1.0, 1.0, 32, 1, "w3", None), (4, 3, 1.0, 1.0, 8, 1, "w5", 0.5),
+              (4, 4, 1.0, 1.0, 12, 1, "w7", None), (3, 4, 1.0, 1.0, 24, 3, "w5", 0.9),
+              (8, 8, 2.0, 2.0, 2, 0, "w1", None), (4, 4, 1.0, 1.0, 16, 4, "wt", None)]
+    for i, (nx, ny, lx, ly, p, n_o, kind, nu_hat) in enumerate(sweeps):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        b = basis.gll_basis(p)
+        lay = mesh.layout_for(msh, p)
+        if nu_hat is None:
+            op = operators.PoissonOperator(b, msh)
+            nb = None
+        else:
+            op = operators.DiffusionOperator(b, msh, operators.diffusivity_field(msh, b, nu_hat, 0.2))
+            nb = op.element_mean_nu()
+        sm = schwarz.AdditiveSchwarz(b, lay, msh.dx, msh.dy, n_o, schwarz.WeightKind(kind), nu_bar=nb)
+        u0 = rng.random((lay.N_y, lay.N_x))
+        f = rng.standard_normal((lay.N_y, lay.N_x))
+        out[f"sw{i}_case"] = np.array([nx, ny, lx, ly, p, n_o, -1.0 if nu_hat is None else nu_hat])
+        out[f"sw{i}_kind"] = np.array(kind)
+        out[f"sw{i}_u0"] = u0
+        out[f"sw{i}_f"] = f
+        out[f"sw{i}_u1"] = sm.smooth(op, u0.copy(), f, 1)
+        out[f"sw{i}_u2"] = sm.smooth(op, u0.copy(), f, 2)
+    out["n_sw"] = np.array(len(sweeps))
+    save("sweeps", **out)
+
+    # -- multigrid.py: transfers, coarse solve, v_cycle
+    out = {}
+    msh = mesh.MeshConfig(4, 3, 2.0, 2.0)
+    h = multigrid.build_hierarchy(msh, 32, multigrid.OverlapRule("fixed", 1))
+    for l in range(1, h.depth + 1):
+        lo, hi = h.levels[l - 1].op.layout, h.levels[l].op.layout
+        uc = rng.standard_normal((lo.N_y, lo.N_x))
+        vf = rng.standard_normal((hi.N_y, hi.N_x))
+        out[f"tr{l}_uc"] = uc
+        out[f"tr{l}_vf"] = vf
+        out[f"tr{l}_P"] = multigrid.prolongate(h, l, uc)
+        out[f"tr{l}_R"] = multigrid.restrict_residual(h, l, vf)
+    for i, (nx, ny, lx, ly, nu_hat) in enumerate([(4, 4, 2.0, 2.0, None), (8, 8, 1.0, 1.0, None),
+                                                   (16, 8, 8.0, 1.0, None), (8, 8, 1.0, 1.0, 0.9)]):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        h = multigrid.build_hierarchy(msh, 2, multigrid.OverlapRule("fixed", 1), nu_hat=nu_hat)
+        f0 = rng.standard_normal((ny, nx))
+        out[f"cs{i}_f0"] = f0
+        out[f"cs{i}_u0"] = multigrid.coarse_solve(h, f0)
+    for i, (nx, ny, lx, ly, p, rule, nu_hat, n_post) in enumerate([
+            (8, 8, 1.0, 1.0, 8, "fixed:1", None, 0), (4, 4, 2.0, 2.0, 16, "ceilp8", None, 0),
+            (6, 4, 8.0, 1.0, 8, "fixed:1", None, 1), (4, 4, 1.0, 1.0, 8, "ceilp8", 0.5, 1)]):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        h = multigrid.build_hierarchy(msh, p, multigrid.OverlapRule.parse(rule), nu_hat=nu_hat,
+                                      n_post=n_post)
+        lay = h.top.op.layout
+        f = operators.project_mean(np.random.default_rng(i).standard_normal((lay.N_y, lay.N_x)))
+        u = rng.random((lay.N_y, lay.N_x))
+        out[f"vc{i}_case"] = np.array([nx, ny, lx, ly, p, -1.0 if nu_hat is None else nu_hat, n_post])
+        out[f"vc{i}_rule"] = np.array(rule)
+        out[f"vc{i}_f"] = f
+        out[f"vc{i}_uin"] = u
+        out[f"vc{i}_uout"] = multigrid.v_cycle(h, u.copy(), f)
+        out[f"vc{i}_uzero"] = multigrid.v_cycle(h, np.zeros_like(f), f)
+    save("multigrid", **out)
+
+    # -- krylov.py: C1 (BASELINE configs[0]) histories, seeds 0,1,2, both solvers
+    out = {}
+    msh = mesh.MeshConfig(8, 8, 1.0, 1.0)
+    h = multigrid.build_hierarchy(msh, 8, multigrid.OverlapRule("fixed", 1))
+    lay = h.top.op.layout
+    for seed in (0, 1, 2):
+        f = operators.project_mean(np.random.default_rng(seed).standard_normal((lay.N_y, lay.N_x)))
+        for solver in ("mg", "mgcg"):
+            cfg = krylov.SolveConfig(solver=solver, tol_reduction=1e10, max_cycles=200, seed=seed)
+            u, rep = krylov.solve(h, f, cfg, u0=np.zeros_like(f))
+            out[f"c1_{solver}_{seed}_res"] = np.array(rep.residuals)
+            out[f"c1_{solver}_{seed}_u"] = u
+            out[f"c1_{solver}_{seed}_rbar"] = np.array(rep.rbar)
+    # the reference's own random-start (krylov.py:36-39) path, seed 5, AR 1, p=8, 4x4
+    msh = mesh.MeshConfig(4, 4)
+    h = multigrid.build_hierarchy(msh, 8, multigrid.OverlapRule("fixed", 1))
+    f, _ = operators.poisson_benchmark(msh, h.top.basis)
+    for solver in ("mg", "mgcg"):
+        u, rep = krylov.solve(h, f, krylov.SolveConfig(solver=solver, tol_reduction=1e8,
+                                                       max_cycles=40, seed=5))
+        out[f"rs_{solver}_res"] = np.array(rep.residuals)
+        out["rs_f"] = f
+    save("krylov", **out)
+
+
+def large():
+    """BASELINE-size runs of the reference (slow; sampled outputs only)."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    # C2: 64x64, p=16, MG solve (13 cycles in the survey), seed 0
+    t = time.time()
+    msh = mesh.MeshConfig(64, 64, 1.0, 1.0)
+    h = multigrid.build_hierarchy(msh, 16, multigrid.OverlapRule("fixed", 1))
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    u1 = multigrid.v_cycle(h, np.zeros_like(f), f)
+    out["c2_vcycle_sample"] = u1[::16, ::16].copy()
+    out["c2_vcycle_norm"] = np.array(np.linalg.norm(u1))
+    out["c2_vcycle_resnorm"] = np.array(np.linalg.norm(f - h.top.op.apply(u1)))
+    for solver in ("mg", "mgcg"):
+        u, rep = krylov.solve(h, f, krylov.SolveConfig(solver=solver, tol_reduction=1e10), u0=np.zeros_like(f))
+        out[f"c2_{solver}_res"] = np.array(rep.residuals)
+        out[f"c2_{solver}_sample"] = u[::16, ::16].copy()
+    print(f"C2 done in {time.time() - t:.1f}s")
+    save("large_c2", **out)
+
+
+def _hand_hierarchy(multigrid, basis, mesh, operators, schwarz, msh, orders, nu_hat, nu_shift=0.0):
+    """Hand-assembled reference hierarchy for non-power-of-two p (build_hierarchy
+    rejects p=24, multigrid.py:139-140) from the reference's own Level,
+    MultigridHierarchy, AdditiveSchwarz, interp_matrix, _global_prolongation."""
+    levels = []
+    for l, p_l in enumerate(orders):
+        b = basis.gll_basis(p_l)
+        lay = mesh.layout_for(msh, p_l)
+        if nu_hat is None:
+            op, nb = operators.PoissonOperator(b, msh), None
+        else:
+            op = operators.DiffusionOperator(b, msh, operators.diffusivity_field(msh, b, nu_hat, nu_shift))
+            nb = op.element_mean_nu()
+        if l == 0:
+            lv = multigrid.Level(l, b, op, None, 0, 0, 0)
+        else:
+            sm = schwarz.AdditiveSchwarz(b, lay, msh.dx, msh.dy, 1, schwarz.WeightKind.QUINTIC, nu_bar=nb)
+            lv = multigrid.Level(l, b, op, sm, 1, 0, 1)
+            j = basis.interp_matrix(levels[-1].basis, b).matrix
+            lv.px = multigrid._global_prolongation(j, orders[l - 1], p_l, msh.n_x)
+            lv.py = multigrid._global_prolongation(j, orders[l - 1], p_l, msh.n_y)
+        lv.u = lay.zeros()
+        lv.f = lay.zeros()
+        levels.append(lv)
+    return multigrid.MultigridHierarchy(msh, levels)
+
+
+def xlarge():
+    """C3 one V-cycle, C5-like reduced MGCG (64^2, p=24), C4 full MGCG (~20 min)."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    t = time.time()
+    msh = mesh.MeshConfig(128, 128, 1.0, 1.0)
+    h = multigrid.build_hierarchy(msh, 32, multigrid.OverlapRule("fixed", 1))
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    r0 = np.linalg.norm(f)
+    u1 = multigrid.v_cycle(h, np.zeros_like(f), f)
+    out["c3_vcycle_sample"] = u1[::64, ::64].copy()
+    out["c3_vcycle_norm"] = np.array(np.linalg.norm(u1))
+    out["c3_res"] = np.array([r0, np.linalg.norm(f - h.top.op.apply(u1))])
+    print(f"C3 done in {time.time() - t:.1f}s")
+    save("xlarge_c3", **out)
+    out = {}
+    t = time.time()
+    msh = mesh.MeshConfig(64, 64, 1.0, 1.0)
+    h = _hand_hierarchy(multigrid, basis, mesh, operators, schwarz, msh, [1, 3, 6, 12, 24], 0.9, 0.0)
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    u, rep = krylov.solve(h, f, krylov.SolveConfig(solver="mgcg", tol_reduction=1e10), u0=np.zeros_like(f))
+    out["c5r_mgcg_res"] = np.array(rep.residuals)
+    out["c5r_mgcg_sample"] = u[::24, ::24].copy()
+    print(f"C5-reduced done in {time.time() - t:.1f}s")
+    save("xlarge_c5r", **out)
+    out = {}
+    t = time.time()
+    msh = mesh.MeshConfig(256, 256, 8.0, 1.0)
+    h = multigrid.build_hierarchy(msh, 16, multigrid.OverlapRule("fixed", 1))
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    u, rep = krylov.solve(h, f, krylov.SolveConfig(solver="mgcg", tol_reduction=1e10), u0=np.zeros_like(f))
+    out["c4_mgcg_res"] = np.array(rep.residuals)
+    out["c4_mgcg_sample"] = u[::64, ::64].copy()
+    out["c4_breakdown"] = np.array(rep.breakdown)
+    print(f"C4 done in {time.time() - t:.1f}s")
+    save("xlarge_c4", **out)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--large", action="store_true")
+    ap.add_argument("--only-large", action="store_true")
+    ap.add_argument("--xlarge", action="store_true")
+    a = ap.parse_args()
+    if not (a.only_large or a.xlarge):
+        small()
+    if a.large or a.only_large:
+        large()
+    if a.xlarge:
+        xlarge()

@@ -1,0 +1,470 @@
+// C ABI of libsmg: handle construction, validation and dispatch.
+// See include/smg.h for the contract and the reference call site each entry
+// point replaces.
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "smg_common.cuh"
+#include "smg_fd.cuh"
+#include "smg_op.cuh"
+#include "smg_transfer.cuh"
+
+namespace smg {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return SMG_ECUDA;
+}
+
+int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro,
+               int rn, double tol, int it, double* ws, cudaStream_t st);
+int ccg_direction(double* p, const double* r, int64_t n, const double* S, int ro, int rn, cudaStream_t st);
+int ccg_dot(const double* x, const double* y, int64_t n, double* out, const double* S, double* ws, cudaStream_t st);
+int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
+         double* C, int ldc, const double* S, cudaStream_t st);
+
+static int largest_divisor_leq(int n, int cap) {
+  if (cap < 1) cap = 1;
+  for (int d = cap; d >= 1; --d)
+    if (n % d == 0) return d;
+  return 1;
+}
+
+int op_tx_max(int p) {
+  switch (p) {
+    case 1: return 32;
+    case 2: return 16;
+    case 3: return 10;
+    case 4: return 8;
+    case 5: case 6: return 5;
+    case 8: return 4;
+    case 12: case 16: return 2;
+    default: return p < 12 ? 32 / p : 1;
+  }
+}
+
+}  // namespace smg
+
+using namespace smg;
+
+// ---------------------------------------------------------------------------
+struct smg_op {
+  int kind, p, n_x, n_y, TX, TY;
+  double dx, dy;
+  std::vector<double> Mt, w, wasm;
+  const double* nu;
+  double* partials;  // device, one per CTA
+  int n_ctas;
+};
+
+struct smg_schwarz {
+  int p, n_o, n_x, n_y, m;
+  std::vector<double> Sx, Sy, wx, wy;
+  double* dinv;
+  const double* inv_nu;
+  struct Cls { int start, stride, count; };
+  std::vector<Cls> cx, cy;
+};
+
+struct smg_transfer {
+  int pc, pf, n_x, n_y;
+  int pTX, pTY, rTX, rTY;
+  std::vector<double> J;
+  smg::TrFn fn;
+};
+
+struct smg_coarse {
+  int n_x, n_y;
+  double* Qx;   // n_x x n_x
+  double* Qy;   // n_y x n_y
+  double* Lp;   // n_y x n_x pseudo-inverse eigenvalues
+};
+
+extern "C" {
+
+const char* smg_last_error(void) { return g_err; }
+int smg_version(void) { return 1; }
+
+int smg_device_ok(void) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_error("no CUDA device: %s", e != cudaSuccess ? cudaGetErrorString(e) : "count=0");
+    return 0;
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) {
+    set_error("libsmg is built for sm_100a; device has compute capability major %d", major);
+    return 0;
+  }
+  return 1;
+}
+
+// ---- operators --------------------------------------------------------------
+int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, double dy,
+                  const double* weights, const double* mat, const double* nu_dev) {
+  if (!h || !weights || !mat || p < 1 || n_x < 2 || n_y < 2 || !(dx > 0) || !(dy > 0) ||
+      (kind != 0 && kind != 1) || (kind == 1 && !nu_dev)) {
+    set_error("smg_op_create: bad argument");
+    return SMG_EINVAL;
+  }
+  if (!op_dispatch(p)) {
+    set_error("smg_op_create: order p=%d not compiled in", p);
+    return SMG_EUNSUPPORTED;
+  }
+  smg_op* o = new (std::nothrow) smg_op();
+  if (!o) return SMG_ENOMEM;
+  o->kind = kind; o->p = p; o->n_x = n_x; o->n_y = n_y; o->dx = dx; o->dy = dy;
+  o->Mt.assign(mat, mat + (p + 1) * (p + 1));
+  o->w.assign(weights, weights + p + 1);
+  o->wasm.resize(p);
+  for (int a = 0; a < p; ++a) o->wasm[a] = weights[a];
+  o->wasm[0] = weights[0] + weights[p];
+  o->nu = nu_dev;
+  const int cap = op_tx_max(p);
+  o->TX = largest_divisor_leq(n_x, cap);
+  o->TY = largest_divisor_leq(n_y, cap);
+  o->n_ctas = (n_x / o->TX) * (n_y / o->TY);
+  cudaError_t e = cudaMalloc(&o->partials, sizeof(double) * o->n_ctas);
+  if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
+  *h = o;
+  return SMG_OK;
+}
+
+int smg_op_destroy(smg_op_t* h) {
+  if (!h) return SMG_OK;
+  cudaFree(h->partials);
+  delete h;
+  return SMG_OK;
+}
+
+static int op_run(const smg_op_t* h, const double* u, const double* f, double* out, bool norm,
+                  cudaStream_t st) {
+  OpLaunch L;
+  L.u = u; L.f = f; L.out = out; L.nu = h->nu; L.partials = norm ? h->partials : nullptr;
+  L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.TX = h->TX; L.TY = h->TY; L.diffusion = h->kind;
+  L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
+  L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
+  return op_dispatch(h->p)(L, st);
+}
+
+int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out, void* stream) {
+  if (!h || !u || !out || u == out) { set_error("smg_op_residual: bad argument"); return SMG_EINVAL; }
+  return op_run(h, u, f, out, false, as_stream(stream));
+}
+
+int smg_sum_partials(const double* part, int nb, double* out, void* stream);
+
+int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
+                          double* norm2_out, double* ws, void* stream) {
+  (void)ws;
+  if (!h || !u || !out || u == out || !norm2_out) {
+    set_error("smg_op_residual_norm2: bad argument");
+    return SMG_EINVAL;
+  }
+  int rc = op_run(h, u, f, out, true, as_stream(stream));
+  if (rc) return rc;
+  return smg_sum_partials(h->partials, h->n_ctas, norm2_out, stream);
+}
+
+// ---- additive Schwarz ---------------------------------------------------------
+static void colour_classes(int n, int c, std::vector<smg_schwarz::Cls>& out) {
+  // c = colours needed so that same-colour windows are disjoint; if n is not
+  // a multiple of c, the trailing n % c elements get a class each.
+  const int full = (n / c) * c;
+  for (int k = 0; k < c && k < full; ++k) out.push_back({k, c, full / c});
+  for (int e = full; e < n; ++e) out.push_back({e, 1, 1});
+}
+
+int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, const double* S_x,
+                       const double* S_y, const double* lam_x, const double* lam_y,
+                       const double* w_x, const double* w_y, const double* inv_nu_dev) {
+  if (!h || !S_x || !S_y || !lam_x || !lam_y || !w_x || !w_y || p < 1 || n_o < 0 || n_o > p - 1 ||
+      n_x < 2 || n_y < 2) {
+    set_error("smg_schwarz_create: bad argument");
+    return SMG_EINVAL;
+  }
+  const int m = p + 1 + 2 * n_o;
+  if (m > p * n_x || m > p * n_y) {
+    set_error("subdomain window (%d nodes) wraps onto itself on a %dx%d mesh at p=%d; reduce n_o", m, n_x, n_y, p);
+    return SMG_EINVAL;
+  }
+  if (!fd_dispatch(m)) {
+    set_error("smg_schwarz_create: window size m=%d not compiled in", m);
+    return SMG_EUNSUPPORTED;
+  }
+  smg_schwarz* s = new (std::nothrow) smg_schwarz();
+  if (!s) return SMG_ENOMEM;
+  s->p = p; s->n_o = n_o; s->n_x = n_x; s->n_y = n_y; s->m = m;
+  s->Sx.assign(S_x, S_x + m * m);
+  s->Sy.assign(S_y, S_y + m * m);
+  s->wx.assign(w_x, w_x + m);
+  s->wy.assign(w_y, w_y + m);
+  s->inv_nu = inv_nu_dev;
+  std::vector<double> dinv(m * m);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) dinv[i * m + j] = 1.0 / (lam_y[i] + lam_x[j]);
+  cudaError_t e = cudaMalloc(&s->dinv, sizeof(double) * m * m);
+  if (e == cudaSuccess) e = cudaMemcpy(s->dinv, dinv.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { delete s; return cuda_fail(e, "smg_schwarz_create"); }
+  // colours per direction: windows of elements c apart are disjoint iff (c-1) p > 2 n_o
+  int c = 2;
+  while ((c - 1) * p <= 2 * n_o) ++c;
+  colour_classes(n_x, c > n_x ? n_x : c, s->cx);
+  colour_classes(n_y, c > n_y ? n_y : c, s->cy);
+  *h = s;
+  return SMG_OK;
+}
+
+int smg_schwarz_destroy(smg_schwarz_t* h) {
+  if (!h) return SMG_OK;
+  cudaFree(h->dinv);
+  delete h;
+  return SMG_OK;
+}
+
+static FDLaunch fd_base(const smg_schwarz_t* h) {
+  FDLaunch L;
+  std::memset(&L, 0, sizeof(L));
+  L.inv_nu = h->inv_nu; L.dinv = h->dinv;
+  L.p = h->p; L.n_o = h->n_o; L.N_x = h->p * h->n_x; L.N_y = h->p * h->n_y; L.n_x = h->n_x;
+  L.Sx = h->Sx.data(); L.Sy = h->Sy.data(); L.wx = h->wx.data(); L.wy = h->wy.data();
+  L.apply_weight = 1;
+  return L;
+}
+
+int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream) {
+  if (!h || !r || !u || r == u) { set_error("smg_schwarz_correct: bad argument"); return SMG_EINVAL; }
+  FDLaunchFn fn = fd_dispatch(h->m);
+  FDLaunch L = fd_base(h);
+  L.src = r; L.dst = u;
+  for (const auto& cy : h->cy)
+    for (const auto& cx : h->cx) {
+      L.x0 = cx.start; L.xs = cx.stride; L.xc = cx.count;
+      L.y0 = cy.start; L.ys = cy.stride; L.yc = cy.count;
+      int rc = fn(L, as_stream(stream));
+      if (rc) return rc;
+    }
+  return SMG_OK;
+}
+
+int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
+                       double* work, int n_it, int u_is_zero, void* stream) {
+  if (!h || !op || !u || !f || !work || n_it < 0 || op->p != h->p || op->n_x != h->n_x || op->n_y != h->n_y) {
+    set_error("smg_schwarz_smooth: bad argument");
+    return SMG_EINVAL;
+  }
+  for (int it = 0; it < n_it; ++it) {
+    const double* r = f;
+    if (!(it == 0 && u_is_zero)) {
+      int rc = smg_op_residual(op, u, f, work, stream);
+      if (rc) return rc;
+      r = work;
+    }
+    int rc = smg_schwarz_correct(h, r, u, stream);
+    if (rc) return rc;
+  }
+  return SMG_OK;
+}
+
+int smg_fd_solve_blocks(const smg_schwarz_t* h, const double* blocks, double* out, int nb,
+                        int apply_weight, void* stream) {
+  if (!h || !blocks || !out || nb < 0) { set_error("smg_fd_solve_blocks: bad argument"); return SMG_EINVAL; }
+  FDLaunch L = fd_base(h);
+  L.src = blocks; L.dst = out; L.inv_nu = nullptr; L.blocks_mode = 1; L.nb = nb;
+  L.apply_weight = apply_weight;
+  L.xc = 1; L.yc = 1;
+  return fd_dispatch(h->m)(L, as_stream(stream));
+}
+
+// ---- transfers --------------------------------------------------------------
+int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, const double* J) {
+  if (!h || !J || p_c < 1 || p_f <= p_c || n_x < 2 || n_y < 2) {
+    set_error("smg_transfer_create: bad argument");
+    return SMG_EINVAL;
+  }
+  TrFn fn = transfer_dispatch(p_c, p_f);
+  if (!fn) { set_error("smg_transfer_create: (p_c,p_f)=(%d,%d) not compiled in", p_c, p_f); return SMG_EUNSUPPORTED; }
+  smg_transfer* t = new (std::nothrow) smg_transfer();
+  if (!t) return SMG_ENOMEM;
+  t->pc = p_c; t->pf = p_f; t->n_x = n_x; t->n_y = n_y; t->fn = fn;
+  t->J.assign(J, J + (p_f + 1) * (p_c + 1));
+  const int cap = p_f >= 32 ? 1 : 32 / p_f;
+  t->pTX = largest_divisor_leq(n_x, cap); t->pTY = largest_divisor_leq(n_y, cap);
+  t->rTX = t->pTX; t->rTY = t->pTY;
+  *h = t;
+  return SMG_OK;
+}
+
+int smg_transfer_destroy(smg_transfer_t* h) { delete h; return SMG_OK; }
+
+static int tr_run(const smg_transfer_t* h, const double* src, double* dst, int acc, bool prolong, cudaStream_t st) {
+  TrArgs A;
+  A.src = src; A.dst = dst; A.pc = h->pc; A.pf = h->pf; A.n_x = h->n_x; A.n_y = h->n_y;
+  A.TX = prolong ? h->pTX : h->rTX; A.TY = prolong ? h->pTY : h->rTY;
+  A.tiles_x = h->n_x / A.TX; A.accumulate = acc;
+  std::memcpy(A.J, h->J.data(), sizeof(double) * h->J.size());
+  const int grid = (h->n_x / A.TX) * (h->n_y / A.TY);
+  return h->fn(A, grid, prolong, st);
+}
+
+int smg_prolongate(const smg_transfer_t* h, const double* uc, double* uf, int accumulate, void* stream) {
+  if (!h || !uc || !uf) { set_error("smg_prolongate: bad argument"); return SMG_EINVAL; }
+  return tr_run(h, uc, uf, accumulate, true, as_stream(stream));
+}
+
+int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* stream) {
+  if (!h || !ff || !fc) { set_error("smg_restrict: bad argument"); return SMG_EINVAL; }
+  return tr_run(h, ff, fc, 0, false, as_stream(stream));
+}
+
+int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,
+                          double* fc, double* work, void* stream) {
+  if (!h || !op || !u || !f || !fc || !work) { set_error("smg_residual_restrict: bad argument"); return SMG_EINVAL; }
+  int rc = smg_op_residual(op, u, f, work, stream);
+  if (rc) return rc;
+  return smg_restrict(h, work, fc, stream);
+}
+
+// ---- coarse pseudo-inverse -----------------------------------------------------
+static void fourier_basis(int n, std::vector<double>& Q, std::vector<double>& mu) {
+  // Orthonormal real eigenbasis of the periodic tridiag(-1, 2, -1); column-major
+  // by mode: Q[j*n + k] = q_k(j).
+  Q.assign((size_t)n * n, 0.0);
+  mu.assign(n, 0.0);
+  const double pi = 3.14159265358979323846;
+  int col = 0;
+  for (int j = 0; j < n; ++j) Q[(size_t)j * n + col] = 1.0 / std::sqrt((double)n);
+  mu[col++] = 0.0;
+  for (int k = 1; 2 * k < n; ++k) {
+    const double lam = 2.0 - 2.0 * std::cos(2.0 * pi * k / n);
+    for (int j = 0; j < n; ++j) {
+      Q[(size_t)j * n + col] = std::sqrt(2.0 / n) * std::cos(2.0 * pi * (double)j * k / n);
+      Q[(size_t)j * n + col + 1] = std::sqrt(2.0 / n) * std::sin(2.0 * pi * (double)j * k / n);
+    }
+    mu[col] = mu[col + 1] = lam;
+    col += 2;
+  }
+  if (n % 2 == 0) {
+    for (int j = 0; j < n; ++j) Q[(size_t)j * n + col] = (j % 2 ? -1.0 : 1.0) / std::sqrt((double)n);
+    mu[col++] = 4.0;
+  }
+}
+
+int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy) {
+  if (!h || n_x < 2 || n_y < 2 || !(dx > 0) || !(dy > 0)) { set_error("smg_coarse_create: bad argument"); return SMG_EINVAL; }
+  std::vector<double> Qx, Qy, mx, my;
+  fourier_basis(n_x, Qx, mx);
+  fourier_basis(n_y, Qy, my);
+  std::vector<double> Lp((size_t)n_y * n_x);
+  for (int ky = 0; ky < n_y; ++ky)
+    for (int kx = 0; kx < n_x; ++kx) {
+      const double lam = (dy / dx) * mx[kx] + (dx / dy) * my[ky];
+      Lp[(size_t)ky * n_x + kx] = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
+    }
+  smg_coarse* c = new (std::nothrow) smg_coarse();
+  if (!c) return SMG_ENOMEM;
+  c->n_x = n_x; c->n_y = n_y;
+  cudaError_t e = cudaMalloc(&c->Qx, sizeof(double) * Qx.size());
+  if (e == cudaSuccess) e = cudaMalloc(&c->Qy, sizeof(double) * Qy.size());
+  if (e == cudaSuccess) e = cudaMalloc(&c->Lp, sizeof(double) * Lp.size());
+  if (e == cudaSuccess) e = cudaMemcpy(c->Qx, Qx.data(), sizeof(double) * Qx.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->Qy, Qy.data(), sizeof(double) * Qy.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->Lp, Lp.data(), sizeof(double) * Lp.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "smg_coarse_create"); }
+  *h = c;
+  return SMG_OK;
+}
+
+int smg_coarse_destroy(smg_coarse_t* h) {
+  if (!h) return SMG_OK;
+  cudaFree(h->Qx); cudaFree(h->Qy); cudaFree(h->Lp);
+  delete h;
+  return SMG_OK;
+}
+
+size_t smg_coarse_ws_doubles(const smg_coarse_t* h) { return h ? 2 * (size_t)h->n_x * h->n_y : 0; }
+
+int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double* ws, void* stream) {
+  if (!h || !f0 || !u0 || !ws || f0 == u0) { set_error("smg_coarse_pinv: bad argument"); return SMG_EINVAL; }
+  cudaStream_t st = as_stream(stream);
+  const int nx = h->n_x, ny = h->n_y;
+  double* T1 = ws;
+  double* T2 = ws + (size_t)nx * ny;
+  int rc;
+  // T1 = Qy^T F ; T2 = (T1 Qx) .* Lp ; T1 = Qy T2 ; U = T1 Qx^T
+  if ((rc = gemm(ny, nx, ny, h->Qy, ny, 1, f0, nx, 0, T1, nx, nullptr, st))) return rc;
+  if ((rc = gemm(ny, nx, nx, T1, nx, 0, h->Qx, nx, 0, T2, nx, h->Lp, st))) return rc;
+  if ((rc = gemm(ny, nx, ny, h->Qy, ny, 0, T2, nx, 0, T1, nx, nullptr, st))) return rc;
+  return gemm(ny, nx, nx, T1, nx, 0, h->Qx, nx, 1, u0, nx, nullptr, st);
+}
+
+
+// ---- coarse plain CG (parity mode): multigrid.py:196-228 on the device ------
+size_t smg_coarse_cg_ws_doubles(int64_t n) { return 4 * (size_t)n + smg_reduce_ws_doubles() + 16; }
+
+int smg_coarse_cg(const smg_op_t* op, const double* f0, double* u0, double* ws, double tol, int max_iter,
+                  int* iters_out, void* stream) {
+  if (!op || !f0 || !u0 || !ws || !iters_out || op->p != 1 || max_iter < 1) {
+    set_error("smg_coarse_cg: bad argument");
+    return SMG_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = (int64_t)op->n_x * op->n_y;
+  double* b = ws;
+  double* r = b + n;
+  double* p = r + n;
+  double* q = p + n;
+  double* red = q + n;
+  double* S = red + smg_reduce_ws_doubles();
+  int rc;
+  cudaError_t e;
+  // b = f0 - mean(f0); x = 0; r = b; p = r
+  if ((e = cudaMemcpyAsync(b, f0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((rc = smg_project_mean(b, n, red, stream))) return rc;
+  if ((e = cudaMemsetAsync(S, 0, sizeof(double) * 16, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((e = cudaMemsetAsync(u0, 0, sizeof(double) * n, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((e = cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((e = cudaMemcpyAsync(p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((rc = ccg_dot(b, b, n, S + 0, nullptr, red, st))) return rc;
+  if ((rc = ccg_dot(r, r, n, S + 2, nullptr, red, st))) return rc;
+  double hs[6];
+  if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 6, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_cg");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_cg");
+  if (hs[0] == 0.0) { *iters_out = 0; return SMG_OK; }
+  int it = 0;
+  const int chunk = 32;
+  while (it < max_iter) {
+    const int stop = it + chunk < max_iter ? it + chunk : max_iter;
+    for (; it < stop; ++it) {
+      const int ro = 2 + (it & 1), rn = 3 - (it & 1);
+      if ((rc = smg_op_residual(op, p, nullptr, q, stream))) return rc;
+      if ((rc = ccg_dot(p, q, n, S + 1, S, red, st))) return rc;
+      if ((rc = ccg_update(u0, r, p, q, n, S, ro, rn, tol, it + 1, red, st))) return rc;
+      if ((rc = ccg_direction(p, r, n, S, ro, rn, st))) return rc;
+    }
+    if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 6, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_cg");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_cg");
+    if (hs[4] != 0.0) break;
+  }
+  const bool ok = hs[4] != 0.0;
+  *iters_out = ok ? (int)hs[5] : -max_iter;
+  // u0 = x - mean(x)  (multigrid.py:228)
+  return smg_project_mean(u0, n, red, stream);
+}
+
+}  // extern "C"

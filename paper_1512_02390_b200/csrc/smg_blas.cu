@@ -1,0 +1,360 @@
+// BLAS-1 with device-resident scalars (subsystem 4) and the p=1 coarse
+// pseudo-inverse.  All reductions use a fixed grid and a fixed summation
+// tree (grid-stride partials -> per-block tree -> last block sums the
+// partials in block order), so results are bitwise reproducible run to run
+// (the reference's test_krylov.py:73-81 demands identical histories).
+#include "smg_common.cuh"
+
+namespace smg {
+
+// ws layout: [kReduceBlocks * 8 partial doubles][1 counter word]
+constexpr int kPartStride = 8;
+
+static int grid_for_reduce(int64_t n) {
+  int64_t g = (n + 4 * kReduceThreads - 1) / (4 * kReduceThreads);
+  if (g > kReduceBlocks) g = kReduceBlocks;
+  return g < 1 ? 1 : (int)g;
+}
+
+static int grid_for(int64_t n) {
+  int64_t g = (n + kReduceThreads - 1) / kReduceThreads;
+  if (g > kReduceBlocks) g = kReduceBlocks;
+  return g < 1 ? 1 : (int)g;
+}
+
+
+__device__ __forceinline__ bool last_block_arrive(double* ws) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + kReduceBlocks * kPartStride);
+    const unsigned int t = atomicAdd(ctr, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  return last;
+}
+
+__device__ __forceinline__ void reset_counter(double* ws) {
+  if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(ws + kReduceBlocks * kPartStride) = 0u;
+}
+
+// Sum NV per-block partials in block order; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void finish(double (&v)[NV], const double* ws, double* red) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += ws[b * kPartStride + k];
+  }
+  block_reduce<NV>(v, red);
+}
+
+template <int NV>
+__device__ __forceinline__ void publish(double (&v)[NV], double* ws, double* red) {
+  block_reduce<NV>(v, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) ws[blockIdx.x * kPartStride + k] = v[k];
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads)
+dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* out,
+           double* ws) {
+  __shared__ double red[32];
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[0] = fma(x[i], y[i], v[0]);
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) out[0] = v[0];
+  reset_counter(ws);
+}
+
+__global__ void __launch_bounds__(kReduceThreads)
+sum_kernel(const double* __restrict__ x, int64_t n, double* out, double* ws) {
+  __shared__ double red[32];
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[0] += x[i];
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) out[0] = v[0];
+  reset_counter(ws);
+}
+
+// out[0] = z.(r - r_old), out[1] = z.r ; also the Polak-Ribiere bookkeeping
+// when scal != nullptr: scal[5] = out0 / scal[0] (beta), scal[0] = out1 (delta).
+__global__ void __launch_bounds__(kReduceThreads)
+dot2_kernel(const double* __restrict__ z, const double* __restrict__ r, const double* __restrict__ ro,
+            int64_t n, double* out, double* scal, double* ws) {
+  __shared__ double red[64];
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double zi = z[i], ri = r[i];
+    v[0] = fma(zi, ro != nullptr ? ri - ro[i] : ri, v[0]);
+    v[1] = fma(zi, ri, v[1]);
+  }
+  publish<2>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<2>(v, ws, red);
+  if (threadIdx.x == 0) {
+    if (out != nullptr) { out[0] = v[0]; out[1] = v[1]; }
+    if (scal != nullptr) { scal[5] = v[0] / scal[0]; scal[0] = v[1]; }
+  }
+  reset_counter(ws);
+}
+
+// krylov.py:95-103 as one pass (breakdown check on device).
+__global__ void __launch_bounds__(kReduceThreads)
+cg_update_kernel(double* __restrict__ u, const double* r_in, double* r_out, const double* __restrict__ p,
+                 const double* __restrict__ q, int64_t n, double* scal, int* flag, double* ws) {
+  __shared__ double red[32];
+  const double pq = scal[1];
+  if (!(pq > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag[0] = 1;
+    return;
+  }
+  const double alpha = scal[0] / pq;
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    u[i] = __dadd_rn(u[i], __dmul_rn(alpha, p[i]));
+    const double rn = __dsub_rn(r_in[i], __dmul_rn(alpha, q[i]));
+    r_out[i] = rn;
+    v[0] = fma(rn, rn, v[0]);
+  }
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) { scal[2] = v[0]; scal[6] = alpha; }
+  reset_counter(ws);
+}
+
+__global__ void cg_direction_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                    const double* scal) {
+  const double beta = scal[5];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+__global__ void axpby_kernel(double a, const double* __restrict__ x, double b, double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
+}
+
+__global__ void sub_mean_kernel(double* __restrict__ f, int64_t n, const double* sum) {
+  const double mean = sum[0] / (double)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    f[i] -= mean;
+}
+
+// Final sum of op_kernel per-CTA partials (fixed order).
+__global__ void __launch_bounds__(kReduceThreads) sum_partials_kernel(const double* __restrict__ part, int nb, double* out) {
+  __shared__ double red[32];
+  double v[1] = {0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v[0] += part[b];
+  block_reduce<1>(v, red);
+  if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// ---- small dense GEMM for the coarse pseudo-inverse ------------------------
+// C[M,N] = op(A) op(B) (.* S when S != nullptr); op = transpose when tX.
+// 64x64 tiles, 256 threads, 4x4 outputs per thread, DFMA.
+__global__ void __launch_bounds__(256)
+gemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda, int tA,
+            const double* __restrict__ B, int ldb, int tB, double* __restrict__ C, int ldc,
+            const double* __restrict__ S) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tid = threadIdx.x;
+  const int tr = tid / 16, tc = tid % 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int idx = tid; idx < 16 * 64; idx += 256) {
+      const int kk = idx / 64, mm = idx % 64;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? (tA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
+      const int gn = n0 + mm;
+      Bs[kk][mm] = (gn < N && gk < K) ? (tB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tr + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tc + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + tr + 16 * i, gn = n0 + tc + 16 * j;
+      if (gm < M && gn < N) {
+        double v = acc[i][j];
+        if (S != nullptr) v *= S[(size_t)gm * N + gn];
+        C[(size_t)gm * ldc + gn] = v;
+      }
+    }
+}
+
+int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
+         double* C, int ldc, const double* S, cudaStream_t st) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, A, lda, tA, B, ldb, tB, C, ldc, S);
+  return check_launch("gemm_kernel");
+}
+
+// ---- plain CG of the coarse level (multigrid.py:196-215), device scalars --
+// S[0] = ||b||^2, S[1] = p.q, S[2]/S[3] = rho (ping-pong), S[4] = done, S[5] = iterations
+__global__ void __launch_bounds__(kReduceThreads)
+ccg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                  const double* __restrict__ q, int64_t n, double* S, int ro, int rn, double tol,
+                  int it, double* ws) {
+  __shared__ double red[32];
+  if (S[4] != 0.0) return;
+  const double alpha = S[ro] / S[1];
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    r[i] = ri;
+    v[0] = fma(ri, ri, v[0]);
+  }
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) {
+    S[rn] = v[0];
+    if (sqrt(v[0]) <= tol * sqrt(S[0])) { S[4] = 1.0; S[5] = (double)it; }
+  }
+  reset_counter(ws);
+}
+
+__global__ void ccg_direction_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t n,
+                                     const double* S, int ro, int rn) {
+  if (S[4] != 0.0) return;
+  const double beta = S[rn] / S[ro];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+}
+
+__global__ void ccg_dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                               double* out, const double* S, double* ws) {
+  __shared__ double red[32];
+  if (S != nullptr && S[4] != 0.0) return;
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[0] = fma(x[i], y[i], v[0]);
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) out[0] = v[0];
+  reset_counter(ws);
+}
+
+int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro,
+               int rn, double tol, int it, double* ws, cudaStream_t st) {
+  ccg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, r, p, q, n, S, ro, rn, tol, it, ws);
+  return check_launch("ccg_update_kernel");
+}
+int ccg_direction(double* p, const double* r, int64_t n, const double* S, int ro, int rn, cudaStream_t st) {
+  ccg_direction_kernel<<<grid_for(n), kReduceThreads, 0, st>>>(p, r, n, S, ro, rn);
+  return check_launch("ccg_direction_kernel");
+}
+int ccg_dot(const double* x, const double* y, int64_t n, double* out, const double* S, double* ws, cudaStream_t st) {
+  ccg_dot_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, y, n, out, S, ws);
+  return check_launch("ccg_dot_kernel");
+}
+
+
+}  // namespace smg
+
+using namespace smg;
+
+extern "C" {
+
+size_t smg_reduce_ws_doubles(void) { return (size_t)kReduceBlocks * kPartStride + 2; }
+
+int smg_dot(const double* x, const double* y, int64_t n, double* out, double* ws, void* stream) {
+  if (!x || !y || !out || !ws || n < 0) { set_error("smg_dot: bad argument"); return SMG_EINVAL; }
+  dot_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, y, n, out, ws);
+  return check_launch("dot_kernel");
+}
+
+int smg_sum(const double* x, int64_t n, double* out, double* ws, void* stream) {
+  if (!x || !out || !ws || n < 0) { set_error("smg_sum: bad argument"); return SMG_EINVAL; }
+  sum_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, n, out, ws);
+  return check_launch("sum_kernel");
+}
+
+int smg_dot2(const double* x, const double* y, const double* z, int64_t n, double* out, double* ws,
+             void* stream) {
+  if (!x || !y || !out || !ws || n < 0) { set_error("smg_dot2: bad argument"); return SMG_EINVAL; }
+  dot2_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, y, z, n, out, nullptr, ws);
+  return check_launch("dot2_kernel");
+}
+
+int smg_cg_beta(const double* z, const double* r, const double* r_old, int64_t n, double* scal,
+                double* ws, void* stream) {
+  if (!z || !r || !scal || !ws || n < 0) { set_error("smg_cg_beta: bad argument"); return SMG_EINVAL; }
+  dot2_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(z, r, r_old, n, nullptr, scal, ws);
+  return check_launch("dot2_kernel");
+}
+
+int smg_axpby(double alpha, const double* x, double beta, double* y, int64_t n, void* stream) {
+  if (!x || !y || n < 0) { set_error("smg_axpby: bad argument"); return SMG_EINVAL; }
+  axpby_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(alpha, x, beta, y, n);
+  return check_launch("axpby_kernel");
+}
+
+int smg_cg_update2(double* u, const double* r_in, double* r_out, const double* p, const double* q,
+                   int64_t n, double* scal, int* flag, double* ws, void* stream) {
+  if (!u || !r_in || !r_out || !p || !q || !scal || !flag || !ws) {
+    set_error("smg_cg_update: bad argument");
+    return SMG_EINVAL;
+  }
+  cg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(u, r_in, r_out, p, q, n, scal, flag, ws);
+  return check_launch("cg_update_kernel");
+}
+
+int smg_cg_update(double* u, double* r, const double* p, const double* q, int64_t n, double* scal,
+                  int* flag, double* ws, void* stream) {
+  return smg_cg_update2(u, r, r, p, q, n, scal, flag, ws, stream);
+}
+
+int smg_cg_direction(double* p, const double* z, int64_t n, double* scal, void* stream) {
+  if (!p || !z || !scal) { set_error("smg_cg_direction: bad argument"); return SMG_EINVAL; }
+  cg_direction_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(p, z, n, scal);
+  return check_launch("cg_direction_kernel");
+}
+
+int smg_project_mean(double* f, int64_t n, double* ws, void* stream) {
+  if (!f || !ws || n <= 0) { set_error("smg_project_mean: bad argument"); return SMG_EINVAL; }
+  double* s = ws + (size_t)kReduceBlocks * kPartStride + 1;
+  sum_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(f, n, s, ws);
+  int rc = check_launch("sum_kernel");
+  if (rc) return rc;
+  sub_mean_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(f, n, s);
+  return check_launch("sub_mean_kernel");
+}
+
+int smg_sum_partials(const double* part, int nb, double* out, void* stream) {
+  sum_partials_kernel<<<1, kReduceThreads, 0, as_stream(stream)>>>(part, nb, out);
+  return check_launch("sum_partials_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Shared helpers for libsmg (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/smg.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libsmg targets sm_100a only"
+#endif
+
+namespace smg {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* where);
+
+// Return SMG_ECUDA with the pending launch error, if any.
+inline int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, where);
+  return SMG_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__host__ __device__ __forceinline__ int wrapi(int i, int n) {
+  // periodic index for i in [-n, 2n)
+  return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
+// Deterministic block reduction of NV doubles (fixed tree order).
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double* sbuf /*32*NV*/) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sbuf[k * 32 + wid] = v[k];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double t = lane < nw ? sbuf[k * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      v[k] = t;
+    }
+  }
+}
+
+constexpr int kReduceBlocks = 592;   // 4 x 148 SMs: fixed => deterministic
+constexpr int kReduceThreads = 512;
+
+}  // namespace smg
