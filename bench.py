@@ -1,0 +1,395 @@
+"""Benchmark: weighted-Schwarz smoother + p-multigrid V-cycle DOF/s on B200.
+
+Workload (BASELINE.json configs[1], "C2"): periodic Poisson on [0,1]^2,
+64x64 elements, p = 16 (1,048,576 DOF), FP64, f = N(0,1) from seed 0 with
+the mean removed, weighted additive Schwarz (w5, fixed:1 overlap), V-cycle
+with one pre-smoothing and no post-smoothing, coarse p=1 pseudo-inverse.
+A step is one V-cycle u <- V(u, f) of the stand-alone MG iteration (full
+work: the top level applies A to a nonzero u).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: CUDA events on the launching stream around each step, L2 flushed
+(256 MiB write) before every timed step, K steps bracketed by barrier +
+synchronize, max over ranks.  N > 1: one process per GPU, each running an
+independent replica (scaling "weak"; strip decomposition is not built yet).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(n_x=64, n_y=64, l_x=1.0, l_y=1.0, p=16, rule="fixed:1", seed=0)
+METRIC = "weighted-Schwarz smoother + V-cycle DOF/s, fraction of FP64/HBM roofline"
+FP64_PEAK_TFLOPS = 37.15   # measured: DMMA m8n8k4 on this pool's B200 (tools/peaks, profiles/fp64_peaks.txt)
+FP64_DFMA_TFLOPS = 34.2    # measured: DFMA register-operand peak
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def fd_flops_per_element(m: int) -> float:
+    """Dense FD as executed by schwarz.py:217-221: 4 contractions + scaling + weight."""
+    return 8.0 * m ** 3 + 3.0 * m ** 2
+
+
+def vcycle_roofline_seconds(n_x, n_y, orders, n_o_of, p64, bw):
+    """sum over levels l >= 1 of max(F/P64, B/BW) for the sweep,
+    the residual+restriction and the prolongation (coarse solve excluded)."""
+    t = 0.0
+    n_el = n_x * n_y
+    for l in range(1, len(orders)):
+        p, pc = orders[l], orders[l - 1]
+        N, Nc = p * p * n_el, pc * pc * n_el
+        m = p + 1 + 2 * n_o_of(p)
+        npp = p + 1
+        f_apply = n_el * (4 * npp ** 3 + 3 * npp ** 2) + N
+        top = l == len(orders) - 1
+        # sweep: residual (top level only; lower levels start from zero) + FD
+        if top:
+            t += max(f_apply / p64, 24.0 * N / bw)
+        t += max(n_el * fd_flops_per_element(m) / p64, 24.0 * N / bw)
+        # residual + restriction, prolongation
+        t += max(f_apply / p64, 24.0 * N / bw)
+        f_tr = 2.0 * n_el * ((p + 1) * (pc + 1) ** 2 + (p + 1) ** 2 * (pc + 1))
+        t += max(f_tr / p64, (8.0 * N + 8.0 * Nc) / bw)
+        t += max(f_tr / p64, (16.0 * N + 8.0 * Nc) / bw)
+    return t
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("internal_api") in ("openblas", "mkl", "blis")]
+        if info:
+            return int(info[0]["num_threads"])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def oracle_problem():
+    from oracle import smg_oracle as O
+    c = CFG
+    h = O.Hierarchy(c["n_x"], c["n_y"], c["l_x"], c["l_y"], c["p"], rule=c["rule"])
+    N = (c["p"] * c["n_y"], c["p"] * c["n_x"])
+    f = O.project_mean(np.random.default_rng(c["seed"]).standard_normal(N))
+    return O, h, f
+
+
+def time_cpu_vcycles(budget_s: float, max_steps: int | None = None, warmup: int = 0):
+    """The oracle port (numpy restatement of the reference, all host threads)."""
+    O, h, f = oracle_problem()
+    u = np.zeros_like(f)
+    for _ in range(warmup):
+        u = O.v_cycle(h, u, f)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        u = O.v_cycle(h, u, f)
+        times.append(time.perf_counter() - t0)
+        if max_steps is not None and len(times) >= max_steps:
+            break
+        if max_steps is None and time.perf_counter() - t_start > budget_s:
+            break
+    return times, f.size
+
+
+def run_reference(args):
+    times, ndof = time_cpu_vcycles(0.0, max_steps=args.steps, warmup=args.warmup)
+    t = float(np.sum(times))
+    value = ndof * len(times) / t
+    cores = cpu_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": args.gpus,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1), mean removed)",
+            "config": {"workload": "C2: periodic Poisson 64x64 elements, p=16 (1,048,576 DOF), stand-alone "
+                                   "V-cycle (1,0), w5, fixed:1", "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
+                             "sample": f"{len(times)} V-cycles of the numpy restatement (oracle/smg_oracle.py) "
+                                       f"of the reference on the C2 workload"},
+            "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-micro", action="store_true", help="skip the smoother microbenchmark")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200 import _native as NV
+    from paper_1512_02390_b200.multigrid import _v_cycle
+
+    lib = NV.lib()
+    c = CFG
+    mesh = P.MeshConfig(c["n_x"], c["n_y"], c["l_x"], c["l_y"])
+    rule = P.OverlapRule.parse(c["rule"])
+    h = P.build_hierarchy(mesh, c["p"], rule)
+    shape = h.top.op.layout.shape
+    ndof = shape[0] * shape[1]
+    f_host = P.project_mean(np.random.default_rng(c["seed"]).standard_normal(shape))
+    f = torch.from_numpy(f_host).to(dev)
+    u = torch.zeros(shape, dtype=torch.float64, device=dev)
+    bw, bw_src = _peaks()
+    p64 = FP64_PEAK_TFLOPS * 1e12
+
+    # eager warm-up (sets kernel attributes) and launch count per step
+    _v_cycle(h, u, f)
+    torch.cuda.synchronize()
+    n0 = lib.smg_launch_count()
+    _v_cycle(h, u, f)
+    torch.cuda.synchronize()
+    launches_per_step = lib.smg_launch_count() - n0
+
+    # capture one step as a CUDA graph
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        _v_cycle(h, u, f)
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        _v_cycle(h, u, f)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        g.replay()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    for a, b in ev:
+        flush.fill_(1.0)
+        a.record()
+        g.replay()
+        b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    t_steps = float(sum(a.elapsed_time(b) for a, b in ev)) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_steps], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_steps = float(tt.item())
+    value = ndof * world * args.steps / t_steps
+    ms_per_step = 1e3 * t_steps / args.steps
+
+    # ---- dominant kernel: the fused FD Schwarz correction on the top level
+    sm = h.top.smoother
+    r = torch.randn(shape, dtype=torch.float64, device=dev)
+    ucor = torch.zeros(shape, dtype=torch.float64, device=dev)
+    reps = 20
+    sm.correct(r, ucor)
+    fd_times = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sm.correct(r, ucor)
+        b.record()
+        fd_times.append((a, b))
+    torch.cuda.synchronize()
+    t_fd = float(np.mean([a.elapsed_time(b) for a, b in fd_times])) / 1e3
+    m = c["p"] + 1 + 2 * rule.layers(c["p"])
+    fd_flops = mesh.n_el * fd_flops_per_element(m)
+    fd_achieved = fd_flops / t_fd / 1e12
+    roofline = {"bound": "tensor", "pipe": "fp64", "kernel": "fd_kernel<19> (fused Schwarz FD, 4 colour launches)",
+                "achieved": fd_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": fd_achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "measured FP64 DMMA peak (tools/peaks/fp64_peaks.cu); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "algorithmic_flops_per_call": fd_flops, "ms_per_call": 1e3 * t_fd}
+    orders = [lv.basis.p for lv in h.levels]
+    t_roof = vcycle_roofline_seconds(mesh.n_x, mesh.n_y, orders, rule.layers, p64, bw * 1e9)
+
+    # ---- end to end through the public API with host buffers
+    f_pin = torch.from_numpy(f_host).pin_memory()
+    u_pin = torch.empty(shape, dtype=torch.float64).pin_memory()
+    e2e_ev = []
+    for _ in range(args.warmup):
+        f.copy_(f_pin, non_blocking=True)
+        g.replay()
+        u_pin.copy_(u, non_blocking=True)
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        f.copy_(f_pin, non_blocking=True)
+        g.replay()
+        u_pin.copy_(u, non_blocking=True)
+        b.record()
+        e2e_ev.append((a, b))
+    torch.cuda.synchronize()
+    t_e2e = float(sum(a.elapsed_time(b) for a, b in e2e_ev)) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = {"value": ndof * world * args.steps / t_e2e, "unit": "DOF/s",
+           "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
+           "path": "pinned host f -> H2D -> v_cycle (graph replay of the public v_cycle) -> D2H u"}
+
+    # ---- smoother-only microbenchmark (64^2 and 256^2 elements, n_o = 1)
+    micro = None
+    if not args.no_micro:
+        micro = {}
+        for n_el1d in (64, 256):
+            for p in (4, 8, 12, 16, 24, 32):
+                msh = P.MeshConfig(n_el1d, n_el1d, 1.0, 1.0)
+                lay = P.layout_for(msh, p)
+                sm2 = P.AdditiveSchwarz(P.gll_basis(p), lay, msh.dx, msh.dy, 1, P.WeightKind.QUINTIC)
+                rr = torch.randn(lay.shape, dtype=torch.float64, device=dev)
+                uu = torch.zeros(lay.shape, dtype=torch.float64, device=dev)
+                sm2.correct(rr, uu)
+                evs = []
+                for _ in range(10):
+                    flush.fill_(1.0)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    sm2.correct(rr, uu)
+                    b.record()
+                    evs.append((a, b))
+                torch.cuda.synchronize()
+                tt = float(np.median([a.elapsed_time(b) for a, b in evs])) / 1e3
+                mm = p + 3
+                fl = msh.n_el * fd_flops_per_element(mm)
+                micro[f"{n_el1d}x{n_el1d}_p{p}"] = {
+                    "gdof_s": lay.size / tt / 1e9, "tflops": fl / tt / 1e12,
+                    "frac_fp64": fl / tt / 1e12 / FP64_PEAK_TFLOPS, "us": 1e6 * tt}
+                del sm2, rr, uu
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times, _ = time_cpu_vcycles(args.cpu_budget)
+        tc = float(np.sum(times))
+        cpu = {"value": ndof * len(times) / tc, "unit": "DOF/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{len(times)} C2 V-cycles of the numpy restatement of the reference "
+                         "(oracle/smg_oracle.py), OpenBLAS threads = cores"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded N(0,1) RHS, mean removed)",
+                "config": {"workload": "C2: periodic Poisson [0,1]^2, 64x64 elements, p=16 (1,048,576 DOF), "
+                                       "stand-alone V-cycle (1 pre-, 0 post-smoothing), w5, fixed:1, "
+                                       "coarse p=1 pseudo-inverse",
+                           "global_dofs": ndof * world, "levels": orders,
+                           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                           "l2": "flushed (256 MiB write) before every timed step",
+                           "cuda_graph": True},
+                "vcycle_roofline": {"t_roof_us": 1e6 * t_roof, "t_measured_us": ms_per_step * 1e3,
+                                    "frac": t_roof / (ms_per_step / 1e3),
+                                    "model": "SURVEY.md §8(d) sum of max(F/P64, B/BW) over levels, "
+                                             f"P64={FP64_PEAK_TFLOPS} TF, BW={bw} GB/s ({bw_src}), coarse excluded"},
+                "roofline": roofline, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+                "clocks": clocks, "wall_s_timed_region": t_wall}
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        if micro is not None:
+            line["smoother_microbench"] = micro
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

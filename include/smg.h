@@ -40,6 +40,9 @@ typedef struct smg_coarse smg_coarse_t;     /* p=1 pseudo-inverse            */
 
 const char* smg_last_error(void);
 int smg_version(void);
+/* Number of kernel launches libsmg has enqueued in this process (evidence
+ * for the bench's gpu_launches claim; graph replays are not re-counted). */
+int64_t smg_launch_count(void);
 /* 1 if a CUDA device is usable, else 0 (and smg_last_error says why). */
 int smg_device_ok(void);
 

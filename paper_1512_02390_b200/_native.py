@@ -28,6 +28,7 @@ _i64 = C.c_int64
 SIGNATURES = {
     "smg_last_error": (C.c_char_p, []),
     "smg_version": (C.c_int, []),
+    "smg_launch_count": (C.c_int64, []),
     "smg_device_ok": (C.c_int, []),
     "smg_op_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                 C.c_double, _hp, _hp, _dp]),

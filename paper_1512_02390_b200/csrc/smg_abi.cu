@@ -1,6 +1,7 @@
 // C ABI of libsmg: handle construction, validation and dispatch.
 // See include/smg.h for the contract and the reference call site each entry
 // point replaces.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -15,6 +16,9 @@
 namespace smg {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -96,6 +100,7 @@ extern "C" {
 
 const char* smg_last_error(void) { return g_err; }
 int smg_version(void) { return 1; }
+int64_t smg_launch_count(void) { return g_launches.load(); }
 
 int smg_device_ok(void) {
   int n = 0;

@@ -16,8 +16,11 @@ namespace smg {
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* where);
 
-// Return SMG_ECUDA with the pending launch error, if any.
+void count_launch();
+
+// Return SMG_ECUDA with the pending launch error, if any (and count the launch).
 inline int check_launch(const char* where) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, where);
   return SMG_OK;
