@@ -4,12 +4,14 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
 
 #include "smg_common.cuh"
 #include "smg_fd.cuh"
+#include "smg_fdt.cuh"
 #include "smg_op.cuh"
 #include "smg_transfer.cuh"
 
@@ -80,6 +82,14 @@ struct smg_schwarz {
   const double* inv_nu;
   struct Cls { int start, stride, count; };
   std::vector<Cls> cx, cy;
+  // tiled even/odd path (smg_fdt.cuh); tiled == false -> coloured dense path
+  bool tiled;
+  smg::FDTLaunchFn fdt;
+  int TX, TY, ntx, nty;
+  std::vector<double> Sye, Syo, Sxe, Sxo;
+  double* dinv_perm;
+  double* ws;
+  unsigned int* ctr;
 };
 
 struct smg_transfer {
@@ -95,6 +105,43 @@ struct smg_coarse {
   double* Qy;   // n_y x n_y
   double* Lp;   // n_y x n_x pseudo-inverse eigenvalues
 };
+
+namespace {
+
+// Split S (m x m, row-major S[k][i]) into symmetrized even/odd halves.
+// Returns false if some eigenvector is not (numerically) even or odd.
+bool even_odd_split(const double* S, int m, std::vector<double>& Se, std::vector<double>& So,
+                    std::vector<int>& perm) {
+  const int HE = (m + 1) / 2, HO = m / 2;
+  double smax = 0.0;
+  for (int i = 0; i < m * m; ++i) smax = std::fmax(smax, std::fabs(S[i]));
+  std::vector<int> ev, od;
+  for (int i = 0; i < m; ++i) {
+    double dot = 0.0, asym_e = 0.0, asym_o = 0.0;
+    for (int k = 0; k < m; ++k) {
+      dot += S[k * m + i] * S[(m - 1 - k) * m + i];
+      asym_e = std::fmax(asym_e, std::fabs(S[k * m + i] - S[(m - 1 - k) * m + i]));
+      asym_o = std::fmax(asym_o, std::fabs(S[k * m + i] + S[(m - 1 - k) * m + i]));
+    }
+    const bool is_even = dot > 0.0;
+    if ((is_even ? asym_e : asym_o) > 1e-6 * smax) return false;
+    (is_even ? ev : od).push_back(i);
+  }
+  if ((int)ev.size() != HE || (int)od.size() != HO) return false;
+  Se.assign((size_t)HE * HE, 0.0);
+  So.assign((size_t)HO * HO + 1, 0.0);
+  for (int k = 0; k < HE; ++k)
+    for (int a = 0; a < HE; ++a)
+      Se[k * HE + a] = 0.5 * (S[k * m + ev[a]] + S[(m - 1 - k) * m + ev[a]]);
+  for (int k = 0; k < HO; ++k)
+    for (int a = 0; a < HO; ++a)
+      So[k * HO + a] = 0.5 * (S[k * m + od[a]] - S[(m - 1 - k) * m + od[a]]);
+  perm = ev;
+  perm.insert(perm.end(), od.begin(), od.end());
+  return true;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -195,6 +242,8 @@ static void colour_classes(int n, int c, std::vector<smg_schwarz::Cls>& out) {
   for (int e = full; e < n; ++e) out.push_back({e, 1, 1});
 }
 
+int smg_schwarz_destroy(smg_schwarz_t* h);
+
 int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, const double* S_x,
                        const double* S_y, const double* lam_x, const double* lam_y,
                        const double* w_x, const double* w_y, const double* inv_nu_dev) {
@@ -231,6 +280,29 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   while ((c - 1) * p <= 2 * n_o) ++c;
   colour_classes(n_x, c > n_x ? n_x : c, s->cx);
   colour_classes(n_y, c > n_y ? n_y : c, s->cy);
+  // tiled even/odd path
+  s->tiled = false;
+  s->dinv_perm = nullptr; s->ws = nullptr; s->ctr = nullptr;
+  std::vector<int> px, py;
+  const char* force = getenv("SMG_FD_DENSE");
+  s->fdt = nullptr;
+  if (!(force && force[0] == '1') &&
+      (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY)) != nullptr &&
+      even_odd_split(S_x, m, s->Sxe, s->Sxo, px) && even_odd_split(S_y, m, s->Sye, s->Syo, py)) {
+    s->ntx = n_x / s->TX; s->nty = n_y / s->TY;
+    const int nt = s->ntx * s->nty;
+    const size_t RX = (size_t)s->TX * p + 2 * n_o + 1, RY = (size_t)s->TY * p + 2 * n_o + 1;
+    std::vector<double> dp((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) dp[i * m + j] = 1.0 / (lam_y[py[i]] + lam_x[px[j]]);
+    e = cudaMalloc(&s->dinv_perm, sizeof(double) * m * m);
+    if (e == cudaSuccess) e = cudaMemcpy(s->dinv_perm, dp.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&s->ws, sizeof(double) * nt * RX * RY);
+    if (e == cudaSuccess) e = cudaMalloc(&s->ctr, sizeof(unsigned int) * 3 * nt);
+    if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, sizeof(unsigned int) * 3 * nt);
+    if (e != cudaSuccess) { smg_schwarz_destroy(s); return cuda_fail(e, "smg_schwarz_create (tiles)"); }
+    s->tiled = true;
+  }
   *h = s;
   return SMG_OK;
 }
@@ -238,6 +310,9 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
 int smg_schwarz_destroy(smg_schwarz_t* h) {
   if (!h) return SMG_OK;
   cudaFree(h->dinv);
+  if (h->dinv_perm) cudaFree(h->dinv_perm);
+  if (h->ws) cudaFree(h->ws);
+  if (h->ctr) cudaFree(h->ctr);
   delete h;
   return SMG_OK;
 }
@@ -254,6 +329,14 @@ static FDLaunch fd_base(const smg_schwarz_t* h) {
 
 int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream) {
   if (!h || !r || !u || r == u) { set_error("smg_schwarz_correct: bad argument"); return SMG_EINVAL; }
+  if (h->tiled) {
+    FDTLaunch T;
+    T.r = r; T.u = u; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
+    T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
+    T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
+    T.wx = h->wx.data(); T.wy = h->wy.data();
+    return h->fdt(T, as_stream(stream));
+  }
   FDLaunchFn fn = fd_dispatch(h->m);
   FDLaunch L = fd_base(h);
   L.src = r; L.dst = u;

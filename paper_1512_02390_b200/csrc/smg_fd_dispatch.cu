@@ -1,4 +1,4 @@
-// Generated: m -> FD launcher table.
+// Generated: m -> coloured dense FD launcher table.
 #include "smg_fd.cuh"
 namespace smg {
 extern template int fd_launch<3>(const FDLaunch&, cudaStream_t);
