@@ -13,10 +13,11 @@
 // 2. Tiles instead of colours.  A CTA owns a TX x TY block of elements (all
 //    compile-time, so every index is a constant-divisor expression), stages
 //    its residual region (TX p + 2 n_o + 1) x (TY p + 2 n_o + 1) and its own u
-//    with cp.async, runs the four contractions with streaming accumulators
-//    (factors in the parameter constant bank), and accumulates the
-//    overlapping element corrections into the region in colour passes
-//    (fixed order => deterministic).
+//    with cp.async, runs the four contractions with TWO threads per line (a
+//    lane pair: even half / odd half, joined by shuffles in the synthesis
+//    stages; factors in the parameter constant bank, streaming independent
+//    accumulators), and accumulates the overlapping element corrections into
+//    the region in colour passes (fixed order => deterministic).
 // 3. Deterministic band protocol.  Nodes within n_o of a tile boundary get
 //    contributions from 2 (edges) or 4 (corners) tiles.  Each tile stores its
 //    band values in a workspace and bumps a per-band counter; the LAST tile to
@@ -47,60 +48,6 @@ struct FDTArgs {
   double wx[M], wy[M];
 };
 
-// t[0..HE) = Se^T xe ; t[HE..M) = So^T xo  -- streaming over k, HE (HO)
-// independent accumulators, Se read along rows (paired constant loads).
-template <int M>
-__device__ __forceinline__ void analyse(const double* __restrict__ Se, const double* __restrict__ So,
-                                        const double (&x)[M], double (&t)[M]) {
-  constexpr int HE = fdt_he(M), HO = fdt_ho(M);
-  double xe[HE], xo[HO > 0 ? HO : 1];
-#pragma unroll
-  for (int k = 0; k < HO; ++k) {
-    xe[k] = x[k] + x[M - 1 - k];
-    xo[k] = x[k] - x[M - 1 - k];
-  }
-  if (M & 1) xe[HO] = x[HO];
-#pragma unroll
-  for (int i = 0; i < HE; ++i) t[i] = Se[i] * xe[0];
-#pragma unroll
-  for (int k = 1; k < HE; ++k)
-#pragma unroll
-    for (int i = 0; i < HE; ++i) t[i] = fma(Se[k * HE + i], xe[k], t[i]);
-#pragma unroll
-  for (int i = 0; i < HO; ++i) t[HE + i] = So[i] * xo[0];
-#pragma unroll
-  for (int k = 1; k < HO; ++k)
-#pragma unroll
-    for (int i = 0; i < HO; ++i) t[HE + i] = fma(So[k * HO + i], xo[k], t[HE + i]);
-}
-
-// y (physical) = S t, t = [even | odd]; streaming over i with the transposed
-// factors SeT[i][k] so the accumulators over k are independent.
-template <int M>
-__device__ __forceinline__ void synthesize(const double* __restrict__ SeT, const double* __restrict__ SoT,
-                                           const double (&t)[M], double (&y)[M]) {
-  constexpr int HE = fdt_he(M), HO = fdt_ho(M);
-  double e[HE], o[HO > 0 ? HO : 1];
-#pragma unroll
-  for (int k = 0; k < HE; ++k) e[k] = SeT[k] * t[0];
-#pragma unroll
-  for (int i = 1; i < HE; ++i)
-#pragma unroll
-    for (int k = 0; k < HE; ++k) e[k] = fma(SeT[i * HE + k], t[i], e[k]);
-#pragma unroll
-  for (int k = 0; k < HO; ++k) o[k] = SoT[k] * t[HE];
-#pragma unroll
-  for (int i = 1; i < HO; ++i)
-#pragma unroll
-    for (int k = 0; k < HO; ++k) o[k] = fma(SoT[i * HO + k], t[HE + i], o[k]);
-#pragma unroll
-  for (int k = 0; k < HO; ++k) {
-    y[k] = e[k] + o[k];
-    y[M - 1 - k] = e[k] - o[k];
-  }
-  if (M & 1) y[HO] = e[HO];  // centre: odd vectors vanish there
-}
-
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -111,23 +58,60 @@ template <int P, int NO, int TX, int TY>
 struct FDTGeom {
   static constexpr int M = P + 1 + 2 * NO;
   static constexpr int MM = M * M;
+  static constexpr int HE = fdt_he(M), HO = fdt_ho(M);
+  static constexpr int HOX = HO > 0 ? HO : 1;
   static constexpr int E = TX * TY;
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int RX = OX + 2 * NO + 1, RY = OY + 2 * NO + 1;
   static constexpr int BW = 2 * NO + 1;
-  static constexpr int THREADS = ((E * M + 31) / 32) * 32;
+  // two threads per (element, line): lane pair = (even half, odd half)
+  static constexpr int THREADS = ((2 * E * M + 31) / 32) * 32;
   static constexpr int NT = THREADS;
   // colours inside the tile: windows of elements C apart are disjoint
   static constexpr int C = (2 * NO < P) ? 2 : 3;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)RX * RY + (size_t)E * MM + (size_t)OX * OY);
 };
 
+// Half analysis of one line.  Even lane: t = Se^T (x_k + x_{m-1-k}) (plus the
+// centre for odd m); odd lane: t = So^T (x_k - x_{m-1-k}).  H = half length.
+template <int M, int H, bool ODD, typename In>
+__device__ __forceinline__ void half_analyse(const double* __restrict__ S, In in, double (&t)[H]) {
+  constexpr int HO = fdt_ho(M);
+  double xk[H];
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    if (k < HO) {
+      const double a = in(k), b = in(M - 1 - k);
+      xk[k] = ODD ? a - b : a + b;
+    } else {
+      xk[k] = in(k);  // centre (even half of odd M)
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) t[i] = S[i] * xk[0];
+#pragma unroll
+  for (int k = 1; k < H; ++k)
+#pragma unroll
+    for (int i = 0; i < H; ++i) t[i] = fma(S[k * H + i], xk[k], t[i]);
+}
+
+// Half synthesis: acc[k] = sum_i ST[i][k] t[i] (even lane: e, odd lane: o).
+template <int H>
+__device__ __forceinline__ void half_synth(const double* __restrict__ ST, const double (&t)[H], double (&acc)[H]) {
+#pragma unroll
+  for (int k = 0; k < H; ++k) acc[k] = ST[k] * t[0];
+#pragma unroll
+  for (int i = 1; i < H; ++i)
+#pragma unroll
+    for (int k = 0; k < H; ++k) acc[k] = fma(ST[i * H + k], t[i], acc[k]);
+}
+
 template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, 1)
+__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::THREADS <= 320 ? 3 : 2)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
-  constexpr int BW = G::BW, NT = G::NT;
+  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT;
   extern __shared__ double sm[];
   double* R = sm;               // RY x RX: residual region, then accumulated correction
   double* EB = R + RX * RY;     // E x M x M element buffers
@@ -148,112 +132,178 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     const int y = idx / OX, x = idx - y * OX;
     cp_async8(UO + idx, A.u + (size_t)(Y0 + y) * N_x + (X0 + x));
   }
-  cp_async_wait_all();
-  __syncthreads();
 
-  const int e = tid / M, c = tid - e * M;
+  const bool odd = tid & 1;
+  const int line = tid >> 1;
+  const int e = line / M, c = line - e * M;
   const bool act = e < E;
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
+  double s = 1.0;  // 1 / nu_bar of this element; fetched while the copies fly
+  if (act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
+  double dl[HE];   // this lane's half row of 1/(lam_y + lam_x), also prefetched
+  {
+    const double* dr = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
+#pragma unroll
+    for (int l = 0; l < HE; ++l) dl[l] = (l < (odd ? HO : HE)) ? __ldg(dr + l) : 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
 
   // ---- stage 1 (physical columns): T1[:, c] = S_y^T R_e[:, c] --------------
   if (act) {
-    double x[M], t[M];
     const double* col = R + (eyl * P) * RX + exl * P + c;
+    auto in = [&](int k) { return col[k * RX]; };
+    if (!odd) {
+      double t[HE];
+      half_analyse<M, HE, false>(A.Sye, in, t);
 #pragma unroll
-    for (int k = 0; k < M; ++k) x[k] = col[k * RX];
-    analyse<M>(A.Sye, A.Syo, x, t);
+      for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
+    } else if (HO > 0) {
+      double t[HOX];
+      half_analyse<M, HOX, true>(A.Syo, in, t);
 #pragma unroll
-    for (int i = 0; i < M; ++i) B[i * M + c] = t[i];
+      for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
+    }
   }
   __syncthreads();
-  // the residual region is consumed: zero it for the accumulation
-  for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;
+  for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
 
   // ---- stage 2 (eigen-y rows): T2[c, :] = (T1[c, :] S_x) * dinv / nu_bar ----
-  if (act) {
-    double x[M], t[M];
+  {
+    double t[HE];
+    const double* row = B + c * M;
+    auto in = [&](int k) { return row[k]; };
+    if (act) {
+      if (!odd) half_analyse<M, HE, false>(A.Sxe, in, t);
+      else if (HO > 0) half_analyse<M, HOX, true>(A.Sxo, in, reinterpret_cast<double(&)[HOX]>(t));
+    }
+    __syncthreads();  // every row read before the in-place writes
+    if (act) {
+      if (!odd) {
 #pragma unroll
-    for (int k = 0; k < M; ++k) x[k] = B[c * M + k];
-    analyse<M>(A.Sxe, A.Sxo, x, t);
-    double s = 1.0;
-    if (A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
-    const double* dr = A.dinv + c * M;
+        for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (dl[l] * s);
+      } else {
 #pragma unroll
-    for (int l = 0; l < M; ++l) B[c * M + l] = t[l] * (__ldg(dr + l) * s);
+        for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (dl[l] * s);
+      }
+    }
   }
   __syncthreads();
 
   // ---- stage 3 (eigen-x columns): T3[:, c] = S_y T2[:, c] -----------------
-  if (act) {
-    double x[M], y[M];
+  {
+    double acc[HE];
 #pragma unroll
-    for (int k = 0; k < M; ++k) x[k] = B[k * M + c];
-    synthesize<M>(A.SyeT, A.SyoT, x, y);
+    for (int k = 0; k < HE; ++k) acc[k] = 0.0;
+    if (act) {
+      if (!odd) {
+        double t[HE];
 #pragma unroll
-    for (int k = 0; k < M; ++k) B[k * M + c] = y[k];
+        for (int i = 0; i < HE; ++i) t[i] = B[i * M + c];
+        half_synth<HE>(A.SyeT, t, acc);
+      } else if (HO > 0) {
+        double t[HOX], a2[HOX];
+#pragma unroll
+        for (int i = 0; i < HO; ++i) t[i] = B[(HE + i) * M + c];
+        half_synth<HOX>(A.SyoT, t, a2);
+#pragma unroll
+        for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+      }
+    }
+    __syncthreads();  // every column read before the in-place writes
+#pragma unroll
+    for (int k = 0; k < HO; ++k) {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
+      if (act) {
+        if (!odd) B[k * M + c] = acc[k] + other;          // y[k]     = e + o
+        else B[(M - 1 - k) * M + c] = other - acc[k];      // y[m-1-k] = e - o
+      }
+    }
+    if ((M & 1) && act && !odd) B[HO * M + c] = acc[HO];
   }
   __syncthreads();
 
   // ---- stage 4 (physical rows): out[c, :] = W .* (T3[c, :] S_x^T), added
   //      into the region in colour passes (disjoint windows per pass) -------
   {
-    double y[M];
+    double acc[HE];
+#pragma unroll
+    for (int k = 0; k < HE; ++k) acc[k] = 0.0;
     if (act) {
-      double x[M];
+      if (!odd) {
+        double t[HE];
 #pragma unroll
-      for (int k = 0; k < M; ++k) x[k] = B[c * M + k];
-      synthesize<M>(A.SxeT, A.SxoT, x, y);
-      const double wyc = A.wy[c];
+        for (int i = 0; i < HE; ++i) t[i] = B[c * M + i];
+        half_synth<HE>(A.SxeT, t, acc);
+      } else if (HO > 0) {
+        double t[HOX], a2[HOX];
 #pragma unroll
-      for (int j = 0; j < M; ++j) y[j] *= wyc * A.wx[j];
+        for (int i = 0; i < HO; ++i) t[i] = B[c * M + HE + i];
+        half_synth<HOX>(A.SxoT, t, a2);
+#pragma unroll
+        for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+      }
     }
+    double y[HE];
+#pragma unroll
+    for (int k = 0; k < HO; ++k) {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
+      y[k] = odd ? other - acc[k] : acc[k] + other;
+    }
+    if (M & 1) y[HO] = acc[HO];
+    const double wyc = act ? A.wy[c] : 0.0;
     constexpr int C = G::C;
 #pragma unroll
     for (int pass = 0; pass < C * C; ++pass) {
       if (act && (eyl % C) * C + (exl % C) == pass) {
         double* dst = R + (eyl * P + c) * RX + exl * P;
+        if (!odd) {
 #pragma unroll
-        for (int j = 0; j < M; ++j) dst[j] += y[j];
+          for (int k = 0; k < HE; ++k) dst[k] += y[k] * (wyc * A.wx[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < HO; ++k) dst[M - 1 - k] += y[k] * (wyc * A.wx[M - 1 - k]);
+        }
       }
       __syncthreads();
     }
   }
 
-  // ---- write-out: exclusive nodes directly, band nodes to the workspace ----
+  // ---- write-out: band nodes to the workspace, publish, then the exclusive
+  //      nodes (their stores overlap the counter round trip) ----------------
   double* W = A.ws + (size_t)tile * (RX * RY);
   for (int idx = tid; idx < RX * RY; idx += NT) {
     const int y = idx / RX, x = idx - y * RX;
     const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
-    if (band) {
-      W[idx] = R[idx];
-    } else {
-      const int oy = y - NO, ox = x - NO;
-      A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = UO[oy * OX + ox] + R[idx];
-    }
+    if (band) W[idx] = R[idx];
   }
+  __threadfence();
   __syncthreads();
-
   __shared__ int last[8];
   const int ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
   const int txm = (tx + ntx - 1) % ntx, txp = (tx + 1) % ntx;
   const int tym = (ty + nty - 1) % nty, typ = (ty + 1) % nty;
-  if (tid == 0) {
-    __threadfence();
+  unsigned int arrived = 0u;
+  if (tid < 8) {
     // 0 left edge, 1 right edge, 2 bottom edge, 3 top edge,
-    // 4 lower-left, 5 lower-right, 6 upper-left, 7 upper-right corner.
-    // Edges are indexed by the tile on their high side, corners likewise.
-    unsigned int* cx = A.ctr;
-    unsigned int* cy = A.ctr + ntiles;
-    unsigned int* cc = A.ctr + 2 * ntiles;
-    last[0] = atomicAdd(cx + ty * ntx + tx, 1u) == 1u;
-    last[1] = atomicAdd(cx + ty * ntx + txp, 1u) == 1u;
-    last[2] = atomicAdd(cy + ty * ntx + tx, 1u) == 1u;
-    last[3] = atomicAdd(cy + typ * ntx + tx, 1u) == 1u;
-    last[4] = atomicAdd(cc + ty * ntx + tx, 1u) == 3u;
-    last[5] = atomicAdd(cc + ty * ntx + txp, 1u) == 3u;
-    last[6] = atomicAdd(cc + typ * ntx + tx, 1u) == 3u;
-    last[7] = atomicAdd(cc + typ * ntx + txp, 1u) == 3u;
+    // 4 lower-left, 5 lower-right, 6 upper-left, 7 upper-right corner;
+    // each indexed by the tile on its high side.
+    const int hx = (tid == 1 || tid == 5 || tid == 7) ? txp : tx;
+    const int hy = (tid == 3 || tid == 6 || tid == 7) ? typ : ty;
+    const int kind = tid < 2 ? 0 : (tid < 4 ? 1 : 2);
+    arrived = atomicAdd(A.ctr + kind * ntiles + hy * ntx + hx, 1u);
+  }
+  for (int idx = tid; idx < RX * RY; idx += NT) {
+    const int y = idx / RX, x = idx - y * RX;
+    const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
+    if (!band) {
+      const int oy = y - NO, ox = x - NO;
+      A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = UO[oy * OX + ox] + R[idx];
+    }
+  }
+  if (tid < 8) {
+    last[tid] = arrived == (tid < 4 ? 1u : 3u);
     __threadfence();
   }
   __syncthreads();
