@@ -41,25 +41,6 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
          double* C, int ldc, const double* S, cudaStream_t st);
 
-static int largest_divisor_leq(int n, int cap) {
-  if (cap < 1) cap = 1;
-  for (int d = cap; d >= 1; --d)
-    if (n % d == 0) return d;
-  return 1;
-}
-
-int op_tx_max(int p) {
-  switch (p) {
-    case 1: return 32;
-    case 2: return 16;
-    case 3: return 10;
-    case 4: return 8;
-    case 5: case 6: return 5;
-    case 8: return 4;
-    case 12: case 16: return 2;
-    default: return p < 12 ? 32 / p : 1;
-  }
-}
 
 }  // namespace smg
 
@@ -67,7 +48,8 @@ using namespace smg;
 
 // ---------------------------------------------------------------------------
 struct smg_op {
-  int kind, p, n_x, n_y, TX, TY;
+  int kind, p, n_x, n_y;
+  smg::OpLaunchFn fn;
   double dx, dy;
   std::vector<double> Mt, w, wasm;
   const double* nu;
@@ -94,7 +76,6 @@ struct smg_schwarz {
 
 struct smg_transfer {
   int pc, pf, n_x, n_y;
-  int pTX, pTY, rTX, rTY;
   std::vector<double> J;
   smg::TrFn fn;
 };
@@ -174,7 +155,9 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
     set_error("smg_op_create: bad argument");
     return SMG_EINVAL;
   }
-  if (!op_dispatch(p)) {
+  int ctas = 0;
+  OpLaunchFn fn = op_dispatch(p, kind == 1, n_x, n_y, &ctas);
+  if (!fn) {
     set_error("smg_op_create: order p=%d not compiled in", p);
     return SMG_EUNSUPPORTED;
   }
@@ -187,10 +170,8 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
   for (int a = 0; a < p; ++a) o->wasm[a] = weights[a];
   o->wasm[0] = weights[0] + weights[p];
   o->nu = nu_dev;
-  const int cap = op_tx_max(p);
-  o->TX = largest_divisor_leq(n_x, cap);
-  o->TY = largest_divisor_leq(n_y, cap);
-  o->n_ctas = (n_x / o->TX) * (n_y / o->TY);
+  o->fn = fn;
+  o->n_ctas = ctas;
   cudaError_t e = cudaMalloc(&o->partials, sizeof(double) * o->n_ctas);
   if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
   *h = o;
@@ -208,10 +189,10 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
                   cudaStream_t st) {
   OpLaunch L;
   L.u = u; L.f = f; L.out = out; L.nu = h->nu; L.partials = norm ? h->partials : nullptr;
-  L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.TX = h->TX; L.TY = h->TY; L.diffusion = h->kind;
+  L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
-  return op_dispatch(h->p)(L, st);
+  return h->fn(L, st);
 }
 
 int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out, void* stream) {
@@ -391,9 +372,6 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   if (!t) return SMG_ENOMEM;
   t->pc = p_c; t->pf = p_f; t->n_x = n_x; t->n_y = n_y; t->fn = fn;
   t->J.assign(J, J + (p_f + 1) * (p_c + 1));
-  const int cap = p_f >= 32 ? 1 : 32 / p_f;
-  t->pTX = largest_divisor_leq(n_x, cap); t->pTY = largest_divisor_leq(n_y, cap);
-  t->rTX = t->pTX; t->rTY = t->pTY;
   *h = t;
   return SMG_OK;
 }
@@ -402,12 +380,10 @@ int smg_transfer_destroy(smg_transfer_t* h) { delete h; return SMG_OK; }
 
 static int tr_run(const smg_transfer_t* h, const double* src, double* dst, int acc, bool prolong, cudaStream_t st) {
   TrArgs A;
-  A.src = src; A.dst = dst; A.pc = h->pc; A.pf = h->pf; A.n_x = h->n_x; A.n_y = h->n_y;
-  A.TX = prolong ? h->pTX : h->rTX; A.TY = prolong ? h->pTY : h->rTY;
-  A.tiles_x = h->n_x / A.TX; A.accumulate = acc;
+  std::memset(&A, 0, sizeof(A));
+  A.src = src; A.dst = dst; A.n_x = h->n_x; A.n_y = h->n_y; A.accumulate = acc;
   std::memcpy(A.J, h->J.data(), sizeof(double) * h->J.size());
-  const int grid = (h->n_x / A.TX) * (h->n_y / A.TY);
-  return h->fn(A, grid, prolong, st);
+  return h->fn(A, h->n_x, h->n_y, prolong, st);
 }
 
 int smg_prolongate(const smg_transfer_t* h, const double* uc, double* uf, int accumulate, void* stream) {

@@ -164,56 +164,47 @@ __global__ void __launch_bounds__(kReduceThreads) sum_partials_kernel(const doub
 
 // ---- small dense GEMM for the coarse pseudo-inverse ------------------------
 // C[M,N] = op(A) op(B) (.* S when S != nullptr); op = transpose when tX.
-// 64x64 tiles, 256 threads, 4x4 outputs per thread, DFMA.
+// 16x16 output tile per CTA, one output per thread, K staged in chunks of 64
+// (the coarse matrices are 8..512 wide: small tiles keep many CTAs busy and
+// the dependent-FMA chain short).
 __global__ void __launch_bounds__(256)
 gemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda, int tA,
             const double* __restrict__ B, int ldb, int tB, double* __restrict__ C, int ldc,
             const double* __restrict__ S) {
   __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
+  __shared__ double Bs[64][16 + 1];
   const int tid = threadIdx.x;
-  const int tr = tid / 16, tc = tid % 16;
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += 16) {
+  const int r = tid / 16, cc = tid % 16;
+  const int m0 = blockIdx.y * 16, n0 = blockIdx.x * 16;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 64) {
     for (int idx = tid; idx < 16 * 64; idx += 256) {
-      const int kk = idx / 64, mm = idx % 64;
+      const int mm = idx / 64, kk = idx % 64;
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < K) ? (tA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
-      const int gn = n0 + mm;
-      Bs[kk][mm] = (gn < N && gk < K) ? (tB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn]) : 0.0;
+      As[mm][kk] = (gm < M && gk < K) ? (tA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.0;
+      const int kb = idx / 16, nn = idx % 16;
+      const int gn = n0 + nn, gkb = k0 + kb;
+      Bs[kb][nn] = (gn < N && gkb < K) ? (tB ? B[(size_t)gn * ldb + gkb] : B[(size_t)gkb * ldb + gn]) : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][tr + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tc + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    for (int kk = 0; kk < 64; kk += 2) {
+      acc0 = fma(As[r][kk], Bs[kk][cc], acc0);
+      acc1 = fma(As[r][kk + 1], Bs[kk + 1][cc], acc1);
     }
     __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gm = m0 + tr + 16 * i, gn = n0 + tc + 16 * j;
-      if (gm < M && gn < N) {
-        double v = acc[i][j];
-        if (S != nullptr) v *= S[(size_t)gm * N + gn];
-        C[(size_t)gm * ldc + gn] = v;
-      }
-    }
+  const int gm = m0 + r, gn = n0 + cc;
+  if (gm < M && gn < N) {
+    double v = acc0 + acc1;
+    if (S != nullptr) v *= S[(size_t)gm * N + gn];
+    C[(size_t)gm * ldc + gn] = v;
+  }
 }
 
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
          double* C, int ldc, const double* S, cudaStream_t st) {
-  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  dim3 grid((N + 15) / 16, (M + 15) / 16);
   gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, A, lda, tA, B, ldb, tB, C, ldc, S);
   return check_launch("gemm_kernel");
 }

@@ -18,12 +18,15 @@
 //    stages; factors in the parameter constant bank, streaming independent
 //    accumulators), and accumulates the overlapping element corrections into
 //    the region in colour passes (fixed order => deterministic).
-// 3. Deterministic band protocol.  Nodes within n_o of a tile boundary get
-//    contributions from 2 (edges) or 4 (corners) tiles.  Each tile stores its
-//    band values in a workspace and bumps a per-band counter; the LAST tile to
-//    arrive adds all contributions to u in a fixed tile order.  The sum never
-//    depends on arrival order: bitwise reproducible, no FP atomics, one launch.
+// 3. Deterministic band fixup.  Nodes within n_o of a tile boundary get
+//    contributions from 2 (edges) or 4 (corners) tiles.  The main kernel
+//    (persistent, next tile's loads in flight while the current computes)
+//    writes exclusive nodes to u and band values to a workspace; a small
+//    second kernel adds the band contributions to u in a fixed tile order.
+//    Bitwise reproducible, no atomics, no inter-CTA waiting.
 #pragma once
+#include <cstdlib>
+
 #include "smg_common.cuh"
 
 namespace smg {
@@ -40,6 +43,7 @@ struct FDTArgs {
   double* __restrict__ ws;            // band workspace: ntiles * RY * RX
   unsigned int* __restrict__ ctr;     // 3 * ntiles counters (x-edge, y-edge, corner), zeroed
   int N_x, N_y, n_x, ntx, nty;
+  int debug_skip;                     // profiling aid: 1 = skip the four contractions
   // analysis factors Se[k][i] (k physical half index), synthesis factors SeT[i][k]
   double Sye[fdt_he(M) * fdt_he(M)], SyeT[fdt_he(M) * fdt_he(M)];
   double Syo[fdt_ho(M) * fdt_ho(M) + 1], SyoT[fdt_ho(M) * fdt_ho(M) + 1];
@@ -53,6 +57,9 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int P, int NO, int TX, int TY>
 struct FDTGeom {
@@ -69,7 +76,8 @@ struct FDTGeom {
   static constexpr int NT = THREADS;
   // colours inside the tile: windows of elements C apart are disjoint
   static constexpr int C = (2 * NO < P) ? 2 : 3;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)RX * RY + (size_t)E * MM + (size_t)OX * OY);
+  static constexpr int STAGE = RX * RY + OX * OY;  // doubles per pipeline stage
+  static constexpr size_t SMEM = sizeof(double) * (2 * (size_t)STAGE + (size_t)E * MM);
 };
 
 // Half analysis of one line.  Even lane: t = Se^T (x_k + x_{m-1-k}) (plus the
@@ -107,31 +115,37 @@ __device__ __forceinline__ void half_synth(const double* __restrict__ ST, const 
 }
 
 template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::THREADS <= 320 ? 3 : 2)
+__device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const double* __restrict__ u, int N_x,
+                                             int N_y, int ntx, int tile, double* buf) {
+  using G = FDTGeom<P, NO, TX, TY>;
+  constexpr int RX = G::RX, RY = G::RY, OX = G::OX, OY = G::OY, NT = G::NT;
+  const int tx = tile % ntx, ty = tile / ntx;
+  const int X0 = tx * OX, Y0 = ty * OY;
+  for (int idx = threadIdx.x; idx < RX * RY; idx += NT) {
+    const int y = idx / RX, x = idx - y * RX;
+    cp_async8(buf + idx, r + (size_t)wrapi(Y0 - NO + y, N_y) * N_x + wrapi(X0 - NO + x, N_x));
+  }
+  double* uo = buf + RX * RY;
+  for (int idx = threadIdx.x; idx < OX * OY; idx += NT) {
+    const int y = idx / OX, x = idx - y * OX;
+    cp_async8(uo + idx, u + (size_t)(Y0 + y) * N_x + (X0 + x));
+  }
+}
+
+// Persistent main kernel: CTA walks tiles blockIdx.x, +gridDim.x, ...; the
+// next tile's residual region and own u are in flight (cp.async group) while
+// the current tile computes.  Exclusive nodes are written to u directly,
+// band nodes (within n_o of a tile edge) to the workspace for fdt_fixup.
+template <int P, int NO, int TX, int TY>
+__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, 2)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
-  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT;
+  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT, STAGE = G::STAGE;
   extern __shared__ double sm[];
-  double* R = sm;               // RY x RX: residual region, then accumulated correction
-  double* EB = R + RX * RY;     // E x M x M element buffers
-  double* UO = EB + E * MM;     // OY x OX own u
+  double* EB = sm + 2 * STAGE;  // E x M x M element buffers
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
-  const int tx = tile % A.ntx, ty = tile / A.ntx;
-  const int X0 = tx * OX, Y0 = ty * OY;
-  const int N_x = A.N_x, N_y = A.N_y;
-
-  // ---- async stage of the residual region and own u ----------------------
-  for (int idx = tid; idx < RX * RY; idx += NT) {
-    const int y = idx / RX, x = idx - y * RX;
-    const int gy = wrapi(Y0 - NO + y, N_y), gx = wrapi(X0 - NO + x, N_x);
-    cp_async8(R + idx, A.r + (size_t)gy * N_x + gx);
-  }
-  for (int idx = tid; idx < OX * OY; idx += NT) {
-    const int y = idx / OX, x = idx - y * OX;
-    cp_async8(UO + idx, A.u + (size_t)(Y0 + y) * N_x + (X0 + x));
-  }
+  const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, ntiles = A.ntx * A.nty;
 
   const bool odd = tid & 1;
   const int line = tid >> 1;
@@ -139,236 +153,224 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const bool act = e < E;
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
-  double s = 1.0;  // 1 / nu_bar of this element; fetched while the copies fly
-  if (act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
-  double dl[HE];   // this lane's half row of 1/(lam_y + lam_x), also prefetched
+  double dl[HE];  // this lane's half row of 1/(lam_y + lam_x)
   {
     const double* dr = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 #pragma unroll
     for (int l = 0; l < HE; ++l) dl[l] = (l < (odd ? HO : HE)) ? __ldg(dr + l) : 0.0;
   }
-  cp_async_wait_all();
-  __syncthreads();
 
-  // ---- stage 1 (physical columns): T1[:, c] = S_y^T R_e[:, c] --------------
-  if (act) {
-    const double* col = R + (eyl * P) * RX + exl * P + c;
-    auto in = [&](int k) { return col[k * RX]; };
-    if (!odd) {
-      double t[HE];
-      half_analyse<M, HE, false>(A.Sye, in, t);
-#pragma unroll
-      for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
-    } else if (HO > 0) {
-      double t[HOX];
-      half_analyse<M, HOX, true>(A.Syo, in, t);
-#pragma unroll
-      for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
+  int tile = blockIdx.x;
+  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, tile, sm);
+  cp_async_commit();
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    double* R = sm + (it & 1) * STAGE;  // residual region, then accumulated correction
+    double* UO = R + RX * RY;           // own u
+    {
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE);
+      cp_async_commit();
     }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
+    const int tx = tile % ntx, ty = tile / ntx;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    double s = 1.0;  // 1 / nu_bar of this element
+    if (act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
+    cp_async_wait<1>();
+    __syncthreads();
 
-  // ---- stage 2 (eigen-y rows): T2[c, :] = (T1[c, :] S_x) * dinv / nu_bar ----
-  {
-    double t[HE];
-    const double* row = B + c * M;
-    auto in = [&](int k) { return row[k]; };
-    if (act) {
-      if (!odd) half_analyse<M, HE, false>(A.Sxe, in, t);
-      else if (HO > 0) half_analyse<M, HOX, true>(A.Sxo, in, reinterpret_cast<double(&)[HOX]>(t));
-    }
-    __syncthreads();  // every row read before the in-place writes
-    if (act) {
-      if (!odd) {
-#pragma unroll
-        for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (dl[l] * s);
-      } else {
-#pragma unroll
-        for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (dl[l] * s);
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- stage 3 (eigen-x columns): T3[:, c] = S_y T2[:, c] -----------------
-  {
-    double acc[HE];
-#pragma unroll
-    for (int k = 0; k < HE; ++k) acc[k] = 0.0;
-    if (act) {
-      if (!odd) {
-        double t[HE];
-#pragma unroll
-        for (int i = 0; i < HE; ++i) t[i] = B[i * M + c];
-        half_synth<HE>(A.SyeT, t, acc);
-      } else if (HO > 0) {
-        double t[HOX], a2[HOX];
-#pragma unroll
-        for (int i = 0; i < HO; ++i) t[i] = B[(HE + i) * M + c];
-        half_synth<HOX>(A.SyoT, t, a2);
-#pragma unroll
-        for (int k = 0; k < HO; ++k) acc[k] = a2[k];
-      }
-    }
-    __syncthreads();  // every column read before the in-place writes
-#pragma unroll
-    for (int k = 0; k < HO; ++k) {
-      const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
+    if (A.debug_skip) {
+      for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;
+      __syncthreads();
+    } else {
+      // ---- stage 1 (physical columns): T1[:, c] = S_y^T R_e[:, c] --------
       if (act) {
-        if (!odd) B[k * M + c] = acc[k] + other;          // y[k]     = e + o
-        else B[(M - 1 - k) * M + c] = other - acc[k];      // y[m-1-k] = e - o
-      }
-    }
-    if ((M & 1) && act && !odd) B[HO * M + c] = acc[HO];
-  }
-  __syncthreads();
-
-  // ---- stage 4 (physical rows): out[c, :] = W .* (T3[c, :] S_x^T), added
-  //      into the region in colour passes (disjoint windows per pass) -------
-  {
-    double acc[HE];
-#pragma unroll
-    for (int k = 0; k < HE; ++k) acc[k] = 0.0;
-    if (act) {
-      if (!odd) {
-        double t[HE];
-#pragma unroll
-        for (int i = 0; i < HE; ++i) t[i] = B[c * M + i];
-        half_synth<HE>(A.SxeT, t, acc);
-      } else if (HO > 0) {
-        double t[HOX], a2[HOX];
-#pragma unroll
-        for (int i = 0; i < HO; ++i) t[i] = B[c * M + HE + i];
-        half_synth<HOX>(A.SxoT, t, a2);
-#pragma unroll
-        for (int k = 0; k < HO; ++k) acc[k] = a2[k];
-      }
-    }
-    double y[HE];
-#pragma unroll
-    for (int k = 0; k < HO; ++k) {
-      const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
-      y[k] = odd ? other - acc[k] : acc[k] + other;
-    }
-    if (M & 1) y[HO] = acc[HO];
-    const double wyc = act ? A.wy[c] : 0.0;
-    constexpr int C = G::C;
-#pragma unroll
-    for (int pass = 0; pass < C * C; ++pass) {
-      if (act && (eyl % C) * C + (exl % C) == pass) {
-        double* dst = R + (eyl * P + c) * RX + exl * P;
+        const double* col = R + (eyl * P) * RX + exl * P + c;
+        auto in = [&](int k) { return col[k * RX]; };
         if (!odd) {
+          double t[HE];
+          half_analyse<M, HE, false>(A.Sye, in, t);
 #pragma unroll
-          for (int k = 0; k < HE; ++k) dst[k] += y[k] * (wyc * A.wx[k]);
-        } else {
+          for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
+        } else if (HO > 0) {
+          double t[HOX];
+          half_analyse<M, HOX, true>(A.Syo, in, t);
 #pragma unroll
-          for (int k = 0; k < HO; ++k) dst[M - 1 - k] += y[k] * (wyc * A.wx[M - 1 - k]);
+          for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
         }
       }
       __syncthreads();
-    }
-  }
+      for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
 
-  // ---- write-out: band nodes to the workspace, publish, then the exclusive
-  //      nodes (their stores overlap the counter round trip) ----------------
-  double* W = A.ws + (size_t)tile * (RX * RY);
-  for (int idx = tid; idx < RX * RY; idx += NT) {
-    const int y = idx / RX, x = idx - y * RX;
-    const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
-    if (band) W[idx] = R[idx];
-  }
-  __threadfence();
-  __syncthreads();
-  __shared__ int last[8];
-  const int ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
-  const int txm = (tx + ntx - 1) % ntx, txp = (tx + 1) % ntx;
-  const int tym = (ty + nty - 1) % nty, typ = (ty + 1) % nty;
-  unsigned int arrived = 0u;
-  if (tid < 8) {
-    // 0 left edge, 1 right edge, 2 bottom edge, 3 top edge,
-    // 4 lower-left, 5 lower-right, 6 upper-left, 7 upper-right corner;
-    // each indexed by the tile on its high side.
-    const int hx = (tid == 1 || tid == 5 || tid == 7) ? txp : tx;
-    const int hy = (tid == 3 || tid == 6 || tid == 7) ? typ : ty;
-    const int kind = tid < 2 ? 0 : (tid < 4 ? 1 : 2);
-    arrived = atomicAdd(A.ctr + kind * ntiles + hy * ntx + hx, 1u);
-  }
-  for (int idx = tid; idx < RX * RY; idx += NT) {
-    const int y = idx / RX, x = idx - y * RX;
-    const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
-    if (!band) {
-      const int oy = y - NO, ox = x - NO;
-      A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = UO[oy * OX + ox] + R[idx];
+      // ---- stage 2 (eigen-y rows): T2[c, :] = (T1[c, :] S_x) * dinv / nu_bar
+      {
+        double t[HE];
+        const double* row = B + c * M;
+        auto in = [&](int k) { return row[k]; };
+        if (act) {
+          if (!odd) half_analyse<M, HE, false>(A.Sxe, in, t);
+          else if (HO > 0) half_analyse<M, HOX, true>(A.Sxo, in, reinterpret_cast<double(&)[HOX]>(t));
+        }
+        __syncthreads();  // every row read before the in-place writes
+        if (act) {
+          if (!odd) {
+#pragma unroll
+            for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (dl[l] * s);
+          } else {
+#pragma unroll
+            for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (dl[l] * s);
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- stage 3 (eigen-x columns): T3[:, c] = S_y T2[:, c] -------------
+      {
+        double acc[HE];
+#pragma unroll
+        for (int k = 0; k < HE; ++k) acc[k] = 0.0;
+        if (act) {
+          if (!odd) {
+            double t[HE];
+#pragma unroll
+            for (int i = 0; i < HE; ++i) t[i] = B[i * M + c];
+            half_synth<HE>(A.SyeT, t, acc);
+          } else if (HO > 0) {
+            double t[HOX], a2[HOX];
+#pragma unroll
+            for (int i = 0; i < HO; ++i) t[i] = B[(HE + i) * M + c];
+            half_synth<HOX>(A.SyoT, t, a2);
+#pragma unroll
+            for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+          }
+        }
+        __syncthreads();  // every column read before the in-place writes
+#pragma unroll
+        for (int k = 0; k < HO; ++k) {
+          const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
+          if (act) {
+            if (!odd) B[k * M + c] = acc[k] + other;         // y[k]     = e + o
+            else B[(M - 1 - k) * M + c] = other - acc[k];     // y[m-1-k] = e - o
+          }
+        }
+        if ((M & 1) && act && !odd) B[HO * M + c] = acc[HO];
+      }
+      __syncthreads();
+
+      // ---- stage 4 (physical rows): out[c, :] = W .* (T3[c, :] S_x^T), added
+      //      into the region in colour passes (disjoint windows per pass) ---
+      {
+        double acc[HE];
+#pragma unroll
+        for (int k = 0; k < HE; ++k) acc[k] = 0.0;
+        if (act) {
+          if (!odd) {
+            double t[HE];
+#pragma unroll
+            for (int i = 0; i < HE; ++i) t[i] = B[c * M + i];
+            half_synth<HE>(A.SxeT, t, acc);
+          } else if (HO > 0) {
+            double t[HOX], a2[HOX];
+#pragma unroll
+            for (int i = 0; i < HO; ++i) t[i] = B[c * M + HE + i];
+            half_synth<HOX>(A.SxoT, t, a2);
+#pragma unroll
+            for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+          }
+        }
+        double y[HE];
+#pragma unroll
+        for (int k = 0; k < HO; ++k) {
+          const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
+          y[k] = odd ? other - acc[k] : acc[k] + other;
+        }
+        if (M & 1) y[HO] = acc[HO];
+        const double wyc = act ? A.wy[c] : 0.0;
+        constexpr int C = G::C;
+#pragma unroll
+        for (int pass = 0; pass < C * C; ++pass) {
+          if (act && (eyl % C) * C + (exl % C) == pass) {
+            double* dst = R + (eyl * P + c) * RX + exl * P;
+            if (!odd) {
+#pragma unroll
+              for (int k = 0; k < HE; ++k) dst[k] += y[k] * (wyc * A.wx[k]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < HO; ++k) dst[M - 1 - k] += y[k] * (wyc * A.wx[M - 1 - k]);
+            }
+          }
+          __syncthreads();
+        }
+      }
     }
+
+    // ---- write-out: exclusive nodes to u, band nodes to the workspace ------
+    double* W = A.ws + (size_t)tile * (RX * RY);
+    for (int idx = tid; idx < RX * RY; idx += NT) {
+      const int y = idx / RX, x = idx - y * RX;
+      const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
+      if (band) {
+        W[idx] = R[idx];
+      } else {
+        const int oy = y - NO, ox = x - NO;
+        A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = UO[oy * OX + ox] + R[idx];
+      }
+    }
+    __syncthreads();  // this stage buffer is refilled two iterations later
   }
-  if (tid < 8) {
-    last[tid] = arrived == (tid < 4 ? 1u : 3u);
-    __threadfence();
-  }
-  __syncthreads();
+  cp_async_wait<0>();
+}
+
+// Band fixup (second launch): every node within n_o of a tile edge receives
+// the contributions of the 2 (edge) or 4 (corner) tiles sharing it, summed in
+// a fixed tile order: u = (((u + c_lo,lo) + c_hi,lo) + c_lo,hi) + c_hi,hi.
+// One thread per band node; deterministic; no atomics.
+template <int P, int NO, int TX, int TY>
+__global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
+                                                 int N_y, int ntx, int nty) {
+  using G = FDTGeom<P, NO, TX, TY>;
+  constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
   constexpr size_t RS = (size_t)RX * RY;
-  // x edges: (left tile, right tile) at X = right tile's X0, y-interior rows
-#pragma unroll
-  for (int sg = 0; sg < 2; ++sg) {
-    if (!last[sg]) continue;
-    const int tl = sg == 0 ? txm : tx, tr = sg == 0 ? tx : txp;
-    const int XB = tr * OX;
-    const double* WL = A.ws + (size_t)(ty * ntx + tl) * RS;
-    const double* WR = A.ws + (size_t)(ty * ntx + tr) * RS;
-    constexpr int NR = RY - 2 * BW;
-    for (int idx = tid; idx < NR * BW; idx += NT) {
-      const int yy = BW + idx / BW, d = idx % BW - NO;
-      const int gx = wrapi(XB + d, N_x), gy = Y0 - NO + yy;
-      const double cl = __ldcg(WL + (size_t)yy * RX + (OX + NO + d));
-      const double cr = __ldcg(WR + (size_t)yy * RX + (NO + d));
-      double* up = A.u + (size_t)gy * N_x + gx;
-      *up = (*up + cl) + cr;
-    }
-    if (tid == 0) A.ctr[ty * ntx + tr] = 0u;
+  // per tile: x-edge segment (BW x (OY - BW)) at its left edge, y-edge
+  // segment ((OX - BW) x BW) at its bottom edge, corner BW x BW at lower-left
+  constexpr int NXE = BW * (OY - BW), NYE = (OX - BW) * BW, NCO = BW * BW;
+  constexpr int PER = NXE + NYE + NCO;
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntiles = ntx * nty;
+  if (gid >= (long)ntiles * PER) return;
+  const int tile = (int)(gid / PER);
+  int k = (int)(gid - (long)tile * PER);
+  const int tx = tile % ntx, ty = tile / ntx;
+  const int txm = (tx + ntx - 1) % ntx, tym = (ty + nty - 1) % nty;
+  const int X0 = tx * OX, Y0 = ty * OY;
+  if (k < NXE) {
+    // left x-edge of (tx, ty): rows of its y-interior, d in [-NO, NO]
+    const int yy = BW + k / BW, d = k % BW - NO;
+    const double cl = ws[(size_t)(ty * ntx + txm) * RS + (size_t)yy * RX + (OX + NO + d)];
+    const double cr = ws[(size_t)(ty * ntx + tx) * RS + (size_t)yy * RX + (NO + d)];
+    double* up = u + (size_t)(Y0 - NO + yy) * N_x + wrapi(X0 + d, N_x);
+    *up = (*up + cl) + cr;
+    return;
   }
-  // y edges: (bottom tile, top tile) at Y = top tile's Y0, x-interior columns
-#pragma unroll
-  for (int sg = 2; sg < 4; ++sg) {
-    if (!last[sg]) continue;
-    const int tb = sg == 2 ? tym : ty, tt = sg == 2 ? ty : typ;
-    const int YB = tt * OY;
-    const double* WB = A.ws + (size_t)(tb * ntx + tx) * RS;
-    const double* WT = A.ws + (size_t)(tt * ntx + tx) * RS;
-    constexpr int NC = RX - 2 * BW;
-    for (int idx = tid; idx < NC * BW; idx += NT) {
-      const int d = idx / NC - NO, xx = BW + idx % NC;
-      const int gy = wrapi(YB + d, N_y), gx = X0 - NO + xx;
-      const double cb = __ldcg(WB + (size_t)(OY + NO + d) * RX + xx);
-      const double ct = __ldcg(WT + (size_t)(NO + d) * RX + xx);
-      double* up = A.u + (size_t)gy * N_x + gx;
-      *up = (*up + cb) + ct;
-    }
-    if (tid == 0) A.ctr[ntiles + tt * ntx + tx] = 0u;
+  k -= NXE;
+  if (k < NYE) {
+    // bottom y-edge of (tx, ty): columns of its x-interior
+    const int d = k / (OX - BW) - NO, xx = BW + k % (OX - BW);
+    const double cb = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + d) * RX + xx];
+    const double ct = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + d) * RX + xx];
+    double* up = u + (size_t)wrapi(Y0 + d, N_y) * N_x + (X0 - NO + xx);
+    *up = (*up + cb) + ct;
+    return;
   }
-  // corners: tiles (lo,lo), (hi,lo), (lo,hi), (hi,hi) in that order
-#pragma unroll
-  for (int sg = 4; sg < 8; ++sg) {
-    if (!last[sg]) continue;
-    const int hx = (sg == 4 || sg == 6) ? tx : txp;
-    const int hy = (sg == 4 || sg == 5) ? ty : typ;
-    const int lx = (hx + ntx - 1) % ntx, ly = (hy + nty - 1) % nty;
-    const int XB = hx * OX, YB = hy * OY;
-    const double* W00 = A.ws + (size_t)(ly * ntx + lx) * RS;
-    const double* W10 = A.ws + (size_t)(ly * ntx + hx) * RS;
-    const double* W01 = A.ws + (size_t)(hy * ntx + lx) * RS;
-    const double* W11 = A.ws + (size_t)(hy * ntx + hx) * RS;
-    for (int idx = tid; idx < BW * BW; idx += NT) {
-      const int dy = idx / BW - NO, dx = idx % BW - NO;
-      const int gy = wrapi(YB + dy, N_y), gx = wrapi(XB + dx, N_x);
-      const double c00 = __ldcg(W00 + (size_t)(OY + NO + dy) * RX + (OX + NO + dx));
-      const double c10 = __ldcg(W10 + (size_t)(OY + NO + dy) * RX + (NO + dx));
-      const double c01 = __ldcg(W01 + (size_t)(NO + dy) * RX + (OX + NO + dx));
-      const double c11 = __ldcg(W11 + (size_t)(NO + dy) * RX + (NO + dx));
-      double* up = A.u + (size_t)gy * N_x + gx;
-      *up = (((*up + c00) + c10) + c01) + c11;
-    }
-    if (tid == 0) A.ctr[2 * ntiles + hy * ntx + hx] = 0u;
+  k -= NYE;
+  {
+    // lower-left corner of (tx, ty): tiles (txm,tym), (tx,tym), (txm,ty), (tx,ty)
+    const int dy = k / BW - NO, dx = k % BW - NO;
+    const double c00 = ws[(size_t)(tym * ntx + txm) * RS + (size_t)(OY + NO + dy) * RX + (OX + NO + dx)];
+    const double c10 = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + dy) * RX + (NO + dx)];
+    const double c01 = ws[(size_t)(ty * ntx + txm) * RS + (size_t)(NO + dy) * RX + (OX + NO + dx)];
+    const double c11 = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + dy) * RX + (NO + dx)];
+    double* up = u + (size_t)wrapi(Y0 + dy, N_y) * N_x + wrapi(X0 + dx, N_x);
+    *up = (((*up + c00) + c10) + c01) + c11;
   }
 }
 
@@ -395,6 +397,10 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
   FDTArgs<M> A;
   A.r = L.r; A.u = L.u; A.inv_nu = L.inv_nu; A.dinv = L.dinv; A.ws = L.ws; A.ctr = L.ctr;
   A.N_x = L.N_x; A.N_y = L.N_y; A.n_x = L.n_x; A.ntx = L.ntx; A.nty = L.nty;
+  {
+    const char* dbg = getenv("SMG_FD_DEBUG_SKIP");
+    A.debug_skip = (dbg && dbg[0] == '1') ? 1 : 0;
+  }
   for (int k = 0; k < HE; ++k)
     for (int i = 0; i < HE; ++i) {
       A.Sye[k * HE + i] = L.Sye[k * HE + i]; A.SyeT[i * HE + k] = L.Sye[k * HE + i];
@@ -407,17 +413,27 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
     }
   A.Syo[HO * HO] = A.SyoT[HO * HO] = A.Sxo[HO * HO] = A.SxoT[HO * HO] = 0.0;
   for (int i = 0; i < M; ++i) { A.wx[i] = L.wx[i]; A.wy[i] = L.wy[i]; }
-  static bool attr = false;
-  if (!attr) {
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
     if (G::SMEM > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fdt_kernel<P, NO, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)G::SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "fdt_kernel smem attribute");
     }
-    attr = true;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdt_kernel<P, NO, TX, TY>, G::THREADS, G::SMEM);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  fdt_kernel<P, NO, TX, TY><<<L.ntx * L.nty, G::THREADS, G::SMEM, st>>>(A);
-  return check_launch("fdt_kernel");
+  const int ntiles = L.ntx * L.nty;
+  fdt_kernel<P, NO, TX, TY><<<ntiles < grid_cap ? ntiles : grid_cap, G::THREADS, G::SMEM, st>>>(A);
+  int rc = check_launch("fdt_kernel");
+  if (rc) return rc;
+  constexpr long PER = (long)G::BW * (G::OY - G::BW) + (long)(G::OX - G::BW) * G::BW + (long)G::BW * G::BW;
+  const long nb = PER * ntiles;
+  fdt_fixup<P, NO, TX, TY><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(L.u, L.ws, L.N_x, L.N_y, L.ntx, L.nty);
+  return check_launch("fdt_fixup");
 }
 
 using FDTLaunchFn = int (*)(const FDTLaunch&, cudaStream_t);

@@ -2,169 +2,191 @@
 //
 // Reference: prolongate / restrict_residual (multigrid.py:180-193) multiply
 // by dense global 1D matrices P_y, P_x (multigrid.py:112-124) whose rows
-// are ASSIGNED per element (a fine vertex node appears once).  Here both
-// are element-local and sum-factorized with the (p_f+1) x (p_c+1) matrix J:
+// are ASSIGNED per element (a fine vertex node appears once).  Here both are
+// element-local, separable (x pass then y pass) with the (p_f+1) x (p_c+1)
+// interpolation matrix J, in gather form -- one thread per output entry:
 //   prolongation : fine node (a,b) owned by element e (0 <= a,b < p_f)
 //                  u_f += sum_{ac,bc} J[a][ac] U_c,e[ac][bc] J[b][bc]
 //   restriction  : owner-computes over fine rows/cols b < p_f of every
-//                  element (so shared fine nodes are counted once, as in
-//                  P^T), gathered onto coarse nodes; the coarse vertex
-//                  (ac = 0) also collects element e-1's ac = p_c term.
-// Both are gather-form per output node: deterministic, no atomics.
+//                  element (so shared fine nodes count once, exactly as in
+//                  P^T); coarse vertex ac = 0 also collects element e-1's
+//                  ac = p_c term, added in a fixed order.
+// Deterministic, no atomics.  Tiles are compile-time; data is staged with
+// cp.async and J lives in shared memory.
 #include "smg_transfer.cuh"
 
 namespace smg {
 
-template <int PC, int PF>
-__global__ void __launch_bounds__(kTrThreads) prolong_kernel(const __grid_constant__ TrArgs A) {
-  constexpr int NC = PC + 1;
+__device__ __forceinline__ void tr_cp_async8(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+template <int PC, int PF, int T>
+struct TrGeom {
+  static constexpr int NC = PC + 1, NF = PF + 1;
+  // prolongation: coarse region incl. high vertex, fine own tile
+  static constexpr int CX = T * PC + 1, OXF = T * PF;
+  // restriction: fine staged incl. the low halo element, coarse own tile
+  static constexpr int FX = (T + 1) * PF, OXC = T * PC;
+  static constexpr int NT = 256;
+  static constexpr size_t SMEM_P = sizeof(double) * ((size_t)CX * CX + (size_t)CX * OXF + (size_t)OXF * OXF + NF * NC);
+  static constexpr size_t SMEM_R = sizeof(double) * ((size_t)FX * FX + (size_t)FX * OXC + NF * NC);
+};
+
+template <int PC, int PF, int T>
+__global__ void __launch_bounds__(256) prolong_kernel(const __grid_constant__ TrArgs A) {
+  using G = TrGeom<PC, PF, T>;
+  constexpr int NC = G::NC, NF = G::NF, CX = G::CX, OX = G::OXF, NT = G::NT;
   extern __shared__ double sm[];
-  const int TX = A.TX, TY = A.TY;
-  const int CX = TX * PC + 1, CY = TY * PC + 1;   // coarse tile incl. high vertex
-  const int OX = TX * PF;                          // fine own cols
-  double* C = sm;                                  // CY x CX
-  double* T = C + CX * CY;                         // CY x OX
-  const int tid = threadIdx.x, nt = blockDim.x;
+  double* C = sm;             // CX x CX coarse values
+  double* Tt = C + CX * CX;   // CX x OX  (x-interpolated)
+  double* UF = Tt + CX * OX;  // OX x OX  old fine values (accumulate)
+  double* Js = UF + OX * OX;  // NF x NC
+  const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
-  const int Xc0 = tx * TX * PC, Yc0 = ty * TY * PC;
-  for (int idx = tid; idx < CX * CY; idx += nt) {
+  const int Xc0 = tx * T * PC, Yc0 = ty * T * PC, Xf0 = tx * OX, Yf0 = ty * OX;
+  for (int idx = tid; idx < CX * CX; idx += NT) {
     const int y = idx / CX, x = idx - y * CX;
-    C[idx] = __ldg(A.src + (size_t)wrapi(Yc0 + y, Nyc) * Nxc + wrapi(Xc0 + x, Nxc));
+    tr_cp_async8(C + idx, A.src + (size_t)wrapi(Yc0 + y, Nyc) * Nxc + wrapi(Xc0 + x, Nxc));
   }
-  __syncthreads();
-  // x: T[rc][exl*PF + b] = sum_bc C[rc][exl*PC + bc] J[b][bc]
-  for (int it = tid; it < CY * TX; it += nt) {
-    const int rc = it / TX, exl = it - rc * TX;
-    double c[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) c[k] = C[rc * CX + exl * PC + k];
-#pragma unroll
-    for (int b = 0; b < PF; ++b) {
-      double s = A.J[b * NC] * c[0];
-#pragma unroll
-      for (int k = 1; k < NC; ++k) s = fma(A.J[b * NC + k], c[k], s);
-      T[rc * OX + exl * PF + b] = s;
+  if (A.accumulate) {
+    for (int idx = tid; idx < OX * OX; idx += NT) {
+      const int y = idx / OX, x = idx - y * OX;
+      tr_cp_async8(UF + idx, A.dst + (size_t)(Yf0 + y) * Nxf + (Xf0 + x));
     }
   }
+  for (int idx = tid; idx < NF * NC; idx += NT) Js[idx] = A.J[idx];
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  // y: out[eyl*PF + a][xf] = sum_ac J[a][ac] T[eyl*PC + ac][xf]
-  for (int it = tid; it < TY * OX; it += nt) {
-    const int eyl = it / OX, xf = it - eyl * OX;
-    double t[NC];
+  // x: Tt[rc][xf] = sum_bc J[b][bc] C[rc][exl*PC + bc]
+  for (int idx = tid; idx < CX * OX; idx += NT) {
+    const int rc = idx / OX, xf = idx - rc * OX;
+    const int exl = xf / PF, b = xf - exl * PF;
+    const double* c = C + rc * CX + exl * PC;
+    const double* j = Js + b * NC;
+    double s = j[0] * c[0];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) t[k] = T[(eyl * PC + k) * OX + xf];
-    const int gyf = (ty * TY + eyl) * PF, gxf = tx * OX + xf;
+    for (int k = 1; k < NC; ++k) s = fma(j[k], c[k], s);
+    Tt[idx] = s;
+  }
+  __syncthreads();
+  // y: out[yf][xf] = sum_ac J[a][ac] Tt[eyl*PC + ac][xf]
+  for (int idx = tid; idx < OX * OX; idx += NT) {
+    const int yf = idx / OX, xf = idx - yf * OX;
+    const int eyl = yf / PF, a = yf - eyl * PF;
+    const double* t = Tt + (eyl * PC) * OX + xf;
+    const double* j = Js + a * NC;
+    double s = j[0] * t[0];
 #pragma unroll
-    for (int a = 0; a < PF; ++a) {
-      double s = A.J[a * NC] * t[0];
-#pragma unroll
-      for (int k = 1; k < NC; ++k) s = fma(A.J[a * NC + k], t[k], s);
-      double* d = A.dst + (size_t)(gyf + a) * Nxf + gxf;
-      *d = A.accumulate ? *d + s : s;
-    }
+    for (int k = 1; k < NC; ++k) s = fma(j[k], t[k * OX], s);
+    A.dst[(size_t)(Yf0 + yf) * Nxf + (Xf0 + xf)] = A.accumulate ? UF[idx] + s : s;
   }
 }
 
-template <int PC, int PF>
-__global__ void __launch_bounds__(kTrThreads) restrict_kernel(const __grid_constant__ TrArgs A) {
-  constexpr int NC = PC + 1;
+template <int PC, int PF, int T>
+__global__ void __launch_bounds__(256) restrict_kernel(const __grid_constant__ TrArgs A) {
+  using G = TrGeom<PC, PF, T>;
+  constexpr int NC = G::NC, NF = G::NF, FX = G::FX, OX = G::OXC, NT = G::NT;
   extern __shared__ double sm[];
-  const int TX = A.TX, TY = A.TY;
-  const int FX = (TX + 1) * PF, FY = (TY + 1) * PF;  // fine own rows/cols incl. low halo element
-  const int OX = TX * PC, OY = TY * PC;              // coarse own nodes
-  double* F = sm;                                    // FY x FX
-  double* TXc = F + FX * FY;                         // FY x OX  (x-restricted, own coarse cols)
-  double* VX = TXc + FY * OX;                        // FY x (TX+1)
-  double* RY = VX + FY * (TX + 1);                   // OY x OX
-  double* VY = RY + OY * OX;                         // OX x (TY+1)
-  const int tid = threadIdx.x, nt = blockDim.x;
+  double* F = sm;              // FX x FX fine own rows/cols of elements [t0-1, t0+T)
+  double* Tx = F + FX * FX;    // FX x OX  (x-restricted)
+  double* Js = Tx + FX * OX;   // NF x NC
+  const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int Nxf = A.n_x * PF, Nyf = A.n_y * PF, Nxc = A.n_x * PC;
-  const int Xf0 = (tx * TX - 1) * PF, Yf0 = (ty * TY - 1) * PF;
-  for (int idx = tid; idx < FX * FY; idx += nt) {
+  const int Xf0 = (tx * T - 1) * PF, Yf0 = (ty * T - 1) * PF;
+  for (int idx = tid; idx < FX * FX; idx += NT) {
     const int y = idx / FX, x = idx - y * FX;
-    F[idx] = __ldg(A.src + (size_t)wrapi(Yf0 + y, Nyf) * Nxf + wrapi(Xf0 + x, Nxf));
+    tr_cp_async8(F + idx, A.src + (size_t)wrapi(Yf0 + y, Nyf) * Nxf + wrapi(Xf0 + x, Nxf));
+  }
+  for (int idx = tid; idx < NF * NC; idx += NT) Js[idx] = A.J[idx];
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  // x: Tx[yf][xc] = sum_{b<PF} J[b][ac] F[yf][(exl+1) PF + b]  (+ left element's ac = PC term)
+  for (int idx = tid; idx < FX * OX; idx += NT) {
+    const int yf = idx / OX, xc = idx - yf * OX;
+    const int exl = xc / PC, ac = xc - exl * PC;
+    const double* f = F + yf * FX + (exl + 1) * PF;
+    double s = Js[ac] * f[0];
+#pragma unroll
+    for (int b = 1; b < PF; ++b) s = fma(Js[b * NC + ac], f[b], s);
+    if (ac == 0) {
+      const double* fl = f - PF;
+      double s2 = Js[PC] * fl[0];
+#pragma unroll
+      for (int b = 1; b < PF; ++b) s2 = fma(Js[b * NC + PC], fl[b], s2);
+      s += s2;
+    }
+    Tx[idx] = s;
   }
   __syncthreads();
-  // x pass over every staged fine row: element exl-1 (exl = 0 is the halo element)
-  for (int it = tid; it < FY * (TX + 1); it += nt) {
-    const int yf = it / (TX + 1), exl = it - yf * (TX + 1);
-    const double* fr = F + yf * FX + exl * PF;
-    double t[NC];
+  // y: out[yc][xc] = sum_{a<PF} J[a][acy] Tx[(eyl+1) PF + a][xc]  (+ lower element's PC term)
+  for (int idx = tid; idx < OX * OX; idx += NT) {
+    const int yc = idx / OX, xc = idx - yc * OX;
+    const int eyl = yc / PC, ac = yc - eyl * PC;
+    const double* t = Tx + ((eyl + 1) * PF) * OX + xc;
+    double s = Js[ac] * t[0];
 #pragma unroll
-    for (int ac = 0; ac < NC; ++ac) t[ac] = A.J[ac] * fr[0];
+    for (int a = 1; a < PF; ++a) s = fma(Js[a * NC + ac], t[a * OX], s);
+    if (ac == 0) {
+      const double* tl = t - PF * OX;
+      double s2 = Js[PC] * tl[0];
 #pragma unroll
-    for (int b = 1; b < PF; ++b) {
-      const double v = fr[b];
-#pragma unroll
-      for (int ac = 0; ac < NC; ++ac) t[ac] = fma(A.J[b * NC + ac], v, t[ac]);
+      for (int a = 1; a < PF; ++a) s2 = fma(Js[a * NC + PC], tl[a * OX], s2);
+      s += s2;
     }
-    if (exl > 0) {
-#pragma unroll
-      for (int ac = 0; ac < PC; ++ac) TXc[yf * OX + (exl - 1) * PC + ac] = t[ac];
-    }
-    VX[yf * (TX + 1) + exl] = t[PC];
-  }
-  __syncthreads();
-  // y pass over own coarse columns: element eyl-1 over its own fine rows
-  for (int it = tid; it < OX * (TY + 1); it += nt) {
-    const int xc = it / (TY + 1), eyl = it - xc * (TY + 1);
-    const bool vert = (xc % PC) == 0;
-    double t[NC];
-    for (int ac = 0; ac < NC; ++ac) t[ac] = 0.0;
-#pragma unroll
-    for (int a = 0; a < PF; ++a) {
-      const int yf = eyl * PF + a;
-      double v = TXc[yf * OX + xc];
-      if (vert) v += VX[yf * (TX + 1) + xc / PC];
-#pragma unroll
-      for (int ac = 0; ac < NC; ++ac) t[ac] = fma(A.J[a * NC + ac], v, t[ac]);
-    }
-    if (eyl > 0) {
-#pragma unroll
-      for (int ac = 0; ac < PC; ++ac) RY[((eyl - 1) * PC + ac) * OX + xc] = t[ac];
-    }
-    VY[xc * (TY + 1) + eyl] = t[PC];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < OX * OY; idx += nt) {
-    const int y = idx / OX, x = idx - y * OX;
-    double v = RY[idx];
-    if (y % PC == 0) v += VY[x * (TY + 1) + y / PC];
-    A.dst[(size_t)(ty * OY + y) * Nxc + (tx * OX + x)] = v;
+    A.dst[(size_t)(ty * OX + yc) * Nxc + (tx * OX + xc)] = s;
   }
 }
 
-size_t prolong_smem(int pc, int pf, int TX, int TY) {
-  const size_t CX = (size_t)TX * pc + 1, CY = (size_t)TY * pc + 1;
-  return sizeof(double) * (CX * CY + CY * (size_t)TX * pf);
-}
-size_t restrict_smem(int pc, int pf, int TX, int TY) {
-  const size_t FX = (size_t)(TX + 1) * pf, FY = (size_t)(TY + 1) * pf;
-  const size_t OX = (size_t)TX * pc, OY = (size_t)TY * pc;
-  return sizeof(double) * (FX * FY + FY * OX + FY * (TX + 1) + OY * OX + OX * (TY + 1));
-}
-
-template <int PC, int PF>
-int transfer_launch(const TrArgs& A, int grid, bool prolong, cudaStream_t st) {
+template <int PC, int PF, int T>
+int tr_launch_t(const TrArgs& A0, bool prolong, cudaStream_t st) {
+  using G = TrGeom<PC, PF, T>;
+  TrArgs A = A0;
+  A.tiles_x = A.n_x / T;
+  const int grid = (A.n_x / T) * (A.n_y / T);
   if (prolong) {
-    const size_t smem = prolong_smem(PC, PF, A.TX, A.TY);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(prolong_kernel<PC, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    prolong_kernel<PC, PF><<<grid, kTrThreads, smem, st>>>(A);
+    static bool attr = false;
+    if (!attr && G::SMEM_P > 48 * 1024)
+      cudaFuncSetAttribute(prolong_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_P);
+    attr = true;
+    prolong_kernel<PC, PF, T><<<grid, G::NT, G::SMEM_P, st>>>(A);
   } else {
-    const size_t smem = restrict_smem(PC, PF, A.TX, A.TY);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(restrict_kernel<PC, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    restrict_kernel<PC, PF><<<grid, kTrThreads, smem, st>>>(A);
+    static bool attr = false;
+    if (!attr && G::SMEM_R > 48 * 1024)
+      cudaFuncSetAttribute(restrict_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_R);
+    attr = true;
+    restrict_kernel<PC, PF, T><<<grid, G::NT, G::SMEM_R, st>>>(A);
   }
   return check_launch(prolong ? "prolong_kernel" : "restrict_kernel");
 }
 
-using TrFn = int (*)(const TrArgs&, int, bool, cudaStream_t);
+// tile T (elements per side) chosen at run time from the compiled set
+template <int PC, int PF>
+int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
+  constexpr int T0 = PF >= 32 ? 1 : 32 / PF;
+  // largest power-of-two T <= T0 dividing the mesh that keeps >= 296 CTAs,
+  // else the one with the most CTAs
+  int best = 1;
+  for (int t = T0; t >= 1; t /= 2) {
+    if (n_x % t || n_y % t) continue;
+    best = t;
+    if ((long)(n_x / t) * (n_y / t) >= 296) break;
+  }
+  switch (best) {
+    case 16: if constexpr (T0 >= 16) return tr_launch_t<PC, PF, (T0 >= 16 ? 16 : 1)>(A, prolong, st); break;
+    case 8: if constexpr (T0 >= 8) return tr_launch_t<PC, PF, (T0 >= 8 ? 8 : 1)>(A, prolong, st); break;
+    case 4: if constexpr (T0 >= 4) return tr_launch_t<PC, PF, (T0 >= 4 ? 4 : 1)>(A, prolong, st); break;
+    case 2: if constexpr (T0 >= 2) return tr_launch_t<PC, PF, (T0 >= 2 ? 2 : 1)>(A, prolong, st); break;
+    default: break;
+  }
+  return tr_launch_t<PC, PF, 1>(A, prolong, st);
+}
+
 TrFn transfer_dispatch(int pc, int pf) {
-#define SMG_TR(a, b) if (pc == a && pf == b) return &transfer_launch<a, b>;
+#define SMG_TR(a, b) if (pc == a && pf == b) return &tr_launch<a, b>;
   SMG_TR(1, 2) SMG_TR(2, 4) SMG_TR(4, 8) SMG_TR(8, 16) SMG_TR(16, 32)
   SMG_TR(1, 3) SMG_TR(3, 6) SMG_TR(6, 12) SMG_TR(12, 24)
 #undef SMG_TR

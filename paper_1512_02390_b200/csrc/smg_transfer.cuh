@@ -4,19 +4,16 @@
 namespace smg {
 
 constexpr int kTrMaxP = 33;   // (p+1) bound
-constexpr int kTrThreads = 256;
 
 struct TrArgs {
   const double* __restrict__ src;
   double* __restrict__ dst;
-  int pc, pf, n_x, n_y;
-  int TX, TY, tiles_x, accumulate;
-  double J[kTrMaxP * kTrMaxP];   // J[a*(pc+1)+ac], a in [0,pf], ac in [0,pc]
+  int n_x, n_y, tiles_x, accumulate;
+  double J[kTrMaxP * 17];   // J[a*(pc+1)+ac], a in [0,pf], ac in [0,pc]
 };
 
-using TrFn = int (*)(const TrArgs&, int, bool, cudaStream_t);
+using TrFn = int (*)(const TrArgs&, int n_x, int n_y, bool prolong, cudaStream_t);
+// launcher for (p_c, p_f) on an n_x x n_y mesh (largest compiled tile that divides it)
 TrFn transfer_dispatch(int pc, int pf);
-size_t prolong_smem(int pc, int pf, int TX, int TY);
-size_t restrict_smem(int pc, int pf, int TX, int TY);
 
 }  // namespace smg
