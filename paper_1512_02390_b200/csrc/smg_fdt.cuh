@@ -71,8 +71,10 @@ struct FDTGeom {
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int RX = OX + 2 * NO + 1, RY = OY + 2 * NO + 1;
   static constexpr int BW = 2 * NO + 1;
-  // two threads per (element, line): lane pair = (even half, odd half)
-  static constexpr int THREADS = ((2 * E * M + 31) / 32) * 32;
+  // two threads per (element, line): warps [0, NH) take the even halves and
+  // warps [NH, 2 NH) the odd halves -- parity is warp-uniform (no divergence)
+  static constexpr int NH = ((E * M + 31) / 32) * 32;
+  static constexpr int THREADS = 2 * NH;
   static constexpr int NT = THREADS;
   // colours inside the tile: windows of elements C apart are disjoint
   static constexpr int C = (2 * NO < P) ? 2 : 3;
@@ -141,19 +143,19 @@ __global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, 2)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
-  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT, STAGE = G::STAGE;
+  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT, NH = G::NH, STAGE = G::STAGE;
   extern __shared__ double sm[];
   double* EB = sm + 2 * STAGE;  // E x M x M element buffers
   const int tid = threadIdx.x;
   const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, ntiles = A.ntx * A.nty;
 
-  const bool odd = tid & 1;
-  const int line = tid >> 1;
+  const bool odd = tid >= NH;     // warp-uniform
+  const int line = odd ? tid - NH : tid;
   const int e = line / M, c = line - e * M;
   const bool act = e < E;
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
-  double dl[HE];  // this lane's half row of 1/(lam_y + lam_x)
+  double dl[HE];  // this thread's half row of 1/(lam_y + lam_x)
   {
     const double* dr = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 #pragma unroll
@@ -182,7 +184,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;
       __syncthreads();
     } else {
-      // ---- stage 1 (physical columns): T1[:, c] = S_y^T R_e[:, c] --------
+      // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
       if (act) {
         const double* col = R + (eyl * P) * RX + exl * P + c;
         auto in = [&](int k) { return col[k * RX]; };
@@ -201,7 +203,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       __syncthreads();
       for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
 
-      // ---- stage 2 (eigen-y rows): T2[c, :] = (T1[c, :] S_x) * dinv / nu_bar
+      // ---- stage 2 (eigen-y rows c): T2[c, :] = ([Se; So]^T fold_x(T1[c, :])) * dinv / nu_bar
       {
         double t[HE];
         const double* row = B + c * M;
@@ -223,11 +225,10 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       }
       __syncthreads();
 
-      // ---- stage 3 (eigen-x columns): T3[:, c] = S_y T2[:, c] -------------
+      // ---- stage 3 (eigen-x columns c): even warps e = SyeT^T T2e[:, c] -> rows [0,HE),
+      //      odd warps o = SyoT^T T2o[:, c] -> rows [HE, M)   (e/o recombined in stage 4)
       {
         double acc[HE];
-#pragma unroll
-        for (int k = 0; k < HE; ++k) acc[k] = 0.0;
         if (act) {
           if (!odd) {
             double t[HE];
@@ -235,67 +236,86 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
             for (int i = 0; i < HE; ++i) t[i] = B[i * M + c];
             half_synth<HE>(A.SyeT, t, acc);
           } else if (HO > 0) {
-            double t[HOX], a2[HOX];
+            double t[HOX];
 #pragma unroll
             for (int i = 0; i < HO; ++i) t[i] = B[(HE + i) * M + c];
-            half_synth<HOX>(A.SyoT, t, a2);
-#pragma unroll
-            for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+            half_synth<HOX>(A.SyoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
         __syncthreads();  // every column read before the in-place writes
+        if (act) {
+          if (!odd) {
 #pragma unroll
-        for (int k = 0; k < HO; ++k) {
-          const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
-          if (act) {
-            if (!odd) B[k * M + c] = acc[k] + other;         // y[k]     = e + o
-            else B[(M - 1 - k) * M + c] = other - acc[k];     // y[m-1-k] = e - o
+            for (int k = 0; k < HE; ++k) B[k * M + c] = acc[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < HO; ++k) B[(HE + k) * M + c] = acc[k];
           }
         }
-        if ((M & 1) && act && !odd) B[HO * M + c] = acc[HO];
       }
       __syncthreads();
 
-      // ---- stage 4 (physical rows): out[c, :] = W .* (T3[c, :] S_x^T), added
-      //      into the region in colour passes (disjoint windows per pass) ---
+      // ---- stage 4 (physical rows c): T3[c, :] = e[c'] +- o[c'] (c' = mirror-folded
+      //      row), then even warps ex = SxeT^T T3e, odd warps ox = SxoT^T T3o ----
       {
+        const int cf = c < HE ? c : M - 1 - c;   // folded physical row
+        const double sg = c < HE ? 1.0 : -1.0;   // y[m-1-k] = e - o
+        const bool centre = (M & 1) && c == HO;
         double acc[HE];
-#pragma unroll
-        for (int k = 0; k < HE; ++k) acc[k] = 0.0;
         if (act) {
+          const double* er = B + cf * M;
+          const double* orow = B + (HE + (cf < HO ? cf : 0)) * M;
+          auto t3 = [&](int j) { return centre ? er[j] : fma(sg, orow[j], er[j]); };
           if (!odd) {
             double t[HE];
 #pragma unroll
-            for (int i = 0; i < HE; ++i) t[i] = B[c * M + i];
+            for (int i = 0; i < HE; ++i) t[i] = t3(i);
             half_synth<HE>(A.SxeT, t, acc);
           } else if (HO > 0) {
-            double t[HOX], a2[HOX];
+            double t[HOX];
 #pragma unroll
-            for (int i = 0; i < HO; ++i) t[i] = B[c * M + HE + i];
-            half_synth<HOX>(A.SxoT, t, a2);
-#pragma unroll
-            for (int k = 0; k < HO; ++k) acc[k] = a2[k];
+            for (int i = 0; i < HO; ++i) t[i] = t3(HE + i);
+            half_synth<HOX>(A.SxoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
-        double y[HE];
+        __syncthreads();  // every row read before B is reused for ex / ox
+        if (act) {
+          // even warps keep ex in B[c][0,HE), odd warps ox in B[c][HE,M)
+          if (!odd) {
 #pragma unroll
-        for (int k = 0; k < HO; ++k) {
-          const double other = __shfl_xor_sync(0xffffffffu, acc[k], 1);
-          y[k] = odd ? other - acc[k] : acc[k] + other;
+            for (int k = 0; k < HE; ++k) B[c * M + k] = acc[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < HO; ++k) B[c * M + HE + k] = acc[k];
+          }
         }
-        if (M & 1) y[HO] = acc[HO];
-        const double wyc = act ? A.wy[c] : 0.0;
+      }
+      __syncthreads();
+
+      // ---- recombine out[c, j] = W (ex +- ox) and add into the region in colour
+      //      passes (disjoint windows per pass); thread = (element, row c, half)
+      {
         constexpr int C = G::C;
+        const double wyc = act ? A.wy[c] : 0.0;
 #pragma unroll
         for (int pass = 0; pass < C * C; ++pass) {
           if (act && (eyl % C) * C + (exl % C) == pass) {
+            const double* br = B + c * M;
             double* dst = R + (eyl * P + c) * RX + exl * P;
             if (!odd) {
+              // columns j in [0, HE): y[j] = ex[j] + ox[j] (centre: ex only)
 #pragma unroll
-              for (int k = 0; k < HE; ++k) dst[k] += y[k] * (wyc * A.wx[k]);
+              for (int j = 0; j < HE; ++j) {
+                const double y = j < HO ? br[j] + br[HE + j] : br[j];
+                dst[j] += y * (wyc * A.wx[j]);
+              }
             } else {
+              // columns m-1-j, j in [0, HO): y = ex[j] - ox[j]
 #pragma unroll
-              for (int k = 0; k < HO; ++k) dst[M - 1 - k] += y[k] * (wyc * A.wx[M - 1 - k]);
+              for (int j = 0; j < HO; ++j) {
+                const double y = br[j] - br[HE + j];
+                dst[M - 1 - j] += y * (wyc * A.wx[M - 1 - j]);
+              }
             }
           }
           __syncthreads();

@@ -275,3 +275,45 @@ def test_tiled_sweep_ragged_meshes(cuda_device, n_o, shape):
     u2 = dev(u0)
     sm.correct(dev(r), u2)
     assert torch.equal(u, u2)
+
+
+def test_c3_vcycle_full_size(cuda_device):
+    """BASELINE configs[2]: 128x128, p=32 (16.8M DOF), one V-cycle from zero."""
+    g = golden("xlarge_c3")
+    mesh = P.MeshConfig(128, 128, 1.0, 1.0)
+    h = P.build_hierarchy(mesh, 32, P.OverlapRule("fixed", 1))
+    f = O.project_mean(np.random.default_rng(0).standard_normal((4096, 4096)))
+    fd = torch.from_numpy(f).cuda()
+    u = P.v_cycle(h, torch.zeros_like(fd), fd)
+    assert maxrel(host(u)[::64, ::64], g["c3_vcycle_sample"]) < 1e-9
+    assert abs(float(torch.linalg.vector_norm(u)) - float(g["c3_vcycle_norm"])) < 1e-9 * float(g["c3_vcycle_norm"])
+    r1 = float(torch.linalg.vector_norm(P.residual(h.top.op, u, fd)))
+    assert abs(r1 - g["c3_res"][1]) < 1e-7 * g["c3_res"][1]
+
+
+def test_c4_mgcg_full_size(cuda_device):
+    """BASELINE configs[3]: [0,8]x[0,1], 256x256 elements (AR 8), p=16, MGCG to 1e-10
+    (the reference took 21 min on 8 CPU cores for the golden history)."""
+    g = golden("xlarge_c4")
+    mesh = P.MeshConfig(256, 256, 8.0, 1.0)
+    h = P.build_hierarchy(mesh, 16, P.OverlapRule("fixed", 1))
+    f = O.project_mean(np.random.default_rng(0).standard_normal((4096, 4096)))
+    u, rep = P.solve(h, f, P.SolveConfig(solver="mgcg"), u0=np.zeros_like(f))
+    assert rep.converged and not rep.breakdown and not bool(g["c4_breakdown"])
+    _check_history(rep.residuals, g["c4_mgcg_res"], "c4")
+
+
+def test_c5_reduced_mgcg(cuda_device):
+    """BASELINE configs[4] geometry and hierarchy at reduced size: variable nu
+    (nu_hat=0.9, shift 0 == 1 + 0.9 sin x sin y on [0,2pi]^2), 64x64 elements,
+    p=24 with levels (1,3,6,12,24), MGCG to 1e-10, coarse solved by the
+    reference's own CG (parity mode)."""
+    g = golden("xlarge_c5r")
+    mesh = P.MeshConfig(64, 64, 1.0, 1.0)
+    h = P.build_hierarchy(mesh, 24, P.OverlapRule("fixed", 1), orders=(1, 3, 6, 12, 24), nu_hat=0.9,
+                          nu_shift=0.0, coarse="cg")
+    f = O.project_mean(np.random.default_rng(0).standard_normal((1536, 1536)))
+    u, rep = P.solve(h, f, P.SolveConfig(solver="mgcg"), u0=np.zeros_like(f))
+    assert rep.converged and not rep.breakdown
+    _check_history(rep.residuals, g["c5r_mgcg_res"], "c5r")
+    assert maxrel(host(u)[::24, ::24], g["c5r_mgcg_sample"]) < 1e-6
