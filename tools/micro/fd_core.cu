@@ -81,25 +81,54 @@ __global__ void __launch_bounds__(2 * ((E / EPT) * M + 31) / 32 * 32, 2) core(do
 }
 
 // E: register-only contraction chain (upper bound of the building block)
+template <int EPT>
 __global__ void __launch_bounds__(320, 2) coreE(double* out, int reps, const __grid_constant__ CArgs C) {
-  double x[HE];
+  double x[EPT][HE];
 #pragma unroll
-  for (int k = 0; k < HE; ++k) x[k] = 1e-3 * (threadIdx.x + k);
+  for (int q = 0; q < EPT; ++q)
+#pragma unroll
+    for (int k = 0; k < HE; ++k) x[q][k] = 1e-3 * (threadIdx.x + k + q);
   for (int r = 0; r < reps; ++r) {
-    double t[HE];
+    double t[EPT][HE];
 #pragma unroll
-    for (int i = 0; i < HE; ++i) t[i] = C.Se[i] * x[0];
+    for (int q = 0; q < EPT; ++q)
+#pragma unroll
+      for (int i = 0; i < HE; ++i) t[q][i] = C.Se[i] * x[q][0];
 #pragma unroll
     for (int k = 1; k < HE; ++k)
 #pragma unroll
-      for (int i = 0; i < HE; ++i) t[i] = fma(C.Se[k * HE + i], x[k], t[i]);
+      for (int i = 0; i < HE; ++i) {
+        const double sv = C.Se[k * HE + i];
 #pragma unroll
-    for (int i = 0; i < HE; ++i) x[i] = t[i];
+        for (int q = 0; q < EPT; ++q) t[q][i] = fma(sv, x[q][k], t[q][i]);
+      }
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+#pragma unroll
+      for (int i = 0; i < HE; ++i) x[q][i] = t[q][i];
   }
   double sacc = 0;
 #pragma unroll
-  for (int i = 0; i < HE; ++i) sacc += x[i];
+  for (int q = 0; q < EPT; ++q)
+#pragma unroll
+    for (int i = 0; i < HE; ++i) sacc += x[q][i];
   if (sacc == 1.2345) out[threadIdx.x] = sacc;
+}
+
+template <int EPT>
+void runE(double* d, const CArgs& C) {
+  const int reps = 2000, grid = 148 * 2;
+  coreE<EPT><<<grid, 320>>>(d, 10, C);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  coreE<EPT><<<grid, 320>>>(d, reps, C);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("E  EPT%d regs : %.2f TFLOP/s (%.3f ms)\n", EPT, 2.0 * grid * 320 * reps * HE * HE * EPT / ms / 1e9, ms);
 }
 
 template <int EPT, bool SMEMS>
@@ -130,19 +159,8 @@ int main() {
   run<2, false>("B  EPT2 const", d, C);
   run<1, true>("C  EPT1 smem ", d, C);
   run<2, true>("D  EPT2 smem ", d, C);
-  {
-    const int reps = 2000, grid = 148 * 2;
-    coreE<<<grid, 320>>>(d, 10, C);
-    cudaDeviceSynchronize();
-    cudaEvent_t a, b;
-    cudaEventCreate(&a); cudaEventCreate(&b);
-    cudaEventRecord(a);
-    coreE<<<grid, 320>>>(d, reps, C);
-    cudaEventRecord(b);
-    cudaEventSynchronize(b);
-    float ms;
-    cudaEventElapsedTime(&ms, a, b);
-    printf("E  EPT1 regs : %.2f TFLOP/s (%.3f ms)\n", 2.0 * grid * 320 * reps * HE * HE / ms / 1e9, ms);
-  }
+  runE<1>(d, C);
+  runE<2>(d, C);
+  runE<4>(d, C);
   return 0;
 }
