@@ -80,6 +80,8 @@ struct FDTGeom {
   static constexpr int C = (2 * NO < P) ? 2 : 3;
   static constexpr int STAGE = RX * RY + OX * OY;  // doubles per pipeline stage
   static constexpr size_t SMEM = sizeof(double) * (2 * (size_t)STAGE + (size_t)E * MM);
+  // two resident CTAs when both fit; the register cap follows from it
+  static constexpr int MINB = (2 * SMEM <= 200 * 1024 && THREADS <= 384) ? 2 : 1;
 };
 
 // Half analysis of one line.  Even lane: t = Se^T (x_k + x_{m-1-k}) (plus the
@@ -139,7 +141,7 @@ __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const
 // the current tile computes.  Exclusive nodes are written to u directly,
 // band nodes (within n_o of a tile edge) to the workspace for fdt_fixup.
 template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, 2)
+__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
@@ -155,12 +157,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const bool act = e < E;
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
-  double dl[HE];  // this thread's half row of 1/(lam_y + lam_x)
-  {
-    const double* dr = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
-#pragma unroll
-    for (int l = 0; l < HE; ++l) dl[l] = (l < (odd ? HO : HE)) ? __ldg(dr + l) : 0.0;
-  }
+  // this thread's half row of 1/(lam_y + lam_x) (L1-resident across tiles)
+  const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 
   int tile = blockIdx.x;
   if (tile < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, tile, sm);
@@ -216,10 +214,10 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         if (act) {
           if (!odd) {
 #pragma unroll
-            for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (dl[l] * s);
+            for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (__ldg(dl + l) * s);
           } else {
 #pragma unroll
-            for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (dl[l] * s);
+            for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (__ldg(dl + l) * s);
           }
         }
       }
