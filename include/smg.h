@@ -77,7 +77,8 @@ int smg_schwarz_destroy(smg_schwarz_t* h);
  * sweep given the residual r.  Deterministic (no atomics). */
 int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream);
 /* One or more full sweeps: r = f - A u; u += correction.  work: N_y*N_x.
- * u_is_zero != 0 lets the first sweep skip A u (u must hold zeros). */
+ * u_is_zero != 0 declares u == 0 on entry: the first sweep skips A u and
+ * WRITES u = correction (u's prior contents are never read). */
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
                        double* work, int n_it, int u_is_zero, void* stream);
 /* FastDiagSolver.solve on nb independent (m,m) blocks: out = W*(S_y(S_y^T B S_x ./ L)S_x^T).

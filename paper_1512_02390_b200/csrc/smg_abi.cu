@@ -38,6 +38,8 @@ int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n
                int rn, double tol, int it, double* ws, cudaStream_t st);
 int ccg_direction(double* p, const double* r, int64_t n, const double* S, int ro, int rn, cudaStream_t st);
 int ccg_dot(const double* x, const double* y, int64_t n, double* out, const double* S, double* ws, cudaStream_t st);
+int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
+               double* tmp, double* u, cudaStream_t st);
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
          double* C, int ldc, const double* S, cudaStream_t st);
 
@@ -308,15 +310,18 @@ static FDLaunch fd_base(const smg_schwarz_t* h) {
   return L;
 }
 
-int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream) {
-  if (!h || !r || !u || r == u) { set_error("smg_schwarz_correct: bad argument"); return SMG_EINVAL; }
+static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, int u_zero, void* stream) {
   if (h->tiled) {
     FDTLaunch T;
-    T.r = r; T.u = u; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
+    T.r = r; T.u = u; T.u_zero = u_zero; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
     T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
     T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
     T.wx = h->wx.data(); T.wy = h->wy.data();
     return h->fdt(T, as_stream(stream));
+  }
+  if (u_zero) {
+    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * h->p * h->n_x * h->p * h->n_y, as_stream(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "schwarz_correct");
   }
   FDLaunchFn fn = fd_dispatch(h->m);
   FDLaunch L = fd_base(h);
@@ -329,6 +334,11 @@ int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void
       if (rc) return rc;
     }
   return SMG_OK;
+}
+
+int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream) {
+  if (!h || !r || !u || r == u) { set_error("smg_schwarz_correct: bad argument"); return SMG_EINVAL; }
+  return schwarz_correct(h, r, u, 0, stream);
 }
 
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
@@ -344,7 +354,7 @@ int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, co
       if (rc) return rc;
       r = work;
     }
-    int rc = smg_schwarz_correct(h, r, u, stream);
+    int rc = schwarz_correct(h, r, u, (it == 0 && u_is_zero) ? 1 : 0, stream);
     if (rc) return rc;
   }
   return SMG_OK;
@@ -469,7 +479,8 @@ int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double*
   const int nx = h->n_x, ny = h->n_y;
   double* T1 = ws;
   double* T2 = ws + (size_t)nx * ny;
-  int rc;
+  int rc = pinv_small(nx, ny, h->Qx, h->Qy, h->Lp, f0, T1, u0, st);
+  if (rc != 1) return rc;
   // T1 = Qy^T F ; T2 = (T1 Qx) .* Lp ; T1 = Qy T2 ; U = T1 Qx^T
   if ((rc = gemm(ny, nx, ny, h->Qy, ny, 1, f0, nx, 0, T1, nx, nullptr, st))) return rc;
   if ((rc = gemm(ny, nx, nx, T1, nx, 0, h->Qx, nx, 0, T2, nx, h->Lp, st))) return rc;

@@ -272,6 +272,106 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 }
 
 
+
+// ---- fused small-grid coarse pseudo-inverse --------------------------------
+// For n_x, n_y <= 128 the four GEMMs u = Q_y (Lp .* (Q_y^T F Q_x)) Q_x^T are
+// done as two launches of row blocks (kRB rows per CTA), each chaining two
+// products through shared memory:
+//   pinv_a: T2[I,:] = ((Q_y^T F)[I,:] Q_x) .* Lp[I,:]
+//   pinv_b: U[J,:]  = ((Q_y T2)[J,:]) Q_x^T
+constexpr int kRB = 4;
+constexpr int kPinvMax = 128;
+
+template <bool FIRST>
+__global__ void __launch_bounds__(256) pinv_rows_kernel(int nx, int ny, const double* __restrict__ Qx,
+                                                        const double* __restrict__ Qy, const double* __restrict__ Lp,
+                                                        const double* __restrict__ in, double* __restrict__ out) {
+  constexpr int KC = 32;
+  __shared__ double T[kRB][kPinvMax];
+  __shared__ double Xs[KC][kPinvMax + 1];
+  __shared__ double Qs[KC][kRB];
+  const int r0 = blockIdx.x * kRB;
+  const int tid = threadIdx.x;
+  // each thread owns outputs (i, x) for idx = tid + 256 j
+  double acc[kRB * kPinvMax / 256];
+  constexpr int NO = kRB * kPinvMax / 256;
+#pragma unroll
+  for (int j = 0; j < NO; ++j) acc[j] = 0.0;
+  // phase 1: T[i][x] = sum_k Qy'[k][r0+i] in[k][x]   (Qy' = Q_y, used transposed when FIRST)
+  for (int k0 = 0; k0 < ny; k0 += KC) {
+    const int kc = min(KC, ny - k0);
+    for (int idx = tid; idx < kc * nx; idx += 256) {
+      const int k = idx / nx, x = idx - k * nx;
+      Xs[k][x] = in[(size_t)(k0 + k) * nx + x];
+    }
+    for (int idx = tid; idx < kc * kRB; idx += 256) {
+      const int k = idx / kRB, i = idx - k * kRB;
+      const int row = min(r0 + i, ny - 1);
+      Qs[k][i] = FIRST ? Qy[(size_t)(k0 + k) * ny + row] : Qy[(size_t)row * ny + (k0 + k)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+      const int idx = tid + 256 * j;
+      const int i = idx / kPinvMax, x = idx - i * kPinvMax;
+      if (x < nx) {
+        double s = acc[j];
+        for (int k = 0; k < kc; ++k) s = fma(Qs[k][i], Xs[k][x], s);
+        acc[j] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    const int idx = tid + 256 * j;
+    T[idx / kPinvMax][idx % kPinvMax] = acc[j];
+    acc[j] = 0.0;
+  }
+  __syncthreads();
+  // phase 2: out[r0+i][x] = sum_j T[i][j] Qx'[j][x]   (Qx' = Q_x when FIRST, else Q_x^T)
+  for (int k0 = 0; k0 < nx; k0 += KC) {
+    const int kc = min(KC, nx - k0);
+    for (int idx = tid; idx < kc * nx; idx += 256) {
+      const int k = idx / nx, x = idx - k * nx;
+      Xs[k][x] = FIRST ? Qx[(size_t)(k0 + k) * nx + x] : Qx[(size_t)x * nx + (k0 + k)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+      const int idx = tid + 256 * j;
+      const int i = idx / kPinvMax, x = idx - i * kPinvMax;
+      if (x < nx) {
+        double s = acc[j];
+        for (int k = 0; k < kc; ++k) s = fma(T[i][k0 + k], Xs[k][x], s);
+        acc[j] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    const int idx = tid + 256 * j;
+    const int i = idx / kPinvMax, x = idx - i * kPinvMax;
+    const int row = r0 + i;
+    if (x < nx && row < ny) {
+      double v = acc[j];
+      if (FIRST) v *= Lp[(size_t)row * nx + x];
+      out[(size_t)row * nx + x] = v;
+    }
+  }
+}
+
+int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
+               double* tmp, double* u, cudaStream_t st) {
+  if (nx > kPinvMax || ny > kPinvMax) return 1;
+  const int grid = (ny + kRB - 1) / kRB;
+  pinv_rows_kernel<true><<<grid, 256, 0, st>>>(nx, ny, Qx, Qy, Lp, f, tmp);
+  int rc = check_launch("pinv_rows_kernel");
+  if (rc) return rc;
+  pinv_rows_kernel<false><<<grid, 256, 0, st>>>(nx, ny, Qx, Qy, Lp, tmp, u);
+  return check_launch("pinv_rows_kernel");
+}
 }  // namespace smg
 
 using namespace smg;

@@ -44,6 +44,7 @@ struct FDTArgs {
   unsigned int* __restrict__ ctr;     // 3 * ntiles counters (x-edge, y-edge, corner), zeroed
   int N_x, N_y, n_x, ntx, nty;
   int debug_skip;                     // profiling aid: 1 = skip the four contractions
+  int u_zero;                         // 1: u holds no valid data and is treated as 0 (write, not add)
   // analysis factors Se[k][i] (k physical half index), synthesis factors SeT[i][k]
   double Sye[fdt_he(M) * fdt_he(M)], SyeT[fdt_he(M) * fdt_he(M)];
   double Syo[fdt_ho(M) * fdt_ho(M) + 1], SyoT[fdt_ho(M) * fdt_ho(M) + 1];
@@ -120,7 +121,7 @@ __device__ __forceinline__ void half_synth(const double* __restrict__ ST, const 
 
 template <int P, int NO, int TX, int TY>
 __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const double* __restrict__ u, int N_x,
-                                             int N_y, int ntx, int tile, double* buf) {
+                                             int N_y, int ntx, int tile, double* buf, bool u_zero) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int RX = G::RX, RY = G::RY, OX = G::OX, OY = G::OY, NT = G::NT;
   const int tx = tile % ntx, ty = tile / ntx;
@@ -129,6 +130,7 @@ __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const
     const int y = idx / RX, x = idx - y * RX;
     cp_async8(buf + idx, r + (size_t)wrapi(Y0 - NO + y, N_y) * N_x + wrapi(X0 - NO + x, N_x));
   }
+  if (u_zero) return;
   double* uo = buf + RX * RY;
   for (int idx = threadIdx.x; idx < OX * OY; idx += NT) {
     const int y = idx / OX, x = idx - y * OX;
@@ -161,14 +163,14 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 
   int tile = blockIdx.x;
-  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, tile, sm);
+  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, tile, sm, A.u_zero != 0);
   cp_async_commit();
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     double* R = sm + (it & 1) * STAGE;  // residual region, then accumulated correction
     double* UO = R + RX * RY;           // own u
     {
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE);
+      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE, A.u_zero != 0);
       cp_async_commit();
     }
     const int tx = tile % ntx, ty = tile / ntx;
@@ -330,7 +332,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         W[idx] = R[idx];
       } else {
         const int oy = y - NO, ox = x - NO;
-        A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = UO[oy * OX + ox] + R[idx];
+        A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = A.u_zero ? R[idx] : UO[oy * OX + ox] + R[idx];
       }
     }
     __syncthreads();  // this stage buffer is refilled two iterations later
@@ -344,7 +346,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 // One thread per band node; deterministic; no atomics.
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
-                                                 int N_y, int ntx, int nty) {
+                                                 int N_y, int ntx, int nty, int u_zero) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
   constexpr size_t RS = (size_t)RX * RY;
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
     const double cl = ws[(size_t)(ty * ntx + txm) * RS + (size_t)yy * RX + (OX + NO + d)];
     const double cr = ws[(size_t)(ty * ntx + tx) * RS + (size_t)yy * RX + (NO + d)];
     double* up = u + (size_t)(Y0 - NO + yy) * N_x + wrapi(X0 + d, N_x);
-    *up = (*up + cl) + cr;
+    *up = ((u_zero ? 0.0 : *up) + cl) + cr;
     return;
   }
   k -= NXE;
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
     const double cb = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + d) * RX + xx];
     const double ct = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + d) * RX + xx];
     double* up = u + (size_t)wrapi(Y0 + d, N_y) * N_x + (X0 - NO + xx);
-    *up = (*up + cb) + ct;
+    *up = ((u_zero ? 0.0 : *up) + cb) + ct;
     return;
   }
   k -= NYE;
@@ -388,13 +390,14 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
     const double c01 = ws[(size_t)(ty * ntx + txm) * RS + (size_t)(NO + dy) * RX + (OX + NO + dx)];
     const double c11 = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + dy) * RX + (NO + dx)];
     double* up = u + (size_t)wrapi(Y0 + dy, N_y) * N_x + wrapi(X0 + dx, N_x);
-    *up = (((*up + c00) + c10) + c01) + c11;
+    *up = ((((u_zero ? 0.0 : *up) + c00) + c10) + c01) + c11;
   }
 }
 
 struct FDTLaunch {
   const double* r;
   double* u;
+  int u_zero;
   const double* inv_nu;
   const double* dinv;
   double* ws;
@@ -419,6 +422,7 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
     const char* dbg = getenv("SMG_FD_DEBUG_SKIP");
     A.debug_skip = (dbg && dbg[0] == '1') ? 1 : 0;
   }
+  A.u_zero = L.u_zero;
   for (int k = 0; k < HE; ++k)
     for (int i = 0; i < HE; ++i) {
       A.Sye[k * HE + i] = L.Sye[k * HE + i]; A.SyeT[i * HE + k] = L.Sye[k * HE + i];
@@ -450,7 +454,8 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
   if (rc) return rc;
   constexpr long PER = (long)G::BW * (G::OY - G::BW) + (long)(G::OX - G::BW) * G::BW + (long)G::BW * G::BW;
   const long nb = PER * ntiles;
-  fdt_fixup<P, NO, TX, TY><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(L.u, L.ws, L.N_x, L.N_y, L.ntx, L.nty);
+  fdt_fixup<P, NO, TX, TY><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(L.u, L.ws, L.N_x, L.N_y, L.ntx, L.nty,
+                                                                          L.u_zero);
   return check_launch("fdt_fixup");
 }
 

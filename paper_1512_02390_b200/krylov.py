@@ -124,7 +124,6 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
     converged = res[0] <= r_max
     cycles = 0
     if not converged:
-        p.zero_()
         _v_cycle(h, p, r_cur, u_zero=True)
         N.check(lib.smg_dot(N.ptr(p), N.ptr(r_cur), n, N.ptr(s.dev[0:1]), N.ptr(ws), st), "dot")
         for it in range(cfg.max_cycles):
@@ -141,7 +140,6 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
             if res[-1] <= r_max:
                 converged = True
                 break
-            z.zero_()
             _v_cycle(h, z, r_new, u_zero=True)
             N.check(lib.smg_cg_beta(N.ptr(z), N.ptr(r_new), N.ptr(r_cur) if it > 0 else None, n,
                                     N.ptr(s.dev), N.ptr(ws), st), "cg_beta")

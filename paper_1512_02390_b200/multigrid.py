@@ -249,9 +249,11 @@ def coarse_solve(h: MultigridHierarchy, f0) -> torch.Tensor:
 
 
 def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bool = False) -> torch.Tensor:
-    """Algorithm 3 on device buffers; u is updated in place.  u_zero asserts
-    u == 0 on entry (MGCG preconditioning), which lets the top smoother use
-    r = f without an operator apply -- bitwise what A 0 = 0 gives."""
+    """Algorithm 3 on device buffers; u is updated in place.  u_zero declares
+    the initial guess to be 0 (MGCG preconditioning): u's prior contents are
+    never read, the top smoother uses r = f without an operator apply
+    (bitwise what A 0 = 0 gives) and WRITES u = correction.  Lower levels
+    always start from zero the same way (multigrid.py:240-241)."""
     lib = N.lib()
     st = N.stream()
     L = h.depth
@@ -260,7 +262,7 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
     for l in range(L, 0, -1):
         lv = h.levels[l]
         zero = u_zero if l == L else True
-        if l < L:
+        if zero and not lv.n_pre:
             lv.u.zero_()
         if lv.n_pre:
             N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
