@@ -118,6 +118,15 @@ size_t smg_coarse_cg_ws_doubles(int64_t n);
 int smg_coarse_cg(const smg_op_t* op, const double* f0, double* u0, double* ws, double tol,
                   int max_iter, int* iters_out, void* stream);
 
+/* Fast mode for the variable-coefficient coarse level: CG on A0 (the p=1
+ * diffusion operator `op`) preconditioned by scale * A0_const^+ (the
+ * constant-coefficient pseudo-inverse of `pc`, typically scale = 1/mean(nu)),
+ * same projections, tolerance and cap semantics as smg_coarse_cg.
+ * ws: smg_coarse_pcg_ws_doubles(pc) doubles. */
+size_t smg_coarse_pcg_ws_doubles(const smg_coarse_t* pc);
+int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0, double* u0, double* ws,
+                   double tol, int max_iter, double scale, int* iters_out, void* stream);
+
 /* ---- BLAS-1 with device scalars (krylov.py:56-111, multigrid.py:199-214)
  * All reductions are deterministic (fixed grid, fixed summation order). */
 size_t smg_reduce_ws_doubles(void);

@@ -52,6 +52,8 @@ SIGNATURES = {
     "smg_coarse_pinv": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
     "smg_coarse_cg": (C.c_int, [_vp, _dp, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "smg_coarse_cg_ws_doubles": (C.c_size_t, [_i64]),
+    "smg_coarse_pcg_ws_doubles": (C.c_size_t, [_vp]),
+    "smg_coarse_pcg": (C.c_int, [_vp, _vp, _dp, _dp, _dp, C.c_double, C.c_int, C.c_double, C.POINTER(C.c_int), _vp]),
     "smg_reduce_ws_doubles": (C.c_size_t, []),
     "smg_dot": (C.c_int, [_dp, _dp, _i64, _dp, _dp, _vp]),
     "smg_dot2": (C.c_int, [_dp, _dp, _dp, _i64, _dp, _dp, _vp]),

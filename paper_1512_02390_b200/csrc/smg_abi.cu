@@ -38,6 +38,9 @@ int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n
                int rn, double tol, int it, double* ws, cudaStream_t st);
 int ccg_direction(double* p, const double* r, int64_t n, const double* S, int ro, int rn, cudaStream_t st);
 int ccg_dot(const double* x, const double* y, int64_t n, double* out, const double* S, double* ws, cudaStream_t st);
+int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
+               int it, double* ws, cudaStream_t st);
+int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
 int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
                double* tmp, double* u, cudaStream_t st);
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
@@ -539,6 +542,71 @@ int smg_coarse_cg(const smg_op_t* op, const double* f0, double* u0, double* ws, 
   const bool ok = hs[4] != 0.0;
   *iters_out = ok ? (int)hs[5] : -max_iter;
   // u0 = x - mean(x)  (multigrid.py:228)
+  return smg_project_mean(u0, n, red, stream);
+}
+
+
+// ---- coarse PCG (fast mode for variable diffusion) -----------------------------
+size_t smg_coarse_pcg_ws_doubles(const smg_coarse_t* h) {
+  return h ? 5 * (size_t)h->n_x * h->n_y + smg_coarse_ws_doubles(h) + smg_reduce_ws_doubles() + 16 : 0;
+}
+
+int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0, double* u0, double* ws,
+                   double tol, int max_iter, double scale, int* iters_out, void* stream) {
+  if (!op || !pc || !f0 || !u0 || !ws || !iters_out || op->p != 1 || op->n_x != pc->n_x || op->n_y != pc->n_y ||
+      max_iter < 1) {
+    set_error("smg_coarse_pcg: bad argument");
+    return SMG_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = (int64_t)op->n_x * op->n_y;
+  double* b = ws;
+  double* r = b + n;
+  double* p = r + n;
+  double* q = p + n;
+  double* z = q + n;
+  double* pws = z + n;
+  double* red = pws + smg_coarse_ws_doubles(pc);
+  double* S = red + smg_reduce_ws_doubles();
+  int rc;
+  cudaError_t e;
+  auto precond = [&](const double* in, double* out) -> int {
+    int rr = smg_coarse_pinv(pc, in, out, pws, stream);
+    if (rr) return rr;
+    return pcg_scale(out, n, scale, S, st);
+  };
+  if ((e = cudaMemcpyAsync(b, f0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((rc = smg_project_mean(b, n, red, stream))) return rc;
+  if ((e = cudaMemsetAsync(S, 0, sizeof(double) * 16, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((e = cudaMemsetAsync(u0, 0, sizeof(double) * n, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((e = cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((rc = ccg_dot(b, b, n, S + 0, nullptr, red, st))) return rc;
+  if ((rc = precond(r, z))) return rc;
+  if ((e = cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((rc = ccg_dot(r, z, n, S + 2, nullptr, red, st))) return rc;
+  double hs[8];
+  if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 8, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_pcg");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_pcg");
+  if (hs[0] == 0.0) { *iters_out = 0; return SMG_OK; }
+  int it = 0;
+  const int chunk = 16;
+  while (it < max_iter) {
+    const int stop = it + chunk < max_iter ? it + chunk : max_iter;
+    for (; it < stop; ++it) {
+      const int ro = 2 + (it & 1), rn = 3 - (it & 1);
+      if ((rc = smg_op_residual(op, p, nullptr, q, stream))) return rc;
+      if ((rc = ccg_dot(p, q, n, S + 1, S, red, st))) return rc;
+      if ((rc = pcg_update(u0, r, p, q, n, S, ro, tol, it + 1, red, st))) return rc;
+      if ((rc = precond(r, z))) return rc;
+      if ((rc = ccg_dot(r, z, n, S + rn, S, red, st))) return rc;
+      if ((rc = ccg_direction(p, z, n, S, ro, rn, st))) return rc;
+    }
+    if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 8, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_pcg");
+    if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_pcg");
+    if (hs[4] != 0.0) break;
+  }
+  const bool ok = hs[4] != 0.0;
+  *iters_out = ok ? (int)hs[5] : -max_iter;
   return smg_project_mean(u0, n, red, stream);
 }
 

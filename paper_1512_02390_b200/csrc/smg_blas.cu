@@ -372,6 +372,49 @@ int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double*
   pinv_rows_kernel<false><<<grid, 256, 0, st>>>(nx, ny, Qx, Qy, Lp, tmp, u);
   return check_launch("pinv_rows_kernel");
 }
+
+// ---- preconditioned CG of the variable-coefficient coarse level -------------
+// S[0] = ||b||^2, S[1] = p.q, S[2]/S[3] = r.z (ping-pong), S[4] = done,
+// S[5] = iterations, S[6] = ||r||^2
+__global__ void __launch_bounds__(kReduceThreads)
+pcg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                  const double* __restrict__ q, int64_t n, double* S, int ro, double tol, int it, double* ws) {
+  __shared__ double red[32];
+  if (S[4] != 0.0) return;
+  const double alpha = S[ro] / S[1];
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    r[i] = ri;
+    v[0] = fma(ri, ri, v[0]);
+  }
+  publish<1>(v, ws, red);
+  if (!last_block_arrive(ws)) return;
+  finish<1>(v, ws, red);
+  if (threadIdx.x == 0) {
+    S[6] = v[0];
+    if (sqrt(v[0]) <= tol * sqrt(S[0])) { S[4] = 1.0; S[5] = (double)it; }
+  }
+  reset_counter(ws);
+}
+
+// z = scale * z (preconditioner scaling), skipped once converged
+__global__ void pcg_scale_kernel(double* __restrict__ z, int64_t n, double scale, const double* S) {
+  if (S[4] != 0.0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] *= scale;
+}
+
+int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
+               int it, double* ws, cudaStream_t st) {
+  pcg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, r, p, q, n, S, ro, tol, it, ws);
+  return check_launch("pcg_update_kernel");
+}
+int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st) {
+  pcg_scale_kernel<<<grid_for(n), kReduceThreads, 0, st>>>(z, n, scale, S);
+  return check_launch("pcg_scale_kernel");
+}
 }  // namespace smg
 
 using namespace smg;

@@ -317,3 +317,28 @@ def test_c5_reduced_mgcg(cuda_device):
     assert rep.converged and not rep.breakdown
     _check_history(rep.residuals, g["c5r_mgcg_res"], "c5r")
     assert maxrel(host(u)[::24, ::24], g["c5r_mgcg_sample"]) < 1e-6
+
+
+def test_diffusion_coarse_pcg_vs_reference(cuda_device):
+    """Fast coarse mode for variable nu: preconditioned CG reaches the
+    reference CG's answer to within its own 1e-12 tolerance (x condition)."""
+    g = golden("multigrid")
+    mesh = P.MeshConfig(8, 8, 1.0, 1.0)
+    h = P.build_hierarchy(mesh, 2, P.OverlapRule("fixed", 1), nu_hat=0.9, coarse="pcg")
+    got = host(P.coarse_solve(h, g["cs3_f0"]))
+    assert maxrel(got, g["cs3_u0"]) < 1e-9
+    assert h.coarse_iterations[-1] < 100
+
+
+def test_c5_reduced_mgcg_fast_coarse(cuda_device):
+    """Reduced C5 with the default (PCG) coarse solver: same history within tolerance."""
+    g = golden("xlarge_c5r")
+    mesh = P.MeshConfig(64, 64, 1.0, 1.0)
+    h = P.build_hierarchy(mesh, 24, P.OverlapRule("fixed", 1), orders=(1, 3, 6, 12, 24), nu_hat=0.9,
+                          nu_shift=0.0)
+    assert h.coarse == "pcg"
+    f = O.project_mean(np.random.default_rng(0).standard_normal((1536, 1536)))
+    u, rep = P.solve(h, f, P.SolveConfig(solver="mgcg"), u0=np.zeros_like(f))
+    assert rep.converged and not rep.breakdown
+    _check_history(rep.residuals, g["c5r_mgcg_res"], "c5r-pcg")
+    assert max(h.coarse_iterations) < 120
