@@ -11,8 +11,9 @@ work: the top level applies A to a nonzero u).
 
 Timing: CUDA events on the launching stream around each step, L2 flushed
 (256 MiB write) before every timed step, K steps bracketed by barrier +
-synchronize, max over ranks.  N > 1: one process per GPU, each running an
-independent replica (scaling "weak"; strip decomposition is not built yet).
+synchronize, max over ranks.  N > 1: one process per GPU; the same C2 problem
+is split into element-row strips (paper_1512_02390_b200/strips.py) with NCCL
+halo exchanges and a replicated coarse solve ("scaling": "strong").
 """
 
 from __future__ import annotations
@@ -176,6 +177,93 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_strips(args, world, rank, local, dev):
+    """N > 1: the C2 V-cycle strong-scaled over element-row strips (strips.py),
+    halos by NCCL send/recv, replicated coarse solve (all-gather)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200 import _native as NV
+    from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, TorchTransport
+
+    lib = NV.lib()
+    c = CFG
+    plan = StripPlan(c["n_x"], c["n_y"], c["l_x"], c["l_y"], world, rank)
+    rule = P.OverlapRule.parse(c["rule"])
+    eng = GpuEngine(plan, c["p"], rule)
+    sol = StripSolver(plan, eng, TorchTransport(plan))
+    p = c["p"]
+    N = (p * c["n_y"], p * c["n_x"])
+    ndof = N[0] * N[1]
+    f_host = P.project_mean(np.random.default_rng(c["seed"]).standard_normal(N))
+    rows = plan.global_rows(p)
+    own = plan.own(p)
+    f = torch.from_numpy(f_host[rows].copy()).to(dev)
+    u = torch.zeros_like(f)
+    sol.v_cycle(u, f)
+    torch.cuda.synchronize()
+    n0 = lib.smg_launch_count()
+    sol.v_cycle(u, f)
+    torch.cuda.synchronize()
+    launches_per_step = lib.smg_launch_count() - n0
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        sol.v_cycle(u, f)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t_steps = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sol.v_cycle(u, f)
+        b.record()
+        torch.cuda.synchronize()
+        t_steps += a.elapsed_time(b) / 1e3
+    dist.barrier()
+    clocks = sampler.stop()
+    tt = torch.tensor([t_steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_steps = float(tt.item())
+    # end to end: own rows of f from pinned host, own rows of u back
+    f_pin = torch.from_numpy(f_host[rows].copy()).pin_memory()
+    u_pin = torch.empty(f.shape, dtype=torch.float64).pin_memory()
+    dist.barrier()
+    t_e2e = 0.0
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        f.copy_(f_pin, non_blocking=True)
+        sol.v_cycle(u, f)
+        u_pin[own].copy_(u[own], non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        t_e2e += a.elapsed_time(b) / 1e3
+    tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_e2e = float(tt.item())
+    if rank == 0:
+        own_bytes = 8 * (own.stop - own.start) * N[1]
+        line = {"metric": METRIC, "value": ndof * args.steps / t_steps, "unit": "DOF/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_steps / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded N(0,1) RHS, mean removed)",
+                "config": {"workload": "C2: periodic Poisson [0,1]^2, 64x64 elements, p=16 (1,048,576 DOF), "
+                                       "stand-alone V-cycle (1,0), w5, fixed:1, coarse p=1 pseudo-inverse",
+                           "global_dofs": ndof, "parallelism": f"{world} element-row strips "
+                           f"({plan.s} rows + 2x{2} ghost rows each), NCCL halo send/recv, replicated coarse",
+                           "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": False},
+                "e2e": {"value": ndof * args.steps / t_e2e, "unit": "DOF/s",
+                        "h2d_bytes_per_step": 8 * f.numel() * world, "d2h_bytes_per_step": own_bytes * world},
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,8 +288,14 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
+        ngpu = torch.cuda.device_count()
+        local = local % max(ngpu, 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SMG_DIST_BACKEND", "nccl" if ngpu >= world else "gloo")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # more ranks than GPUs (testing only): gloo, host-staged halos
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -210,6 +304,8 @@ def main():
     from paper_1512_02390_b200.multigrid import _v_cycle
 
     lib = NV.lib()
+    if world > 1:
+        return run_strips(args, world, rank, local, dev)
     c = CFG
     mesh = P.MeshConfig(c["n_x"], c["n_y"], c["l_x"], c["l_y"])
     rule = P.OverlapRule.parse(c["rule"])

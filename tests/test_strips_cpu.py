@@ -1,0 +1,158 @@
+"""World-size-2 (and 3) CPU tests of the strip decomposition (strips.py) over
+torch.distributed/gloo, with the CPU oracle as the per-rank engine: the
+assembled strip V-cycle and solver histories must match the global oracle."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import smg_oracle as O
+from paper_1512_02390_b200.strips import G, StripPlan, StripSolver, TorchTransport
+
+
+class OracleEngine:
+    """Engine interface of StripSolver implemented with the numpy oracle on
+    the rank's local periodic mesh (torch CPU tensors at the boundary)."""
+
+    def __init__(self, plan, p, rule="fixed:1", nu_hat=None):
+        self.plan = plan
+        nx, nyl, lx, lyl = plan.local_mesh_args()
+        self.h = O.Hierarchy(nx, nyl, lx, lyl, p, rule=rule, nu_hat=None)
+        self.hg = O.Hierarchy(plan.n_x, plan.n_y, plan.l_x, plan.l_y, 2, rule=rule)
+        self.orders = [lv.p for lv in self.h.levels]
+        self.n_pre = [lv.n_pre for lv in self.h.levels]
+        self.n_post = [lv.n_post for lv in self.h.levels]
+        self.us = [self.zeros(l) for l in range(len(self.orders))]
+        self.fs = [self.zeros(l) for l in range(len(self.orders))]
+        self._work = [self.zeros(l) for l in range(len(self.orders))]
+
+    def zeros(self, l):
+        return torch.zeros(self.h.levels[l].op.shape, dtype=torch.float64)
+
+    def work(self, l):
+        return self._work[l]
+
+    def clone(self, a):
+        return a.clone()
+
+    def copy(self, dst, src):
+        dst.copy_(torch.as_tensor(src))
+
+    def fill_zero(self, a):
+        a.zero_()
+
+    def residual(self, l, u, f, out):
+        Au = self.h.levels[l].op.apply(u.numpy())
+        out.copy_(torch.from_numpy(Au if f is None else f.numpy() - Au))
+
+    def correct(self, l, r, u, zero):
+        c = torch.from_numpy(self.h.levels[l].sm.correction(r.numpy()))
+        if zero:
+            u.copy_(c)
+        else:
+            u.add_(c)
+
+    def restrict(self, l, fine, out):
+        out.copy_(torch.from_numpy(O.restrict(self.h, l, fine.numpy())))
+
+    def prolong_add(self, l, coarse, fine):
+        fine.add_(torch.from_numpy(O.prolongate(self.h, l, coarse.numpy())))
+
+    def full_zeros0(self):
+        return torch.zeros((self.plan.n_y, self.plan.n_x), dtype=torch.float64)
+
+    def coarse_full(self, f0):
+        return torch.from_numpy(O.coarse_solve(self.hg, f0.numpy()))
+
+    def local_dot(self, a, b):
+        return float(torch.sum(a * b))
+
+    def axpy(self, alpha, x, y):
+        y.add_(x, alpha=alpha)
+
+    def xpby(self, x, beta, y):
+        y.mul_(beta).add_(x)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+CASE = dict(n_x=6, n_y=8, l_x=1.5, l_y=1.0, p=8)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = CASE
+        plan = StripPlan(c["n_x"], c["n_y"], c["l_x"], c["l_y"], world, rank)
+        eng = OracleEngine(plan, c["p"])
+        sol = StripSolver(plan, eng, TorchTransport(plan))
+        N = (c["p"] * c["n_y"], c["p"] * c["n_x"])
+        f = O.project_mean(np.random.default_rng(3).standard_normal(N))
+        u0 = np.random.default_rng(4).random(N)
+        rows = plan.global_rows(c["p"])
+        own = plan.own(c["p"])
+        # one V-cycle from a nonzero start
+        u = torch.from_numpy(u0[rows].copy())
+        fl = torch.from_numpy(f[rows].copy())
+        sol.v_cycle(u, fl)
+        vc_own = u[own].numpy().copy()
+        # MG and MGCG histories from zero
+        _, rep_mg = sol.solve_mg(torch.from_numpy(f[rows].copy()), torch.zeros_like(u))
+        u_cg, rep_cg = sol.solve_mgcg(torch.from_numpy(f[rows].copy()), torch.zeros_like(u))
+        q.put((rank, vc_own, rep_mg.residuals, rep_cg.residuals, u_cg[own].numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_strip_decomposition_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    c = CASE
+    h = O.Hierarchy(c["n_x"], c["n_y"], c["l_x"], c["l_y"], c["p"])
+    N = (c["p"] * c["n_y"], c["p"] * c["n_x"])
+    f = O.project_mean(np.random.default_rng(3).standard_normal(N))
+    u0 = np.random.default_rng(4).random(N)
+    want = O.v_cycle(h, u0.copy(), f)
+    got = np.concatenate([t[1] for t in out], 0)
+    assert np.abs(got - want).max() / np.abs(want).max() < 1e-11
+    _, res_mg, _ = O.solve_mg(h, f, u0=np.zeros_like(f))
+    _, res_cg, _, _ = O.solve_mgcg(h, f, u0=np.zeros_like(f))
+    for t in out:  # every rank reports the same (allreduced) history
+        assert len(t[2]) == len(res_mg) and np.allclose(t[2], res_mg, rtol=1e-9)
+        assert len(t[3]) == len(res_cg) and np.allclose(t[3], res_cg, rtol=1e-8)
+
+
+def test_strip_plan_geometry():
+    pl = StripPlan(4, 8, 2.0, 2.0, 4, 1)
+    assert pl.s == 2 and pl.ey0 == 2 and pl.local_ny == 2 + 2 * G
+    rows = pl.global_rows(4)
+    assert rows[0] == (2 - G) * 4 and len(rows) == 4 * pl.local_ny
+    own = pl.own(4)
+    assert list(rows[own]) == list(range(8, 16))
+    with pytest.raises(ValueError):
+        StripPlan(4, 6, 2.0, 2.0, 4, 0)
+    assert StripPlan(4, 8, 2.0, 2.0, 4, 0).below() == 3
