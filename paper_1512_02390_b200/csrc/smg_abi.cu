@@ -11,7 +11,7 @@
 
 #include "smg_common.cuh"
 #include "smg_fd.cuh"
-#include "smg_fdt.cuh"
+#include "smg_fdm.cuh"
 #include "smg_op.cuh"
 #include "smg_transfer.cuh"
 
@@ -77,6 +77,10 @@ struct smg_schwarz {
   double* dinv_perm;
   double* ws;
   unsigned int* ctr;
+  double* Sx_dev;
+  double* Sy_dev;
+  double* frag_dev;
+  bool dmma;
 };
 
 struct smg_transfer {
@@ -93,6 +97,12 @@ struct smg_coarse {
 };
 
 namespace {
+
+// Measured per-m choice of the contraction engine (profiles/: DMMA vs DFMA).
+bool fd_prefers_dmma(int m) {
+  (void)m;
+  return false;
+}
 
 // Split S (m x m, row-major S[k][i]) into symmetrized even/odd halves.
 // Returns false if some eigenvector is not (numerically) even or odd.
@@ -272,9 +282,19 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   std::vector<int> px, py;
   const char* force = getenv("SMG_FD_DENSE");
   s->fdt = nullptr;
-  if (!(force && force[0] == '1') &&
-      (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY)) != nullptr &&
-      even_odd_split(S_x, m, s->Sxe, s->Sxo, px) && even_odd_split(S_y, m, s->Sye, s->Syo, py)) {
+  s->Sx_dev = s->Sy_dev = s->frag_dev = nullptr;
+  // contraction engine: FP64 tensor cores (DMMA) or CUDA-core DFMA even/odd;
+  // SMG_FD_ENGINE=dmma|dfma overrides the per-m default
+  const char* eng = getenv("SMG_FD_ENGINE");
+  s->dmma = eng ? (std::strcmp(eng, "dmma") == 0) : fd_prefers_dmma(m);
+  const bool eo_ok = s->dmma || (even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
+                                 even_odd_split(S_y, m, s->Sye, s->Syo, py));
+  if (s->dmma) {
+    px.resize(m); py.resize(m);
+    for (int i = 0; i < m; ++i) px[i] = py[i] = i;
+  }
+  if (!(force && force[0] == '1') && eo_ok &&
+      (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY, s->dmma)) != nullptr) {
     s->ntx = n_x / s->TX; s->nty = n_y / s->TY;
     const int nt = s->ntx * s->nty;
     const size_t RX = (size_t)s->TX * p + 2 * n_o + 1, RY = (size_t)s->TY * p + 2 * n_o + 1;
@@ -286,6 +306,16 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
     if (e == cudaSuccess) e = cudaMalloc(&s->ws, sizeof(double) * nt * RX * RY);
     if (e == cudaSuccess) e = cudaMalloc(&s->ctr, sizeof(unsigned int) * 3 * nt);
     if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, sizeof(unsigned int) * 3 * nt);
+    if (e == cudaSuccess) e = cudaMalloc(&s->Sx_dev, sizeof(double) * m * m);
+    if (e == cudaSuccess) e = cudaMalloc(&s->Sy_dev, sizeof(double) * m * m);
+    if (e == cudaSuccess) e = cudaMemcpy(s->Sx_dev, S_x, sizeof(double) * m * m, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(s->Sy_dev, S_y, sizeof(double) * m * m, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      std::vector<double> fr;
+      fdm_fragments(m, S_x, S_y, fr);
+      e = cudaMalloc(&s->frag_dev, sizeof(double) * fr.size());
+      if (e == cudaSuccess) e = cudaMemcpy(s->frag_dev, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) { smg_schwarz_destroy(s); return cuda_fail(e, "smg_schwarz_create (tiles)"); }
     s->tiled = true;
   }
@@ -299,6 +329,9 @@ int smg_schwarz_destroy(smg_schwarz_t* h) {
   if (h->dinv_perm) cudaFree(h->dinv_perm);
   if (h->ws) cudaFree(h->ws);
   if (h->ctr) cudaFree(h->ctr);
+  if (h->Sx_dev) cudaFree(h->Sx_dev);
+  if (h->Sy_dev) cudaFree(h->Sy_dev);
+  if (h->frag_dev) cudaFree(h->frag_dev);
   delete h;
   return SMG_OK;
 }
@@ -316,7 +349,8 @@ static FDLaunch fd_base(const smg_schwarz_t* h) {
 static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, int u_zero, void* stream) {
   if (h->tiled) {
     FDTLaunch T;
-    T.r = r; T.u = u; T.u_zero = u_zero; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
+    T.r = r; T.u = u; T.u_zero = u_zero;
+    T.dinv_dense = h->dinv; T.Sx_dev = h->Sx_dev; T.Sy_dev = h->Sy_dev; T.frag_dev = h->frag_dev; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
     T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
     T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
     T.wx = h->wx.data(); T.wy = h->wy.data();

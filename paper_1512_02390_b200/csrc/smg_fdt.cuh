@@ -119,11 +119,11 @@ __device__ __forceinline__ void half_synth(const double* __restrict__ ST, const 
     for (int k = 0; k < H; ++k) acc[k] = fma(ST[i * H + k], t[i], acc[k]);
 }
 
-template <int P, int NO, int TX, int TY>
+template <int P, int NO, int TX, int TY, int NT>
 __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const double* __restrict__ u, int N_x,
                                              int N_y, int ntx, int tile, double* buf, bool u_zero) {
   using G = FDTGeom<P, NO, TX, TY>;
-  constexpr int RX = G::RX, RY = G::RY, OX = G::OX, OY = G::OY, NT = G::NT;
+  constexpr int RX = G::RX, RY = G::RY, OX = G::OX, OY = G::OY;
   const int tx = tile % ntx, ty = tile / ntx;
   const int X0 = tx * OX, Y0 = ty * OY;
   for (int idx = threadIdx.x; idx < RX * RY; idx += NT) {
@@ -163,14 +163,14 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 
   int tile = blockIdx.x;
-  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, tile, sm, A.u_zero != 0);
+  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY, NT>(A.r, A.u, N_x, N_y, ntx, tile, sm, A.u_zero != 0);
   cp_async_commit();
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     double* R = sm + (it & 1) * STAGE;  // residual region, then accumulated correction
     double* UO = R + RX * RY;           // own u
     {
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE, A.u_zero != 0);
+      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY, NT>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE, A.u_zero != 0);
       cp_async_commit();
     }
     const int tx = tile % ntx, ty = tile / ntx;
@@ -399,7 +399,11 @@ struct FDTLaunch {
   double* u;
   int u_zero;
   const double* inv_nu;
-  const double* dinv;
+  const double* dinv;        // permuted (even/odd) 1/(lam_y + lam_x)
+  const double* dinv_dense;  // natural order (DMMA variant)
+  const double* Sx_dev;      // device factors (DMMA variant)
+  const double* Sy_dev;
+  const double* frag_dev;    // lane-ordered DMMA fragments (fdm_fragments)
   double* ws;
   unsigned int* ctr;
   int N_x, N_y, n_x, ntx, nty;
@@ -461,6 +465,7 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
 
 using FDTLaunchFn = int (*)(const FDTLaunch&, cudaStream_t);
 // Tiled kernel for (p, n_o) on an n_x x n_y mesh, or nullptr; sets TX, TY.
-FDTLaunchFn fdt_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY);
+// dmma selects the FP64 tensor-core variant (smg_fdm.cuh) of the same tiling.
+FDTLaunchFn fdt_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY, bool dmma);
 
 }  // namespace smg
