@@ -30,12 +30,8 @@ struct FDMGeom {
   static constexpr int MT = (M + 7) / 8;     // 8-row tiles of the factor dimension
   static constexpr int KT = (M + 3) / 4;     // 4-deep k steps
   static constexpr int NL = E * M;           // lines (element, row or column) in a tile
-  // each warp owns EPW whole elements through all four contractions
-  static constexpr int WARPS = E >= 8 ? 4 : (E >= 4 ? 4 : E);
-  static constexpr int EPW = (E + WARPS - 1) / WARPS;
-  static constexpr int NLW = EPW * M;        // lines per warp
-  static constexpr int BT = (NLW + 7) / 8;   // 8-line batch tiles per warp
-  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int BT = (NL + 7) / 8;    // 8-line batch tiles
+  static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int NFRAG = MT * KT;      // factor fragments per stage and lane
   static constexpr size_t SMEM = T::SMEM + sizeof(double) * 4 * NFRAG * 32;
 };
@@ -58,7 +54,7 @@ __global__ void __launch_bounds__(FDMGeom<P, NO, TX, TY>::THREADS, 2)
 fdm_kernel(const __grid_constant__ FDMArgs A) {
   using G = FDMGeom<P, NO, TX, TY>;
   using GT = FDTGeom<P, NO, TX, TY>;
-  constexpr int M = G::M, MM = G::MM, MT = G::MT, KT = G::KT, NL = G::NL, BT = G::BT, EPW = G::EPW;
+  constexpr int M = G::M, MM = G::MM, MT = G::MT, KT = G::KT, NL = G::NL, BT = G::BT;
   constexpr int OX = GT::OX, OY = GT::OY, RX = GT::RX, RY = GT::RY, BW = GT::BW, STAGE = GT::STAGE;
   constexpr int NT = G::THREADS, WARPS = G::WARPS, E = G::E;
   extern __shared__ double sm[];
@@ -87,12 +83,6 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
     cp_async_wait<1>();
     __syncthreads();
 
-    // The warp's elements e = warp*EPW .. warp*EPW+EPW-1; local line n in [0, NLW)
-    // maps to (e = e0 + n / M, line n % M).  Stages touch only the warp's own
-    // element buffers, so they are separated by __syncwarp, not block barriers.
-    const int e0 = warp * EPW;
-    const int nel = (E - e0) < EPW ? (E - e0) : EPW;  // elements this warp really owns
-    const int nlw = nel > 0 ? nel * M : 0;
     // ---- stage 1: T1[i][(e,c)] = sum_k S_y[k][i] R_e[k][c]   (batch along N)
     {
       double a[MT][KT];
@@ -100,11 +90,10 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) a[mt][kt] = FR[(0 * NFRAG + mt * KT + kt) * 32 + lane];
-#pragma unroll 1
-      for (int bt = 0; bt < BT; ++bt) {
+      for (int bt = warp; bt < BT; bt += WARPS) {
         const int n = 8 * bt + g;
-        const bool vn = n < nlw;
-        const int e = e0 + (vn ? n / M : 0), c = vn ? n % M : 0;
+        const bool vn = n < NL;
+        const int e = vn ? n / M : 0, c = vn ? n - e * M : 0;
         const double* col = R + ((e / TX) * P) * RX + (e % TX) * P + c;
         double acc[MT][2];
 #pragma unroll
@@ -119,8 +108,8 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int n2 = 8 * bt + 2 * t + j;
-          if (n2 < nlw) {
-            const int e2 = e0 + n2 / M, c2 = n2 % M;
+          if (n2 < NL) {
+            const int e2 = n2 / M, c2 = n2 - e2 * M;
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               const int i = 8 * mt + g;
@@ -130,7 +119,8 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
         }
       }
     }
-    __syncwarp();
+    __syncthreads();
+    for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
 
     // ---- stage 2: T2[(e,i)][l] = (sum_j T1[e][i][j] S_x[j][l]) / (lam_y+lam_x) / nu_bar
     {
@@ -139,11 +129,10 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
       for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
         for (int nt = 0; nt < MT; ++nt) b[kt][nt] = FR[(1 * NFRAG + nt * KT + kt) * 32 + lane];
-#pragma unroll 1
-      for (int bt = 0; bt < BT; ++bt) {
+      for (int bt = warp; bt < BT; bt += WARPS) {
         const int m = 8 * bt + g;
-        const bool vm = m < nlw;
-        const double* row = EB + (e0 * M + (vm ? m : 0)) * M;   // rows (e,i) contiguous
+        const bool vm = m < NL;
+        const double* row = EB + (vm ? m : 0) * M;  // rows (e,i) are contiguous
         double acc[MT][2];
 #pragma unroll
         for (int nt = 0; nt < MT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
@@ -156,22 +145,21 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
         }
         __syncwarp();
         if (vm) {
-          const int e2 = e0 + m / M, i2 = m % M;
+          const int e2 = m / M, i2 = m - e2 * M;
           double s = 1.0;
           if (A.inv_nu != nullptr)
             s = __ldg(A.inv_nu + (size_t)(ty * TY + e2 / TX) * A.n_x + (tx * TX + e2 % TX));
-          double* orow = EB + (e0 * M + m) * M;
 #pragma unroll
           for (int nt = 0; nt < MT; ++nt)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int l = 8 * nt + 2 * t + j;
-              if (l < M) orow[l] = acc[nt][j] * (__ldg(A.dinv + i2 * M + l) * s);
+              if (l < M) EB[m * M + l] = acc[nt][j] * (__ldg(A.dinv + i2 * M + l) * s);
             }
         }
-        __syncwarp();
       }
     }
+    __syncthreads();
 
     // ---- stage 3: T3[k][(e,l)] = sum_i S_y[k][i] T2[e][i][l]   (batch along N)
     {
@@ -180,11 +168,10 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) a[mt][kt] = FR[(2 * NFRAG + mt * KT + kt) * 32 + lane];
-#pragma unroll 1
-      for (int bt = 0; bt < BT; ++bt) {
+      for (int bt = warp; bt < BT; bt += WARPS) {
         const int n = 8 * bt + g;
-        const bool vn = n < nlw;
-        const int e = e0 + (vn ? n / M : 0), l = vn ? n % M : 0;
+        const bool vn = n < NL;
+        const int e = vn ? n / M : 0, l = vn ? n - e * M : 0;
         const double* col = EB + e * MM + l;
         double acc[MT][2];
 #pragma unroll
@@ -200,8 +187,8 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int n2 = 8 * bt + 2 * t + j;
-          if (n2 < nlw) {
-            const int e2 = e0 + n2 / M, l2 = n2 % M;
+          if (n2 < NL) {
+            const int e2 = n2 / M, l2 = n2 - e2 * M;
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               const int k = 8 * mt + g;
@@ -209,9 +196,9 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
             }
           }
         }
-        __syncwarp();
       }
     }
+    __syncthreads();
 
     // ---- stage 4: out[(e,k)][j] = W[k][j] sum_l T3[e][k][l] S_x[j][l]   (batch along M)
     {
@@ -220,11 +207,10 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
       for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
         for (int nt = 0; nt < MT; ++nt) b[kt][nt] = FR[(3 * NFRAG + nt * KT + kt) * 32 + lane];
-#pragma unroll 1
-      for (int bt = 0; bt < BT; ++bt) {
+      for (int bt = warp; bt < BT; bt += WARPS) {
         const int m = 8 * bt + g;
-        const bool vm = m < nlw;
-        const double* row = EB + (e0 * M + (vm ? m : 0)) * M;
+        const bool vm = m < NL;
+        const double* row = EB + (vm ? m : 0) * M;
         double acc[MT][2];
 #pragma unroll
         for (int nt = 0; nt < MT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
@@ -238,20 +224,16 @@ fdm_kernel(const __grid_constant__ FDMArgs A) {
         __syncwarp();
         if (vm) {
           const double wyk = A.wy[m % M];
-          double* orow = EB + (e0 * M + m) * M;
 #pragma unroll
           for (int nt = 0; nt < MT; ++nt)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int jj = 8 * nt + 2 * t + j;
-              if (jj < M) orow[jj] = acc[nt][j] * (wyk * A.wx[jj]);
+              if (jj < M) EB[m * M + jj] = acc[nt][j] * (wyk * A.wx[jj]);
             }
         }
-        __syncwarp();
       }
     }
-    __syncthreads();
-    for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
     __syncthreads();
 
     // ---- accumulate element windows into the region, colour passes ---------
