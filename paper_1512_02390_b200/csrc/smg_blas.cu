@@ -64,6 +64,7 @@ __device__ __forceinline__ void publish(double (&v)[NV], double* ws, double* red
 __global__ void __launch_bounds__(kReduceThreads)
 dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* out,
            double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   double v[1] = {0.0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -77,6 +78,7 @@ dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n
 
 __global__ void __launch_bounds__(kReduceThreads)
 sum_kernel(const double* __restrict__ x, int64_t n, double* out, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   double v[1] = {0.0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -93,6 +95,7 @@ sum_kernel(const double* __restrict__ x, int64_t n, double* out, double* ws) {
 __global__ void __launch_bounds__(kReduceThreads)
 dot2_kernel(const double* __restrict__ z, const double* __restrict__ r, const double* __restrict__ ro,
             int64_t n, double* out, double* scal, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[64];
   double v[2] = {0.0, 0.0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -114,6 +117,7 @@ dot2_kernel(const double* __restrict__ z, const double* __restrict__ r, const do
 __global__ void __launch_bounds__(kReduceThreads)
 cg_update_kernel(double* __restrict__ u, const double* r_in, double* r_out, const double* __restrict__ p,
                  const double* __restrict__ q, int64_t n, double* scal, int* flag, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   const double pq = scal[1];
   if (!(pq > 0.0)) {
@@ -137,17 +141,20 @@ cg_update_kernel(double* __restrict__ u, const double* r_in, double* r_out, cons
 
 __global__ void cg_direction_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
                                     const double* scal) {
+  SMG_PDL_ENTRY();
   const double beta = scal[5];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
 
 __global__ void axpby_kernel(double a, const double* __restrict__ x, double b, double* __restrict__ y, int64_t n) {
+  SMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
 }
 
 __global__ void sub_mean_kernel(double* __restrict__ f, int64_t n, const double* sum) {
+  SMG_PDL_ENTRY();
   const double mean = sum[0] / (double)n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     f[i] -= mean;
@@ -155,6 +162,7 @@ __global__ void sub_mean_kernel(double* __restrict__ f, int64_t n, const double*
 
 // Final sum of op_kernel per-CTA partials (fixed order).
 __global__ void __launch_bounds__(kReduceThreads) sum_partials_kernel(const double* __restrict__ part, int nb, double* out) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   double v[1] = {0.0};
   for (int b = threadIdx.x; b < nb; b += blockDim.x) v[0] += part[b];
@@ -171,6 +179,7 @@ __global__ void __launch_bounds__(256)
 gemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda, int tA,
             const double* __restrict__ B, int ldb, int tB, double* __restrict__ C, int ldc,
             const double* __restrict__ S) {
+  SMG_PDL_ENTRY();
   __shared__ double As[16][64 + 1];
   __shared__ double Bs[64][16 + 1];
   const int tid = threadIdx.x;
@@ -205,7 +214,7 @@ gemm_kernel(int M, int N, int K, const double* __restrict__ A, int lda, int tA,
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
          double* C, int ldc, const double* S, cudaStream_t st) {
   dim3 grid((N + 15) / 16, (M + 15) / 16);
-  gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, A, lda, tA, B, ldb, tB, C, ldc, S);
+  launch(gemm_kernel, dim3(grid), dim3(256), 0, st, M, N, K, A, lda, tA, B, ldb, tB, C, ldc, S);
   return check_launch("gemm_kernel");
 }
 
@@ -215,6 +224,7 @@ __global__ void __launch_bounds__(kReduceThreads)
 ccg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                   const double* __restrict__ q, int64_t n, double* S, int ro, int rn, double tol,
                   int it, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   if (S[4] != 0.0) return;
   const double alpha = S[ro] / S[1];
@@ -237,6 +247,7 @@ ccg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* 
 
 __global__ void ccg_direction_kernel(double* __restrict__ p, const double* __restrict__ r, int64_t n,
                                      const double* S, int ro, int rn) {
+  SMG_PDL_ENTRY();
   if (S[4] != 0.0) return;
   const double beta = S[rn] / S[ro];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -245,6 +256,7 @@ __global__ void ccg_direction_kernel(double* __restrict__ p, const double* __res
 
 __global__ void ccg_dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                                double* out, const double* S, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   if (S != nullptr && S[4] != 0.0) return;
   double v[1] = {0.0};
@@ -259,15 +271,15 @@ __global__ void ccg_dot_kernel(const double* __restrict__ x, const double* __res
 
 int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro,
                int rn, double tol, int it, double* ws, cudaStream_t st) {
-  ccg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, r, p, q, n, S, ro, rn, tol, it, ws);
+  launch(ccg_update_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, st, x, r, p, q, n, S, ro, rn, tol, it, ws);
   return check_launch("ccg_update_kernel");
 }
 int ccg_direction(double* p, const double* r, int64_t n, const double* S, int ro, int rn, cudaStream_t st) {
-  ccg_direction_kernel<<<grid_for(n), kReduceThreads, 0, st>>>(p, r, n, S, ro, rn);
+  launch(ccg_direction_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, st, p, r, n, S, ro, rn);
   return check_launch("ccg_direction_kernel");
 }
 int ccg_dot(const double* x, const double* y, int64_t n, double* out, const double* S, double* ws, cudaStream_t st) {
-  ccg_dot_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, y, n, out, S, ws);
+  launch(ccg_dot_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, st, x, y, n, out, S, ws);
   return check_launch("ccg_dot_kernel");
 }
 
@@ -286,6 +298,7 @@ template <bool FIRST>
 __global__ void __launch_bounds__(256) pinv_rows_kernel(int nx, int ny, const double* __restrict__ Qx,
                                                         const double* __restrict__ Qy, const double* __restrict__ Lp,
                                                         const double* __restrict__ in, double* __restrict__ out) {
+  SMG_PDL_ENTRY();
   constexpr int KC = 32;
   __shared__ double T[kRB][kPinvMax];
   __shared__ double Xs[KC][kPinvMax + 1];
@@ -366,10 +379,10 @@ int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double*
                double* tmp, double* u, cudaStream_t st) {
   if (nx > kPinvMax || ny > kPinvMax) return 1;
   const int grid = (ny + kRB - 1) / kRB;
-  pinv_rows_kernel<true><<<grid, 256, 0, st>>>(nx, ny, Qx, Qy, Lp, f, tmp);
+  launch(pinv_rows_kernel<true>, dim3(grid), dim3(256), 0, st, nx, ny, Qx, Qy, Lp, f, tmp);
   int rc = check_launch("pinv_rows_kernel");
   if (rc) return rc;
-  pinv_rows_kernel<false><<<grid, 256, 0, st>>>(nx, ny, Qx, Qy, Lp, tmp, u);
+  launch(pinv_rows_kernel<false>, dim3(grid), dim3(256), 0, st, nx, ny, Qx, Qy, Lp, tmp, u);
   return check_launch("pinv_rows_kernel");
 }
 
@@ -379,6 +392,7 @@ int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double*
 __global__ void __launch_bounds__(kReduceThreads)
 pcg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                   const double* __restrict__ q, int64_t n, double* S, int ro, double tol, int it, double* ws) {
+  SMG_PDL_ENTRY();
   __shared__ double red[32];
   if (S[4] != 0.0) return;
   const double alpha = S[ro] / S[1];
@@ -401,6 +415,7 @@ pcg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* 
 
 // z = scale * z (preconditioner scaling), skipped once converged
 __global__ void pcg_scale_kernel(double* __restrict__ z, int64_t n, double scale, const double* S) {
+  SMG_PDL_ENTRY();
   if (S[4] != 0.0) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     z[i] *= scale;
@@ -408,11 +423,11 @@ __global__ void pcg_scale_kernel(double* __restrict__ z, int64_t n, double scale
 
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st) {
-  pcg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, st>>>(x, r, p, q, n, S, ro, tol, it, ws);
+  launch(pcg_update_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, st, x, r, p, q, n, S, ro, tol, it, ws);
   return check_launch("pcg_update_kernel");
 }
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st) {
-  pcg_scale_kernel<<<grid_for(n), kReduceThreads, 0, st>>>(z, n, scale, S);
+  launch(pcg_scale_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, st, z, n, scale, S);
   return check_launch("pcg_scale_kernel");
 }
 }  // namespace smg
@@ -425,33 +440,33 @@ size_t smg_reduce_ws_doubles(void) { return (size_t)kReduceBlocks * kPartStride 
 
 int smg_dot(const double* x, const double* y, int64_t n, double* out, double* ws, void* stream) {
   if (!x || !y || !out || !ws || n < 0) { set_error("smg_dot: bad argument"); return SMG_EINVAL; }
-  dot_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, y, n, out, ws);
+  launch(dot_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), x, y, n, out, ws);
   return check_launch("dot_kernel");
 }
 
 int smg_sum(const double* x, int64_t n, double* out, double* ws, void* stream) {
   if (!x || !out || !ws || n < 0) { set_error("smg_sum: bad argument"); return SMG_EINVAL; }
-  sum_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, n, out, ws);
+  launch(sum_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), x, n, out, ws);
   return check_launch("sum_kernel");
 }
 
 int smg_dot2(const double* x, const double* y, const double* z, int64_t n, double* out, double* ws,
              void* stream) {
   if (!x || !y || !out || !ws || n < 0) { set_error("smg_dot2: bad argument"); return SMG_EINVAL; }
-  dot2_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(x, y, z, n, out, nullptr, ws);
+  launch(dot2_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), x, y, z, n, out, nullptr, ws);
   return check_launch("dot2_kernel");
 }
 
 int smg_cg_beta(const double* z, const double* r, const double* r_old, int64_t n, double* scal,
                 double* ws, void* stream) {
   if (!z || !r || !scal || !ws || n < 0) { set_error("smg_cg_beta: bad argument"); return SMG_EINVAL; }
-  dot2_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(z, r, r_old, n, nullptr, scal, ws);
+  launch(dot2_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), z, r, r_old, n, nullptr, scal, ws);
   return check_launch("dot2_kernel");
 }
 
 int smg_axpby(double alpha, const double* x, double beta, double* y, int64_t n, void* stream) {
   if (!x || !y || n < 0) { set_error("smg_axpby: bad argument"); return SMG_EINVAL; }
-  axpby_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(alpha, x, beta, y, n);
+  launch(axpby_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, as_stream(stream), alpha, x, beta, y, n);
   return check_launch("axpby_kernel");
 }
 
@@ -461,7 +476,7 @@ int smg_cg_update2(double* u, const double* r_in, double* r_out, const double* p
     set_error("smg_cg_update: bad argument");
     return SMG_EINVAL;
   }
-  cg_update_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(u, r_in, r_out, p, q, n, scal, flag, ws);
+  launch(cg_update_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), u, r_in, r_out, p, q, n, scal, flag, ws);
   return check_launch("cg_update_kernel");
 }
 
@@ -472,22 +487,22 @@ int smg_cg_update(double* u, double* r, const double* p, const double* q, int64_
 
 int smg_cg_direction(double* p, const double* z, int64_t n, double* scal, void* stream) {
   if (!p || !z || !scal) { set_error("smg_cg_direction: bad argument"); return SMG_EINVAL; }
-  cg_direction_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(p, z, n, scal);
+  launch(cg_direction_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, as_stream(stream), p, z, n, scal);
   return check_launch("cg_direction_kernel");
 }
 
 int smg_project_mean(double* f, int64_t n, double* ws, void* stream) {
   if (!f || !ws || n <= 0) { set_error("smg_project_mean: bad argument"); return SMG_EINVAL; }
   double* s = ws + (size_t)kReduceBlocks * kPartStride + 1;
-  sum_kernel<<<grid_for_reduce(n), kReduceThreads, 0, as_stream(stream)>>>(f, n, s, ws);
+  launch(sum_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, as_stream(stream), f, n, s, ws);
   int rc = check_launch("sum_kernel");
   if (rc) return rc;
-  sub_mean_kernel<<<grid_for(n), kReduceThreads, 0, as_stream(stream)>>>(f, n, s);
+  launch(sub_mean_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, as_stream(stream), f, n, s);
   return check_launch("sub_mean_kernel");
 }
 
 int smg_sum_partials(const double* part, int nb, double* out, void* stream) {
-  sum_partials_kernel<<<1, kReduceThreads, 0, as_stream(stream)>>>(part, nb, out);
+  launch(sum_partials_kernel, dim3(1), dim3(kReduceThreads), 0, as_stream(stream), part, nb, out);
   return check_launch("sum_partials_kernel");
 }
 

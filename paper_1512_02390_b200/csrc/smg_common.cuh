@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/smg.h"
 
@@ -56,6 +57,38 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double* sbuf /*32*
       v[k] = t;
     }
   }
+}
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every libsmg kernel starts with SMG_PDL_ENTRY(): it waits until the
+// preceding grid on the stream has completed and flushed (griddepcontrol.wait)
+// before touching global memory, then lets the next grid begin launching
+// (griddepcontrol.launch_dependents).  Launched with the programmatic
+// stream-serialization attribute, a dependent grid's CTAs are scheduled while
+// the previous grid drains, hiding the launch/ramp latency that dominates the
+// small per-level kernels of a V-cycle.  SMG_PDL=0 disables the attribute.
+#define SMG_PDL_ENTRY()                                            \
+  do {                                                             \
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");           \
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
+  } while (0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 constexpr int kReduceBlocks = 592;   // 4 x 148 SMs: fixed => deterministic

@@ -45,6 +45,7 @@ __host__ __device__ constexpr size_t fd_smem() { return sizeof(double) * fd_elem
 template <int M>
 __global__ void __launch_bounds__(fd_threads<M>())
 fd_kernel(const __grid_constant__ FDArgs<M> A) {
+  SMG_PDL_ENTRY();
   constexpr int E = fd_elems<M>();
   constexpr int MM = M * M;
   extern __shared__ double sm[];
@@ -205,7 +206,7 @@ int fd_launch(const FDLaunch& L, cudaStream_t st) {
   const int nel = L.blocks_mode ? L.nb : L.xc * L.yc;
   if (nel <= 0) return SMG_OK;
   const int grid = (nel + fd_elems<M>() - 1) / fd_elems<M>();
-  fd_kernel<M><<<grid, fd_threads<M>(), fd_smem<M>(), st>>>(A);
+  launch(fd_kernel<M>, dim3(grid), dim3(fd_threads<M>()), fd_smem<M>(), st, A);
   return check_launch("fd_kernel");
 }
 

@@ -52,6 +52,7 @@ struct FDMArgs {
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(FDMGeom<P, NO, TX, TY>::THREADS, 2)
 fdm_kernel(const __grid_constant__ FDMArgs A) {
+  SMG_PDL_ENTRY();
   using G = FDMGeom<P, NO, TX, TY>;
   using GT = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, MT = G::MT, KT = G::KT, NL = G::NL, BT = G::BT;
@@ -319,13 +320,13 @@ int fdm_launch(const FDTLaunch& L, cudaStream_t st) {
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int ntiles = L.ntx * L.nty;
-  fdm_kernel<P, NO, TX, TY><<<ntiles < grid_cap ? ntiles : grid_cap, G::THREADS, G::SMEM, st>>>(A);
+  launch(fdm_kernel<P, NO, TX, TY>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(G::THREADS), G::SMEM, st, A);
   int rc = check_launch("fdm_kernel");
   if (rc) return rc;
   constexpr long PER = (long)GT::BW * (GT::OY - GT::BW) + (long)(GT::OX - GT::BW) * GT::BW + (long)GT::BW * GT::BW;
   const long nb = PER * ntiles;
-  fdt_fixup<P, NO, TX, TY><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(L.u, L.ws, L.N_x, L.N_y, L.ntx, L.nty,
-                                                                          L.u_zero);
+  launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.N_y,
+         L.ntx, L.nty, L.u_zero);
   return check_launch("fdt_fixup");
 }
 

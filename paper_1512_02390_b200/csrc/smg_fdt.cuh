@@ -145,6 +145,7 @@ __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
+  SMG_PDL_ENTRY();
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
   constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT, NH = G::NH, STAGE = G::STAGE;
@@ -347,6 +348,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
                                                  int N_y, int ntx, int nty, int u_zero) {
+  SMG_PDL_ENTRY();
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
   constexpr size_t RS = (size_t)RX * RY;
@@ -453,13 +455,13 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int ntiles = L.ntx * L.nty;
-  fdt_kernel<P, NO, TX, TY><<<ntiles < grid_cap ? ntiles : grid_cap, G::THREADS, G::SMEM, st>>>(A);
+  launch(fdt_kernel<P, NO, TX, TY>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(G::THREADS), G::SMEM, st, A);
   int rc = check_launch("fdt_kernel");
   if (rc) return rc;
   constexpr long PER = (long)G::BW * (G::OY - G::BW) + (long)(G::OX - G::BW) * G::BW + (long)G::BW * G::BW;
   const long nb = PER * ntiles;
-  fdt_fixup<P, NO, TX, TY><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(L.u, L.ws, L.N_x, L.N_y, L.ntx, L.nty,
-                                                                          L.u_zero);
+  launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.N_y,
+         L.ntx, L.nty, L.u_zero);
   return check_launch("fdt_fixup");
 }
 

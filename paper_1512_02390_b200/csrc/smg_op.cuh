@@ -111,6 +111,7 @@ __device__ __forceinline__ void line_op(const OpArgs<P>& A, const double* x, con
 template <int P, int TX, int TY, bool DIFF>
 __global__ void __launch_bounds__(OpGeom<P, TX, TY, DIFF>::THREADS)
 op_kernel(const __grid_constant__ OpArgs<P> A) {
+  SMG_PDL_ENTRY();
   using G = OpGeom<P, TX, TY, DIFF>;
   constexpr int NP = G::NP, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, NT = G::THREADS;
   extern __shared__ double sm[];
@@ -228,7 +229,7 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
     }
     attr = true;
   }
-  op_kernel<P, TX, TY, DIFF><<<(L.n_x / TX) * (L.n_y / TY), G::THREADS, G::SMEM, st>>>(A);
+  launch(op_kernel<P, TX, TY, DIFF>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(G::THREADS), G::SMEM, st, A);
   return check_launch("op_kernel");
 }
 

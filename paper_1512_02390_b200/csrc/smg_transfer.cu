@@ -36,6 +36,7 @@ struct TrGeom {
 
 template <int PC, int PF, int T>
 __global__ void __launch_bounds__(256) prolong_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
   using G = TrGeom<PC, PF, T>;
   constexpr int NC = G::NC, NF = G::NF, CX = G::CX, OX = G::OXF, NT = G::NT;
   extern __shared__ double sm[];
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(256) prolong_kernel(const __grid_constant__ Tr
 
 template <int PC, int PF, int T>
 __global__ void __launch_bounds__(256) restrict_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
   using G = TrGeom<PC, PF, T>;
   constexpr int NC = G::NC, NF = G::NF, FX = G::FX, OX = G::OXC, NT = G::NT;
   extern __shared__ double sm[];
@@ -152,13 +154,13 @@ int tr_launch_t(const TrArgs& A0, bool prolong, cudaStream_t st) {
     if (!attr && G::SMEM_P > 48 * 1024)
       cudaFuncSetAttribute(prolong_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_P);
     attr = true;
-    prolong_kernel<PC, PF, T><<<grid, G::NT, G::SMEM_P, st>>>(A);
+    launch(prolong_kernel<PC, PF, T>, dim3(grid), dim3(G::NT), G::SMEM_P, st, A);
   } else {
     static bool attr = false;
     if (!attr && G::SMEM_R > 48 * 1024)
       cudaFuncSetAttribute(restrict_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_R);
     attr = true;
-    restrict_kernel<PC, PF, T><<<grid, G::NT, G::SMEM_R, st>>>(A);
+    launch(restrict_kernel<PC, PF, T>, dim3(grid), dim3(G::NT), G::SMEM_R, st, A);
   }
   return check_launch(prolong ? "prolong_kernel" : "restrict_kernel");
 }
