@@ -295,7 +295,15 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   // SMG_FD_ENGINE=dmma|dfma overrides the per-m default
   const char* eng = getenv("SMG_FD_ENGINE");
   s->dmma = eng ? (std::strcmp(eng, "dmma") == 0) : fd_prefers_dmma(m);
-  const bool eo_ok = s->dmma || (even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
+  // the tiled kernel folds the weights into its synthesis factors, which needs
+  // mirror-symmetric weights (true for every reference weight kind, to 1 ulp)
+  double wasym = 0.0, wmax = 0.0;
+  for (int k = 0; k < m; ++k) {
+    wasym = std::fmax(wasym, std::fmax(std::fabs(w_x[k] - w_x[m - 1 - k]), std::fabs(w_y[k] - w_y[m - 1 - k])));
+    wmax = std::fmax(wmax, std::fmax(std::fabs(w_x[k]), std::fabs(w_y[k])));
+  }
+  const bool w_sym = wasym <= 1e-14 * (wmax > 0.0 ? wmax : 1.0);
+  const bool eo_ok = s->dmma || (w_sym && even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
                                  even_odd_split(S_y, m, s->Sye, s->Syo, py));
   if (s->dmma) {
     px.resize(m); py.resize(m);
@@ -362,7 +370,10 @@ static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, i
     T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
     T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
     T.wx = h->wx.data(); T.wy = h->wy.data();
-    return h->fdt(T, as_stream(stream));
+    const int rc = h->fdt(T, as_stream(stream));
+    if (rc != SMG_EUNSUPPORTED) return rc;
+    // TMA cannot describe these buffers (odd row length or unaligned base):
+    // the coloured dense kernel below computes the same correction
   }
   if (u_zero) {
     cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * h->p * h->n_x * h->p * h->n_y, as_stream(stream));

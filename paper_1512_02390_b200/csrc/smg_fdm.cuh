@@ -325,9 +325,9 @@ int fdm_launch(const FDTLaunch& L, cudaStream_t st) {
   if (rc) return rc;
   constexpr long PER = (long)GT::BW * (GT::OY - GT::BW) + (long)(GT::OX - GT::BW) * GT::BW + (long)GT::BW * GT::BW;
   const long nb = PER * ntiles;
-  launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.N_y,
+  launch(fdm_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.N_y,
          L.ntx, L.nty, L.u_zero);
-  return check_launch("fdt_fixup");
+  return check_launch("fdm_fixup");
 }
 
 }  // namespace smg

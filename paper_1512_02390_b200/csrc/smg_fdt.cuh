@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "smg_common.cuh"
+#include "smg_tma.cuh"
 
 namespace smg {
 
@@ -36,21 +37,22 @@ __host__ __device__ constexpr int fdt_ho(int M) { return M / 2; }        // odd 
 
 template <int M>
 struct FDTArgs {
+  CUtensorMap rmap;                   // residual (N_y, N_x), box (BRX, RY)
+  CUtensorMap umap;                   // u (N_y, N_x), box (OX, OY): own block load + store
   const double* __restrict__ r;       // residual (N_y, N_x)
   double* __restrict__ u;             // u += correction
   const double* __restrict__ inv_nu;  // (n_y, n_x) or nullptr
   const double* __restrict__ dinv;    // (M,M), [even | odd] eigen order in both dims
-  double* __restrict__ ws;            // band workspace: ntiles * RY * RX
-  unsigned int* __restrict__ ctr;     // 3 * ntiles counters (x-edge, y-edge, corner), zeroed
+  double* __restrict__ ws;            // ring workspace: ntiles * RY * RX
   int N_x, N_y, n_x, ntx, nty;
   int debug_skip;                     // profiling aid: 1 = skip the four contractions
   int u_zero;                         // 1: u holds no valid data and is treated as 0 (write, not add)
-  // analysis factors Se[k][i] (k physical half index), synthesis factors SeT[i][k]
+  // analysis factors Se[k][i] (k physical half index); synthesis factors
+  // SeT[i][k] pre-multiplied by the (mirror-symmetric) Schwarz weight w[k]
   double Sye[fdt_he(M) * fdt_he(M)], SyeT[fdt_he(M) * fdt_he(M)];
   double Syo[fdt_ho(M) * fdt_ho(M) + 1], SyoT[fdt_ho(M) * fdt_ho(M) + 1];
   double Sxe[fdt_he(M) * fdt_he(M)], SxeT[fdt_he(M) * fdt_he(M)];
   double Sxo[fdt_ho(M) * fdt_ho(M) + 1], SxoT[fdt_ho(M) * fdt_ho(M) + 1];
-  double wx[M], wy[M];
 };
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
@@ -83,6 +85,22 @@ struct FDTGeom {
   static constexpr size_t SMEM = sizeof(double) * (2 * (size_t)STAGE + (size_t)E * MM);
   // two resident CTAs when both fit; the register cap follows from it
   static constexpr int MINB = (2 * SMEM <= 200 * 1024 && THREADS <= 384) ? 2 : 1;
+  // ---- TMA-staged kernel (fdt_kernel) ----
+  // residual box: starts at the even column at or below the region origin
+  // (TMA boxes must start on a 16-byte boundary), hence one spare column
+  static constexpr int BRX = (RX + 2) & ~1;
+  static constexpr int RBOX = BRX * RY, UBOX = OX * OY;
+  // one buffer per pipeline stage holds the residual box, and -- once stage 1
+  // has consumed it -- the tile's own block of u (loaded, updated, stored)
+  static constexpr int STR = (((RBOX > UBOX ? RBOX : UBOX) + 15) & ~15);  // 128-byte multiple
+  static constexpr int NRING = RX * RY - OX * OY;    // region nodes owned by neighbour tiles
+  static constexpr int KC = (M + P - 1) / P;         // max elements covering one node per direction
+  static constexpr size_t smem_for(int ns) { return sizeof(double) * ((size_t)ns * STR + (size_t)E * MM) + 16 * (size_t)ns; }
+  static constexpr size_t HALF_SM = 112 * 1024;      // two CTAs per SM
+  // stages: 4 when two CTAs still fit, else 3, else the most that fit one CTA
+  static constexpr int NS = smem_for(4) <= HALF_SM ? 4 : smem_for(3) <= HALF_SM ? 3 : smem_for(4) <= 227 * 1024 ? 4 : 3;
+  static constexpr size_t TSMEM = smem_for(NS);
+  static constexpr int TMINB = (TSMEM <= HALF_SM && THREADS <= 384) ? 2 : 1;
 };
 
 // Half analysis of one line.  Even lane: t = Se^T (x_k + x_{m-1-k}) (plus the
@@ -138,21 +156,97 @@ __device__ __forceinline__ void fdt_prefetch(const double* __restrict__ r, const
   }
 }
 
-// Persistent main kernel: CTA walks tiles blockIdx.x, +gridDim.x, ...; the
-// next tile's residual region and own u are in flight (cp.async group) while
-// the current tile computes.  Exclusive nodes are written to u directly,
-// band nodes (within n_o of a tile edge) to the workspace for fdt_fixup.
+// Gather of the element corrections.  After the recombination pass EB holds,
+// per element, the weighted correction on its whole M x M window (the weight
+// is folded into the synthesis factors).  A region node (y, x) sums the
+// elements (ey, ex) whose window [e P, e P + M) covers it, in a fixed order
+// (deterministic).
+//
+// Column part, computed once per thread for its column x: for each of the
+// <= KC candidate element columns, the byte offset of column x in it and a
+// 0/1 weight (0 when the candidate does not cover x: branch-free sums).
 template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::MINB)
+struct FDTCol {
+  static constexpr int KC = FDTGeom<P, NO, TX, TY>::KC;
+  int xo[KC];
+  double wx[KC];
+  __device__ __forceinline__ explicit FDTCol(int x) {
+    using G = FDTGeom<P, NO, TX, TY>;
+    constexpr int M = G::M, MM = G::MM;
+    const int ex0 = min(x / P, TX - 1);
+#pragma unroll
+    for (int b = 0; b < KC; ++b) {
+      const int ex = ex0 - b, cx = x - ex * P;
+      const bool ok = ex >= 0 && cx < M;
+      xo[b] = ok ? (ex * MM + cx) * 8 : 0;
+      wx[b] = ok ? 1.0 : 0.0;
+    }
+  }
+  // correction at region row y
+  __device__ __forceinline__ double at(const double* EB, int y) const {
+    using G = FDTGeom<P, NO, TX, TY>;
+    constexpr int M = G::M, MM = G::MM;
+    const int ey0 = min(y / P, TY - 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < KC; ++a) {
+      const int ey = ey0 - a, cy = y - ey * P;
+      const bool ok = ey >= 0 && cy < M;
+      const char* rp = reinterpret_cast<const char*>(EB) + (ok ? (ey * (TX * MM) + cy * M) * 8 : 0);
+      double v = 0.0;
+#pragma unroll
+      for (int b = 0; b < KC; ++b) v = fma(wx[b], *reinterpret_cast<const double*>(rp + xo[b]), v);
+      acc = fma(ok ? 1.0 : 0.0, v, acc);
+    }
+    return acc;
+  }
+};
+
+// Seam tiles (their residual region wraps around the periodic mesh, which TMA
+// cannot express): per-node cp.async into the box layout (row pitch BRX).
+template <int P, int NO, int TX, int TY, int NT>
+__device__ __forceinline__ void fdt_region_cpasync(const double* __restrict__ r, int N_x, int N_y, int X0, int Y0,
+                                                   double* R) {
+  using G = FDTGeom<P, NO, TX, TY>;
+  constexpr int RX = G::RX, RY = G::RY, BRX = G::BRX;
+  for (int idx = threadIdx.x; idx < RX * RY; idx += NT) {
+    const int y = idx / RX, x = idx - y * RX;
+    cp_async8(R + y * BRX + x, r + (size_t)wrapi(Y0 - NO + y, N_y) * N_x + wrapi(X0 - NO + x, N_x));
+  }
+}
+
+// Column of the region origin inside the residual box (0 or 1).
+__device__ __forceinline__ int fdt_box_shift(int X0, int NO) { return (X0 - NO) & 1; }
+
+// Persistent main kernel.  Per tile (TX x TY elements), in an NS-buffer ring:
+//   * the (RY x BRX) residual box is TMA-loaded NS-2 tiles ahead (one thread
+//     issues it; completion on the buffer's mbarrier; seam tiles, whose region
+//     wraps around the periodic mesh, use per-node cp.async instead);
+//   * stage 1 consumes the box; the tile's (OY x OX) own block of u is then
+//     TMA-loaded into the same buffer and lands while stages 2-4 run
+//     (even/odd halves in separate warps);
+//   * gather: every own node adds the element corrections covering it to its
+//     u in the buffer, which ONE TMA store writes back; region nodes owned by
+//     neighbour tiles (the ring) go to the workspace for fdt_fixup.
+template <int P, int NO, int TX, int TY>
+__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::TMINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   SMG_PDL_ENTRY();
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
-  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BW = G::BW, NT = G::NT, NH = G::NH, STAGE = G::STAGE;
-  extern __shared__ double sm[];
-  double* EB = sm + 2 * STAGE;  // E x M x M element buffers
+  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, NT = G::NT, NH = G::NH, BRX = G::BRX;
+  constexpr int STR = G::STR, NS = G::NS, NRING = G::NRING;
+  static_assert(G::TSMEM <= 227 * 1024, "tile does not fit in shared memory");
+  static_assert(NS >= 3, "pipeline needs >= 3 buffers");
+  // dynamic shared memory starts 1024-byte aligned (no static shared memory in
+  // this kernel); TMA boxes need 128-byte aligned destinations
+  extern __shared__ __align__(1024) double sm[];
+  double* EB = sm + NS * STR;  // E x M x M element buffers
+  uint64_t* barR = reinterpret_cast<uint64_t*>(EB + E * MM);
+  uint64_t* barU = barR + NS;
   const int tid = threadIdx.x;
-  const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, ntiles = A.ntx * A.nty;
+  const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
+  const bool u_zero = A.u_zero != 0;
 
   const bool odd = tid >= NH;     // warp-uniform
   const int line = odd ? tid - NH : tid;
@@ -163,47 +257,81 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   // this thread's half row of 1/(lam_y + lam_x) (L1-resident across tiles)
   const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 
-  int tile = blockIdx.x;
-  if (tile < ntiles) fdt_prefetch<P, NO, TX, TY, NT>(A.r, A.u, N_x, N_y, ntx, tile, sm, A.u_zero != 0);
-  cp_async_commit();
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    double* R = sm + (it & 1) * STAGE;  // residual region, then accumulated correction
-    double* UO = R + RX * RY;           // own u
-    {
-      const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) fdt_prefetch<P, NO, TX, TY, NT>(A.r, A.u, N_x, N_y, ntx, nxt, sm + ((it + 1) & 1) * STAGE, A.u_zero != 0);
-      cp_async_commit();
+  if (tid == 0) {
+    if (smem_u32(sm) & 127) __trap();  // alignment assumption above
+    for (int k = 0; k < 2 * NS; ++k) mbar_init(barR + k, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
+  // The caller guarantees the buffer is free (its last store has been read).
+  auto issue_r = [&](int t, int b) {
+    const int tx = t % ntx, ty = t / ntx;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    const bool seam = tx == 0 || ty == 0 || tx == ntx - 1 || ty == nty - 1;
+    if (tid == 0) {
+      fence_proxy_async_smem();   // generic writes to the buffer precede the async-proxy refill
+      mbar_arrive_expect_tx(barR + b, seam ? 0u : (unsigned)(G::RBOX * 8));
+      if (!seam) tma_load_2d(sm + b * STR, &A.rmap, (X0 - NO) & ~1, Y0 - NO, barR + b);
     }
+    if (seam) fdt_region_cpasync<P, NO, TX, TY, NT>(A.r, N_x, N_y, X0, Y0, sm + b * STR + fdt_box_shift(X0, NO));
+  };
+
+#pragma unroll
+  for (int j = 0; j < NS - 2; ++j) {
+    const int t = blockIdx.x + j * gridDim.x;
+    if (t < ntiles) issue_r(t, j);
+    cp_async_commit();
+  }
+  int tile = blockIdx.x;
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int b = it % NS;
+    const unsigned par = (unsigned)(it / NS) & 1u;
+    double* buf = sm + b * STR;
     const int tx = tile % ntx, ty = tile / ntx;
     const int X0 = tx * OX, Y0 = ty * OY;
     double s = 1.0;  // 1 / nu_bar of this element
     if (act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
-    cp_async_wait<1>();
+    cp_async_wait<NS - 3>();
+    mbar_wait(barR + b, par);
     __syncthreads();
 
+    // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
+    if (!A.debug_skip && act) {
+      const double* col = buf + fdt_box_shift(X0, NO) + (eyl * P) * BRX + exl * P + c;
+      auto in = [&](int k) { return col[k * BRX]; };
+      if (!odd) {
+        double t[HE];
+        half_analyse<M, HE, false>(A.Sye, in, t);
+#pragma unroll
+        for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
+      } else if (HO > 0) {
+        double t[HOX];
+        half_analyse<M, HOX, true>(A.Syo, in, t);
+#pragma unroll
+        for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
+      }
+    }
+    if (tid == 0) bulk_wait_read<1>();  // the store of tile it-2 has left its buffer
+    __syncthreads();
+    // this buffer's residual is consumed: bring in the own block of u; and
+    // refill the buffer of tile it-2 with the residual of tile it+NS-2
+    if (tid == 0 && !u_zero) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(barU + b, (unsigned)(G::UBOX * 8));
+      tma_load_2d(buf, &A.umap, X0, Y0, barU + b);
+    }
+    {
+      const int nxt = tile + (NS - 2) * gridDim.x;
+      if (nxt < ntiles) issue_r(nxt, (it + NS - 2) % NS);
+      cp_async_commit();
+    }
+
     if (A.debug_skip) {
-      for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;
+      for (int idx = tid; idx < E * MM; idx += NT) EB[idx] = 0.0;
       __syncthreads();
     } else {
-      // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
-      if (act) {
-        const double* col = R + (eyl * P) * RX + exl * P + c;
-        auto in = [&](int k) { return col[k * RX]; };
-        if (!odd) {
-          double t[HE];
-          half_analyse<M, HE, false>(A.Sye, in, t);
-#pragma unroll
-          for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
-        } else if (HO > 0) {
-          double t[HOX];
-          half_analyse<M, HOX, true>(A.Syo, in, t);
-#pragma unroll
-          for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
-        }
-      }
-      __syncthreads();
-      for (int idx = tid; idx < RX * RY; idx += NT) R[idx] = 0.0;  // residual consumed
-
       // ---- stage 2 (eigen-y rows c): T2[c, :] = ([Se; So]^T fold_x(T1[c, :])) * dinv / nu_bar
       {
         double t[HE];
@@ -292,68 +420,134 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       }
       __syncthreads();
+      // ---- recombine row c in place (even warps): out[j] = ex[j] + ox[j],
+      //      out[M-1-j] = ex[j] - ox[j] (j < HO); the centre of odd M is ex
+      if (act && !odd) {
+        double* br = B + c * M;
+        double ev[HE], ov[HOX];
+#pragma unroll
+        for (int j = 0; j < HE; ++j) ev[j] = br[j];
+#pragma unroll
+        for (int j = 0; j < HO; ++j) ov[j] = br[HE + j];
+#pragma unroll
+        for (int j = 0; j < HO; ++j) {
+          br[j] = ev[j] + ov[j];
+          br[M - 1 - j] = ev[j] - ov[j];
+        }
+      }
+      __syncthreads();
+    }
+    if (!u_zero) mbar_wait(barU + b, par);
 
-      // ---- recombine out[c, j] = W (ex +- ox) and add into the region in colour
-      //      passes (disjoint windows per pass); thread = (element, row c, half)
-      {
-        constexpr int C = G::C;
-        const double wyc = act ? A.wy[c] : 0.0;
-#pragma unroll
-        for (int pass = 0; pass < C * C; ++pass) {
-          if (act && (eyl % C) * C + (exl % C) == pass) {
-            const double* br = B + c * M;
-            double* dst = R + (eyl * P + c) * RX + exl * P;
-            if (!odd) {
-              // columns j in [0, HE): y[j] = ex[j] + ox[j] (centre: ex only)
-#pragma unroll
-              for (int j = 0; j < HE; ++j) {
-                const double y = j < HO ? br[j] + br[HE + j] : br[j];
-                dst[j] += y * (wyc * A.wx[j]);
-              }
-            } else {
-              // columns m-1-j, j in [0, HO): y = ex[j] - ox[j]
-#pragma unroll
-              for (int j = 0; j < HO; ++j) {
-                const double y = br[j] - br[HE + j];
-                dst[M - 1 - j] += y * (wyc * A.wx[M - 1 - j]);
-              }
-            }
-          }
-          __syncthreads();
+    // ---- gather: own block (in buf, TMA-stored), ring -> workspace ----------
+    // own block: thread = (column, row group); lanes walk consecutive columns
+    {
+      constexpr int NG = NT / OX;  // >= 2: NT >= 2 E M > 2 OX
+      if (tid < NG * OX) {
+        const int ox = tid % OX, g = tid / OX;
+        const FDTCol<P, NO, TX, TY> col(ox + NO);
+        for (int oy = g; oy < OY; oy += NG) {
+          const double cor = col.at(EB, oy + NO);
+          double* uo = buf + oy * OX + ox;
+          *uo = u_zero ? cor : *uo + cor;
         }
       }
     }
-
-    // ---- write-out: exclusive nodes to u, band nodes to the workspace ------
-    double* W = A.ws + (size_t)tile * (RX * RY);
-    for (int idx = tid; idx < RX * RY; idx += NT) {
-      const int y = idx / RX, x = idx - y * RX;
-      const bool band = (x < BW) || (x >= RX - BW) || (y < BW) || (y >= RY - BW);
-      if (band) {
-        W[idx] = R[idx];
-      } else {
-        const int oy = y - NO, ox = x - NO;
-        A.u[(size_t)(Y0 + oy) * N_x + (X0 + ox)] = A.u_zero ? R[idx] : UO[oy * OX + ox] + R[idx];
+    // ring (compact, tile-major): rows [0,NO) and [NO+OY,RY) full width, then
+    // the side columns [0,NO) u [NO+OX,RX) of the own rows
+    {
+      double* W = A.ws + (size_t)tile * NRING;
+      constexpr int NTB = (RY - OY) * RX;
+      for (int k = tid; k < NRING; k += NT) {
+        int y, x;
+        if (k < NTB) {
+          const int yy = k / RX;
+          x = k - yy * RX;
+          y = yy < NO ? yy : yy + OY;
+        } else {
+          const int k2 = k - NTB, yy = k2 / (RX - OX), xx = k2 - yy * (RX - OX);
+          y = NO + yy;
+          x = xx < NO ? xx : xx + OX;
+        }
+        W[k] = FDTCol<P, NO, TX, TY>(x).at(EB, y);
       }
     }
-    __syncthreads();  // this stage buffer is refilled two iterations later
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_2d(&A.umap, buf, X0, Y0);
+      bulk_commit();
+    }
   }
+  if (tid == 0) bulk_wait0();
   cp_async_wait<0>();
 }
 
-// Band fixup (second launch): every node within n_o of a tile edge receives
-// the contributions of the 2 (edge) or 4 (corner) tiles sharing it, summed in
-// a fixed tile order: u = (((u + c_lo,lo) + c_hi,lo) + c_lo,hi) + c_hi,hi.
-// One thread per band node; deterministic; no atomics.
+// Ring fixup (second launch): an own node within n_o (+1) of its tile's edge
+// also lies in the regions of the neighbour tiles; it receives their ring
+// contributions from the workspace, added in a fixed neighbour order
+// (dy, dx) = (-1,-1), (-1,0), ..., (1,1).  One thread per band node; no
+// atomics; deterministic.
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
+                                                 int ntx, int nty) {
+  SMG_PDL_ENTRY();
+  using G = FDTGeom<P, NO, TX, TY>;
+  constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
+  constexpr int NRING = G::NRING, NTB = (RY - OY) * RX;
+  // band of the own block: rows [0, BW-NO) u [OY-NO, OY) full width, and the
+  // columns [0, BW-NO) u [OX-NO, OX) of the rows in between
+  constexpr int LO = NO + 1;
+  constexpr int NROWS = LO + NO;
+  constexpr int PER = NROWS * OX + (OY - NROWS) * (LO + NO);
+  static_assert(OY >= NROWS && OX >= LO + NO, "tile smaller than its band");
+  (void)BW;
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntiles = ntx * nty;
+  if (gid >= (long)ntiles * PER) return;
+  const int tile = (int)(gid / PER);
+  const int k = (int)(gid - (long)tile * PER);
+  int oy, ox;
+  if (k < NROWS * OX) {
+    const int yy = k / OX;
+    ox = k - yy * OX;
+    oy = yy < LO ? yy : OY - NROWS + yy;
+  } else {
+    const int k2 = k - NROWS * OX, yy = k2 / (LO + NO), xx = k2 - yy * (LO + NO);
+    oy = LO + yy;
+    ox = xx < LO ? xx : OX - (LO + NO) + xx;
+  }
+  const int tx = tile % ntx, ty = tile / ntx;
+  double* up = u + (size_t)(ty * OY + oy) * N_x + (tx * OX + ox);
+  double acc = *up;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int ry = oy + NO - dy * OY;
+    if (ry < 0 || ry >= RY) continue;
+    const int tyn = wrapi(ty + dy, nty);
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dx == 0 && dy == 0) continue;
+      const int rx = ox + NO - dx * OX;
+      if (rx < 0 || rx >= RX) continue;
+      int k;  // compact ring index of region node (ry, rx) of the neighbour
+      if (ry < NO || ry >= NO + OY) k = (ry < NO ? ry : ry - OY) * RX + rx;
+      else k = NTB + (ry - NO) * (RX - OX) + (rx < NO ? rx : rx - OX);
+      acc += ws[(size_t)(tyn * ntx + wrapi(tx + dx, ntx)) * NRING + k];
+    }
+  }
+  *up = acc;
+}
+
+// Band fixup of the DMMA variant (smg_fdm.cuh), which writes every band node
+// of its region to the workspace: u = (((u + c_lo,lo) + c_hi,lo) + c_lo,hi) + c_hi,hi.
+template <int P, int NO, int TX, int TY>
+__global__ void __launch_bounds__(256) fdm_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
                                                  int N_y, int ntx, int nty, int u_zero) {
   SMG_PDL_ENTRY();
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
   constexpr size_t RS = (size_t)RX * RY;
-  // per tile: x-edge segment (BW x (OY - BW)) at its left edge, y-edge
-  // segment ((OX - BW) x BW) at its bottom edge, corner BW x BW at lower-left
   constexpr int NXE = BW * (OY - BW), NYE = (OX - BW) * BW, NCO = BW * BW;
   constexpr int PER = NXE + NYE + NCO;
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,7 +559,6 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   const int txm = (tx + ntx - 1) % ntx, tym = (ty + nty - 1) % nty;
   const int X0 = tx * OX, Y0 = ty * OY;
   if (k < NXE) {
-    // left x-edge of (tx, ty): rows of its y-interior, d in [-NO, NO]
     const int yy = BW + k / BW, d = k % BW - NO;
     const double cl = ws[(size_t)(ty * ntx + txm) * RS + (size_t)yy * RX + (OX + NO + d)];
     const double cr = ws[(size_t)(ty * ntx + tx) * RS + (size_t)yy * RX + (NO + d)];
@@ -375,7 +568,6 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   }
   k -= NXE;
   if (k < NYE) {
-    // bottom y-edge of (tx, ty): columns of its x-interior
     const int d = k / (OX - BW) - NO, xx = BW + k % (OX - BW);
     const double cb = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + d) * RX + xx];
     const double ct = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + d) * RX + xx];
@@ -385,7 +577,6 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   }
   k -= NYE;
   {
-    // lower-left corner of (tx, ty): tiles (txm,tym), (tx,tym), (txm,ty), (tx,ty)
     const int dy = k / BW - NO, dx = k % BW - NO;
     const double c00 = ws[(size_t)(tym * ntx + txm) * RS + (size_t)(OY + NO + dy) * RX + (OX + NO + dx)];
     const double c10 = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + dy) * RX + (NO + dx)];
@@ -422,46 +613,52 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int M = G::M, HE = fdt_he(M), HO = fdt_ho(M);
   FDTArgs<M> A;
-  A.r = L.r; A.u = L.u; A.inv_nu = L.inv_nu; A.dinv = L.dinv; A.ws = L.ws; A.ctr = L.ctr;
+  // TMA needs 16-byte rows and base addresses; the caller falls back to the
+  // coloured dense kernel on SMG_EUNSUPPORTED
+  if (!tmap_2d(&A.rmap, L.r, L.N_x, L.N_y, G::BRX, G::RY) || !tmap_2d(&A.umap, L.u, L.N_x, L.N_y, G::OX, G::OY))
+    return SMG_EUNSUPPORTED;
+  A.r = L.r; A.u = L.u; A.inv_nu = L.inv_nu; A.dinv = L.dinv; A.ws = L.ws;
   A.N_x = L.N_x; A.N_y = L.N_y; A.n_x = L.n_x; A.ntx = L.ntx; A.nty = L.nty;
   {
     const char* dbg = getenv("SMG_FD_DEBUG_SKIP");
     A.debug_skip = (dbg && dbg[0] == '1') ? 1 : 0;
   }
   A.u_zero = L.u_zero;
+  // synthesis factors carry the weight of their output node: W (S t S^T) =
+  // (diag(w_y) S_y) t (diag(w_x) S_x)^T, and w is mirror-symmetric, so the
+  // even/odd recombination e +- o inherits it
   for (int k = 0; k < HE; ++k)
     for (int i = 0; i < HE; ++i) {
-      A.Sye[k * HE + i] = L.Sye[k * HE + i]; A.SyeT[i * HE + k] = L.Sye[k * HE + i];
-      A.Sxe[k * HE + i] = L.Sxe[k * HE + i]; A.SxeT[i * HE + k] = L.Sxe[k * HE + i];
+      A.Sye[k * HE + i] = L.Sye[k * HE + i]; A.SyeT[i * HE + k] = L.Sye[k * HE + i] * L.wy[k];
+      A.Sxe[k * HE + i] = L.Sxe[k * HE + i]; A.SxeT[i * HE + k] = L.Sxe[k * HE + i] * L.wx[k];
     }
   for (int k = 0; k < HO; ++k)
     for (int i = 0; i < HO; ++i) {
-      A.Syo[k * HO + i] = L.Syo[k * HO + i]; A.SyoT[i * HO + k] = L.Syo[k * HO + i];
-      A.Sxo[k * HO + i] = L.Sxo[k * HO + i]; A.SxoT[i * HO + k] = L.Sxo[k * HO + i];
+      A.Syo[k * HO + i] = L.Syo[k * HO + i]; A.SyoT[i * HO + k] = L.Syo[k * HO + i] * L.wy[k];
+      A.Sxo[k * HO + i] = L.Sxo[k * HO + i]; A.SxoT[i * HO + k] = L.Sxo[k * HO + i] * L.wx[k];
     }
   A.Syo[HO * HO] = A.SyoT[HO * HO] = A.Sxo[HO * HO] = A.SxoT[HO * HO] = 0.0;
-  for (int i = 0; i < M; ++i) { A.wx[i] = L.wx[i]; A.wy[i] = L.wy[i]; }
   static int grid_cap = 0;
   if (grid_cap == 0) {
-    if (G::SMEM > 48 * 1024) {
+    if (G::TSMEM > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fdt_kernel<P, NO, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)G::SMEM);
+                                           (int)G::TSMEM);
       if (e != cudaSuccess) return cuda_fail(e, "fdt_kernel smem attribute");
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdt_kernel<P, NO, TX, TY>, G::THREADS, G::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdt_kernel<P, NO, TX, TY>, G::THREADS, G::TSMEM);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int ntiles = L.ntx * L.nty;
-  launch(fdt_kernel<P, NO, TX, TY>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(G::THREADS), G::SMEM, st, A);
+  launch(fdt_kernel<P, NO, TX, TY>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(G::THREADS), G::TSMEM, st, A);
   int rc = check_launch("fdt_kernel");
   if (rc) return rc;
-  constexpr long PER = (long)G::BW * (G::OY - G::BW) + (long)(G::OX - G::BW) * G::BW + (long)G::BW * G::BW;
+  constexpr long PER = (long)(2 * NO + 1) * G::OX + (long)(G::OY - 2 * NO - 1) * (2 * NO + 1);
   const long nb = PER * ntiles;
-  launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.N_y,
-         L.ntx, L.nty, L.u_zero);
+  launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.ntx,
+         L.nty);
   return check_launch("fdt_fixup");
 }
 
