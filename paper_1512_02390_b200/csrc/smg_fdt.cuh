@@ -436,18 +436,50 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       }
       __syncthreads();
+      // ---- fold the overlaps onto the home cells.  Window cell (cy, cx) of an
+      //      element is "home" when NO <= cx, cy < NO + P (the element's own
+      //      nodes).  Only the immediate neighbours reach a home cell: the
+      //      right one at cx = P..P+NO-1 (its cells 0..NO-1), the left one at
+      //      cx = NO..2NO (its cells P+NO..P+2NO).  Each thread reads only
+      //      non-home cells and writes only its own element's home cells.
+      //      x first (all rows), then y (all columns): corners come along.
+      if (act && !odd) {
+        double* br = B + c * M;  // row c
+        if (exl + 1 < TX) {
+#pragma unroll
+          for (int k = 0; k < NO; ++k) br[P + k] += br[MM + k];
+        }
+        if (exl > 0) {
+#pragma unroll
+          for (int k = NO; k <= 2 * NO; ++k) br[k] += br[P + k - MM];
+        }
+      }
+      __syncthreads();
+      if (act && !odd) {
+        double* bc = B + c;      // column c
+        if (eyl + 1 < TY) {
+#pragma unroll
+          for (int k = 0; k < NO; ++k) bc[(P + k) * M] += bc[TX * MM + k * M];
+        }
+        if (eyl > 0) {
+#pragma unroll
+          for (int k = NO; k <= 2 * NO; ++k) bc[k * M] += bc[(P + k) * M - TX * MM];
+        }
+      }
+      __syncthreads();
     }
     if (!u_zero) mbar_wait(barU + b, par);
 
-    // ---- gather: own block (in buf, TMA-stored), ring -> workspace ----------
+    // ---- gather: every region node reads ONE cell -- its home element's, or
+    //      for ring nodes the edge element covering it ----------------------
     // own block: thread = (column, row group); lanes walk consecutive columns
     {
       constexpr int NG = NT / OX;  // >= 2: NT >= 2 E M > 2 OX
       if (tid < NG * OX) {
         const int ox = tid % OX, g = tid / OX;
-        const FDTCol<P, NO, TX, TY> col(ox + NO);
+        const double* cb = EB + (ox / P) * MM + (ox % P + NO);
         for (int oy = g; oy < OY; oy += NG) {
-          const double cor = col.at(EB, oy + NO);
+          const double cor = cb[(oy / P) * (TX * MM) + (oy % P + NO) * M];
           double* uo = buf + oy * OX + ox;
           *uo = u_zero ? cor : *uo + cor;
         }
@@ -469,7 +501,9 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           y = NO + yy;
           x = xx < NO ? xx : xx + OX;
         }
-        W[k] = FDTCol<P, NO, TX, TY>(x).at(EB, y);
+        const int ey = y < NO ? 0 : min((y - NO) / P, TY - 1);
+        const int ex = x < NO ? 0 : min((x - NO) / P, TX - 1);
+        W[k] = EB[(ey * TX + ex) * MM + (y - ey * P) * M + (x - ex * P)];
       }
     }
     fence_proxy_async_smem();
