@@ -539,8 +539,11 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int ntiles = ntx * nty;
   if (gid >= (long)ntiles * PER) return;
-  const int tile = (int)(gid / PER);
-  const int k = (int)(gid - (long)tile * PER);
+  // last tiles first: the main kernel finished with them, so their u and ring
+  // entries are the ones still resident in L2
+  const int tr = (int)(gid / PER);
+  const int tile = ntiles - 1 - tr;
+  const int k = (int)(gid - (long)tr * PER);
   int oy, ox;
   if (k < NROWS * OX) {
     const int yy = k / OX;
