@@ -23,6 +23,7 @@
 // r = f - A u (f may be absent) and per-CTA partials of ||r||^2.
 #pragma once
 #include "smg_common.cuh"
+#include "smg_tma.cuh"
 
 namespace smg {
 
@@ -34,6 +35,7 @@ struct OpArgs {
   const double* __restrict__ nu;     // diffusion only
   double* __restrict__ partials;     // nullable: per-CTA sum of out^2
   int N_x, N_y, tiles_x;
+  int bulk;                          // 1: bulk row copies (N_x even, 16-byte aligned fields)
   double cx, cy;
   double Mt[(P + 1) * (P + 1)];      // Poisson: stiffness L-hat; diffusion: D (row-major)
   double w[P + 1];
@@ -45,10 +47,12 @@ struct OpGeom {
   static constexpr int NP = P + 1;
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int HX = OX + P + 1, HY = OY + P + 1;
+  static constexpr int DP = (HX + 2) & ~1;     // staged row pitch (room for the bulk-copy shift)
+  static constexpr int DPF = (OX + 2) & ~1;
   static constexpr int ROWJ = OY * (TX + 1), COLJ = OX * (TY + 1);
   static constexpr int THREADS = (ROWJ > COLJ ? ROWJ : COLJ) >= 256 ? 256 : (((ROWJ > COLJ ? ROWJ : COLJ) + 31) / 32) * 32;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)HX * HY * (DIFF ? 2 : 1) + 3 * (size_t)OX * OY +
-                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1));
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY * (DIFF ? 2 : 1) + (size_t)DPF * OY + 2 * (size_t)OX * OY +
+                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1)) + 16;
 };
 
 __device__ __forceinline__ void op_cp_async8(double* smem, const double* gmem) {
@@ -114,39 +118,62 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   SMG_PDL_ENTRY();
   using G = OpGeom<P, TX, TY, DIFF>;
   constexpr int NP = G::NP, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, NT = G::THREADS;
-  extern __shared__ double sm[];
-  double* U = sm;                                  // HY x HX, origin (Y0-P, X0-P)
-  double* NU = U + HX * HY;                        // diffusion only
-  double* F = NU + (DIFF ? HX * HY : 0);           // OY x OX
-  double* AX = F + OX * OY;                        // OY x OX
+  extern __shared__ __align__(16) double sm[];
+  constexpr int DP = G::DP, DPF = G::DPF;
+  double* U = sm;                                  // HY x DP, origin (Y0-P, X0-P) at column sh
+  double* NU = U + DP * HY;                        // diffusion only
+  double* F = NU + (DIFF ? DP * HY : 0);           // OY x DPF, origin (Y0, X0) at column shf
+  double* AX = F + DPF * OY;                       // OY x OX
   double* AY = AX + OX * OY;                       // OY x OX
   double* VX = AY + OX * OY;                       // OY x (TX+1): right-vertex value of element exl-1
   double* VY = VX + OY * (TX + 1);                 // OX x (TY+1)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(VY + OX * (TY + 1));
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int X0 = tx * OX, Y0 = ty * OY;
   const int N_x = A.N_x, N_y = A.N_y;
 
-  for (int idx = tid; idx < HX * HY; idx += NT) {
-    const int hy = idx / HX, hx = idx - hy * HX;
-    const size_t g = (size_t)wrapi(Y0 - P + hy, N_y) * N_x + wrapi(X0 - P + hx, N_x);
-    op_cp_async8(U + idx, A.u + g);
-    if (DIFF) op_cp_async8(NU + idx, A.nu + g);
-  }
-  if (A.f != nullptr) {
-    for (int idx = tid; idx < OX * OY; idx += NT) {
-      const int y = idx / OX, x = idx - y * OX;
-      op_cp_async8(F + idx, A.f + (size_t)(Y0 + y) * N_x + (X0 + x));
+  int sh = 0, shf = 0;
+  if (A.bulk) {
+    // bulk row copies issued by warp 0 (periodic wrap handled per row)
+    sh = pwin_shift(X0 - P, N_x);
+    shf = pwin_shift(X0, N_x);
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      unsigned bytes = pwin_bytes(HX, HY, sh) * (DIFF ? 2u : 1u);
+      if (A.f != nullptr) bytes += pwin_bytes(OX, OY, shf);
+      mbar_arrive_expect_tx(bar, bytes);
     }
+    __syncthreads();
+    if (tid < 32) {
+      pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
+      if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
+      if (A.f != nullptr) pwin_issue_warp(A.f, N_x, N_y, X0, Y0, OX, OY, F, DPF, bar);
+    }
+    mbar_wait(bar, 0);
+  } else {
+    for (int idx = tid; idx < HX * HY; idx += NT) {
+      const int hy = idx / HX, hx = idx - hy * HX;
+      const size_t g = (size_t)wrapi(Y0 - P + hy, N_y) * N_x + wrapi(X0 - P + hx, N_x);
+      op_cp_async8(U + hy * DP + hx, A.u + g);
+      if (DIFF) op_cp_async8(NU + hy * DP + hx, A.nu + g);
+    }
+    if (A.f != nullptr) {
+      for (int idx = tid; idx < OX * OY; idx += NT) {
+        const int y = idx / OX, x = idx - y * OX;
+        op_cp_async8(F + y * DPF + x, A.f + (size_t)(Y0 + y) * N_x + (X0 + x));
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
   }
-  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 
   // row passes: item = (own row y, element exl-1), exl in [0, TX]
   for (int it = tid; it < OY * (TX + 1); it += NT) {
     const int y = it / (TX + 1), exl = it - y * (TX + 1);
-    const double* ur = U + (y + P) * HX + exl * P;
-    const double* nr = NU + (y + P) * HX + exl * P;
+    const double* ur = U + (y + P) * DP + sh + exl * P;
+    const double* nr = NU + (y + P) * DP + sh + exl * P;
     double v[NP];
     if (exl == 0) {
       line_op<P, DIFF, true, 1>(A, ur, nr, v);
@@ -161,13 +188,13 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   // column passes: item = (own column x, element eyl-1), eyl in [0, TY]
   for (int it = tid; it < OX * (TY + 1); it += NT) {
     const int x = it / (TY + 1), eyl = it - x * (TY + 1);
-    const double* uc = U + (eyl * P) * HX + (x + P);
-    const double* nc = NU + (eyl * P) * HX + (x + P);
+    const double* uc = U + (eyl * P) * DP + sh + (x + P);
+    const double* nc = NU + (eyl * P) * DP + sh + (x + P);
     double v[NP];
     if (eyl == 0) {
-      line_op<P, DIFF, true, HX>(A, uc, nc, v);
+      line_op<P, DIFF, true, DP>(A, uc, nc, v);
     } else {
-      line_op<P, DIFF, false, HX>(A, uc, nc, v);
+      line_op<P, DIFF, false, DP>(A, uc, nc, v);
       double* ay = AY + ((eyl - 1) * P) * OX + x;
 #pragma unroll
       for (int a = 0; a < P; ++a) ay[a * OX] = v[a];
@@ -184,7 +211,7 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
     if (b == 0) ax += VX[y * (TX + 1) + x / P];
     if (a == 0) ay += VY[x * (TY + 1) + y / P];
     const double val = A.cx * A.wasm[a] * ax + A.cy * A.wasm[b] * ay;
-    const double r = A.f != nullptr ? F[idx] - val : val;
+    const double r = A.f != nullptr ? F[y * DPF + shf + x] - val : val;
     A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = r;
     nrm = fma(r, r, nrm);
   }
@@ -217,6 +244,8 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = L.partials;
   A.N_x = L.n_x * P; A.N_y = L.n_y * P; A.tiles_x = L.n_x / TX;
   A.cx = L.cx; A.cy = L.cy;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) && (L.f == nullptr || al16(L.f)) ? 1 : 0;
   for (int i = 0; i < (P + 1) * (P + 1); ++i) A.Mt[i] = L.Mt[i];
   for (int i = 0; i < P + 1; ++i) A.w[i] = L.w[i];
   for (int i = 0; i < P; ++i) A.wasm[i] = L.wasm[i];

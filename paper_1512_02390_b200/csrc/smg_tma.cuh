@@ -77,4 +77,44 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // Wait until every committed bulk store has completed (writes performed).
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// 1D bulk copy global -> shared (16-byte aligned addresses, size % 16 == 0),
+// completing on bar (complete_tx).
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Row width (doubles) that pwin_load_warp moves per window row.
+__host__ __device__ constexpr int pwin_width(int W, int sh) { return (W + sh + 1) & ~1; }
+
+// Periodic window loader, issued by the 32 lanes of ONE warp: rows
+// [y0, y0+H) x columns [x0, x0+W) of the periodic field f (N_y x N_x, N_x
+// even, |x0| < N_x) land in dst with row pitch DP (even, >= pwin_width);
+// window column j of row r is dst[r*DP + pwin_shift(x0, N_x) + j] (bulk
+// copies move 16-byte aligned pieces).  One copy per row, two where the row
+// wraps around the seam (the piece past the seam restarts at column 0 of the
+// same row).  The caller arms the mbarrier with pwin_bytes() beforehand.
+__host__ __device__ __forceinline__ int pwin_shift(int x0, int N_x) { return (x0 < 0 ? x0 + N_x : x0) & 1; }
+__host__ __device__ __forceinline__ unsigned pwin_bytes(int W, int H, int sh) {
+  return (unsigned)(H * pwin_width(W, sh) * 8);
+}
+__device__ __forceinline__ void pwin_issue_warp(const double* __restrict__ f, int N_x, int N_y, int x0, int y0, int W,
+                                                int H, double* dst, int DP, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const int xs = x0 < 0 ? x0 + N_x : (x0 >= N_x ? x0 - N_x : x0);
+  const int sh = xs & 1, xa = xs - sh;
+  const int width = pwin_width(W, sh);
+  const int lenA = min(width, N_x - xa);
+  for (int r = lane; r < H; r += 32) {
+    int gy = y0 + r;
+    gy = gy < 0 ? gy + N_y : (gy >= N_y ? gy - N_y : gy);
+    const double* row = f + (size_t)gy * N_x;
+    double* d = dst + r * DP;
+    bulk_g2s(d, row + xa, (unsigned)(lenA * 8), bar);
+    if (lenA < width) bulk_g2s(d + lenA, row, (unsigned)((width - lenA) * 8), bar);
+  }
+}
+
 }  // namespace smg

@@ -14,6 +14,7 @@
 // Deterministic, no atomics.  Tiles are compile-time; data is staged with
 // cp.async and J lives in shared memory.
 #include "smg_transfer.cuh"
+#include "smg_tma.cuh"
 
 namespace smg {
 
@@ -27,11 +28,14 @@ struct TrGeom {
   static constexpr int NC = PC + 1, NF = PF + 1;
   // prolongation: coarse region incl. high vertex, fine own tile
   static constexpr int CX = T * PC + 1, OXF = T * PF;
+  static constexpr int DC = (CX + 2) & ~1, DF = (OXF + 2) & ~1;   // staged row pitches
   // restriction: fine staged incl. the low halo element, coarse own tile
   static constexpr int FX = (T + 1) * PF, OXC = T * PC;
+  static constexpr int DX = (FX + 2) & ~1;
   static constexpr int NT = 256;
-  static constexpr size_t SMEM_P = sizeof(double) * ((size_t)CX * CX + (size_t)CX * OXF + (size_t)OXF * OXF + NF * NC);
-  static constexpr size_t SMEM_R = sizeof(double) * ((size_t)FX * FX + (size_t)FX * OXC + NF * NC);
+  static constexpr size_t SMEM_P = sizeof(double) * ((size_t)DC * CX + (size_t)CX * OXF + (size_t)DF * OXF) + 16;
+  static constexpr size_t SMEM_R = sizeof(double) * ((size_t)DX * FX + (size_t)FX * OXC + (size_t)FX * (T + 1) +
+                                                     (size_t)OXC * OXC + (size_t)(T + 1) * OXC) + 16;
 };
 
 template <int PC, int PF, int T>
@@ -39,50 +43,80 @@ __global__ void __launch_bounds__(256) prolong_kernel(const __grid_constant__ Tr
   SMG_PDL_ENTRY();
   using G = TrGeom<PC, PF, T>;
   constexpr int NC = G::NC, NF = G::NF, CX = G::CX, OX = G::OXF, NT = G::NT;
-  extern __shared__ double sm[];
-  double* C = sm;             // CX x CX coarse values
-  double* Tt = C + CX * CX;   // CX x OX  (x-interpolated)
-  double* UF = Tt + CX * OX;  // OX x OX  old fine values (accumulate)
-  double* Js = UF + OX * OX;  // NF x NC
+  extern __shared__ __align__(16) double sm[];
+  constexpr int DC = G::DC, DF = G::DF;
+  double* C = sm;             // CX x DC coarse values (column shift shc)
+  double* Tt = C + DC * CX;   // CX x OX  (x-interpolated)
+  double* UF = Tt + CX * OX;  // OX x DF  old fine values (accumulate; column shift shf)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(UF + DF * OX);
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
-  const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
+  const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF, Nyf = A.n_y * PF;
   const int Xc0 = tx * T * PC, Yc0 = ty * T * PC, Xf0 = tx * OX, Yf0 = ty * OX;
-  for (int idx = tid; idx < CX * CX; idx += NT) {
-    const int y = idx / CX, x = idx - y * CX;
-    tr_cp_async8(C + idx, A.src + (size_t)wrapi(Yc0 + y, Nyc) * Nxc + wrapi(Xc0 + x, Nxc));
-  }
-  if (A.accumulate) {
-    for (int idx = tid; idx < OX * OX; idx += NT) {
-      const int y = idx / OX, x = idx - y * OX;
-      tr_cp_async8(UF + idx, A.dst + (size_t)(Yf0 + y) * Nxf + (Xf0 + x));
+  int shc = 0, shf = 0;
+  if (A.bulk) {
+    shc = pwin_shift(Xc0, Nxc);
+    shf = pwin_shift(Xf0, Nxf);
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar, pwin_bytes(CX, CX, shc) + (A.accumulate ? pwin_bytes(OX, OX, shf) : 0u));
+    }
+    __syncthreads();
+    if (tid < 32) {
+      pwin_issue_warp(A.src, Nxc, Nyc, Xc0, Yc0, CX, CX, C, DC, bar);
+      if (A.accumulate) pwin_issue_warp(A.dst, Nxf, Nyf, Xf0, Yf0, OX, OX, UF, DF, bar);
+    }
+  } else {
+    for (int idx = tid; idx < CX * CX; idx += NT) {
+      const int y = idx / CX, x = idx - y * CX;
+      tr_cp_async8(C + y * DC + x, A.src + (size_t)wrapi(Yc0 + y, Nyc) * Nxc + wrapi(Xc0 + x, Nxc));
+    }
+    if (A.accumulate) {
+      for (int idx = tid; idx < OX * OX; idx += NT) {
+        const int y = idx / OX, x = idx - y * OX;
+        tr_cp_async8(UF + y * DF + x, A.dst + (size_t)(Yf0 + y) * Nxf + (Xf0 + x));
+      }
     }
   }
-  for (int idx = tid; idx < NF * NC; idx += NT) Js[idx] = A.J[idx];
-  asm volatile("cp.async.wait_all;\n" ::);
+  if (A.bulk) mbar_wait(bar, 0);
+  else asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  // x: Tt[rc][xf] = sum_bc J[b][bc] C[rc][exl*PC + bc]
-  for (int idx = tid; idx < CX * OX; idx += NT) {
-    const int rc = idx / OX, xf = idx - rc * OX;
-    const int exl = xf / PF, b = xf - exl * PF;
-    const double* c = C + rc * CX + exl * PC;
-    const double* j = Js + b * NC;
-    double s = j[0] * c[0];
+  // Register-blocked passes: a thread owns one (line, element) and produces
+  // all of its outputs, so every J entry is a uniform parameter-bank operand
+  // and each staged value is read from shared memory once.
+  // x: Tt[rc][exl*PF + b] = sum_bc J[b][bc] C[rc][exl*PC + bc]
+  for (int it = tid; it < CX * T; it += NT) {
+    const int rc = it / T, exl = it - rc * T;
+    const double* c = C + rc * DC + shc + exl * PC;
+    double cv[NC];
 #pragma unroll
-    for (int k = 1; k < NC; ++k) s = fma(j[k], c[k], s);
-    Tt[idx] = s;
+    for (int k = 0; k < NC; ++k) cv[k] = c[k];
+    double* out = Tt + rc * OX + exl * PF;
+#pragma unroll
+    for (int bb = 0; bb < PF; ++bb) {
+      double s = A.J[bb * NC] * cv[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) s = fma(A.J[bb * NC + k], cv[k], s);
+      out[bb] = s;
+    }
   }
   __syncthreads();
-  // y: out[yf][xf] = sum_ac J[a][ac] Tt[eyl*PC + ac][xf]
-  for (int idx = tid; idx < OX * OX; idx += NT) {
-    const int yf = idx / OX, xf = idx - yf * OX;
-    const int eyl = yf / PF, a = yf - eyl * PF;
+  // y: out[eyl*PF + a][xf] = sum_ac J[a][ac] Tt[eyl*PC + ac][xf]
+  for (int it = tid; it < T * OX; it += NT) {
+    const int eyl = it / OX, xf = it - eyl * OX;
     const double* t = Tt + (eyl * PC) * OX + xf;
-    const double* j = Js + a * NC;
-    double s = j[0] * t[0];
+    double tv[NC];
 #pragma unroll
-    for (int k = 1; k < NC; ++k) s = fma(j[k], t[k * OX], s);
-    A.dst[(size_t)(Yf0 + yf) * Nxf + (Xf0 + xf)] = A.accumulate ? UF[idx] + s : s;
+    for (int k = 0; k < NC; ++k) tv[k] = t[k * OX];
+#pragma unroll
+    for (int a = 0; a < PF; ++a) {
+      double s = A.J[a * NC] * tv[0];
+#pragma unroll
+      for (int k = 1; k < NC; ++k) s = fma(A.J[a * NC + k], tv[k], s);
+      const int yf = eyl * PF + a;
+      A.dst[(size_t)(Yf0 + yf) * Nxf + (Xf0 + xf)] = A.accumulate ? UF[yf * DF + shf + xf] + s : s;
+    }
   }
 }
 
@@ -91,55 +125,97 @@ __global__ void __launch_bounds__(256) restrict_kernel(const __grid_constant__ T
   SMG_PDL_ENTRY();
   using G = TrGeom<PC, PF, T>;
   constexpr int NC = G::NC, NF = G::NF, FX = G::FX, OX = G::OXC, NT = G::NT;
-  extern __shared__ double sm[];
-  double* F = sm;              // FX x FX fine own rows/cols of elements [t0-1, t0+T)
-  double* Tx = F + FX * FX;    // FX x OX  (x-restricted)
-  double* Js = Tx + FX * OX;   // NF x NC
+  extern __shared__ __align__(16) double sm[];
+  constexpr int DX = G::DX;
+  double* F = sm;              // FX x DX fine own rows/cols of elements [t0-1, t0+T) (column shift shx)
+  double* Tx = F + DX * FX;    // FX x OX  (x-restricted)
+  double* VT = Tx + FX * OX;   // FX x (T+1) vertex terms of the x pass
+  double* S = VT + FX * (T + 1);  // OX x OX  (y-restricted, before the vertex terms)
+  double* VY = S + OX * OX;    // (T+1) x OX vertex terms of the y pass
+  uint64_t* bar = reinterpret_cast<uint64_t*>(VY + (T + 1) * OX);
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int Nxf = A.n_x * PF, Nyf = A.n_y * PF, Nxc = A.n_x * PC;
   const int Xf0 = (tx * T - 1) * PF, Yf0 = (ty * T - 1) * PF;
-  for (int idx = tid; idx < FX * FX; idx += NT) {
-    const int y = idx / FX, x = idx - y * FX;
-    tr_cp_async8(F + idx, A.src + (size_t)wrapi(Yf0 + y, Nyf) * Nxf + wrapi(Xf0 + x, Nxf));
-  }
-  for (int idx = tid; idx < NF * NC; idx += NT) Js[idx] = A.J[idx];
-  asm volatile("cp.async.wait_all;\n" ::);
-  __syncthreads();
-  // x: Tx[yf][xc] = sum_{b<PF} J[b][ac] F[yf][(exl+1) PF + b]  (+ left element's ac = PC term)
-  for (int idx = tid; idx < FX * OX; idx += NT) {
-    const int yf = idx / OX, xc = idx - yf * OX;
-    const int exl = xc / PC, ac = xc - exl * PC;
-    const double* f = F + yf * FX + (exl + 1) * PF;
-    double s = Js[ac] * f[0];
-#pragma unroll
-    for (int b = 1; b < PF; ++b) s = fma(Js[b * NC + ac], f[b], s);
-    if (ac == 0) {
-      const double* fl = f - PF;
-      double s2 = Js[PC] * fl[0];
-#pragma unroll
-      for (int b = 1; b < PF; ++b) s2 = fma(Js[b * NC + PC], fl[b], s2);
-      s += s2;
+  int shx = 0;
+  if (A.bulk) {
+    shx = pwin_shift(Xf0, Nxf);
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar, pwin_bytes(FX, FX, shx));
     }
-    Tx[idx] = s;
+    __syncthreads();
+    if (tid < 32) pwin_issue_warp(A.src, Nxf, Nyf, Xf0, Yf0, FX, FX, F, DX, bar);
+  } else {
+    for (int idx = tid; idx < FX * FX; idx += NT) {
+      const int y = idx / FX, x = idx - y * FX;
+      tr_cp_async8(F + y * DX + x, A.src + (size_t)wrapi(Yf0 + y, Nyf) * Nxf + wrapi(Xf0 + x, Nxf));
+    }
+  }
+  if (A.bulk) mbar_wait(bar, 0);
+  else asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  // Register-blocked passes (see prolong_kernel).  Element e in [0, T] of
+  // the staged fine rows is tile element e-1 (e = 0: the left/lower halo
+  // element, which only contributes its ac = PC vertex term).
+  // x: s[ac] = sum_{b<PF} J[b][ac] F[yf][e PF + b]; the coarse vertex ac = 0
+  //    of element e-1 later adds element e-2's ac = PC term (VT)
+  for (int it = tid; it < FX * (T + 1); it += NT) {
+    const int yf = it / (T + 1), e = it - yf * (T + 1);
+    const double* f = F + yf * DX + shx + e * PF;
+    double s[NC];
+    {
+      const double f0 = f[0];
+#pragma unroll
+      for (int ac = 0; ac < NC; ++ac) s[ac] = A.J[ac] * f0;
+    }
+#pragma unroll
+    for (int bb = 1; bb < PF; ++bb) {
+      const double fb = f[bb];
+#pragma unroll
+      for (int ac = 0; ac < NC; ++ac) s[ac] = fma(A.J[bb * NC + ac], fb, s[ac]);
+    }
+    VT[yf * (T + 1) + e] = s[PC];
+    if (e > 0) {
+#pragma unroll
+      for (int ac = 0; ac < PC; ++ac) Tx[yf * OX + (e - 1) * PC + ac] = s[ac];
+    }
   }
   __syncthreads();
-  // y: out[yc][xc] = sum_{a<PF} J[a][acy] Tx[(eyl+1) PF + a][xc]  (+ lower element's PC term)
+  // y: same along columns on the vertex-combined rows Tx[yf][xc] (+ VT at ac = 0)
+  for (int it = tid; it < (T + 1) * OX; it += NT) {
+    const int e = it / OX, xc = it - e * OX;
+    const int exl = xc / PC;
+    const bool v0 = xc - exl * PC == 0;
+    auto tv = [&](int yf) {
+      const double v = Tx[yf * OX + xc];
+      return v0 ? v + VT[yf * (T + 1) + exl] : v;
+    };
+    double s[NC];
+    {
+      const double t0 = tv(e * PF);
+#pragma unroll
+      for (int ac = 0; ac < NC; ++ac) s[ac] = A.J[ac] * t0;
+    }
+#pragma unroll
+    for (int a = 1; a < PF; ++a) {
+      const double ta = tv(e * PF + a);
+#pragma unroll
+      for (int ac = 0; ac < NC; ++ac) s[ac] = fma(A.J[a * NC + ac], ta, s[ac]);
+    }
+    VY[e * OX + xc] = s[PC];
+    if (e > 0) {
+#pragma unroll
+      for (int ac = 0; ac < PC; ++ac) S[((e - 1) * PC + ac) * OX + xc] = s[ac];
+    }
+  }
+  __syncthreads();
   for (int idx = tid; idx < OX * OX; idx += NT) {
     const int yc = idx / OX, xc = idx - yc * OX;
-    const int eyl = yc / PC, ac = yc - eyl * PC;
-    const double* t = Tx + ((eyl + 1) * PF) * OX + xc;
-    double s = Js[ac] * t[0];
-#pragma unroll
-    for (int a = 1; a < PF; ++a) s = fma(Js[a * NC + ac], t[a * OX], s);
-    if (ac == 0) {
-      const double* tl = t - PF * OX;
-      double s2 = Js[PC] * tl[0];
-#pragma unroll
-      for (int a = 1; a < PF; ++a) s2 = fma(Js[a * NC + PC], tl[a * OX], s2);
-      s += s2;
-    }
-    A.dst[(size_t)(ty * OX + yc) * Nxc + (tx * OX + xc)] = s;
+    const int eyl = yc / PC;
+    const double v = S[idx];
+    A.dst[(size_t)(ty * OX + yc) * Nxc + (tx * OX + xc)] = (yc - eyl * PC == 0) ? v + VY[eyl * OX + xc] : v;
   }
 }
 
@@ -148,6 +224,11 @@ int tr_launch_t(const TrArgs& A0, bool prolong, cudaStream_t st) {
   using G = TrGeom<PC, PF, T>;
   TrArgs A = A0;
   A.tiles_x = A.n_x / T;
+  {
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const int nxc = A.n_x * PC, nxf = A.n_x * PF;
+    A.bulk = (nxc % 2 == 0) && (nxf % 2 == 0) && al16(A.src) && al16(A.dst) ? 1 : 0;
+  }
   const int grid = (A.n_x / T) * (A.n_y / T);
   if (prolong) {
     static bool attr = false;

@@ -9,6 +9,7 @@ struct TrArgs {
   const double* __restrict__ src;
   double* __restrict__ dst;
   int n_x, n_y, tiles_x, accumulate;
+  int bulk;                 // 1: bulk row copies (even row lengths, 16-byte aligned fields)
   double J[kTrMaxP * 17];   // J[a*(pc+1)+ac], a in [0,pf], ac in [0,pc]
 };
 
