@@ -52,6 +52,40 @@ def fd_flops_per_element(m: int) -> float:
     return 8.0 * m ** 3 + 3.0 * m ** 2
 
 
+def fd_eo_flops_per_element(m: int) -> float:
+    """Even/odd FD as executed by fdt_kernel (declare and report against
+    this): 4 contractions as two half-size ones each, 2 flops per FMA, + the
+    1/(lam_y+lam_x) scaling (the weight is folded into the synthesis factors)."""
+    he, ho = (m + 1) // 2, m // 2
+    return 8.0 * m * (he * he + ho * ho) + m * m
+
+
+def load_traffic():
+    """ncu dram__bytes_{read,write}.sum per launch of the C2 top-level kernels,
+    written by tools/ncu_traffic.py from one `ncu --set full` capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_c2.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def roofline_entry(name, t, flops, bytes_, p64, bw, traffic=None, note=None):
+    """Roofline of one kernel (call): bound = the larger of flops/P64 and bytes/BW."""
+    t_f, t_b = flops / p64, bytes_ / bw
+    if t_b >= t_f:
+        ent = {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": bw / 1e9, "unit": "GB/s"}
+    else:
+        ent = {"bound": "tensor", "pipe": "fp64", "achieved": flops / t / 1e12, "peak": p64 / 1e12,
+               "unit": "TFLOP/s"}
+    ent["frac"] = ent["achieved"] / ent["peak"]
+    ent.update({"kernel": name, "us_per_call": 1e6 * t, "algorithmic_flops": flops, "algorithmic_bytes": bytes_,
+                "t_roof_us": 1e6 * max(t_f, t_b), "traffic": traffic})
+    if note:
+        ent["note"] = note
+    return ent
+
+
 def vcycle_roofline_seconds(n_x, n_y, orders, n_o_of, p64, bw):
     """sum over levels l >= 1 of max(F/P64, B/BW) for the sweep,
     the residual+restriction and the prolongation (coarse solve excluded)."""
@@ -67,7 +101,7 @@ def vcycle_roofline_seconds(n_x, n_y, orders, n_o_of, p64, bw):
         # sweep: residual (top level only; lower levels start from zero) + FD
         if top:
             t += max(f_apply / p64, 24.0 * N / bw)
-        t += max(n_el * fd_flops_per_element(m) / p64, 24.0 * N / bw)
+        t += max(n_el * fd_eo_flops_per_element(m) / p64, 24.0 * N / bw)
         # residual + restriction, prolongation
         t += max(f_apply / p64, 24.0 * N / bw)
         f_tr = 2.0 * n_el * ((p + 1) * (pc + 1) ** 2 + (p + 1) ** 2 * (pc + 1))
@@ -366,35 +400,68 @@ def main():
         t_steps = float(tt.item())
     value = ndof * world * args.steps / t_steps
     ms_per_step = 1e3 * t_steps / args.steps
-
-    # ---- dominant kernel: the fused FD Schwarz correction on the top level
-    sm = h.top.smoother
-    r = torch.randn(shape, dtype=torch.float64, device=dev)
-    ucor = torch.zeros(shape, dtype=torch.float64, device=dev)
-    reps = 20
-    sm.correct(r, ucor)
-    fd_times = []
-    for _ in range(reps):
-        flush.fill_(1.0)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        sm.correct(r, ucor)
-        b.record()
-        fd_times.append((a, b))
-    torch.cuda.synchronize()
-    t_fd = float(np.mean([a.elapsed_time(b) for a, b in fd_times])) / 1e3
-    m = c["p"] + 1 + 2 * rule.layers(c["p"])
-    fd_flops = mesh.n_el * fd_flops_per_element(m)
-    fd_achieved = fd_flops / t_fd / 1e12
-    roofline = {"bound": "tensor", "pipe": "fp64", "kernel": "fd_kernel<19> (fused Schwarz FD, 4 colour launches)",
-                "achieved": fd_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": fd_achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "measured FP64 DMMA peak (tools/peaks/fp64_peaks.cu); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "algorithmic_flops_per_call": fd_flops, "ms_per_call": 1e3 * t_fd}
     orders = [lv.basis.p for lv in h.levels]
-    t_roof = vcycle_roofline_seconds(mesh.n_x, mesh.n_y, orders, rule.layers, p64, bw * 1e9)
+    t_roof_vc = vcycle_roofline_seconds(mesh.n_x, mesh.n_y, orders, rule.layers, p64, bw * 1e9)
 
+    # ---- top-level kernels, each timed alone (CUDA events on the launching
+    # stream, L2 flushed before every call); the dominant one (largest share of
+    # a V-cycle: the residual runs twice per cycle) is reported as `roofline`
+    top = h.top
+    st = NV.stream()
+    r_in = torch.randn(shape, dtype=torch.float64, device=dev)
+    u_in = torch.randn(shape, dtype=torch.float64, device=dev)
+    out = torch.empty_like(r_in)
+    fc = h.levels[-2].f
+    uc = torch.randn(h.levels[-2].f.shape, dtype=torch.float64, device=dev)
+    calls = {
+        "residual": (lambda: NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(u_in), NV.ptr(r_in), NV.ptr(out), st)), 2),
+        "schwarz": (lambda: NV.check(lib.smg_schwarz_correct(top.smoother._h.raw, NV.ptr(r_in), NV.ptr(out), st)), 1),
+        "restrict": (lambda: NV.check(lib.smg_restrict(top.transfer.handle.raw, NV.ptr(r_in), NV.ptr(fc), st)), 1),
+        "prolong": (lambda: NV.check(lib.smg_prolongate(top.transfer.handle.raw, NV.ptr(uc), NV.ptr(out), 1, st)), 1),
+    }
+    t_call = {}
+    for nm, (fn, _) in calls.items():
+        fn()
+        evs = []
+        for _ in range(20):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        t_call[nm] = float(np.mean([a.elapsed_time(b) for a, b in evs])) / 1e3
+    m = c["p"] + 1 + 2 * rule.layers(c["p"])
+    pc = h.levels[-2].basis.p
+    npp = c["p"] + 1
+    n_el = mesh.n_el
+    ndof_c = n_el * pc * pc
+    f_tr = 2.0 * n_el * ((c["p"] + 1) * (pc + 1) ** 2 + (c["p"] + 1) ** 2 * (pc + 1))
+    tr_all = load_traffic()
+
+    def tb(*names):
+        v = [tr_all[n]["bytes_per_launch"] for n in names if n in tr_all]
+        return float(sum(v)) if len(v) == len(names) else None
+    kern = {
+        "residual": roofline_entry("op_kernel<16,2,2,Poisson> (r = f - A u)", t_call["residual"],
+                                   n_el * (4 * npp ** 3 + 3 * npp ** 2) + ndof, 24.0 * ndof, p64, bw * 1e9,
+                                   tb("op_kernel")),
+        "schwarz": roofline_entry("fdt_kernel<16,1,4,2> + fdt_fixup (one Schwarz correction)", t_call["schwarz"],
+                                  n_el * fd_eo_flops_per_element(m), 24.0 * ndof, p64, bw * 1e9,
+                                  tb("fdt_kernel", "fdt_fixup"),
+                                  note="even/odd flop count (SURVEY 8(d)); dense-FD equivalent "
+                                       f"{n_el * fd_flops_per_element(m) / t_call['schwarz'] / 1e12:.2f} TF"),
+        "restrict": roofline_entry("restrict_kernel<8,16,2>", t_call["restrict"], f_tr, 8.0 * ndof + 8.0 * ndof_c,
+                                   p64, bw * 1e9, tb("restrict_kernel")),
+        "prolong": roofline_entry("prolong_kernel<8,16,2> (u_f += P u_c)", t_call["prolong"], f_tr,
+                                  16.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9, tb("prolong_kernel")),
+    }
+    dom = max(calls, key=lambda k: calls[k][1] * t_call[k])
+    roofline = dict(kern[dom])
+    roofline["share_of_step"] = calls[dom][1] * t_call[dom] / (ms_per_step / 1e3)
+    roofline["peak_source"] = (f"HBM {bw} GB/s ({bw_src}); FP64 {FP64_PEAK_TFLOPS} TF = measured DMMA "
+                               "peak (tools/peaks/fp64_peaks.cu; MEASURED_PEAKS.json has no FP64 entry)")
     # ---- end to end through the public API with host buffers
     f_pin = torch.from_numpy(f_host).pin_memory()
     u_pin = torch.empty(shape, dtype=torch.float64).pin_memory()
@@ -446,10 +513,14 @@ def main():
                 torch.cuda.synchronize()
                 tt = float(np.median([a.elapsed_time(b) for a, b in evs])) / 1e3
                 mm = p + 3
-                fl = msh.n_el * fd_flops_per_element(mm)
+                fl = msh.n_el * fd_eo_flops_per_element(mm)
+                by = 24.0 * lay.size
+                t_roof = max(fl / p64, by / (bw * 1e9))
                 micro[f"{n_el1d}x{n_el1d}_p{p}"] = {
-                    "gdof_s": lay.size / tt / 1e9, "tflops": fl / tt / 1e12,
-                    "frac_fp64": fl / tt / 1e12 / FP64_PEAK_TFLOPS, "us": 1e6 * tt}
+                    "gdof_s": lay.size / tt / 1e9, "us": 1e6 * tt, "tflops_eo": fl / tt / 1e12,
+                    "gbs": by / tt / 1e9, "bound": "hbm" if by / (bw * 1e9) >= fl / p64 else "fp64",
+                    "frac": t_roof / tt,
+                    "tflops_dense_equiv": msh.n_el * fd_flops_per_element(mm) / tt / 1e12}
                 del sm2, rr, uu
 
     cpu = None
@@ -472,11 +543,12 @@ def main():
                            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
                            "l2": "flushed (256 MiB write) before every timed step",
                            "cuda_graph": True},
-                "vcycle_roofline": {"t_roof_us": 1e6 * t_roof, "t_measured_us": ms_per_step * 1e3,
-                                    "frac": t_roof / (ms_per_step / 1e3),
+                "vcycle_roofline": {"t_roof_us": 1e6 * t_roof_vc, "t_measured_us": ms_per_step * 1e3,
+                                    "frac": t_roof_vc / (ms_per_step / 1e3),
                                     "model": "SURVEY.md §8(d) sum of max(F/P64, B/BW) over levels, "
                                              f"P64={FP64_PEAK_TFLOPS} TF, BW={bw} GB/s ({bw_src}), coarse excluded"},
-                "roofline": roofline, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+                "roofline": roofline, "top_level_kernels": kern, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks, "wall_s_timed_region": t_wall}
         if cpu is not None:
             line["cpu_baseline"] = cpu
