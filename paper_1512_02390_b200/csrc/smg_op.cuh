@@ -22,6 +22,7 @@
 // contributions of neighbouring elements in shared memory.  Fused outputs:
 // r = f - A u (f may be absent) and per-CTA partials of ||r||^2.
 #pragma once
+#include <cmath>
 #include "smg_common.cuh"
 #include "smg_tma.cuh"
 
@@ -38,6 +39,12 @@ struct OpArgs {
   int bulk;                          // 1: bulk row copies (N_x even, 16-byte aligned fields)
   double cx, cy;
   double Mt[(P + 1) * (P + 1)];      // Poisson: stiffness L-hat; diffusion: D (row-major)
+  // Poisson even/odd halves of L-hat (centro-symmetric): row b, pair k
+  //   Le[b][k] = (L[b][k] + L[b][P-k]) / 2 (k < H), Le[b][H] = L[b][H] (odd P+1)
+  //   Lo[b][k] = (L[b][k] - L[b][P-k]) / 2
+  double Le[((P + 1) / 2 + 1) * ((P + 1) / 2 + 1)];
+  double Lo[((P + 1) / 2) * ((P + 1) / 2) + 1];
+  int eo;                            // 1: use the even/odd halves (host-checked symmetry)
   double w[P + 1];
   double wasm[P];                    // assembled weight by local index a in [0,p)
 };
@@ -48,11 +55,10 @@ struct OpGeom {
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int HX = OX + P + 1, HY = OY + P + 1;
   static constexpr int DP = (HX + 2) & ~1;     // staged row pitch (room for the bulk-copy shift)
-  static constexpr int DPF = (OX + 2) & ~1;
   static constexpr int ROWJ = OY * (TX + 1), COLJ = OX * (TY + 1);
   static constexpr int THREADS = (ROWJ > COLJ ? ROWJ : COLJ) >= 256 ? 256 : (((ROWJ > COLJ ? ROWJ : COLJ) + 31) / 32) * 32;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY * (DIFF ? 2 : 1) + (size_t)DPF * OY + 2 * (size_t)OX * OY +
-                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1)) + 16;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY * (DIFF ? 2 : 1) + (size_t)OX * OY +
+                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1) + P) + 16;
 };
 
 __device__ __forceinline__ void op_cp_async8(double* smem, const double* gmem) {
@@ -67,7 +73,51 @@ __device__ __forceinline__ void op_cp_async8(double* smem, const double* gmem) {
 template <int P, bool DIFF, bool ONLY_LAST, int ST>
 __device__ __forceinline__ void line_op(const OpArgs<P>& A, const double* x, const double* nu, double (&v)[P + 1]) {
   constexpr int NP = P + 1;
-  if (!DIFF) {
+  if (!DIFF && A.eo) {
+    // x = sym + antisym: L maps each onto itself (JLJ = L), so with
+    // a_k = x_k + x_{P-k}, d_k = x_k - x_{P-k} (and the centre c):
+    //   E_b = sum_k Le[b][k] a_k (+ Le[b][H] c),  O_b = sum_k Lo[b][k] d_k,
+    //   v_b = E_b + O_b,  v_{P-b} = E_b - O_b   -- half the FMAs
+    constexpr int H = NP / 2;
+    constexpr bool MID = (NP & 1) != 0;
+    constexpr int HC = H + (MID ? 1 : 0);
+    double a[H], d[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const double xk = x[k * ST], xm = x[(P - k) * ST];
+      a[k] = xk + xm;
+      d[k] = xk - xm;
+    }
+    const double c = MID ? x[H * ST] : 0.0;
+    if (ONLY_LAST) {
+      double e = MID ? A.Le[H] * c : 0.0, o = 0.0;
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        e = fma(A.Le[k], a[k], e);
+        o = fma(A.Lo[k], d[k], o);
+      }
+      v[P] = e - o;
+    } else {
+      double e[HC], o[H > 0 ? H : 1];
+#pragma unroll
+      for (int b = 0; b < HC; ++b) e[b] = MID ? A.Le[b * HC + H] * c : 0.0;
+#pragma unroll
+      for (int b = 0; b < H; ++b) o[b] = 0.0;
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+#pragma unroll
+        for (int b = 0; b < HC; ++b) e[b] = fma(A.Le[b * HC + k], a[k], e[b]);
+#pragma unroll
+        for (int b = 0; b < H; ++b) o[b] = fma(A.Lo[b * H + k], d[k], o[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < H; ++b) {
+        v[b] = e[b] + o[b];
+        v[P - b] = e[b] - o[b];
+      }
+      if (MID) v[H] = e[H];
+    }
+  } else if (!DIFF) {
     if (ONLY_LAST) {
       double s = A.Mt[P] * x[0];
 #pragma unroll
@@ -119,39 +169,34 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   using G = OpGeom<P, TX, TY, DIFF>;
   constexpr int NP = G::NP, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, NT = G::THREADS;
   extern __shared__ __align__(16) double sm[];
-  constexpr int DP = G::DP, DPF = G::DPF;
+  constexpr int DP = G::DP;
+  constexpr int KO = (OX * OY + NT - 1) / NT;     // output nodes per thread
   double* U = sm;                                  // HY x DP, origin (Y0-P, X0-P) at column sh
   double* NU = U + DP * HY;                        // diffusion only
-  double* F = NU + (DIFF ? DP * HY : 0);           // OY x DPF, origin (Y0, X0) at column shf
-  double* AX = F + DPF * OY;                       // OY x OX
-  double* AY = AX + OX * OY;                       // OY x OX
-  double* VX = AY + OX * OY;                       // OY x (TX+1): right-vertex value of element exl-1
+  double* AX = NU + (DIFF ? DP * HY : 0);          // OY x OX: row-pass values, then x+y parts
+  double* VX = AX + OX * OY;                       // OY x (TX+1): right-vertex value of element exl-1
   double* VY = VX + OY * (TX + 1);                 // OX x (TY+1)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(VY + OX * (TY + 1));
+  double* WS = VY + OX * (TY + 1);                 // P assembled weights (indexed per thread)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WS + P);
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int X0 = tx * OX, Y0 = ty * OY;
   const int N_x = A.N_x, N_y = A.N_y;
 
-  int sh = 0, shf = 0;
+  int sh = 0;
   if (A.bulk) {
     // bulk row copies issued by warp 0 (periodic wrap handled per row)
     sh = pwin_shift(X0 - P, N_x);
-    shf = pwin_shift(X0, N_x);
     if (tid == 0) {
       mbar_init(bar, 1);
       fence_mbar_init();
-      unsigned bytes = pwin_bytes(HX, HY, sh) * (DIFF ? 2u : 1u);
-      if (A.f != nullptr) bytes += pwin_bytes(OX, OY, shf);
-      mbar_arrive_expect_tx(bar, bytes);
+      mbar_arrive_expect_tx(bar, pwin_bytes(HX, HY, sh) * (DIFF ? 2u : 1u));
     }
     __syncthreads();
     if (tid < 32) {
       pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
       if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
-      if (A.f != nullptr) pwin_issue_warp(A.f, N_x, N_y, X0, Y0, OX, OY, F, DPF, bar);
     }
-    mbar_wait(bar, 0);
   } else {
     for (int idx = tid; idx < HX * HY; idx += NT) {
       const int hy = idx / HX, hx = idx - hy * HX;
@@ -159,14 +204,18 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
       op_cp_async8(U + hy * DP + hx, A.u + g);
       if (DIFF) op_cp_async8(NU + hy * DP + hx, A.nu + g);
     }
-    if (A.f != nullptr) {
-      for (int idx = tid; idx < OX * OY; idx += NT) {
-        const int y = idx / OX, x = idx - y * OX;
-        op_cp_async8(F + y * DPF + x, A.f + (size_t)(Y0 + y) * N_x + (X0 + x));
-      }
-    }
-    asm volatile("cp.async.wait_all;\n" ::);
   }
+  // f of this thread's output nodes: in flight while the window lands and
+  // the line passes run
+  double fv[KO];
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int idx = tid + k * NT;
+    fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
+  }
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  if (A.bulk) mbar_wait(bar, 0);
+  else asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 
   // row passes: item = (own row y, element exl-1), exl in [0, TX]
@@ -185,7 +234,11 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
     }
     VX[y * (TX + 1) + exl] = v[P];
   }
-  // column passes: item = (own column x, element eyl-1), eyl in [0, TY]
+  __syncthreads();
+  // column passes: item = (own column x, element eyl-1), eyl in [0, TY]; each
+  // node of the item's column gets its full x-part (with the vertex term of
+  // the left element) and its own y-part; the y-vertex term of the element
+  // below (a == 0) is added in the output pass
   for (int it = tid; it < OX * (TY + 1); it += NT) {
     const int x = it / (TY + 1), eyl = it - x * (TY + 1);
     const double* uc = U + (eyl * P) * DP + sh + (x + P);
@@ -195,25 +248,34 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
       line_op<P, DIFF, true, DP>(A, uc, nc, v);
     } else {
       line_op<P, DIFF, false, DP>(A, uc, nc, v);
-      double* ay = AY + ((eyl - 1) * P) * OX + x;
+      const int exl = x / P, b = x - exl * P;
+      const double wyb = A.cy * WS[b];
+      double* axc = AX + ((eyl - 1) * P) * OX + x;
+      const double* vx = VX + ((eyl - 1) * P) * (TX + 1) + exl;
 #pragma unroll
-      for (int a = 0; a < P; ++a) ay[a * OX] = v[a];
+      for (int a = 0; a < P; ++a) {
+        double ax = axc[a * OX];
+        if (b == 0) ax += vx[a * (TX + 1)];
+        axc[a * OX] = fma(A.cx * A.wasm[a], ax, wyb * v[a]);
+      }
     }
     VY[x * (TY + 1) + eyl] = v[P];
   }
   __syncthreads();
 
   double nrm = 0.0;
-  for (int idx = tid; idx < OX * OY; idx += NT) {
-    const int y = idx / OX, x = idx - y * OX;
-    const int a = y % P, b = x % P;
-    double ax = AX[idx], ay = AY[idx];
-    if (b == 0) ax += VX[y * (TX + 1) + x / P];
-    if (a == 0) ay += VY[x * (TY + 1) + y / P];
-    const double val = A.cx * A.wasm[a] * ax + A.cy * A.wasm[b] * ay;
-    const double r = A.f != nullptr ? F[y * DPF + shf + x] - val : val;
-    A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = r;
-    nrm = fma(r, r, nrm);
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int idx = tid + k * NT;
+    if (idx < OX * OY) {
+      const int y = idx / OX, x = idx - y * OX;
+      const int a = y % P, b = x % P;
+      double val = AX[idx];
+      if (a == 0) val = fma(A.cy * WS[b], VY[x * (TY + 1) + y / P], val);
+      const double r = A.f != nullptr ? fv[k] - val : val;
+      A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = r;
+      nrm = fma(r, r, nrm);
+    }
   }
   if (A.partials != nullptr) {
     __shared__ double red[32];
@@ -245,8 +307,27 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   A.N_x = L.n_x * P; A.N_y = L.n_y * P; A.tiles_x = L.n_x / TX;
   A.cx = L.cx; A.cy = L.cy;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) && (L.f == nullptr || al16(L.f)) ? 1 : 0;
+  A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) ? 1 : 0;
   for (int i = 0; i < (P + 1) * (P + 1); ++i) A.Mt[i] = L.Mt[i];
+  {
+    // even/odd halves of the Poisson stiffness when it is centro-symmetric
+    constexpr int NP = P + 1, H = NP / 2, HC = H + (NP & 1);
+    auto Lbk = [&](int b, int k) { return L.Mt[k * NP + b]; };
+    double asym = 0.0, mx = 0.0;
+    for (int b = 0; b < NP; ++b)
+      for (int k = 0; k < NP; ++k) {
+        asym = std::fmax(asym, std::fabs(Lbk(b, k) - Lbk(P - b, P - k)));
+        mx = std::fmax(mx, std::fabs(Lbk(b, k)));
+      }
+    A.eo = (!DIFF && asym <= 1e-14 * mx) ? 1 : 0;
+    for (int b = 0; b < HC; ++b) {
+      for (int k = 0; k < H; ++k) A.Le[b * HC + k] = 0.5 * (Lbk(b, k) + Lbk(b, P - k));
+      if (NP & 1) A.Le[b * HC + H] = Lbk(b, H);
+    }
+    for (int b = 0; b < H; ++b)
+      for (int k = 0; k < H; ++k) A.Lo[b * H + k] = 0.5 * (Lbk(b, k) - Lbk(b, P - k));
+    A.Lo[H * H] = 0.0;
+  }
   for (int i = 0; i < P + 1; ++i) A.w[i] = L.w[i];
   for (int i = 0; i < P; ++i) A.wasm[i] = L.wasm[i];
   static bool attr = false;
