@@ -22,6 +22,14 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool sync_check_enabled() {
+  static const bool on = [] {
+    const char* s = getenv("SMG_SYNC_CHECK");
+    return s && s[0] == '1';
+  }();
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("SMG_PDL");
@@ -49,6 +57,8 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st);
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
+int pinv_cluster(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f, double* u,
+                 cudaStream_t st);
 int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
                double* tmp, double* u, cudaStream_t st);
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
@@ -535,7 +545,12 @@ int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double*
   const int nx = h->n_x, ny = h->n_y;
   double* T1 = ws;
   double* T2 = ws + (size_t)nx * ny;
-  int rc = pinv_small(nx, ny, h->Qx, h->Qy, h->Lp, f0, T1, u0, st);
+  // single-launch cluster variant: opt-in (SMG_PINV_CLUSTER=1) until it beats
+  // the two-launch row-block path (measured 30 us vs 16 us at 64 x 64)
+  int rc = getenv("SMG_PINV_CLUSTER") && getenv("SMG_PINV_CLUSTER")[0] == '1'
+               ? pinv_cluster(nx, ny, h->Qx, h->Qy, h->Lp, f0, u0, st) : 1;
+  if (rc != 1) return rc;
+  rc = pinv_small(nx, ny, h->Qx, h->Qy, h->Lp, f0, T1, u0, st);
   if (rc != 1) return rc;
   // T1 = Qy^T F ; T2 = (T1 Qx) .* Lp ; T1 = Qy T2 ; U = T1 Qx^T
   if ((rc = gemm(ny, nx, ny, h->Qy, ny, 1, f0, nx, 0, T1, nx, nullptr, st))) return rc;

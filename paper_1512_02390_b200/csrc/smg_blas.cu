@@ -3,7 +3,10 @@
 // tree (grid-stride partials -> per-block tree -> last block sums the
 // partials in block order), so results are bitwise reproducible run to run
 // (the reference's test_krylov.py:73-81 demands identical histories).
+#include <cooperative_groups.h>
+
 #include "smg_common.cuh"
+#include "smg_tma.cuh"
 
 namespace smg {
 
@@ -373,6 +376,109 @@ __global__ void __launch_bounds__(256) pinv_rows_kernel(int nx, int ny, const do
       out[(size_t)row * nx + x] = v;
     }
   }
+}
+
+// ---- single-launch coarse pseudo-inverse on a thread-block cluster ----------
+// For n_x, n_y <= 64 (the C1/C2 coarse levels) the whole solve
+//   u = Q_y (Lp .* ((Q_y^T F) Q_x)) Q_x^T
+// runs in ONE launch of a cluster of kCl CTAs (one SM each).  Every CTA
+// bulk-copies F, Q_x, Q_y and its Lp rows into shared memory, computes its
+// block of rows of T2 = (Q_y^T F) Q_x .* Lp, the cluster exchanges the T2
+// blocks through distributed shared memory (after barrier.cluster), and each
+// CTA finishes its rows of U = (Q_y T2) Q_x^T.  Same products, same k order
+// as the two-launch path.
+constexpr int kCl = 8;
+constexpr int kClMax = 64;
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(256)
+pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double* __restrict__ Qy,
+                    const double* __restrict__ Lp, const double* __restrict__ f, double* __restrict__ u) {
+  SMG_PDL_ENTRY();
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  extern __shared__ __align__(16) double smc[];
+  const int rank = (int)cl.block_rank();
+  const int rb = (ny + kCl - 1) / kCl;          // rows per CTA
+  const int i0 = rank * rb, ni = max(0, min(rb, ny - i0));
+  double* F = smc;                               // ny x nx
+  double* QY = F + ny * nx;                      // ny x ny
+  double* QX = QY + ny * ny;                     // nx x nx
+  double* T2 = QX + nx * nx;                     // ny x nx (own rows computed, the rest gathered)
+  double* T1 = T2 + ny * nx;                     // rb x nx
+  double* LP = T1 + rb * nx;                     // rb x nx
+  uint64_t* bar = reinterpret_cast<uint64_t*>(LP + rb * nx);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const unsigned b = (unsigned)(8 * (ny * nx + ny * ny + nx * nx)) + (unsigned)(8 * ni * nx);
+    mbar_arrive_expect_tx(bar, b);
+    bulk_g2s(F, f, (unsigned)(8 * ny * nx), bar);
+    bulk_g2s(QY, Qy, (unsigned)(8 * ny * ny), bar);
+    bulk_g2s(QX, Qx, (unsigned)(8 * nx * nx), bar);
+    if (ni > 0) bulk_g2s(LP, Lp + (size_t)i0 * nx, (unsigned)(8 * ni * nx), bar);
+  }
+  __syncthreads();  // nobody polls the mbarrier before thread 0 has initialised it
+  mbar_wait(bar, 0);
+  __syncthreads();
+  // T1[i][x] = sum_k Qy[k][i0+i] F[k][x]
+  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+    const int i = idx / nx, x = idx - i * nx;
+    double s = 0.0;
+    for (int k = 0; k < ny; ++k) s = fma(QY[k * ny + i0 + i], F[k * nx + x], s);
+    T1[idx] = s;
+  }
+  __syncthreads();
+  // T2[i0+i][x] = (sum_j T1[i][j] Qx[j][x]) * Lp[i0+i][x]
+  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+    const int i = idx / nx, x = idx - i * nx;
+    double s = 0.0;
+    for (int j = 0; j < nx; ++j) s = fma(T1[i * nx + j], QX[j * nx + x], s);
+    T2[(i0 + i) * nx + x] = s * LP[idx];
+  }
+  cl.sync();
+  // gather the other CTAs' T2 rows through distributed shared memory
+  for (int c = 0; c < kCl; ++c) {
+    const int c0 = c * rb, cn = max(0, min(rb, ny - c0));
+    if (c == rank || cn == 0) continue;
+    const double* rem = cl.map_shared_rank(T2, c);
+    for (int idx = tid; idx < cn * nx; idx += blockDim.x) T2[c0 * nx + idx] = rem[c0 * nx + idx];
+  }
+  __syncthreads();
+  // T1[i][x] = sum_k Qy[i0+i][k] T2[k][x]
+  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+    const int i = idx / nx, x = idx - i * nx;
+    double s = 0.0;
+    for (int k = 0; k < ny; ++k) s = fma(QY[(i0 + i) * ny + k], T2[k * nx + x], s);
+    T1[idx] = s;
+  }
+  __syncthreads();
+  // u[i0+i][x] = sum_j T1[i][j] Qx[x][j]
+  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+    const int i = idx / nx, x = idx - i * nx;
+    double s = 0.0;
+    for (int j = 0; j < nx; ++j) s = fma(T1[i * nx + j], QX[x * nx + j], s);
+    u[(size_t)(i0 + i) * nx + x] = s;
+  }
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+}
+
+int pinv_cluster(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f, double* u,
+                 cudaStream_t st) {
+  if (nx > kClMax || ny > kClMax || (nx * ny) % 2 || (nx * nx) % 2 || (ny * ny) % 2) return 1;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(f) || !al16(Qx) || !al16(Qy) || !al16(Lp)) return 1;
+  const int rb = (ny + kCl - 1) / kCl;
+  if (((size_t)rb * nx) % 2) return 1;  // keep every row block 16-byte aligned
+  const size_t smem = sizeof(double) * (2 * (size_t)ny * nx + (size_t)ny * ny + (size_t)nx * nx + 2 * (size_t)rb * nx) + 16;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(pinv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "pinv_cluster_kernel smem attribute");
+    attr = smem;
+  }
+  launch(pinv_cluster_kernel, dim3(kCl), dim3(256), smem, st, nx, ny, Qx, Qy, Lp, f, u);
+  return check_launch("pinv_cluster_kernel");
 }
 
 int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,

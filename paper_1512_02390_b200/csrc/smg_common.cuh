@@ -19,10 +19,13 @@ int cuda_fail(cudaError_t e, const char* where);
 
 void count_launch();
 
+bool sync_check_enabled();  // SMG_SYNC_CHECK=1: synchronize after every launch (debug aid)
+
 // Return SMG_ECUDA with the pending launch error, if any (and count the launch).
 inline int check_launch(const char* where) {
   count_launch();
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_check_enabled()) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, where);
   return SMG_OK;
 }
