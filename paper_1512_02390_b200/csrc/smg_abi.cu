@@ -22,6 +22,11 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int env_int(const char* name, int def) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : def;
+}
+
 bool sync_check_enabled() {
   static const bool on = [] {
     const char* s = getenv("SMG_SYNC_CHECK");

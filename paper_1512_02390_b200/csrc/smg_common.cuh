@@ -77,6 +77,8 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double* sbuf /*32*
   } while (0)
 
 bool pdl_enabled();
+// Integer tuning knob from the environment (read once per name by the caller).
+int env_int(const char* name, int def);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -256,7 +256,8 @@ int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) 
   for (int t = T0; t >= 1; t /= 2) {
     if (n_x % t || n_y % t) continue;
     best = t;
-    if ((long)(n_x / t) * (n_y / t) >= 296) break;
+    static const int min_ctas = env_int("SMG_TR_MIN_CTAS", 296);
+    if ((long)(n_x / t) * (n_y / t) >= min_ctas) break;
   }
   switch (best) {
     case 16: if constexpr (T0 >= 16) return tr_launch_t<PC, PF, (T0 >= 16 ? 16 : 1)>(A, prolong, st); break;
