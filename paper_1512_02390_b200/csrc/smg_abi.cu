@@ -14,6 +14,7 @@
 #include "smg_fdm.cuh"
 #include "smg_op.cuh"
 #include "smg_transfer.cuh"
+#include "smg_rr.cuh"
 
 namespace smg {
 
@@ -480,6 +481,26 @@ int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* st
 int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,
                           double* fc, double* work, void* stream) {
   if (!h || !op || !u || !f || !fc || !work) { set_error("smg_residual_restrict: bad argument"); return SMG_EINVAL; }
+  // fused single launch (r never leaves shared memory) when compiled in and
+  // the fields allow 16-byte bulk row copies
+  // measured (tools/vcycle_breakdown.py, C2): fused wins at p_f <= 8 (4.3 vs
+  // 6.9 us at p_f = 2), loses at p_f = 16 (33 vs 22 us: 2.25x residual
+  // recompute, 63 KB tiles); SMG_RR_FUSED = 0 never, 1 p_f <= 8, 2 always
+  static const int fused = env_int("SMG_RR_FUSED", 1);
+  if ((fused == 2 || (fused == 1 && h->pf <= 8)) && op->p == h->pf && op->n_x == h->n_x && op->n_y == h->n_y && ((long)h->n_x * h->pf) % 2 == 0) {
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    RRFn fn = rr_dispatch(h->pc, h->pf, op->kind != 0, h->n_x, h->n_y);
+    if (fn && al16(u) && al16(f) && (op->kind == 0 || al16(op->nu))) {
+      RRLaunch R;
+      R.op.u = u; R.op.f = f; R.op.out = nullptr; R.op.nu = op->nu; R.op.partials = nullptr;
+      R.op.p = op->p; R.op.n_x = op->n_x; R.op.n_y = op->n_y; R.op.diffusion = op->kind;
+      R.op.cx = op->dy / op->dx; R.op.cy = op->dx / op->dy;
+      R.op.Mt = op->Mt.data(); R.op.w = op->w.data(); R.op.wasm = op->wasm.data();
+      R.fc = fc;
+      R.J = h->J.data();
+      return fn(R, as_stream(stream));
+    }
+  }
   int rc = smg_op_residual(op, u, f, work, stream);
   if (rc) return rc;
   return smg_restrict(h, work, fc, stream);

@@ -299,15 +299,11 @@ struct OpLaunch {
   const double* wasm; // host p
 };
 
-template <int P, int TX, int TY, bool DIFF>
-int op_launch_t(const OpLaunch& L, cudaStream_t st) {
-  using G = OpGeom<P, TX, TY, DIFF>;
-  OpArgs<P> A;
-  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = L.partials;
-  A.N_x = L.n_x * P; A.N_y = L.n_y * P; A.tiles_x = L.n_x / TX;
+// Host: operator constants of OpArgs (everything but the pointers / tiling).
+template <int P>
+void op_fill_consts(OpArgs<P>& A, const OpLaunch& L, bool diff) {
+  A.N_x = L.n_x * P; A.N_y = L.n_y * P;
   A.cx = L.cx; A.cy = L.cy;
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) ? 1 : 0;
   for (int i = 0; i < (P + 1) * (P + 1); ++i) A.Mt[i] = L.Mt[i];
   {
     // even/odd halves of the Poisson stiffness when it is centro-symmetric
@@ -319,7 +315,7 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
         asym = std::fmax(asym, std::fabs(Lbk(b, k) - Lbk(P - b, P - k)));
         mx = std::fmax(mx, std::fabs(Lbk(b, k)));
       }
-    A.eo = (!DIFF && asym <= 1e-14 * mx) ? 1 : 0;
+    A.eo = (!diff && asym <= 1e-14 * mx) ? 1 : 0;
     for (int b = 0; b < HC; ++b) {
       for (int k = 0; k < H; ++k) A.Le[b * HC + k] = 0.5 * (Lbk(b, k) + Lbk(b, P - k));
       if (NP & 1) A.Le[b * HC + H] = Lbk(b, H);
@@ -330,6 +326,17 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   }
   for (int i = 0; i < P + 1; ++i) A.w[i] = L.w[i];
   for (int i = 0; i < P; ++i) A.wasm[i] = L.wasm[i];
+}
+
+template <int P, int TX, int TY, bool DIFF>
+int op_launch_t(const OpLaunch& L, cudaStream_t st) {
+  using G = OpGeom<P, TX, TY, DIFF>;
+  OpArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = L.partials;
+  op_fill_consts<P>(A, L, DIFF);
+  A.tiles_x = L.n_x / TX;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
     if (G::SMEM > 48 * 1024) {

@@ -115,6 +115,33 @@ def test_transfers_vs_reference_and_adjoint(cuda_device):
         P.prolongate(h, 0, np.zeros((1, 1)))
 
 
+@pytest.mark.parametrize("case", [(64, 64, 16, None, (1, 2, 4, 8, 16)), (12, 8, 8, None, (1, 2, 4, 8)),
+                                  (16, 16, 24, 0.9, (1, 3, 6, 12, 24)), (6, 6, 32, None, (1, 2, 4, 8, 16, 32))])
+def test_fused_residual_restrict_bitwise(cuda_device, case):
+    """smg_residual_restrict (one fused launch where enabled: p_f <= 8 by default,
+    SMG_RR_FUSED=2 for all) == residual launch + restriction launch, bitwise."""
+    from paper_1512_02390_b200 import _native as NV
+    nx, ny, p, nu_hat, orders = case
+    h = P.build_hierarchy(P.MeshConfig(nx, ny, 1.0, 1.0), p, P.OverlapRule("fixed", 1), nu_hat=nu_hat,
+                          orders=orders)
+    lib = NV.lib()
+    st = NV.stream()
+    rng = np.random.default_rng(3)
+    for l in range(h.depth, 0, -1):
+        lv = h.levels[l]
+        u = dev(rng.standard_normal(lv.op.layout.shape))
+        f = dev(rng.standard_normal(lv.op.layout.shape))
+        fc1 = torch.empty_like(h.levels[l - 1].f)
+        fc2 = torch.empty_like(h.levels[l - 1].f)
+        work = torch.empty_like(u)
+        NV.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, NV.ptr(u), NV.ptr(f),
+                                           NV.ptr(fc1), NV.ptr(work), st), "rr")
+        NV.check(lib.smg_op_residual(lv.op._handle.raw, NV.ptr(u), NV.ptr(f), NV.ptr(work), st), "res")
+        NV.check(lib.smg_restrict(lv.transfer.handle.raw, NV.ptr(work), NV.ptr(fc2), st), "restrict")
+        torch.cuda.synchronize()
+        assert torch.equal(fc1, fc2), (case, l, float((fc1 - fc2).abs().max()))
+
+
 def test_transfers_p24_chain(cuda_device):
     mesh = P.MeshConfig(3, 4, 1.0, 1.0)
     h = P.build_hierarchy(mesh, 24, P.OverlapRule("fixed", 1), orders=(1, 3, 6, 12, 24), nu_hat=0.9, nu_shift=0.0)

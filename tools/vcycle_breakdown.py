@@ -42,13 +42,15 @@ for l in range(h.depth, 0, -1):
     t_rs = timeit(lambda: N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.work), N.ptr(fc), st)))
     uc = h.levels[l - 1].u
     t_pr = timeit(lambda: N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(uc), N.ptr(lv.u), 1, st)))
+    t_rr = timeit(lambda: N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                           N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st)))
     n_res = 2 if l == h.depth else 1
-    rows.append((lv.basis.p, t_res, t_fd, t_rs, t_pr))
+    rows.append((lv.basis.p, t_res, t_fd, t_rs, t_pr, t_rr))
     tot += n_res * t_res + t_fd + t_rs + t_pr
 f0, u0 = h.levels[0].f, h.levels[0].u
 t_c = timeit(lambda: N.check(lib.smg_coarse_pinv(h._pinv.handle.raw, N.ptr(f0), N.ptr(u0), N.ptr(h._pinv.ws), N.stream())))
 tot += t_c
-print(f"{'p':>3} {'residual':>9} {'schwarz':>9} {'restrict':>9} {'prolong':>9}   (us, warm, back-to-back)")
+print(f"{'p':>3} {'residual':>9} {'schwarz':>9} {'restrict':>9} {'prolong':>9} {'res+restr':>9}   (us, warm, back-to-back)")
 for r in rows:
-    print(f"{r[0]:3d} {r[1]:9.2f} {r[2]:9.2f} {r[3]:9.2f} {r[4]:9.2f}")
+    print(f"{r[0]:3d} {r[1]:9.2f} {r[2]:9.2f} {r[3]:9.2f} {r[4]:9.2f} {r[5]:9.2f}")
 print(f"coarse pinv {t_c:.2f} us;  sum of components (top residual x2) = {tot:.1f} us")
