@@ -390,7 +390,27 @@ __global__ void __launch_bounds__(256) pinv_rows_kernel(int nx, int ny, const do
 constexpr int kCl = 8;
 constexpr int kClMax = 64;
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(256)
+// K-term dot product with four independent partial sums (fixed order:
+// ((s0 + s1) + (s2 + s3))): the shared-memory load latency of one chain is
+// overlapped by the other three.
+__device__ __forceinline__ double dot4(const double* __restrict__ a, int sa, const double* __restrict__ b, int sb,
+                                       int K) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+#pragma unroll 4
+  for (; k + 3 < K; k += 4) {
+    s0 = fma(a[k * sa], b[k * sb], s0);
+    s1 = fma(a[(k + 1) * sa], b[(k + 1) * sb], s1);
+    s2 = fma(a[(k + 2) * sa], b[(k + 2) * sb], s2);
+    s3 = fma(a[(k + 3) * sa], b[(k + 3) * sb], s3);
+  }
+  for (; k < K; ++k) s0 = fma(a[k * sa], b[k * sb], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+
+constexpr int kClThreads = 512;
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
 pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double* __restrict__ Qy,
                     const double* __restrict__ Lp, const double* __restrict__ f, double* __restrict__ u) {
   SMG_PDL_ENTRY();
@@ -420,21 +440,16 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
   }
   __syncthreads();  // nobody polls the mbarrier before thread 0 has initialised it
   mbar_wait(bar, 0);
-  __syncthreads();
   // T1[i][x] = sum_k Qy[k][i0+i] F[k][x]
-  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+  for (int idx = tid; idx < ni * nx; idx += kClThreads) {
     const int i = idx / nx, x = idx - i * nx;
-    double s = 0.0;
-    for (int k = 0; k < ny; ++k) s = fma(QY[k * ny + i0 + i], F[k * nx + x], s);
-    T1[idx] = s;
+    T1[idx] = dot4(QY + i0 + i, ny, F + x, nx, ny);
   }
   __syncthreads();
   // T2[i0+i][x] = (sum_j T1[i][j] Qx[j][x]) * Lp[i0+i][x]
-  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+  for (int idx = tid; idx < ni * nx; idx += kClThreads) {
     const int i = idx / nx, x = idx - i * nx;
-    double s = 0.0;
-    for (int j = 0; j < nx; ++j) s = fma(T1[i * nx + j], QX[j * nx + x], s);
-    T2[(i0 + i) * nx + x] = s * LP[idx];
+    T2[(i0 + i) * nx + x] = dot4(T1 + i * nx, 1, QX + x, nx, nx) * LP[idx];
   }
   cl.sync();
   // gather the other CTAs' T2 rows through distributed shared memory
@@ -442,23 +457,19 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
     const int c0 = c * rb, cn = max(0, min(rb, ny - c0));
     if (c == rank || cn == 0) continue;
     const double* rem = cl.map_shared_rank(T2, c);
-    for (int idx = tid; idx < cn * nx; idx += blockDim.x) T2[c0 * nx + idx] = rem[c0 * nx + idx];
+    for (int idx = tid; idx < cn * nx; idx += kClThreads) T2[c0 * nx + idx] = rem[c0 * nx + idx];
   }
   __syncthreads();
   // T1[i][x] = sum_k Qy[i0+i][k] T2[k][x]
-  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+  for (int idx = tid; idx < ni * nx; idx += kClThreads) {
     const int i = idx / nx, x = idx - i * nx;
-    double s = 0.0;
-    for (int k = 0; k < ny; ++k) s = fma(QY[(i0 + i) * ny + k], T2[k * nx + x], s);
-    T1[idx] = s;
+    T1[idx] = dot4(QY + (i0 + i) * ny, 1, T2 + x, nx, ny);
   }
   __syncthreads();
   // u[i0+i][x] = sum_j T1[i][j] Qx[x][j]
-  for (int idx = tid; idx < ni * nx; idx += blockDim.x) {
+  for (int idx = tid; idx < ni * nx; idx += kClThreads) {
     const int i = idx / nx, x = idx - i * nx;
-    double s = 0.0;
-    for (int j = 0; j < nx; ++j) s = fma(T1[i * nx + j], QX[x * nx + j], s);
-    u[(size_t)(i0 + i) * nx + x] = s;
+    u[(size_t)(i0 + i) * nx + x] = dot4(T1 + i * nx, 1, QX + x * nx, 1, nx);
   }
   cl.sync();  // no CTA leaves while its shared memory may still be read
 }
@@ -477,7 +488,7 @@ int pinv_cluster(int nx, int ny, const double* Qx, const double* Qy, const doubl
     if (e != cudaSuccess) return cuda_fail(e, "pinv_cluster_kernel smem attribute");
     attr = smem;
   }
-  launch(pinv_cluster_kernel, dim3(kCl), dim3(256), smem, st, nx, ny, Qx, Qy, Lp, f, u);
+  launch(pinv_cluster_kernel, dim3(kCl), dim3(kClThreads), smem, st, nx, ny, Qx, Qy, Lp, f, u);
   return check_launch("pinv_cluster_kernel");
 }
 
