@@ -104,7 +104,8 @@ struct smg_schwarz {
   double* Sx_dev;
   double* Sy_dev;
   double* frag_dev;
-  bool dmma;
+  bool dmma;      // block-level dense DMMA kernel (smg_fdm.cuh)
+  bool eo_dmma;   // even/odd DMMA stages inside the TMA-pipelined tiled kernel
 };
 
 struct smg_transfer {
@@ -127,6 +128,9 @@ bool fd_prefers_dmma(int m) {
   (void)m;
   return false;
 }
+// tools/time_fd1.py on B200 (us, DFMA vs even/odd DMMA): 256^2 p=16 230 / 286,
+// p=24 585 / 593, 128^2 p=32 401 / 372 -> DMMA from m = 35 (p = 32) up
+bool fd_prefers_eo_dmma(int m) { return m >= 33; }
 
 // Split S (m x m, row-major S[k][i]) into symmetrized even/odd halves.
 // Returns false if some eigenvector is not (numerically) even or odd.
@@ -311,6 +315,7 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   // SMG_FD_ENGINE=dmma|dfma overrides the per-m default
   const char* eng = getenv("SMG_FD_ENGINE");
   s->dmma = eng ? (std::strcmp(eng, "dmma") == 0) : fd_prefers_dmma(m);
+  s->eo_dmma = eng ? (std::strcmp(eng, "dmma_eo") == 0) : fd_prefers_eo_dmma(m);
   // the tiled kernel folds the weights into its synthesis factors, which needs
   // mirror-symmetric weights (true for every reference weight kind, to 1 ulp)
   double wasym = 0.0, wmax = 0.0;
@@ -386,6 +391,7 @@ static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, i
     T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
     T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
     T.wx = h->wx.data(); T.wy = h->wy.data();
+    T.eo_dmma = h->eo_dmma ? 1 : 0;
     const int rc = h->fdt(T, as_stream(stream));
     if (rc != SMG_EUNSUPPORTED) return rc;
     // TMA cannot describe these buffers (odd row length or unaligned base):

@@ -218,6 +218,124 @@ __device__ __forceinline__ void fdt_region_cpasync(const double* __restrict__ r,
 // Column of the region origin inside the residual box (0 or 1).
 __device__ __forceinline__ int fdt_box_shift(int X0, int NO) { return (X0 - NO) & 1; }
 
+// Epilogue part 1 (after stage 4): recombine every window row in place
+// (out[j] = ex[j] + ox[j], out[M-1-j] = ex[j] - ox[j]; the centre of odd M is
+// ex), then fold the overlaps onto the home cells.  Window cell (cy, cx) of
+// an element is "home" when NO <= cx, cy < NO + P (the element's own nodes).
+// Only the immediate neighbours reach a home cell: the right one at
+// cx = P..P+NO-1 (its cells 0..NO-1), the left one at cx = NO..2NO (its cells
+// P+NO..P+2NO).  Each item reads only non-home cells and writes only its own
+// element's home cells; x first (all rows), then y (all columns): corners
+// come along.  Ends with a barrier.
+template <int P, int NO, int TX, int TY, int NT>
+__device__ __forceinline__ void fdt_epilogue_fold(double* EB) {
+  using G = FDTGeom<P, NO, TX, TY>;
+  constexpr int M = G::M, MM = G::MM, E = G::E, HE = G::HE, HO = G::HO, HOX = G::HOX;
+  for (int it = threadIdx.x; it < E * M; it += NT) {
+    double* br = EB + it * M;   // row c of element e (rows are contiguous)
+    double ev[HE], ov[HOX];
+#pragma unroll
+    for (int j = 0; j < HE; ++j) ev[j] = br[j];
+#pragma unroll
+    for (int j = 0; j < HO; ++j) ov[j] = br[HE + j];
+#pragma unroll
+    for (int j = 0; j < HO; ++j) {
+      br[j] = ev[j] + ov[j];
+      br[M - 1 - j] = ev[j] - ov[j];
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < E * M; it += NT) {
+    const int e = it / M, exl = e % TX;
+    double* br = EB + it * M;   // row c
+    if (exl + 1 < TX) {
+#pragma unroll
+      for (int k = 0; k < NO; ++k) br[P + k] += br[MM + k];
+    }
+    if (exl > 0) {
+#pragma unroll
+      for (int k = NO; k <= 2 * NO; ++k) br[k] += br[P + k - MM];
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < E * M; it += NT) {
+    const int e = it / M, c = it - e * M, eyl = e / TX;
+    double* bc = EB + e * MM + c;  // column c
+    if (eyl + 1 < TY) {
+#pragma unroll
+      for (int k = 0; k < NO; ++k) bc[(P + k) * M] += bc[TX * MM + k * M];
+    }
+    if (eyl > 0) {
+#pragma unroll
+      for (int k = NO; k <= 2 * NO; ++k) bc[k * M] += bc[(P + k) * M - TX * MM];
+    }
+  }
+  __syncthreads();
+}
+
+// FP64 tensor-core MMA, m8n8k4: lane (g = lane/4, t = lane%4) holds A[g][t],
+// B[t][g] and accumulates C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Kernel-level constants: DM selects the even/odd DMMA contraction stages
+// (8 warps; factor fragments in shared memory) instead of the DFMA stages.
+template <int P, int NO, int TX, int TY, bool DM>
+struct FDTK {
+  using G = FDTGeom<P, NO, TX, TY>;
+  static constexpr int M = G::M, HE = G::HE, HO = G::HO, E = G::E;
+  static constexpr int MTE = (HE + 7) / 8, KTE = (HE + 3) / 4;   // even half: output / k tiles
+  static constexpr int MTO = (HO + 7) / 8, KTO = (HO + 3) / 4;   // odd half
+  static constexpr int FE = MTE * KTE, FO = MTO * KTO;
+  static constexpr int FRN = DM ? 4 * (FE + FO) * 32 : 0;        // fragment table (doubles)
+  static constexpr int WARPS = 8;
+  static constexpr int NT = DM ? 32 * WARPS : G::THREADS;
+  static constexpr int BT = (E * M + 7) / 8;                     // 8-line batches
+  static constexpr int MAXB = (BT + WARPS - 1) / WARPS;
+  static constexpr size_t extra = sizeof(double) * ((size_t)FRN + (DM ? E : 0));
+  static constexpr size_t smem_for(int ns) { return G::smem_for(ns) + extra; }
+  static constexpr size_t HALF_SM = 112 * 1024;
+  static constexpr int NS = smem_for(4) <= HALF_SM ? 4 : smem_for(3) <= HALF_SM ? 3 : smem_for(4) <= 227 * 1024 ? 4 : 3;
+  static constexpr size_t TSMEM = smem_for(NS);
+  static constexpr int MINB = (TSMEM <= HALF_SM && NT <= 384) ? 2 : 1;
+};
+
+// The fragments of one stage (even and odd halves) into registers.
+template <int FE, int FO>
+__device__ __forceinline__ void dm_load_frags(const double* FR, int stage, int lane, double (&fe)[FE], double (&fo)[FO]) {
+#pragma unroll
+  for (int f = 0; f < FE; ++f) fe[f] = FR[(stage * (FE + FO) + f) * 32 + lane];
+#pragma unroll
+  for (int f = 0; f < FO; ++f) fo[f] = FR[(stage * (FE + FO) + FE + f) * 32 + lane];
+}
+
+// Fragment table of the 4 contraction stages (even, odd), built per CTA from
+// the factor arrays in the parameter bank.  Stages 1/3 use the factor as the
+// A operand (A[out][in]), stages 2/4 as the B operand (B[in][out]).
+template <int M, class Args, int FE, int FO, int KTE, int KTO>
+__device__ __forceinline__ void dm_build_frags(const Args& A, double* FR, int NT) {
+  constexpr int HE = fdt_he(M), HO = fdt_ho(M);
+  for (int idx = threadIdx.x; idx < 4 * (FE + FO) * 32; idx += NT) {
+    const int lane = idx & 31, fa = idx >> 5;
+    const int st = fa / (FE + FO), r = fa - st * (FE + FO);
+    const bool od = r >= FE;
+    const int f = od ? r - FE : r, KT = od ? KTO : KTE, H = od ? HO : HE;
+    const int mt = f / KT, kt = f - mt * KT, g = lane >> 2, t = lane & 3;
+    const int o = 8 * mt + g, k = 4 * kt + t;   // output index, input index
+    double v = 0.0;
+    if (o < H && k < H) {
+      if (st == 0) v = od ? A.Syo[k * H + o] : A.Sye[k * H + o];       // A[i][k] = Sy[k][i]
+      else if (st == 1) v = od ? A.Sxo[k * H + o] : A.Sxe[k * H + o];  // B[k][l] = Sx[k][l]
+      else if (st == 2) v = od ? A.SyoT[k * H + o] : A.SyeT[k * H + o];  // A[k][i] = SyT[i][k]
+      else v = od ? A.SxoT[k * H + o] : A.SxeT[k * H + o];             // B[i][k] = SxT[i][k]
+    }
+    FR[idx] = v;
+  }
+}
+
 // Persistent main kernel.  Per tile (TX x TY elements), in an NS-buffer ring:
 //   * the (RY x BRX) residual box is TMA-loaded NS-2 tiles ahead (one thread
 //     issues it; completion on the buffer's mbarrier; seam tiles, whose region
@@ -228,22 +346,26 @@ __device__ __forceinline__ int fdt_box_shift(int X0, int NO) { return (X0 - NO) 
 //   * gather: every own node adds the element corrections covering it to its
 //     u in the buffer, which ONE TMA store writes back; region nodes owned by
 //     neighbour tiles (the ring) go to the workspace for fdt_fixup.
-template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(FDTGeom<P, NO, TX, TY>::THREADS, FDTGeom<P, NO, TX, TY>::TMINB)
+template <int P, int NO, int TX, int TY, bool DM>
+__global__ void __launch_bounds__(FDTK<P, NO, TX, TY, DM>::NT, FDTK<P, NO, TX, TY, DM>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   SMG_PDL_ENTRY();
   using G = FDTGeom<P, NO, TX, TY>;
+  using K = FDTK<P, NO, TX, TY, DM>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
-  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, NT = G::NT, NH = G::NH, BRX = G::BRX;
-  constexpr int STR = G::STR, NS = G::NS, NRING = G::NRING;
-  static_assert(G::TSMEM <= 227 * 1024, "tile does not fit in shared memory");
+  constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, NT = K::NT, NH = G::NH, BRX = G::BRX;
+  constexpr int STR = G::STR, NS = K::NS, NRING = G::NRING;
+  static_assert(K::TSMEM <= 227 * 1024, "tile does not fit in shared memory");
   static_assert(NS >= 3, "pipeline needs >= 3 buffers");
   // dynamic shared memory starts 1024-byte aligned (no static shared memory in
   // this kernel); TMA boxes need 128-byte aligned destinations
   extern __shared__ __align__(1024) double sm[];
   double* EB = sm + NS * STR;  // E x M x M element buffers
-  uint64_t* barR = reinterpret_cast<uint64_t*>(EB + E * MM);
+  double* FR = EB + E * MM;    // DMMA fragment table (DM only)
+  double* SN = FR + K::FRN;    // per-element 1/nu_bar of the current tile (DM only)
+  uint64_t* barR = reinterpret_cast<uint64_t*>(SN + (DM ? E : 0));
   uint64_t* barU = barR + NS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, t4 = lane & 3;
   const int tid = threadIdx.x;
   const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
   const bool u_zero = A.u_zero != 0;
@@ -262,6 +384,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     for (int k = 0; k < 2 * NS; ++k) mbar_init(barR + k, 1);
     fence_mbar_init();
   }
+  if constexpr (DM) dm_build_frags<M, FDTArgs<M>, K::FE, K::FO, K::KTE, K::KTO>(A, FR, NT);
   __syncthreads();
 
   // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
@@ -292,13 +415,62 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     const int tx = tile % ntx, ty = tile / ntx;
     const int X0 = tx * OX, Y0 = ty * OY;
     double s = 1.0;  // 1 / nu_bar of this element
-    if (act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
+    if (!DM && act && A.inv_nu != nullptr) s = __ldg(A.inv_nu + (size_t)(ty * TY + eyl) * A.n_x + (tx * TX + exl));
+    if (DM && tid < E) SN[tid] = A.inv_nu != nullptr ? __ldg(A.inv_nu + (size_t)(ty * TY + tid / TX) * A.n_x + (tx * TX + tid % TX)) : 1.0;
     cp_async_wait<NS - 3>();
     mbar_wait(barR + b, par);
     __syncthreads();
 
     // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
-    if (!A.debug_skip && act) {
+    if constexpr (DM) {
+      if (!A.debug_skip) {
+        const double* R0 = buf + fdt_box_shift(X0, NO);
+        double fe[K::FE], fo[K::FO];
+        dm_load_frags<K::FE, K::FO>(FR, 0, lane, fe, fo);
+        for (int bt = warp; bt < K::BT; bt += K::WARPS) {
+          const int n = 8 * bt + g8;
+          const bool vn = n < E * M;
+          const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
+          const double* col = R0 + ((en / TX) * P) * BRX + (en % TX) * P + cn;
+          double ae[K::MTE][2], ao[K::MTO][2];
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+#pragma unroll
+          for (int kt = 0; kt < K::KTE; ++kt) {
+            const int k = 4 * kt + t4;
+            double x0 = 0.0, x1 = 0.0;
+            if (vn && k < HE) {
+              x0 = col[k * BRX];
+              if (k < HO) x1 = col[(M - 1 - k) * BRX];
+            }
+            const double be = x0 + x1, bo = (k < HO) ? x0 - x1 : 0.0;
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], fe[m * K::KTE + kt], be);
+            if (kt < K::KTO) {
+#pragma unroll
+              for (int m = 0; m < K::MTO; ++m)
+                dmma884(ao[m][0], ao[m][1], fo[m * K::KTO + kt], bo);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int n2 = 8 * bt + 2 * t4 + j;
+            if (n2 < E * M) {
+              const int e2 = n2 / M, c2 = n2 - e2 * M;
+              double* o = EB + e2 * MM + c2;
+#pragma unroll
+              for (int m = 0; m < K::MTE; ++m)
+                if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[m][j];
+#pragma unroll
+              for (int m = 0; m < K::MTO; ++m)
+                if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[m][j];
+            }
+          }
+        }
+      }
+    } else if (!A.debug_skip && act) {
       const double* col = buf + fdt_box_shift(X0, NO) + (eyl * P) * BRX + exl * P + c;
       auto in = [&](int k) { return col[k * BRX]; };
       if (!odd) {
@@ -331,6 +503,166 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     if (A.debug_skip) {
       for (int idx = tid; idx < E * MM; idx += NT) EB[idx] = 0.0;
       __syncthreads();
+    } else if constexpr (DM) {
+      double fe[K::FE], fo[K::FO];
+      // ---- stage 2 (rows n = (e, c)): T2[n][l] = fold_x(T1[n][:]) . [Se | So] * dinv * (1/nu_bar);
+      //      a batch's 8 rows are read and rewritten by one warp only
+      dm_load_frags<K::FE, K::FO>(FR, 1, lane, fe, fo);
+      for (int bt = warp; bt < K::BT; bt += K::WARPS) {
+        const int n = 8 * bt + g8;
+        const bool vn = n < E * M;
+        const double* row = EB + (vn ? n : 0) * M;
+        double ae[K::MTE][2], ao[K::MTO][2];
+#pragma unroll
+        for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < K::KTE; ++kt) {
+          const int k = 4 * kt + t4;
+          double x0 = 0.0, x1 = 0.0;
+          if (vn && k < HE) {
+            x0 = row[k];
+            if (k < HO) x1 = row[M - 1 - k];
+          }
+          const double a_e = x0 + x1, a_o = (k < HO) ? x0 - x1 : 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], a_e, fe[m * K::KTE + kt]);
+          if (kt < K::KTO) {
+#pragma unroll
+            for (int m = 0; m < K::MTO; ++m)
+              dmma884(ao[m][0], ao[m][1], a_o, fo[m * K::KTO + kt]);
+          }
+        }
+        __syncwarp();
+        if (vn) {
+          const int en = n / M, cn = n - en * M;
+          const double sc = SN[en];
+          double* w = EB + n * M;
+          const double* dn = A.dinv + cn * M;
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int l = 8 * m + 2 * t4 + j;
+              if (l < HE) w[l] = ae[m][j] * (__ldg(dn + l) * sc);
+            }
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int l = 8 * m + 2 * t4 + j;
+              if (l < HO) w[HE + l] = ao[m][j] * (__ldg(dn + HE + l) * sc);
+            }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      // ---- stage 3 (columns n = (e, c)): e = SyeT' T2e[:, c] (rows [0,HE)), o = SyoT' T2o[:, c]
+      dm_load_frags<K::FE, K::FO>(FR, 2, lane, fe, fo);
+      for (int bt = warp; bt < K::BT; bt += K::WARPS) {
+        const int n = 8 * bt + g8;
+        const bool vn = n < E * M;
+        const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
+        const double* col = EB + en * MM + cn;
+        double ae[K::MTE][2], ao[K::MTO][2];
+#pragma unroll
+        for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < K::KTE; ++kt) {
+          const int i = 4 * kt + t4;
+          const double be = (vn && i < HE) ? col[i * M] : 0.0;
+          const double bo = (vn && i < HO) ? col[(HE + i) * M] : 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], fe[m * K::KTE + kt], be);
+          if (kt < K::KTO) {
+#pragma unroll
+            for (int m = 0; m < K::MTO; ++m)
+              dmma884(ao[m][0], ao[m][1], fo[m * K::KTO + kt], bo);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int n2 = 8 * bt + 2 * t4 + j;
+          if (n2 < E * M) {
+            const int e2 = n2 / M, c2 = n2 - e2 * M;
+            double* o = EB + e2 * MM + c2;
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m)
+              if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[m][j];
+#pragma unroll
+            for (int m = 0; m < K::MTO; ++m)
+              if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[m][j];
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      // ---- stage 4 (physical rows c): t3 = e[c'] +- o[c'] (mirror-folded row), then
+      //      ex = t3e . SxeT', ox = t3o . SxoT'; rows read across warps -> results in
+      //      registers until every warp has read
+      double re[K::MAXB][K::MTE][2], ro[K::MAXB][K::MTO][2];
+      dm_load_frags<K::FE, K::FO>(FR, 3, lane, fe, fo);
+#pragma unroll
+      for (int q = 0; q < K::MAXB; ++q) {
+        const int bt = warp + q * K::WARPS;
+        const int n = 8 * bt + g8;
+        const bool vn = bt < K::BT && n < E * M;
+        const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
+        const int cf = cn < HE ? cn : M - 1 - cn;
+        const double sg = cn < HE ? 1.0 : -1.0;
+        const bool centre = (M & 1) && cn == HO;
+        const double* er = EB + en * MM + cf * M;
+        const double* orow = EB + en * MM + (HE + (cf < HO ? cf : 0)) * M;
+#pragma unroll
+        for (int m = 0; m < K::MTE; ++m) re[q][m][0] = re[q][m][1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < K::MTO; ++m) ro[q][m][0] = ro[q][m][1] = 0.0;
+        if (bt < K::BT) {
+#pragma unroll
+          for (int kt = 0; kt < K::KTE; ++kt) {
+            const int i = 4 * kt + t4;
+            double a_e = 0.0, a_o = 0.0;
+            if (vn && i < HE) a_e = centre ? er[i] : fma(sg, orow[i], er[i]);
+            if (vn && i < HO) a_o = centre ? er[HE + i] : fma(sg, orow[HE + i], er[HE + i]);
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m) dmma884(re[q][m][0], re[q][m][1], a_e, fe[m * K::KTE + kt]);
+            if (kt < K::KTO) {
+#pragma unroll
+              for (int m = 0; m < K::MTO; ++m)
+                dmma884(ro[q][m][0], ro[q][m][1], a_o, fo[m * K::KTO + kt]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < K::MAXB; ++q) {
+        const int bt = warp + q * K::WARPS;
+        const int n = 8 * bt + g8;
+        if (bt < K::BT && n < E * M) {
+          double* w = EB + n * M;
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int k = 8 * m + 2 * t4 + j;
+              if (k < HE) w[k] = re[q][m][j];
+            }
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int k = 8 * m + 2 * t4 + j;
+              if (k < HO) w[HE + k] = ro[q][m][j];
+            }
+        }
+      }
+      __syncthreads();
+      fdt_epilogue_fold<P, NO, TX, TY, NT>(EB);
     } else {
       // ---- stage 2 (eigen-y rows c): T2[c, :] = ([Se; So]^T fold_x(T1[c, :])) * dinv / nu_bar
       {
@@ -420,53 +752,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       }
       __syncthreads();
-      // ---- recombine row c in place (even warps): out[j] = ex[j] + ox[j],
-      //      out[M-1-j] = ex[j] - ox[j] (j < HO); the centre of odd M is ex
-      if (act && !odd) {
-        double* br = B + c * M;
-        double ev[HE], ov[HOX];
-#pragma unroll
-        for (int j = 0; j < HE; ++j) ev[j] = br[j];
-#pragma unroll
-        for (int j = 0; j < HO; ++j) ov[j] = br[HE + j];
-#pragma unroll
-        for (int j = 0; j < HO; ++j) {
-          br[j] = ev[j] + ov[j];
-          br[M - 1 - j] = ev[j] - ov[j];
-        }
-      }
-      __syncthreads();
-      // ---- fold the overlaps onto the home cells.  Window cell (cy, cx) of an
-      //      element is "home" when NO <= cx, cy < NO + P (the element's own
-      //      nodes).  Only the immediate neighbours reach a home cell: the
-      //      right one at cx = P..P+NO-1 (its cells 0..NO-1), the left one at
-      //      cx = NO..2NO (its cells P+NO..P+2NO).  Each thread reads only
-      //      non-home cells and writes only its own element's home cells.
-      //      x first (all rows), then y (all columns): corners come along.
-      if (act && !odd) {
-        double* br = B + c * M;  // row c
-        if (exl + 1 < TX) {
-#pragma unroll
-          for (int k = 0; k < NO; ++k) br[P + k] += br[MM + k];
-        }
-        if (exl > 0) {
-#pragma unroll
-          for (int k = NO; k <= 2 * NO; ++k) br[k] += br[P + k - MM];
-        }
-      }
-      __syncthreads();
-      if (act && !odd) {
-        double* bc = B + c;      // column c
-        if (eyl + 1 < TY) {
-#pragma unroll
-          for (int k = 0; k < NO; ++k) bc[(P + k) * M] += bc[TX * MM + k * M];
-        }
-        if (eyl > 0) {
-#pragma unroll
-          for (int k = NO; k <= 2 * NO; ++k) bc[k * M] += bc[(P + k) * M - TX * MM];
-        }
-      }
-      __syncthreads();
+      fdt_epilogue_fold<P, NO, TX, TY, NT>(EB);
     }
     if (!u_zero) mbar_wait(barU + b, par);
 
@@ -643,11 +929,13 @@ struct FDTLaunch {
   const double* Sxo;
   const double* wx;
   const double* wy;
+  int eo_dmma;         // 1: even/odd DMMA contraction stages
 };
 
-template <int P, int NO, int TX, int TY>
-int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
+template <int P, int NO, int TX, int TY, bool DM>
+int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
   using G = FDTGeom<P, NO, TX, TY>;
+  using K = FDTK<P, NO, TX, TY, DM>;
   constexpr int M = G::M, HE = fdt_he(M), HO = fdt_ho(M);
   FDTArgs<M> A;
   // TMA needs 16-byte rows and base addresses; the caller falls back to the
@@ -677,19 +965,19 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
   A.Syo[HO * HO] = A.SyoT[HO * HO] = A.Sxo[HO * HO] = A.SxoT[HO * HO] = 0.0;
   static int grid_cap = 0;
   if (grid_cap == 0) {
-    if (G::TSMEM > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(fdt_kernel<P, NO, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)G::TSMEM);
+    if (K::TSMEM > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(fdt_kernel<P, NO, TX, TY, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)K::TSMEM);
       if (e != cudaSuccess) return cuda_fail(e, "fdt_kernel smem attribute");
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdt_kernel<P, NO, TX, TY>, G::THREADS, G::TSMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdt_kernel<P, NO, TX, TY, DM>, K::NT, K::TSMEM);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int ntiles = L.ntx * L.nty;
-  launch(fdt_kernel<P, NO, TX, TY>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(G::THREADS), G::TSMEM, st, A);
+  launch(fdt_kernel<P, NO, TX, TY, DM>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(K::NT), K::TSMEM, st, A);
   int rc = check_launch("fdt_kernel");
   if (rc) return rc;
   constexpr long PER = (long)(2 * NO + 1) * G::OX + (long)(G::OY - 2 * NO - 1) * (2 * NO + 1);
@@ -697,6 +985,13 @@ int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
   launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.ntx,
          L.nty);
   return check_launch("fdt_fixup");
+}
+
+// Contraction engine per launch: DFMA stages, or the even/odd DMMA stages
+// (FDTLaunch::eo_dmma) -- same pipeline, epilogue and results to rounding.
+template <int P, int NO, int TX, int TY>
+int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
+  return L.eo_dmma ? fdt_launch_k<P, NO, TX, TY, true>(L, st) : fdt_launch_k<P, NO, TX, TY, false>(L, st);
 }
 
 using FDTLaunchFn = int (*)(const FDTLaunch&, cudaStream_t);

@@ -168,10 +168,10 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   SMG_PDL_ENTRY();
   using G = OpGeom<P, TX, TY, DIFF>;
   constexpr int NP = G::NP, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, NT = G::THREADS;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(16) double smo[];
   constexpr int DP = G::DP;
   constexpr int KO = (OX * OY + NT - 1) / NT;     // output nodes per thread
-  double* U = sm;                                  // HY x DP, origin (Y0-P, X0-P) at column sh
+  double* U = smo;                                  // HY x DP, origin (Y0-P, X0-P) at column sh
   double* NU = U + DP * HY;                        // diffusion only
   double* AX = NU + (DIFF ? DP * HY : 0);          // OY x OX: row-pass values, then x+y parts
   double* VX = AX + OX * OY;                       // OY x (TX+1): right-vertex value of element exl-1

@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
   constexpr int NC = G::NC, FX = G::FX, OXC = G::OXC;
   constexpr int KO = (OX * OY + NT - 1) / NT;
   const OpArgs<PF>& A = R.op;
-  extern __shared__ __align__(16) double sm[];
-  double* U = sm;                                  // HY x DP window of u (column shift sh)
+  extern __shared__ __align__(16) double smr[];
+  double* U = smr;                                  // HY x DP window of u (column shift sh)
   double* NU = U + DP * HY;                        // diffusion only
   double* AX = NU + (DIFF ? DP * HY : 0);          // OY x OX: x+y parts, then r
   double* VX = AX + OX * OY;                       // OY x (TX+1)
