@@ -111,29 +111,47 @@ def vcycle_roofline_seconds(n_x, n_y, orders, n_o_of, p64, bw):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled every ~0.5 ms from a thread (the timed region is only milliseconds
+    long), nvidia-smi as the fallback."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []   # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            hd = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(hd, pynvml.NVML_CLOCK_SM)
+            why = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def sample():
+                return (pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM), mx, why(hd))
+        except Exception:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
+
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip().split(",")
+                return float(out[0]), float(out[1]), int(out[2].strip(), 16)
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self.rows.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.1)
+                self._stop.wait(0.0005)
+        self.rows.append(sample())
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -141,17 +159,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        reasons = set()
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if len(r) > 4 + k and r[4 + k].lower() == "active":
-                    reasons.add(nm)
+        sm = [float(r[0]) for r in self.rows]
+        reasons = sorted({nm for r in self.rows for nm, bit in self.REASONS.items() if int(r[2]) & bit})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "sm_max_mhz": max(float(r[1]) for r in self.rows) if self.rows else None,
+                "reasons": reasons, "samples": len(self.rows)}
 
 
 def cpu_threads():
