@@ -339,7 +339,7 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
-    if (G::SMEM > 48 * 1024) {
+    {  // always: static shared memory adds to the dynamic size
       cudaError_t e = cudaFuncSetAttribute(op_kernel<P, TX, TY, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)G::SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "op_kernel smem attribute");

@@ -219,7 +219,7 @@ int rr_launch_t(const RRLaunch& L, cudaStream_t st) {
   for (int i = 0; i < (PF + 1) * (PC + 1); ++i) R.J[i] = L.J[i];
   static bool attr = false;
   if (!attr) {
-    if (G::SMEM > 48 * 1024) {
+    {  // always: static shared memory adds to the dynamic size
       cudaError_t e = cudaFuncSetAttribute(rr_kernel<PC, PF, T, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)G::SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "rr_kernel smem attribute");
