@@ -296,14 +296,77 @@ def xlarge():
     save("xlarge_c4", **out)
 
 
+def harness():
+    """variable/post-smoothed cycles and the reference's
+    run_single / CSV harness (presets.py:90-111, :159-204) on small specs."""
+    import json
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    from schwarzmg import presets
+    out = {}
+    # f1: variable V-cycle (2^(L-l) smoothing steps, n_pre = n_post = 1), Poisson and diffusion
+    for i, (nx, ny, p, nu_hat) in enumerate([(4, 4, 8, None), (4, 4, 8, 0.9), (6, 4, 16, 0.5)]):
+        msh = mesh.MeshConfig(nx, ny, 1.0, 1.0)
+        h = multigrid.build_hierarchy(msh, p, multigrid.OverlapRule("fixed", 1), n_pre=1, n_post=1,
+                                      variable=True, nu_hat=nu_hat)
+        lay = h.top.op.layout
+        f = operators.project_mean(np.random.default_rng(10 + i).standard_normal((lay.N_y, lay.N_x)))
+        u = np.random.default_rng(20 + i).random((lay.N_y, lay.N_x))
+        out[f"var{i}_case"] = np.array([nx, ny, p, -1.0 if nu_hat is None else nu_hat])
+        out[f"var{i}_f"] = f
+        out[f"var{i}_uin"] = u
+        out[f"var{i}_uout"] = multigrid.v_cycle(h, u.copy(), f)
+    # f2: run_single records for small specs (the CSV schema's numbers)
+    specs = [presets.RunSpec(p=8, n_x=4, n_y=4),
+             presets.RunSpec(solver="mgcg", p=8, n_x=4, n_y=4, ar=2.0, overlap_rule="ceilp8"),
+             presets.RunSpec(p=4, n_x=8, n_y=8, weight="w3"),
+             presets.RunSpec(solver="mgcg", p=8, n_x=4, n_y=4, n_pre=1, n_post=1, nu_hat=0.5),
+             presets.RunSpec(solver="mgcg", p=8, n_x=4, n_y=4, ar=2.0, overlap_rule="ceilp2", n_pre=1,
+                             n_post=1, cycle="var", nu_hat=0.9)]
+    recs = []
+    for k, sp in enumerate(specs):
+        for seed in (0, 1):
+            r = presets.run_single(sp, seed)
+            recs.append(r)
+    out["rs_specs"] = np.array(json.dumps([presets.asdict(sp) for sp in specs]))
+    out["rs_records"] = np.array(presets.records_to_json(recs))
+    out["rs_csv"] = np.array(presets.records_to_csv(recs))
+    grids = {name: [presets.asdict(sp) for sp in presets.preset_grid(name, full=full)]
+             for name in presets.PRESET_NAMES for full in (False,)}
+    grids.update({name + ":full": [presets.asdict(sp) for sp in presets.preset_grid(name, full=True)]
+                  for name in ("table4",)})
+    out["grids"] = np.array(json.dumps(grids))
+    refs = {name: [presets.reference_rbar(name, sp) for sp in presets.preset_grid(name)]
+            for name in presets.PRESET_NAMES}
+    out["grid_refs"] = np.array(json.dumps(refs))
+    save("harness", **out)
+    # the published mean rates the reference's presets compare against
+    # (presets.py TABLE2_RBAR..TABLE5), as data for the B200 harness
+    pub = {"table2": {str(k): list(v) for k, v in presets.TABLE2_RBAR.items()},
+           "table3": {str(k): list(v) for k, v in presets.TABLE3_RBAR.items()},
+           "table4": {f"{k[0]},{k[1]}": {m: list(x) for m, x in v.items()} for k, v in presets.TABLE4.items()},
+           "table5": {f"{k[0]},{k[1]}": {m: list(x) for m, x in v.items()} for k, v in presets.TABLE5.items()},
+           "columns": list(presets._WEIGHT_COLUMNS)}
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1512_02390_b200", "data",
+                        "published_rates.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump(pub, fh, indent=1)
+    print(f"wrote {path}")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
     ap.add_argument("--only-large", action="store_true")
     ap.add_argument("--xlarge", action="store_true")
+    ap.add_argument("--harness", action="store_true", help="only the f1/f2 harness fixtures")
     a = ap.parse_args()
+    if a.harness:
+        harness()
+        sys.exit(0)
     if not (a.only_large or a.xlarge):
         small()
+        harness()
     if a.large or a.only_large:
         large()
     if a.xlarge:
