@@ -157,6 +157,19 @@ int smg_sum(const double* x, int64_t n, double* out, double* ws, void* stream);
 /* out = sum of nb per-CTA partials (fixed order) */
 int smg_sum_partials(const double* part, int nb, double* out, void* stream);
 
+/* ---- device-side problem generation (operators.py:110-199) -------------- */
+/* Field on the (n_y p, n_x p) level nodes of GLL order p (nodes, weights:
+ * host arrays of p+1): kind 0 diffusivity 1 + nu_hat sin 2pi(x-s) sin 2pi(y-s)
+ * (:167-173); 1 Poisson load of the sin(pi x) sin(pi y) benchmark (:154-164,
+ * before project_mean); 2 variable-diffusion manufactured load (:176-199,
+ * before project_mean); 3 / 4 exact-solution samples of 1 / 2. */
+int smg_problem_field(int kind, int p, int n_x, int n_y, double dx, double dy, const double* nodes,
+                      const double* weights, double nu_hat, double shift, double* out, void* stream);
+/* Quadrature-weighted element means of a nodal field, out (n_y, n_x)
+ * (DiffusionOperator.element_mean_nu, operators.py:94-98). */
+int smg_element_mean(int p, int n_x, int n_y, const double* weights, const double* nu, double* out,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

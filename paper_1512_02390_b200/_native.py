@@ -65,6 +65,9 @@ SIGNATURES = {
     "smg_project_mean": (C.c_int, [_dp, _i64, _dp, _vp]),
     "smg_sum": (C.c_int, [_dp, _i64, _dp, _dp, _vp]),
     "smg_sum_partials": (C.c_int, [_dp, C.c_int, _dp, _vp]),
+    "smg_problem_field": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _hp, _hp,
+                                    C.c_double, C.c_double, _dp, _vp]),
+    "smg_element_mean": (C.c_int, [C.c_int, C.c_int, C.c_int, _hp, _dp, _dp, _vp]),
 }
 
 _lib = None
@@ -109,6 +112,11 @@ def check(rc: int, what: str = ""):
 
 def stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def hptr(a: np.ndarray):
+    """ctypes double* into a contiguous float64 numpy array (kept alive by the caller)."""
+    return a.ctypes.data_as(_hp)
 
 
 def ptr(t) -> int | None:

@@ -30,7 +30,7 @@ import torch
 from . import _native as N
 from .basis import Basis1D, gll_basis, interp_matrix
 from .mesh import MeshConfig, layout_for
-from .operators import DiffusionOperator, PoissonOperator, diffusivity_field, to_device
+from .operators import DiffusionOperator, PoissonOperator, diffusivity_field, diffusivity_field_device, to_device
 from .schwarz import AdditiveSchwarz, SweepCounter, WeightKind
 
 log = logging.getLogger(__name__)
@@ -189,7 +189,7 @@ def build_hierarchy(mesh: MeshConfig, p: int, rule: OverlapRule, smoother: str =
             op = PoissonOperator(basis, mesh)
             nu_bar = None
         else:
-            op = DiffusionOperator(basis, mesh, diffusivity_field(mesh, basis, nu_hat, nu_shift))
+            op = DiffusionOperator(basis, mesh, diffusivity_field_device(mesh, basis, nu_hat, nu_shift))
             nu_bar = op.element_mean_nu()
         if l == 0:
             lv = Level(l, basis, op, None, 0, 0, 0)

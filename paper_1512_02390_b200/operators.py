@@ -101,17 +101,35 @@ class DiffusionOperator(_DeviceOperator):
         self.basis = basis
         self.mesh = mesh
         self.layout = layout_for(mesh, basis.p)
-        nu_h = np.asarray(nu.cpu() if isinstance(nu, torch.Tensor) else nu, dtype=np.float64)
-        _check_layout(self.layout, nu_h)
-        if np.any(nu_h <= 0.0):
-            raise ValueError("diffusivity must be positive at every node")
-        self.nu = nu_h
-        self._nu_dev = to_device(nu_h)
+        if isinstance(nu, torch.Tensor) and nu.is_cuda:
+            # device-generated field (diffusivity_field_device): stays on the
+            # device; the host copy is made only if a host-side method needs it
+            nu_d = nu.to(torch.float64).contiguous()
+            if tuple(nu_d.shape) != self.layout.shape:
+                raise ValueError(f"field shape {tuple(nu_d.shape)} does not match layout {self.layout.shape}")
+            if bool((nu_d <= 0.0).any()):
+                raise ValueError("diffusivity must be positive at every node")
+            self._nu_host = None
+            self._nu_dev = nu_d
+        else:
+            nu_h = np.asarray(nu.cpu() if isinstance(nu, torch.Tensor) else nu, dtype=np.float64)
+            _check_layout(self.layout, nu_h)
+            if np.any(nu_h <= 0.0):
+                raise ValueError("diffusivity must be positive at every node")
+            self._nu_host = nu_h
+            self._nu_dev = to_device(nu_h)
         self._cx = mesh.dy / mesh.dx
         self._cy = mesh.dx / mesh.dy
         self.mass_x = (mesh.dx / 2.0) * basis.weights
         self.mass_y = (mesh.dy / 2.0) * basis.weights
         self._create(basis.diff, self._nu_dev)
+
+    @property
+    def nu(self) -> np.ndarray:
+        """Nodal diffusivity on the host (copied from the device on first use)."""
+        if self._nu_host is None:
+            self._nu_host = self._nu_dev.cpu().numpy()
+        return self._nu_host
 
     def _element_nu(self, e_x, e_y):
         p = self.basis.p
@@ -128,8 +146,15 @@ class DiffusionOperator(_DeviceOperator):
 
     def element_mean_nu(self) -> np.ndarray:
         """Quadrature-weighted element mean of nu, (n_y, n_x) (operators.py:94-98).
-        Host setup (feeds the smoother's 1/nu_bar)."""
+        Host setup (feeds the smoother's 1/nu_bar); computed on the device
+        when the field was generated there."""
         p = self.basis.p
+        if self._nu_host is None:
+            out = torch.empty((self.layout.n_y, self.layout.n_x), dtype=torch.float64, device="cuda")
+            w = np.ascontiguousarray(self.basis.weights, dtype=np.float64)
+            N.check(N.lib().smg_element_mean(p, self.layout.n_x, self.layout.n_y, N.hptr(w), N.ptr(self._nu_dev),
+                                             N.ptr(out), N.stream()), "element_mean")
+            return out.cpu().numpy()
         L = self.layout
         off = np.arange(p + 1)
         iy = (p * np.arange(L.n_y)[:, None] + off[None, :]) % L.N_y
@@ -232,3 +257,38 @@ def manufactured_rhs_diffusion(mesh: MeshConfig, basis: Basis1D, nu_hat: float, 
     f = project_mean(load_vector(mesh, basis, source))
     X, Y = nodal_coordinates(mesh, basis)
     return f, nu, np.sin(tp * X) * np.sin(tp * Y)
+
+
+# ---------------------------------------------------------------------------
+# Device-side problem generation: the same fields as the
+# host builders above, evaluated per node on the GPU (smg_problem_field), so a
+# 151 M-DOF level never exists on the host.  Same expressions and order; the
+# FP64 sin/cos differ from numpy's by <= 2 ulp.
+
+def _device_field(kind: int, mesh: MeshConfig, basis: Basis1D, nu_hat: float = 0.0, s: float = 0.2):
+    lay = layout_for(mesh, basis.p)
+    out = torch.empty(lay.shape, dtype=torch.float64, device="cuda")
+    nodes = np.ascontiguousarray(basis.nodes, dtype=np.float64)
+    w = np.ascontiguousarray(basis.weights, dtype=np.float64)
+    N.check(N.lib().smg_problem_field(kind, basis.p, mesh.n_x, mesh.n_y, mesh.dx, mesh.dy, N.hptr(nodes),
+                                      N.hptr(w), float(nu_hat), float(s), N.ptr(out), N.stream()),
+            "problem_field")
+    return out
+
+
+def diffusivity_field_device(mesh: MeshConfig, basis: Basis1D, nu_hat: float, s: float = 0.2) -> torch.Tensor:
+    """diffusivity_field on the device (operators.py:167-173)."""
+    if not 0.0 <= nu_hat < 1.0:
+        raise ValueError(f"diffusivity amplitude must be in [0, 1), got {nu_hat}")
+    return _device_field(0, mesh, basis, nu_hat, s)
+
+
+def poisson_benchmark_device(mesh: MeshConfig, basis: Basis1D):
+    """poisson_benchmark on the device (operators.py:154-164): (f, u_samples)."""
+    return project_mean(_device_field(1, mesh, basis)), _device_field(3, mesh, basis)
+
+
+def manufactured_rhs_diffusion_device(mesh: MeshConfig, basis: Basis1D, nu_hat: float, s: float = 0.2):
+    """manufactured_rhs_diffusion on the device (operators.py:176-199): (f, nu, u_samples)."""
+    nu = diffusivity_field_device(mesh, basis, nu_hat, s)
+    return project_mean(_device_field(2, mesh, basis, nu_hat, s)), nu, _device_field(4, mesh, basis)

@@ -104,3 +104,26 @@ def test_gpu_cli_solve(cuda_device, capsys):
     rc = cli.main(["solve", "--p", "8", "--nel", "4"])
     out = capsys.readouterr().out.splitlines()
     assert rc == 0 and out[0] == ",".join(presets.CSV_FIELDS) and out[1].startswith("mg,add,w5,8,4,4,1,fixed:1")
+
+
+@pytest.mark.gpu
+def test_gpu_problem_generation_matches_host(cuda_device):
+    """device-generated fields == the host builders."""
+    import paper_1512_02390_b200 as P
+    for nx, ny, lx, ly, p, nu_hat in [(4, 4, 1.0, 1.0, 8, 0.9), (6, 4, 2.0, 1.0, 16, 0.5), (8, 8, 8.0, 1.0, 3, 0.0),
+                                      (3, 5, 1.0, 2.0, 24, 0.3)]:
+        mesh = P.MeshConfig(nx, ny, lx, ly)
+        b = P.gll_basis(p)
+        f_h, u_h = P.poisson_benchmark(mesh, b)
+        f_d, u_d = P.poisson_benchmark_device(mesh, b)
+        assert np.abs(f_d.cpu().numpy() - f_h).max() <= 1e-13 * np.abs(f_h).max()
+        assert np.abs(u_d.cpu().numpy() - u_h).max() <= 1e-14
+        f_h, nu_h, u_h = P.manufactured_rhs_diffusion(mesh, b, nu_hat)
+        f_d, nu_d, u_d = P.manufactured_rhs_diffusion_device(mesh, b, nu_hat)
+        assert np.abs(f_d.cpu().numpy() - f_h).max() <= 1e-13 * np.abs(f_h).max()
+        assert np.abs(nu_d.cpu().numpy() - nu_h).max() <= 1e-14
+        assert np.abs(u_d.cpu().numpy() - u_h).max() <= 1e-14
+        op_h = P.DiffusionOperator(b, mesh, nu_h)
+        op_d = P.DiffusionOperator(b, mesh, nu_d)
+        assert np.abs(op_d.element_mean_nu() - op_h.element_mean_nu()).max() <= 1e-14
+        assert op_d.nu.shape == nu_h.shape
