@@ -1,0 +1,235 @@
+// Coarse pseudo-inverse by 2D FFT (subsystem a10, coarse="pinv").
+//
+// The p = 1 periodic operator A_0 = (dy/dx) I (x) T_x + (dx/dy) T_y (x) I,
+// T = circulant tridiag(-1, 2, -1), is diagonalised by the 2D DFT with
+// eigenvalues lam(ky, kx) = (dy/dx) mu_x(kx) + (dx/dy) mu_y(ky),
+// mu(k) = 2 - 2 cos(2 pi k / n).  Its pseudo-inverse (zero mode dropped) --
+// what the reference's CG approximates to 1e-12 (multigrid.py:196-228) -- is
+//   u = IDFT( DFT(f) / lam ),  u_hat(0, 0) = 0,
+// i.e. the dense Q_y (Lp .* (Q_y^T f Q_x)) Q_x^T of smg_coarse_pinv's GEMM
+// path in O(n^2 log n) instead of 4 n^3 (n = 512 at C5: 0.6 GFLOP per solve,
+// once per coarse PCG iteration).  Power-of-two n_x, n_y (every BASELINE
+// coarse level); iterative radix-2 complex FFTs in shared memory.
+//   larger than 64 x 64 : rows (forward x) -> columns (y, scale, inverse y)
+//                         -> rows (inverse x), three launches through a
+//                         complex workspace of n_x n_y entries (the coarse ws)
+//   up to 64 x 64       : the dense two-launch path is faster; a one-CTA FFT
+//                         kernel is kept behind SMG_PINV_FFT=2.
+#include <cmath>
+
+#include "smg_common.cuh"
+
+namespace smg {
+
+constexpr int kFftMax = 1024;
+
+struct FftConsts {
+  double twx[kFftMax];   // cos, sin of 2 pi k / n_x, k < n_x / 2 (interleaved)
+  double twy[kFftMax];
+};
+
+__device__ __forceinline__ int brev(int i, int logn) { return (int)(__brev((unsigned)i) >> (32 - logn)); }
+
+// In-place radix-2 DIT FFTs of `lines` lines of n points (input in
+// bit-reversed order, output natural), line l at buf + l*ls, point i at
+// + i*ps.  inv: conjugate twiddles.  All threads of the CTA participate; ends
+// with a barrier.
+__device__ __forceinline__ void fft_lines(double2* buf, int n, int logn, int lines, int ls, int ps,
+                                          const double* tw, bool inv) {
+  const int nh = n >> 1;
+  for (int s = 0; s < logn; ++s) {
+    const int half = 1 << s, stride = nh >> s;   // twiddle step: W_n^(pos * n / (2 half))
+    for (int b = threadIdx.x; b < lines * nh; b += blockDim.x) {
+      const int l = b >> (logn - 1), j = b & (nh - 1);
+      const int grp = j >> s, pos = j & (half - 1);
+      const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+      double2* x = buf + (size_t)l * ls;
+      const double c = tw[2 * (pos * stride)], sn = inv ? tw[2 * (pos * stride) + 1] : -tw[2 * (pos * stride) + 1];
+      const double2 a = x[(size_t)i0 * ps], bb = x[(size_t)i1 * ps];
+      const double tr = bb.x * c - bb.y * sn, ti = bb.x * sn + bb.y * c;
+      x[(size_t)i0 * ps] = make_double2(a.x + tr, a.y + ti);
+      x[(size_t)i1 * ps] = make_double2(a.x - tr, a.y - ti);
+    }
+    __syncthreads();
+  }
+}
+
+// mu(k) = 2 - 2 cos(2 pi k / n) from the twiddle table (cos is even in k)
+__device__ __forceinline__ double mu_of(int k, int n, const double* tw) {
+  const int kk = k <= n / 2 ? k : n - k;
+  const double c = kk < n / 2 ? tw[2 * kk] : -1.0;   // k = n/2: cos(pi) = -1
+  return 2.0 - 2.0 * c;
+}
+
+// ---- one CTA: n_x, n_y <= 64 -------------------------------------------------
+__global__ void __launch_bounds__(1024) fft_pinv_small_kernel(int nx, int ny, int lx, int ly, double cx, double cy,
+                                                              const __grid_constant__ FftConsts C,
+                                                              const double* __restrict__ f, double* __restrict__ u) {
+  SMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double2 zs[];
+  const int PX = nx + 1;      // padded row pitch: column FFTs are bank-conflict free
+  double2* Z = zs;            // ny x PX
+  double2* Z2 = zs + ny * PX;
+  double* TX = reinterpret_cast<double*>(Z2 + ny * PX);   // twiddles in shared memory: the
+  double* TY = TX + nx;                                    // param bank serialises divergent reads
+  const int n = nx * ny;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
+  for (int i = threadIdx.x; i < ny; i += blockDim.x) TY[i] = C.twy[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int y = i >> lx, x = i & (nx - 1);
+    Z[y * PX + brev(x, lx)] = make_double2(f[i], 0.0);
+  }
+  __syncthreads();
+  fft_lines(Z, nx, lx, ny, PX, 1, TX, false);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int y = i >> lx, x = i & (nx - 1);
+    Z2[brev(y, ly) * PX + x] = Z[y * PX + x];
+  }
+  __syncthreads();
+  fft_lines(Z2, ny, ly, nx, 1, PX, TY, false);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int ky = i >> lx, kx = i & (nx - 1);
+    const double lam = cx * mu_of(kx, nx, TX) + cy * mu_of(ky, ny, TY);
+    const double s = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
+    const double2 z = Z2[ky * PX + kx];
+    Z[brev(ky, ly) * PX + kx] = make_double2(z.x * s, z.y * s);
+  }
+  __syncthreads();
+  fft_lines(Z, ny, ly, nx, 1, PX, TY, true);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int y = i >> lx, x = i & (nx - 1);
+    Z2[y * PX + brev(x, lx)] = Z[y * PX + x];
+  }
+  __syncthreads();
+  fft_lines(Z2, nx, lx, ny, PX, 1, TX, true);
+  const double sc = 1.0 / ((double)nx * ny);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] = Z2[(i >> lx) * PX + (i & (nx - 1))].x * sc;
+}
+
+// ---- three launches for larger meshes ------------------------------------------
+constexpr int kFftLines = 8;
+
+// rows [r0, r0+8): forward (inv = false, real input f) or inverse (inv = true,
+// complex input W, real output u) FFT along x
+__global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, const __grid_constant__ FftConsts C,
+                                                       const double* __restrict__ f, double2* __restrict__ W,
+                                                       double* __restrict__ u, int inv) {
+  SMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double2 zs[];
+  double* TX = reinterpret_cast<double*>(zs + kFftLines * nx);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
+  const int r0 = blockIdx.x * kFftLines, nr = min(kFftLines, ny - r0);
+  for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) {
+    const int l = i / nx, x = i - l * nx;
+    const size_t g = (size_t)(r0 + l) * nx + x;
+    zs[l * nx + brev(x, lx)] = inv ? W[g] : make_double2(f[g], 0.0);
+  }
+  __syncthreads();
+  fft_lines(zs, nx, lx, nr, nx, 1, TX, inv != 0);
+  if (!inv) {
+    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) W[(size_t)r0 * nx + i] = zs[i];
+  } else {
+    const double sc = 1.0 / ((double)nx * ny);
+    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) u[(size_t)r0 * nx + i] = zs[i].x * sc;
+  }
+}
+
+// columns [c0, c0+8): forward FFT along y, divide by lambda, inverse FFT along y
+__global__ void __launch_bounds__(512) fft_cols_kernel(int nx, int ny, int ly, double cx, double cy,
+                                                       const __grid_constant__ FftConsts C, double2* __restrict__ W) {
+  SMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double2 zs[];   // kFftLines x ny (line = column)
+  double2* Z2 = zs + kFftLines * ny;
+  double* TY = reinterpret_cast<double*>(Z2 + kFftLines * ny);
+  double* TX = TY + ny;
+  for (int i = threadIdx.x; i < ny; i += blockDim.x) TY[i] = C.twy[i];
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
+  const int c0 = blockIdx.x * kFftLines, nc = min(kFftLines, nx - c0);
+  for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
+    const int y = i / nc, l = i - y * nc;
+    zs[l * ny + brev(y, ly)] = W[(size_t)y * nx + c0 + l];
+  }
+  __syncthreads();
+  fft_lines(zs, ny, ly, nc, ny, 1, TY, false);
+  for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
+    const int l = i / ny, ky = i - l * ny, kx = c0 + l;
+    const double lam = cx * mu_of(kx, nx, TX) + cy * mu_of(ky, ny, TY);
+    const double s = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
+    const double2 z = zs[i];
+    Z2[l * ny + brev(ky, ly)] = make_double2(z.x * s, z.y * s);
+  }
+  __syncthreads();
+  fft_lines(Z2, ny, ly, nc, ny, 1, TY, true);
+  for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
+    const int y = i / nc, l = i - y * nc;
+    W[(size_t)y * nx + c0 + l] = Z2[l * ny + y];
+  }
+}
+
+static bool pow2(int n, int* lg) {
+  if (n < 2 || (n & (n - 1))) return false;
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  *lg = l;
+  return true;
+}
+
+// 1 = not applicable (caller falls back to the GEMM path)
+int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, cudaStream_t st) {
+  int lx = 0, ly = 0;
+  if (!pow2(nx, &lx) || !pow2(ny, &ly) || nx > kFftMax || ny > 512) return 1;
+  // SMG_PINV_FFT: 0 never, 1 (default) beyond 64 x 64, 2 always.  Measured
+  // (tools/vcycle_breakdown.py): at 64 x 64 the one-CTA FFT takes 36 us vs
+  // 16 us for the two-launch dense path; at C4 (256^2) the MGCG solve drops
+  // 0.40 -> 0.10 s, at C5 (512^2, coarse PCG) 1.61 -> 0.98 s.
+  static const int mode = env_int("SMG_PINV_FFT", 1);
+  if (mode == 0 || (mode == 1 && (long)nx * ny <= 64 * 64)) return 1;
+  FftConsts C;
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < kFftMax / 2; ++k) {
+    C.twx[2 * k] = k < nx / 2 ? std::cos(2.0 * pi * k / nx) : 0.0;
+    C.twx[2 * k + 1] = k < nx / 2 ? std::sin(2.0 * pi * k / nx) : 0.0;
+    C.twy[2 * k] = k < ny / 2 ? std::cos(2.0 * pi * k / ny) : 0.0;
+    C.twy[2 * k + 1] = k < ny / 2 ? std::sin(2.0 * pi * k / ny) : 0.0;
+  }
+  const double cx = dy / dx, cy = dx / dy;
+  if (nx <= 64 && ny <= 64) {
+    const size_t smem = sizeof(double2) * 2 * (size_t)(nx + 1) * ny + sizeof(double) * (nx + ny);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(fft_pinv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(double2) * 2 * 65 * 64 + sizeof(double) * 128));
+      if (e != cudaSuccess) return cuda_fail(e, "fft_pinv_small_kernel smem attribute");
+      attr = true;
+    }
+    launch(fft_pinv_small_kernel, dim3(1), dim3(1024), smem, st, nx, ny, lx, ly, cx, cy, C, f, u);
+    return check_launch("fft_pinv_small_kernel");
+  }
+  double2* W = reinterpret_cast<double2*>(ws);   // the coarse ws holds 2 nx ny doubles
+  const size_t smr = sizeof(double2) * kFftLines * nx + sizeof(double) * nx;
+  const size_t smc = sizeof(double2) * 2 * kFftLines * ny + sizeof(double) * (nx + ny);
+  static size_t attr_r = 0, attr_c = 0;
+  if (smr > attr_r) {
+    cudaError_t e = cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+    if (e != cudaSuccess) return cuda_fail(e, "fft_rows_kernel smem attribute");
+    attr_r = smr;
+  }
+  if (smc > attr_c) {
+    cudaError_t e = cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+    if (e != cudaSuccess) return cuda_fail(e, "fft_cols_kernel smem attribute");
+    attr_c = smc;
+  }
+  const int gr = (ny + kFftLines - 1) / kFftLines, gc = (nx + kFftLines - 1) / kFftLines;
+  launch(fft_rows_kernel, dim3(gr), dim3(512), sizeof(double2) * kFftLines * nx + sizeof(double) * nx, st, nx, ny, lx, C, f, W,
+         static_cast<double*>(nullptr), 0);
+  int rc = check_launch("fft_rows_kernel");
+  if (rc) return rc;
+  launch(fft_cols_kernel, dim3(gc), dim3(512), sizeof(double2) * 2 * kFftLines * ny + sizeof(double) * (nx + ny), st, nx, ny, ly, cx, cy, C, W);
+  rc = check_launch("fft_cols_kernel");
+  if (rc) return rc;
+  launch(fft_rows_kernel, dim3(gr), dim3(512), sizeof(double2) * kFftLines * nx + sizeof(double) * nx, st, nx, ny, lx, C,
+         static_cast<const double*>(nullptr), W, u, 1);
+  return check_launch("fft_rows_kernel");
+}
+
+}  // namespace smg
