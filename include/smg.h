@@ -37,6 +37,7 @@ typedef struct smg_op smg_op_t;             /* one level's operator          */
 typedef struct smg_schwarz smg_schwarz_t;   /* one level's additive smoother */
 typedef struct smg_transfer smg_transfer_t; /* level l-1 <-> l transfers     */
 typedef struct smg_coarse smg_coarse_t;     /* p=1 pseudo-inverse            */
+typedef struct smg_vtail smg_vtail_t;       /* V-cycle levels 1..K + coarse  */
 
 const char* smg_last_error(void);
 int smg_version(void);
@@ -108,6 +109,24 @@ size_t smg_coarse_ws_doubles(const smg_coarse_t* h);
 /* u0 = A0^+ (f0 - mean f0) */
 int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double* ws,
                     void* stream);
+
+/* ---- V-cycle tail (replaces the lower part of multigrid.py:231-251 v_cycle:
+ *      levels K..1 smoothing from zero, residual, restriction, the p=1
+ *      pseudo-inverse and the prolongations back up to level K) as ONE
+ *      cooperative launch.  Poisson, additive smoother, n_pre=1, n_post=0 on
+ *      levels 1..K (K <= 3) of orders p_l = 2^l with one overlap layer,
+ *      coarse mesh <= 64 x 64.
+ * ops/sm/tr/f/u: K+1 entries indexed by level (sm[0], tr[0] unused); f[K]
+ * is the input, u[K] the output (overwritten, u[K] = V-cycle correction);
+ * f[l], u[l] for l < K are level work fields.  All pointers must outlive h. */
+int smg_vtail_create(smg_vtail_t** h, int K, const smg_op_t* const* ops, const smg_schwarz_t* const* sm,
+                     const smg_transfer_t* const* tr, const smg_coarse_t* coarse, double* const* f,
+                     double* const* u);
+int smg_vtail_destroy(smg_vtail_t* h);
+int smg_vtail_run(const smg_vtail_t* h, void* stream);
+/* Debug aid: globaltimer (ns) at the phase boundaries of the last run, CTA 0
+ * (handle created with SMG_VTAIL_PROF=1; synchronous copy of n entries). */
+int smg_vtail_profile(const smg_vtail_t* h, int64_t* out, int n);
 
 /* Parity mode: the reference's plain CG (multigrid.py:196-228) on the device:
  * u0 = mean0(CG(A0, f0 - mean f0)) to ||r|| <= tol ||b||, at most max_iter

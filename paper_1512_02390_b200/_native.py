@@ -50,6 +50,11 @@ SIGNATURES = {
     "smg_coarse_destroy": (C.c_int, [_vp]),
     "smg_coarse_ws_doubles": (C.c_size_t, [_vp]),
     "smg_coarse_pinv": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
+    "smg_vtail_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _vp,
+                                   C.POINTER(_vp), C.POINTER(_vp)]),
+    "smg_vtail_destroy": (C.c_int, [_vp]),
+    "smg_vtail_run": (C.c_int, [_vp, _vp]),
+    "smg_vtail_profile": (C.c_int, [_vp, C.POINTER(_i64), C.c_int]),
     "smg_coarse_cg": (C.c_int, [_vp, _dp, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "smg_coarse_cg_ws_doubles": (C.c_size_t, [_i64]),
     "smg_coarse_pcg_ws_doubles": (C.c_size_t, [_vp]),

@@ -15,6 +15,7 @@
 #include "smg_op.cuh"
 #include "smg_transfer.cuh"
 #include "smg_rr.cuh"
+#include "smg_vtail.cuh"
 
 namespace smg {
 
@@ -713,6 +714,141 @@ int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0,
   const bool ok = hs[4] != 0.0;
   *iters_out = ok ? (int)hs[5] : -max_iter;
   return smg_project_mean(u0, n, red, stream);
+}
+
+// ---- V-cycle tail (smg_vtail.cu): levels 1..K + coarse pinv in one launch ----
+struct smg_vtail {
+  int K, n_x, n_y, grid;
+  VtArgs* dev;                 // device copy of the launch arguments
+  long long* prof = nullptr;   // SMG_VTAIL_PROF=1: phase timestamps
+  std::vector<void*> owned;    // device buffers owned by the handle
+};
+
+int smg_vtail_destroy(smg_vtail_t* h) {
+  if (!h) return SMG_OK;
+  for (void* p : h->owned) cudaFree(p);
+  delete h;
+  return SMG_OK;
+}
+
+int smg_vtail_create(smg_vtail_t** out, int K, const smg_op_t* const* ops, const smg_schwarz_t* const* sm,
+                     const smg_transfer_t* const* tr, const smg_coarse_t* coarse, double* const* f,
+                     double* const* u) {
+  if (!out || K < 1 || K > kVtMaxLevels || !ops || !sm || !tr || !coarse || !f || !u) {
+    set_error("smg_vtail_create: bad argument");
+    return SMG_EINVAL;
+  }
+  const int n_x = coarse->n_x, n_y = coarse->n_y;
+  if (n_x > kVtMaxN0 || n_y > kVtMaxN0) {
+    set_error("smg_vtail_create: coarse mesh %dx%d exceeds %d^2", n_x, n_y, kVtMaxN0);
+    return SMG_EUNSUPPORTED;
+  }
+  for (int l = 0; l <= K; ++l) {
+    if (!f[l] || !u[l] || !ops[l] || ops[l]->kind != 0 || ops[l]->n_x != n_x || ops[l]->n_y != n_y) {
+      set_error("smg_vtail_create: level %d: needs a Poisson operator on the %dx%d mesh and its fields", l, n_x, n_y);
+      return SMG_EINVAL;
+    }
+  }
+  if (ops[0]->p != 1) { set_error("smg_vtail_create: level 0 must be p = 1"); return SMG_EINVAL; }
+  for (int l = 1; l <= K; ++l) {
+    const smg_schwarz_t* s = sm[l];
+    const smg_transfer_t* t = tr[l];
+    if (!s || !t || s->p != ops[l]->p || s->n_x != n_x || s->n_y != n_y || s->inv_nu != nullptr ||
+        t->pf != ops[l]->p || t->pc != ops[l - 1]->p) {
+      set_error("smg_vtail_create: level %d: inconsistent smoother / transfer", l);
+      return SMG_EINVAL;
+    }
+    if (s->p != (1 << l) || s->n_o != 1 || l > 3) {
+      set_error("smg_vtail_create: level %d: p=%d, n_o=%d not compiled into the tail kernel (orders 2, 4, 8 "
+                "with one overlap layer)", l, s->p, s->n_o);
+      return SMG_EUNSUPPORTED;
+    }
+  }
+  const int grid = vtail_grid();
+  if (grid <= 0) { set_error("smg_vtail_create: cooperative grid unavailable"); return SMG_EUNSUPPORTED; }
+  smg_vtail* h = new (std::nothrow) smg_vtail();
+  if (!h) return SMG_ENOMEM;
+  h->K = K; h->n_x = n_x; h->n_y = n_y; h->grid = grid;
+  auto upload = [&](const double* src, size_t n, const double** dst) -> cudaError_t {
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double) * (n ? n : 1));
+    if (e != cudaSuccess) return e;
+    h->owned.push_back(d);
+    *dst = static_cast<const double*>(d);
+    return n ? cudaMemcpy(d, src, sizeof(double) * n, cudaMemcpyHostToDevice) : cudaSuccess;
+  };
+  VtArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.K = K; A.n_x = n_x; A.n_y = n_y;
+  A.Qx = coarse->Qx; A.Qy = coarse->Qy; A.Lp = coarse->Lp;
+  A.lv[0].p = 1; A.lv[0].f = f[0]; A.lv[0].u = u[0];
+  cudaError_t e = cudaSuccess;
+  // the EF tile edge (the level-K tiling) and the BC tile edges: largest of
+  // 4, 2, 1 elements that still gives every SM a tile
+  // tile edge of the BC / EF phases: the smallest that gives every CTA at
+  // most one tile (one round), capped at kVtTE and at the mesh
+  auto tile_edge = [&](void) {
+    int te = 1;
+    while (te < kVtTE && te < n_x && te < n_y && ((n_x + te - 1) / te) * ((n_y + te - 1) / te) > grid) ++te;
+    return te;
+  };
+  const int te = tile_edge();
+  for (int l = 1; l <= K && e == cudaSuccess; ++l) {
+    const smg_schwarz_t* s = sm[l];
+    const smg_op_t* o = ops[l];
+    VtLevel& L = A.lv[l];
+    L.p = s->p; L.n_o = s->n_o; L.m = s->m; L.te = te;
+    L.cx = o->dy / o->dx; L.cy = o->dx / o->dy;
+    L.f = f[l]; L.u = u[l];
+    const int m = s->m;
+    e = upload(s->Sx.data(), (size_t)m * m, &L.Sx);
+    if (e == cudaSuccess) e = upload(s->Sy.data(), (size_t)m * m, &L.Sy);
+    if (e == cudaSuccess) { L.dinv = s->dinv; }
+    if (e == cudaSuccess) e = upload(s->wx.data(), m, &L.wx);
+    if (e == cudaSuccess) e = upload(s->wy.data(), m, &L.wy);
+    if (e == cudaSuccess) e = upload(o->Mt.data(), o->Mt.size(), &L.L);
+    if (e == cudaSuccess) e = upload(o->wasm.data(), o->wasm.size(), &L.wasm);
+    if (e == cudaSuccess) e = upload(tr[l]->J.data(), tr[l]->J.size(), &L.J);
+    if (e == cudaSuccess) {
+      void* d = nullptr;
+      e = cudaMalloc(&d, sizeof(double) * (size_t)n_x * n_y * m * m);
+      if (e == cudaSuccess) { h->owned.push_back(d); L.corr = static_cast<double*>(d); }
+    }
+  }
+  if (e == cudaSuccess) {
+    void* d = nullptr;
+    e = cudaMalloc(&d, sizeof(double) * (size_t)n_x * n_y);
+    if (e == cudaSuccess) { h->owned.push_back(d); A.T2 = static_cast<double*>(d); }
+  }
+  if (e == cudaSuccess && env_int("SMG_VTAIL_PROF", 0)) {
+    void* d = nullptr;
+    e = cudaMalloc(&d, sizeof(long long) * 64);
+    if (e == cudaSuccess) { h->owned.push_back(d); A.prof = static_cast<long long*>(d); h->prof = A.prof; }
+  }
+  if (e == cudaSuccess) {
+    void* d = nullptr;
+    e = cudaMalloc(&d, sizeof(VtArgs));
+    if (e == cudaSuccess) {
+      h->owned.push_back(d);
+      h->dev = static_cast<VtArgs*>(d);
+      e = cudaMemcpy(d, &A, sizeof(VtArgs), cudaMemcpyHostToDevice);
+    }
+  }
+  if (e != cudaSuccess) { smg_vtail_destroy(h); return cuda_fail(e, "smg_vtail_create"); }
+  *out = h;
+  return SMG_OK;
+}
+
+int smg_vtail_profile(const smg_vtail_t* h, int64_t* out, int n) {
+  if (!h || !out || n < 1 || n > 64) { set_error("smg_vtail_profile: bad argument"); return SMG_EINVAL; }
+  if (!h->prof) { set_error("smg_vtail_profile: create the handle with SMG_VTAIL_PROF=1"); return SMG_EUNSUPPORTED; }
+  cudaError_t e = cudaMemcpy(out, h->prof, sizeof(long long) * n, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SMG_OK : cuda_fail(e, "smg_vtail_profile");
+}
+
+int smg_vtail_run(const smg_vtail_t* h, void* stream) {
+  if (!h) { set_error("smg_vtail_run: bad argument"); return SMG_EINVAL; }
+  return vtail_launch(h->dev, 1 << h->K, h->grid, as_stream(stream));
 }
 
 }  // extern "C"
