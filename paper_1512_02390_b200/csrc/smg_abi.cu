@@ -65,8 +65,8 @@ int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n
                int it, double* ws, cudaStream_t st);
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
 int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, cudaStream_t st);
-int pinv_cluster(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f, double* u,
-                 cudaStream_t st);
+int pinv_cluster(int nx, int ny, const double* Qx, const double* QxT, const double* Qy, const double* Lp,
+                 const double* f, double* u, cudaStream_t st);
 int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
                double* tmp, double* u, cudaStream_t st);
 int gemm(int M, int N, int K, const double* A, int lda, int tA, const double* B, int ldb, int tB,
@@ -120,6 +120,7 @@ struct smg_coarse {
   int n_x, n_y;
   double dx, dy;
   double* Qx;   // n_x x n_x
+  double* QxT;  // its transpose
   double* Qy;   // n_y x n_y
   double* Lp;   // n_y x n_x pseudo-inverse eigenvalues
 };
@@ -554,7 +555,13 @@ int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy) 
   smg_coarse* c = new (std::nothrow) smg_coarse();
   if (!c) return SMG_ENOMEM;
   c->n_x = n_x; c->n_y = n_y; c->dx = dx; c->dy = dy;
+  std::vector<double> QxT(Qx.size());
+  for (int i = 0; i < n_x; ++i)
+    for (int j = 0; j < n_x; ++j) QxT[(size_t)j * n_x + i] = Qx[(size_t)i * n_x + j];
+  c->QxT = nullptr;
   cudaError_t e = cudaMalloc(&c->Qx, sizeof(double) * Qx.size());
+  if (e == cudaSuccess) e = cudaMalloc(&c->QxT, sizeof(double) * QxT.size());
+  if (e == cudaSuccess) e = cudaMemcpy(c->QxT, QxT.data(), sizeof(double) * QxT.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&c->Qy, sizeof(double) * Qy.size());
   if (e == cudaSuccess) e = cudaMalloc(&c->Lp, sizeof(double) * Lp.size());
   if (e == cudaSuccess) e = cudaMemcpy(c->Qx, Qx.data(), sizeof(double) * Qx.size(), cudaMemcpyHostToDevice);
@@ -567,7 +574,7 @@ int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy) 
 
 int smg_coarse_destroy(smg_coarse_t* h) {
   if (!h) return SMG_OK;
-  cudaFree(h->Qx); cudaFree(h->Qy); cudaFree(h->Lp);
+  cudaFree(h->Qx); cudaFree(h->QxT); cudaFree(h->Qy); cudaFree(h->Lp);
   delete h;
   return SMG_OK;
 }
@@ -583,10 +590,10 @@ int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double*
   // power-of-two meshes: 2D FFT (one launch up to 64 x 64, three beyond)
   int rf = pinv_fft(nx, ny, h->dx, h->dy, f0, u0, ws, st);
   if (rf != 1) return rf;
-  // single-launch cluster variant: opt-in (SMG_PINV_CLUSTER=1) until it beats
-  // the two-launch row-block path (measured 30 us vs 16 us at 64 x 64)
-  int rc = getenv("SMG_PINV_CLUSTER") && getenv("SMG_PINV_CLUSTER")[0] == '1'
-               ? pinv_cluster(nx, ny, h->Qx, h->Qy, h->Lp, f0, u0, st) : 1;
+  // single-launch cluster variant (SMG_PINV_CLUSTER=0 selects the two-launch
+  // row-block path)
+  int rc = !(getenv("SMG_PINV_CLUSTER") && getenv("SMG_PINV_CLUSTER")[0] == '0')
+               ? pinv_cluster(nx, ny, h->Qx, h->QxT, h->Qy, h->Lp, f0, u0, st) : 1;
   if (rc != 1) return rc;
   rc = pinv_small(nx, ny, h->Qx, h->Qy, h->Lp, f0, T1, u0, st);
   if (rc != 1) return rc;

@@ -411,8 +411,9 @@ __device__ __forceinline__ double dot4(const double* __restrict__ a, int sa, con
 constexpr int kClThreads = 512;
 
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
-pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double* __restrict__ Qy,
-                    const double* __restrict__ Lp, const double* __restrict__ f, double* __restrict__ u) {
+pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double* __restrict__ QxT,
+                    const double* __restrict__ Qy, const double* __restrict__ Lp, const double* __restrict__ f,
+                    double* __restrict__ u) {
   SMG_PDL_ENTRY();
   namespace cgx = cooperative_groups;
   cgx::cluster_group cl = cgx::this_cluster();
@@ -423,7 +424,8 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
   double* F = smc;                               // ny x nx
   double* QY = F + ny * nx;                      // ny x ny
   double* QX = QY + ny * ny;                     // nx x nx
-  double* T2 = QX + nx * nx;                     // ny x nx (own rows computed, the rest gathered)
+  double* QXT = QX + nx * nx;                    // nx x nx, QXT[j][x] = Q_x[x][j]
+  double* T2 = QXT + nx * nx;                    // ny x nx (own rows computed, the rest gathered)
   double* T1 = T2 + ny * nx;                     // rb x nx
   double* LP = T1 + rb * nx;                     // rb x nx
   uint64_t* bar = reinterpret_cast<uint64_t*>(LP + rb * nx);
@@ -431,11 +433,12 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    const unsigned b = (unsigned)(8 * (ny * nx + ny * ny + nx * nx)) + (unsigned)(8 * ni * nx);
+    const unsigned b = (unsigned)(8 * (ny * nx + ny * ny + 2 * nx * nx)) + (unsigned)(8 * ni * nx);
     mbar_arrive_expect_tx(bar, b);
     bulk_g2s(F, f, (unsigned)(8 * ny * nx), bar);
     bulk_g2s(QY, Qy, (unsigned)(8 * ny * ny), bar);
     bulk_g2s(QX, Qx, (unsigned)(8 * nx * nx), bar);
+    bulk_g2s(QXT, QxT, (unsigned)(8 * nx * nx), bar);
     if (ni > 0) bulk_g2s(LP, Lp + (size_t)i0 * nx, (unsigned)(8 * ni * nx), bar);
   }
   __syncthreads();  // nobody polls the mbarrier before thread 0 has initialised it
@@ -469,26 +472,26 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
   // u[i0+i][x] = sum_j T1[i][j] Qx[x][j]
   for (int idx = tid; idx < ni * nx; idx += kClThreads) {
     const int i = idx / nx, x = idx - i * nx;
-    u[(size_t)(i0 + i) * nx + x] = dot4(T1 + i * nx, 1, QX + x * nx, 1, nx);
+    u[(size_t)(i0 + i) * nx + x] = dot4(T1 + i * nx, 1, QXT + x, nx, nx);
   }
   cl.sync();  // no CTA leaves while its shared memory may still be read
 }
 
-int pinv_cluster(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f, double* u,
-                 cudaStream_t st) {
+int pinv_cluster(int nx, int ny, const double* Qx, const double* QxT, const double* Qy, const double* Lp,
+                 const double* f, double* u, cudaStream_t st) {
   if (nx > kClMax || ny > kClMax || (nx * ny) % 2 || (nx * nx) % 2 || (ny * ny) % 2) return 1;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!al16(f) || !al16(Qx) || !al16(Qy) || !al16(Lp)) return 1;
+  if (!al16(f) || !al16(Qx) || !al16(QxT) || !al16(Qy) || !al16(Lp)) return 1;
   const int rb = (ny + kCl - 1) / kCl;
   if (((size_t)rb * nx) % 2) return 1;  // keep every row block 16-byte aligned
-  const size_t smem = sizeof(double) * (2 * (size_t)ny * nx + (size_t)ny * ny + (size_t)nx * nx + 2 * (size_t)rb * nx) + 16;
+  const size_t smem = sizeof(double) * (2 * (size_t)ny * nx + (size_t)ny * ny + 2 * (size_t)nx * nx + 2 * (size_t)rb * nx) + 16;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(pinv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "pinv_cluster_kernel smem attribute");
     attr = smem;
   }
-  launch(pinv_cluster_kernel, dim3(kCl), dim3(kClThreads), smem, st, nx, ny, Qx, Qy, Lp, f, u);
+  launch(pinv_cluster_kernel, dim3(kCl), dim3(kClThreads), smem, st, nx, ny, Qx, QxT, Qy, Lp, f, u);
   return check_launch("pinv_cluster_kernel");
 }
 
