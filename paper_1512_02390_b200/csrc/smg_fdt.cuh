@@ -25,6 +25,7 @@
 //    second kernel adds the band contributions to u in a fixed tile order.
 //    Bitwise reproducible, no atomics, no inter-CTA waiting.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "smg_common.cuh"
@@ -47,6 +48,7 @@ struct FDTArgs {
   int N_x, N_y, n_x, ntx, nty;
   int debug_skip;                     // profiling aid: 1 = skip the four contractions
   int u_zero;                         // 1: u holds no valid data and is treated as 0 (write, not add)
+  int fused_fixup;                    // 1: cooperative launch, ring fixup after a grid barrier
   // analysis factors Se[k][i] (k physical half index); synthesis factors
   // SeT[i][k] pre-multiplied by the (mirror-symmetric) Schwarz weight w[k]
   double Sye[fdt_he(M) * fdt_he(M)], SyeT[fdt_he(M) * fdt_he(M)];
@@ -346,6 +348,15 @@ __device__ __forceinline__ void dm_build_frags(const Args& A, double* FR, int NT
 //   * gather: every own node adds the element corrections covering it to its
 //     u in the buffer, which ONE TMA store writes back; region nodes owned by
 //     neighbour tiles (the ring) go to the workspace for fdt_fixup.
+template <int P, int NO, int TX, int TY>
+__device__ __forceinline__ void fdt_fixup_node(double* __restrict__ u, const double* __restrict__ ws, int N_x,
+                                               int ntx, int nty, long gid);
+template <int P, int NO, int TX, int TY>
+constexpr long fdt_fixup_per_tile() {
+  using G = FDTGeom<P, NO, TX, TY>;
+  return (long)(2 * NO + 1) * G::OX + (long)(G::OY - 2 * NO - 1) * (2 * NO + 1);
+}
+
 template <int P, int NO, int TX, int TY, bool DM>
 __global__ void __launch_bounds__(FDTK<P, NO, TX, TY, DM>::NT, FDTK<P, NO, TX, TY, DM>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
@@ -801,6 +812,15 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   }
   if (tid == 0) bulk_wait0();
   cp_async_wait<0>();
+  if (A.fused_fixup) {
+    // cooperative launch: every tile's own block (TMA store, complete) and
+    // ring entries are written before any CTA applies the ring fixup
+    if (tid == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    cooperative_groups::this_grid().sync();
+    const long nb = fdt_fixup_per_tile<P, NO, TX, TY>() * ntiles;
+    for (long gid = (long)blockIdx.x * NT + tid; gid < nb; gid += (long)gridDim.x * NT)
+      fdt_fixup_node<P, NO, TX, TY>(A.u, A.ws, N_x, ntx, nty, gid);
+  }
 }
 
 // Ring fixup (second launch): an own node within n_o (+1) of its tile's edge
@@ -809,9 +829,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 // (dy, dx) = (-1,-1), (-1,0), ..., (1,1).  One thread per band node; no
 // atomics; deterministic.
 template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
-                                                 int ntx, int nty) {
-  SMG_PDL_ENTRY();
+__device__ __forceinline__ void fdt_fixup_node(double* __restrict__ u, const double* __restrict__ ws, int N_x,
+                                               int ntx, int nty, long gid) {
   using G = FDTGeom<P, NO, TX, TY>;
   constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
   constexpr int NRING = G::NRING, NTB = (RY - OY) * RX;
@@ -822,7 +841,6 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   constexpr int PER = NROWS * OX + (OY - NROWS) * (LO + NO);
   static_assert(OY >= NROWS && OX >= LO + NO, "tile smaller than its band");
   (void)BW;
-  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int ntiles = ntx * nty;
   if (gid >= (long)ntiles * PER) return;
   // last tiles first: the main kernel finished with them, so their u and ring
@@ -860,6 +878,13 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
     }
   }
   *up = acc;
+}
+
+template <int P, int NO, int TX, int TY>
+__global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
+                                                 int ntx, int nty) {
+  SMG_PDL_ENTRY();
+  fdt_fixup_node<P, NO, TX, TY>(u, ws, N_x, ntx, nty, (long)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // Band fixup of the DMMA variant (smg_fdm.cuh), which writes every band node
@@ -977,11 +1002,32 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int ntiles = L.ntx * L.nty;
-  launch(fdt_kernel<P, NO, TX, TY, DM>, dim3(ntiles < grid_cap ? ntiles : grid_cap), dim3(K::NT), K::TSMEM, st, A);
+  const int grid = ntiles < grid_cap ? ntiles : grid_cap;
+  // SMG_FDT_FUSED=1: one cooperative launch with the ring fixup after a grid
+  // barrier.  Measured slower on B200 at C2 (V-cycle 145.6 vs 135.2 us: the
+  // barrier and the lost PDL overlap cost more than the second launch), so
+  // the fixup stays a second (PDL) launch by default.
+  static const int fused = env_int("SMG_FDT_FUSED", 0);
+  A.fused_fixup = fused;
+  if (fused) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(K::NT);
+    cfg.dynamicSmemBytes = K::TSMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fdt_kernel<P, NO, TX, TY, DM>, A);
+    if (e != cudaSuccess) return cuda_fail(e, "fdt_kernel (cooperative) launch");
+    return check_launch("fdt_kernel");
+  }
+  launch(fdt_kernel<P, NO, TX, TY, DM>, dim3(grid), dim3(K::NT), K::TSMEM, st, A);
   int rc = check_launch("fdt_kernel");
   if (rc) return rc;
-  constexpr long PER = (long)(2 * NO + 1) * G::OX + (long)(G::OY - 2 * NO - 1) * (2 * NO + 1);
-  const long nb = PER * ntiles;
+  const long nb = fdt_fixup_per_tile<P, NO, TX, TY>() * ntiles;
   launch(fdt_fixup<P, NO, TX, TY>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.u, L.ws, L.N_x, L.ntx,
          L.nty);
   return check_launch("fdt_fixup");

@@ -15,11 +15,22 @@ import tempfile
 
 rep, lib, kname = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+kshow = sys.argv[5] if len(sys.argv) > 5 else None   # substring of the demangled name in the report
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+sections, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = [r[1], None, []]
+        sections.append(cur)
+    elif cur is not None and cur[1] is None:
+        cur[1] = r
+    elif cur is not None:
+        cur[2].append(r)
+sec = next(s_ for s_ in sections if kshow is None or kshow in s_[0])
+hdr = sec[1]
+data = [r for r in sec[2] if len(r) == len(hdr)]
 A, I, S = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 base = int(data[0][A], 16)
