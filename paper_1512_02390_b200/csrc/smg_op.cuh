@@ -219,8 +219,11 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   __syncthreads();
 
   // row passes: item = (own row y, element exl-1), exl in [0, TX]
+  // full lines (exl >= 1) first, the vertex-only lines (exl == 0) last, so
+  // that warps do not diverge between the two
   for (int it = tid; it < OY * (TX + 1); it += NT) {
-    const int y = it / (TX + 1), exl = it - y * (TX + 1);
+    const bool full = it < OY * TX;
+    const int y = full ? it / TX : it - OY * TX, exl = full ? 1 + (it - (it / TX) * TX) : 0;
     const double* ur = U + (y + P) * DP + sh + exl * P;
     const double* nr = NU + (y + P) * DP + sh + exl * P;
     double v[NP];
@@ -240,7 +243,8 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   // the left element) and its own y-part; the y-vertex term of the element
   // below (a == 0) is added in the output pass
   for (int it = tid; it < OX * (TY + 1); it += NT) {
-    const int x = it / (TY + 1), eyl = it - x * (TY + 1);
+    const bool full = it < OX * TY;
+    const int x = full ? it / TY : it - OX * TY, eyl = full ? 1 + (it - (it / TY) * TY) : 0;
     const double* uc = U + (eyl * P) * DP + sh + (x + P);
     const double* nc = NU + (eyl * P) * DP + sh + (x + P);
     double v[NP];
