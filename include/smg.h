@@ -38,6 +38,7 @@ typedef struct smg_schwarz smg_schwarz_t;   /* one level's additive smoother */
 typedef struct smg_transfer smg_transfer_t; /* level l-1 <-> l transfers     */
 typedef struct smg_coarse smg_coarse_t;     /* p=1 pseudo-inverse            */
 typedef struct smg_vtail smg_vtail_t;       /* V-cycle levels 1..K + coarse  */
+typedef struct smg_mult smg_mult_t;         /* multiplicative smoother       */
 
 const char* smg_last_error(void);
 int smg_version(void);
@@ -109,6 +110,22 @@ size_t smg_coarse_ws_doubles(const smg_coarse_t* h);
 /* u0 = A0^+ (f0 - mean f0) */
 int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double* ws,
                     void* stream);
+
+/* ---- multiplicative Schwarz (replaces schwarz.py:293-353
+ *      MultiplicativeSchwarz)
+ * Factors as smg_schwarz_create (the solver is unweighted, kind=None);
+ * nu_bar_dev: device (n_y, n_x) element means of nu (diffusion; the local
+ * correction is divided by it) or NULL.  Must outlive h. */
+int smg_mult_create(smg_mult_t** h, int p, int n_o, int n_x, int n_y, const double* S_x,
+                    const double* S_y, const double* lam_x, const double* lam_y,
+                    const double* nu_bar_dev);
+int smg_mult_destroy(smg_mult_t* h);
+/* One ordered sweep over all n_x*n_y subdomains (forward != 0: lexicographic
+ * (e_y, e_x); else reversed) given the residual r = f - A u: for each
+ * subdomain u[win] += du and r -= A du on the touched elements, in place.
+ * Sequential by construction (one CTA walks the chain). */
+int smg_mult_sweep(const smg_mult_t* h, const smg_op_t* op, double* u, double* r, int forward,
+                   void* stream);
 
 /* ---- V-cycle tail (replaces the lower part of multigrid.py:231-251 v_cycle:
  *      levels K..1 smoothing from zero, residual, restriction, the p=1

@@ -354,19 +354,71 @@ def harness():
     print(f"wrote {path}")
 
 
+
+def mult():
+    """the multiplicative smoother (schwarz.py:293-353) --
+    single sweeps (forward, then reverse) and a multiplicative V-cycle and
+    MG / MGCG histories, all from the reference."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    cases = [(4, 4, 4, 1, None, 1.0, 1.0), (3, 5, 8, 2, None, 1.0, 2.0), (2, 2, 4, 1, None, 1.0, 1.0),
+             (4, 4, 4, 1, 0.5, 1.0, 1.0), (4, 3, 3, 1, None, 1.0, 1.0), (6, 4, 8, 1, 0.9, 2.0, 1.0)]
+    for i, (nx, ny, p, n_o, nu_hat, lx, ly) in enumerate(cases):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        b = basis.gll_basis(p)
+        lay = mesh.layout_for(msh, p)
+        if nu_hat is None:
+            op = operators.PoissonOperator(b, msh)
+            nu_bar = None
+        else:
+            op = operators.DiffusionOperator(b, msh, operators.diffusivity_field(msh, b, nu_hat, 0.2))
+            nu_bar = op.element_mean_nu()
+        cnt = schwarz.SweepCounter()
+        sm = schwarz.MultiplicativeSchwarz(b, lay, msh.dx, msh.dy, n_o, nu_bar=nu_bar, counter=cnt)
+        rng = np.random.default_rng(300 + i)
+        u = rng.standard_normal((lay.N_y, lay.N_x))
+        f = rng.standard_normal((lay.N_y, lay.N_x))
+        out[f"ms{i}_case"] = np.array([nx, ny, p, n_o, -1.0 if nu_hat is None else nu_hat, lx, ly])
+        out[f"ms{i}_u"] = u.copy()
+        out[f"ms{i}_f"] = f
+        u1 = sm.smooth(op, u.copy(), f, 1)          # forward sweep
+        out[f"ms{i}_u1"] = u1.copy()
+        out[f"ms{i}_u2"] = sm.smooth(op, u1, f, 1)  # reverse sweep
+    # multiplicative V-cycle and solver histories (C1-like, smaller mesh)
+    for j, (nx, p, nu_hat) in enumerate([(4, 8, None), (4, 8, 0.5)]):
+        msh = mesh.MeshConfig(nx, nx, 1.0, 1.0)
+        h = multigrid.build_hierarchy(msh, p, multigrid.OverlapRule("fixed", 1), smoother="mult", nu_hat=nu_hat)
+        lay = h.top.op.layout
+        f = operators.project_mean(np.random.default_rng(400 + j).standard_normal((lay.N_y, lay.N_x)))
+        u = np.random.default_rng(500 + j).standard_normal((lay.N_y, lay.N_x))
+        out[f"mv{j}_case"] = np.array([nx, p, -1.0 if nu_hat is None else nu_hat])
+        out[f"mv{j}_f"] = f
+        out[f"mv{j}_uin"] = u.copy()
+        h.reset_smoothers()
+        out[f"mv{j}_uout"] = multigrid.v_cycle(h, u.copy(), f)
+        for solver in ("mg", "mgcg"):
+            _, rep = krylov.solve(h, f, krylov.SolveConfig(solver=solver, seed=0), u0=np.zeros_like(f))
+            out[f"mv{j}_{solver}_res"] = np.array(rep.residuals)
+    save("mult", **out)
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
     ap.add_argument("--only-large", action="store_true")
     ap.add_argument("--xlarge", action="store_true")
     ap.add_argument("--harness", action="store_true", help="only the f1/f2 harness fixtures")
+    ap.add_argument("--mult", action="store_true", help="only the f3 multiplicative fixtures")
     a = ap.parse_args()
+    if a.mult:
+        mult()
+        sys.exit(0)
     if a.harness:
         harness()
         sys.exit(0)
     if not (a.only_large or a.xlarge):
         small()
         harness()
+        mult()
     if a.large or a.only_large:
         large()
     if a.xlarge:

@@ -50,6 +50,9 @@ SIGNATURES = {
     "smg_coarse_destroy": (C.c_int, [_vp]),
     "smg_coarse_ws_doubles": (C.c_size_t, [_vp]),
     "smg_coarse_pinv": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
+    "smg_mult_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, _hp, _hp, _hp, _hp, _dp]),
+    "smg_mult_destroy": (C.c_int, [_vp]),
+    "smg_mult_sweep": (C.c_int, [_vp, _vp, _dp, _dp, C.c_int, _vp]),
     "smg_vtail_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _vp,
                                    C.POINTER(_vp), C.POINTER(_vp)]),
     "smg_vtail_destroy": (C.c_int, [_vp]),

@@ -16,6 +16,7 @@
 #include "smg_transfer.cuh"
 #include "smg_rr.cuh"
 #include "smg_vtail.cuh"
+#include "smg_mult.cuh"
 
 namespace smg {
 
@@ -856,6 +857,87 @@ int smg_vtail_profile(const smg_vtail_t* h, int64_t* out, int n) {
 int smg_vtail_run(const smg_vtail_t* h, void* stream) {
   if (!h) { set_error("smg_vtail_run: bad argument"); return SMG_EINVAL; }
   return vtail_launch(h->dev, 1 << h->K, h->grid, as_stream(stream));
+}
+
+}  // extern "C"
+
+// ---- multiplicative Schwarz (smg_mult.cu) -----------------------------------
+
+struct smg_mult {
+  int p, n_o, n_x, n_y, m;
+  const double* nu_bar;   // caller's device (n_y, n_x), nullable
+  std::vector<void*> owned;
+  const double *Sx, *Sy, *dinv;
+};
+
+extern "C" {
+
+int smg_mult_destroy(smg_mult_t* h) {
+  if (!h) return SMG_OK;
+  for (void* p : h->owned) cudaFree(p);
+  delete h;
+  return SMG_OK;
+}
+
+int smg_mult_create(smg_mult_t** out, int p, int n_o, int n_x, int n_y, const double* S_x, const double* S_y,
+                    const double* lam_x, const double* lam_y, const double* nu_bar_dev) {
+  if (!out || !S_x || !S_y || !lam_x || !lam_y || p < 1 || n_o < 0 || n_o > p - 1 || n_x < 1 || n_y < 1) {
+    set_error("smg_mult_create: bad argument");
+    return SMG_EINVAL;
+  }
+  const int m = p + 1 + 2 * n_o;
+  if (m > p * n_x || m > p * n_y) {
+    set_error("subdomain window (%d nodes) wraps onto itself on a %dx%d mesh at p=%d; reduce n_o", m, n_x, n_y, p);
+    return SMG_EINVAL;
+  }
+  smg_mult* h = new (std::nothrow) smg_mult();
+  if (!h) return SMG_ENOMEM;
+  h->p = p; h->n_o = n_o; h->n_x = n_x; h->n_y = n_y; h->m = m; h->nu_bar = nu_bar_dev;
+  std::vector<double> dinv((size_t)m * m);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) dinv[(size_t)i * m + j] = 1.0 / (lam_y[i] + lam_x[j]);
+  auto upload = [&](const double* src, size_t n, const double** dst) -> cudaError_t {
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double) * n);
+    if (e != cudaSuccess) return e;
+    h->owned.push_back(d);
+    *dst = static_cast<const double*>(d);
+    return cudaMemcpy(d, src, sizeof(double) * n, cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = upload(S_x, (size_t)m * m, &h->Sx);
+  if (e == cudaSuccess) e = upload(S_y, (size_t)m * m, &h->Sy);
+  if (e == cudaSuccess) e = upload(dinv.data(), dinv.size(), &h->dinv);
+  if (e != cudaSuccess) { smg_mult_destroy(h); return cuda_fail(e, "smg_mult_create"); }
+  *out = h;
+  return SMG_OK;
+}
+
+int smg_mult_sweep(const smg_mult_t* h, const smg_op_t* op, double* u, double* r, int forward, void* stream) {
+  if (!h || !op || !u || !r || u == r || op->p != h->p || op->n_x != h->n_x || op->n_y != h->n_y) {
+    set_error("smg_mult_sweep: bad argument");
+    return SMG_EINVAL;
+  }
+  // operator constants in the reference's element_kernel form
+  // (operators.py:44-47 Poisson, :80-84 diffusion), by value per launch
+  const int NP = h->p + 1;
+  if (NP > kMsMaxNP) { set_error("smg_mult_sweep: p=%d beyond %d", h->p, kMsMaxNP - 1); return SMG_EUNSUPPORTED; }
+  MsArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.u = u; A.r = r; A.Sx = h->Sx; A.Sy = h->Sy; A.dinv = h->dinv; A.nu_bar = h->nu_bar;
+  for (int i = 0; i < NP * NP; ++i) {
+    A.Ly[i] = op->kind == 0 ? (2.0 / op->dy) * op->Mt[i] : op->Mt[i];
+    A.Lx[i] = (2.0 / op->dx) * op->Mt[i];
+  }
+  for (int i = 0; i < NP; ++i) {
+    A.my[i] = (op->dy / 2.0) * op->w[i];
+    A.mx[i] = (op->dx / 2.0) * op->w[i];
+    A.w[i] = op->w[i];
+  }
+  A.diffusion = op->kind == 1;
+  A.nu = op->kind == 1 ? op->nu : nullptr;
+  A.cx = op->dy / op->dx; A.cy = op->dx / op->dy;
+  A.p = h->p; A.n_o = h->n_o; A.m = h->m; A.n_x = h->n_x; A.n_y = h->n_y; A.forward = forward ? 1 : 0;
+  return mult_sweep_launch(A, as_stream(stream));
 }
 
 }  // extern "C"

@@ -32,7 +32,7 @@ from . import _native as N
 from .basis import Basis1D, gll_basis, interp_matrix
 from .mesh import MeshConfig, layout_for
 from .operators import DiffusionOperator, PoissonOperator, diffusivity_field, diffusivity_field_device, to_device
-from .schwarz import AdditiveSchwarz, SweepCounter, WeightKind
+from .schwarz import AdditiveSchwarz, MultiplicativeSchwarz, SweepCounter, WeightKind
 
 log = logging.getLogger(__name__)
 
@@ -74,7 +74,7 @@ class Level:
     l: int
     basis: Basis1D
     op: object
-    smoother: AdditiveSchwarz | None
+    smoother: AdditiveSchwarz | MultiplicativeSchwarz | None
     n_pre: int
     n_post: int
     n_o: int
@@ -162,7 +162,7 @@ class MultigridHierarchy:
             lv = self.levels[l]
             p = lv.basis.p
             if (lv.n_pre != 1 or lv.n_post != 0 or p != (1 << l) or p > 8 or lv.n_o != 1
-                    or lv.smoother is None or lv.smoother._inv_nu is not None
+                    or not isinstance(lv.smoother, AdditiveSchwarz) or lv.smoother._inv_nu is not None
                     or lv.op.layout.size > maxdof):
                 break
             K = l
@@ -222,9 +222,7 @@ def build_hierarchy(mesh: MeshConfig, p: int, rule: OverlapRule, smoother: str =
             raise ValueError(f"orders must rise from 1 to p={p}, got {orders}")
     if smoother not in ("add", "mult"):
         raise ValueError(f"smoother must be 'add' or 'mult', got {smoother!r}")
-    if smoother == "mult":
-        raise NotImplementedError("the multiplicative smoother (schwarz.py:294-353) is outside "
-                                  "the B200 hot path; use smoother='add'")
+    counter = SweepCounter() if smoother == "mult" else None   # multigrid.py:144
     if coarse is None:
         coarse = "pinv" if nu_hat is None else "pcg"
     depth = len(orders) - 1
@@ -243,7 +241,10 @@ def build_hierarchy(mesh: MeshConfig, p: int, rule: OverlapRule, smoother: str =
         else:
             n_o = rule.layers(p_l)
             fac = 2 ** (depth - l) if variable else 1
-            sm = AdditiveSchwarz(basis, layout, mesh.dx, mesh.dy, n_o, weight, nu_bar=nu_bar)
+            if smoother == "add":
+                sm = AdditiveSchwarz(basis, layout, mesh.dx, mesh.dy, n_o, weight, nu_bar=nu_bar)
+            else:
+                sm = MultiplicativeSchwarz(basis, layout, mesh.dx, mesh.dy, n_o, nu_bar=nu_bar, counter=counter)
             lv = Level(l, basis, op, sm, n_pre * fac, n_post * fac, n_o)
             J = interp_matrix(levels[l - 1].basis, basis).matrix
             lv.transfer = _Transfer(orders[l - 1], p_l, mesh.n_x, mesh.n_y, J)
@@ -251,7 +252,7 @@ def build_hierarchy(mesh: MeshConfig, p: int, rule: OverlapRule, smoother: str =
         lv.f = torch.zeros(layout.shape, dtype=torch.float64, device="cuda")
         lv.work = torch.empty(layout.shape, dtype=torch.float64, device="cuda")
         levels.append(lv)
-    return MultigridHierarchy(mesh, levels, coarse_tol=coarse_tol, coarse=coarse)
+    return MultigridHierarchy(mesh, levels, coarse_tol=coarse_tol, coarse=coarse, sweep_counter=counter)
 
 
 def prolongate(h: MultigridHierarchy, l: int, coarse) -> torch.Tensor:
@@ -330,8 +331,13 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
         if zero and not lv.n_pre:
             lv.u.zero_()
         if lv.n_pre:
-            N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                           N.ptr(lv.work), lv.n_pre, int(zero), st), "smooth")
+            if isinstance(lv.smoother, MultiplicativeSchwarz):
+                if zero:
+                    lv.u.zero_()
+                lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_pre)
+            else:
+                N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
+                                               N.ptr(lv.work), lv.n_pre, int(zero), st), "smooth")
             zero = False
         fc = h.levels[l - 1].f
         if zero:
@@ -349,8 +355,11 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
         N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
                 "prolongate")
         if lv.n_post:
-            N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                           N.ptr(lv.work), lv.n_post, 0, st), "smooth")
+            if isinstance(lv.smoother, MultiplicativeSchwarz):
+                lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)
+            else:
+                N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
+                                               N.ptr(lv.work), lv.n_post, 0, st), "smooth")
     return u
 
 

@@ -294,7 +294,8 @@ class AdditiveSchwarz:
 
 
 class SweepCounter:
-    """API placeholder for the multiplicative smoother's sweep parity (schwarz.py:278-291)."""
+    """Running count of multiplicative sweeps, shared across a hierarchy
+    (schwarz.py:278-291): the traversal direction alternates with it."""
 
     def __init__(self, i: int = 0):
         self.i = i
@@ -304,10 +305,53 @@ class SweepCounter:
 
 
 class MultiplicativeSchwarz:
-    """Out of scope for this B200 build: the strictly
-    sequential subdomain sweep of schwarz.py:294-353 is not on the north-star
-    path.  Constructing it raises so callers never silently get another smoother."""
+    """Sequential Schwarz sweep with local residual refresh (schwarz.py:293-353;
+    SURVEY 8(f) row f3).
 
-    def __init__(self, *args, **kwargs):
-        raise NotImplementedError("MultiplicativeSchwarz (schwarz.py:294-353) is not part of the "
-                                  "B200 hot path; use smoother='add'")
+    Subdomains in lexicographic (e_y, e_x) order, reversed on every
+    even-numbered sweep of the shared ``counter``; unweighted local FD solves
+    (kind=None), the correction divided by ``nu_bar`` for diffusion, and the
+    residual refreshed by the element kernels of the touched elements.  The
+    chain is sequential by construction: one persistent CTA walks it
+    (``smg_mult_sweep``, smg_mult.cu)."""
+
+    def __init__(self, basis: Basis1D, layout: FieldLayout, dx: float, dy: float, n_o: int,
+                 nu_bar=None, counter: SweepCounter | None = None):
+        self.counter = SweepCounter() if counter is None else counter
+        _check_no_alias(layout, n_o)
+        self.n_o = n_o
+        self.layout = layout
+        self.solver = build_fast_diag(basis, dx, dy, n_o, kind=None)
+        self._nu_bar = None
+        if nu_bar is not None:
+            nb = np.asarray(nu_bar.cpu() if isinstance(nu_bar, torch.Tensor) else nu_bar, dtype=np.float64)
+            self._nu_bar = _as_device(nb)
+        keep = [N.host(a) for a in (self.solver.S_x, self.solver.S_y, self.solver.lam_x, self.solver.lam_y)]
+        raw = C.c_void_p()
+        N.check(N.lib().smg_mult_create(C.byref(raw), layout.p, n_o, layout.n_x, layout.n_y,
+                                        *[k[1] for k in keep], N.ptr(self._nu_bar)), "mult_create")
+        self._h = N.Handle(raw, "smg_mult_destroy")
+        self._work = None
+
+    def _workspace(self):
+        if self._work is None:
+            self._work = torch.empty(self.layout.shape, dtype=torch.float64, device="cuda")
+        return self._work
+
+    def sweep(self, op, u, r, forward: bool):
+        """One ordered pass given the residual r (both updated in place)."""
+        N.check(N.lib().smg_mult_sweep(self._h.raw, op._handle.raw, N.ptr(u), N.ptr(r), int(bool(forward)),
+                                       N.stream()), "mult_sweep")
+        return u
+
+    def smooth(self, op, u, f, n_it: int):
+        """schwarz.py:336-353: n_it sweeps, r = f - A u before each."""
+        if not isinstance(u, torch.Tensor) or not u.is_cuda:
+            raise TypeError("MultiplicativeSchwarz.smooth mutates u in place: pass a CUDA float64 tensor")
+        f = _as_device(f)
+        r = self._workspace()
+        for _ in range(int(n_it)):
+            self.counter.i += 1
+            N.check(N.lib().smg_op_residual(op._handle.raw, N.ptr(u), N.ptr(f), N.ptr(r), N.stream()), "residual")
+            self.sweep(op, u, r, self.counter.i % 2 == 1)
+        return u

@@ -118,3 +118,48 @@ def test_c1_histories():
     np.testing.assert_allclose(res, g["rs_mg_res"], rtol=1e-9)
     _, res, _, _ = O.solve_mgcg(h, f, tol=1e8, max_cycles=40, seed=5)
     np.testing.assert_allclose(res, g["rs_mgcg_res"], rtol=1e-9)
+
+
+def _mult_op(nx, ny, p, nu_hat, lx, ly):
+    b = O.gll(p)
+    dx, dy = lx / nx, ly / ny
+    if nu_hat < 0:
+        return b, O.Poisson(b, nx, ny, dx, dy), None
+    op = O.Diffusion(b, nx, ny, dx, dy, O.diffusivity(b, nx, ny, dx, dy, nu_hat, 0.2))
+    return b, op, op.element_mean_nu()
+
+
+def test_multiplicative_sweeps_vs_reference():
+    """schwarz.py:293-353 forward then reverse sweep."""
+    g = golden("mult")
+    for i in range(6):
+        nx, ny, p, n_o, nu_hat, lx, ly = g[f"ms{i}_case"]
+        nx, ny, p, n_o = int(nx), int(ny), int(p), int(n_o)
+        b, op, nu_bar = _mult_op(nx, ny, p, nu_hat, lx, ly)
+        sm = O.MultSweep(b, nx, ny, lx / nx, ly / ny, n_o, nu_bar)
+        u = g[f"ms{i}_u"].copy()
+        f = g[f"ms{i}_f"]
+        sm.smooth(op, u, f, 1)
+        assert maxrel(u, g[f"ms{i}_u1"]) < 1e-12, (i, maxrel(u, g[f"ms{i}_u1"]))
+        sm.smooth(op, u, f, 1)
+        assert maxrel(u, g[f"ms{i}_u2"]) < 1e-12, (i, maxrel(u, g[f"ms{i}_u2"]))
+
+
+def test_multiplicative_vcycle_and_histories():
+    g = golden("mult")
+    for j in range(2):
+        nx, p, nu_hat = g[f"mv{j}_case"]
+        nx, p = int(nx), int(p)
+        h = O.Hierarchy(nx, nx, 1.0, 1.0, p, smoother="mult", nu_hat=None if nu_hat < 0 else nu_hat)
+        f = g[f"mv{j}_f"]
+        h.reset_smoothers()
+        out = O.v_cycle(h, g[f"mv{j}_uin"].copy(), f)
+        assert maxrel(out, g[f"mv{j}_uout"]) < 1e-10
+        _, res, ok = O.solve_mg(h, f, u0=np.zeros_like(f))
+        want = g[f"mv{j}_mg_res"]
+        assert ok and len(res) == len(want)
+        np.testing.assert_allclose(res, want, rtol=1e-8)
+        _, res, ok, brk = O.solve_mgcg(h, f, u0=np.zeros_like(f))
+        want = g[f"mv{j}_mgcg_res"]
+        assert ok and not brk and len(res) == len(want)
+        np.testing.assert_allclose(res, want, rtol=1e-8)
