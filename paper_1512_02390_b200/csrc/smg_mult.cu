@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
   double* EO = W + NP;               // 9 x (p+1)^2 element outputs
   double* NW = EO + 9 * NP * NP;     // diffusion: 9 x (p+1)^2 nu*w2
   double* DR = NW + 9 * NP * NP;     // (3p+1)^2 du on the element region (wide meshes)
+  __shared__ int TL[20];             // touched elements (tx, ty) x 9, count
   for (int i = tid; i < mm; i += kMsThreads) {
     Sx[i] = A.Sx[i];
     Sy[i] = A.Sy[i];
@@ -124,18 +125,26 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
     }
     // the touched elements (deduplicated, as the reference's set) and their
     // du blocks: du at a node = DU at its window position, 0 outside the window
-    int tx_[9], ty_[9], nt = 0;
-    for (int dyl = -1; dyl <= 1; ++dyl)
-      for (int dxl = -1; dxl <= 1; ++dxl) {
-        const int tx = ms_mod(ex + dxl, n_x), ty = ms_mod(ey + dyl, n_y);
-        bool dup = false;
-        for (int q = 0; q < nt; ++q) dup |= (tx_[q] == tx && ty_[q] == ty);
-        if (!dup) {
-          tx_[nt] = tx;
-          ty_[nt] = ty;
-          ++nt;
+    // (thread 0 builds the list in shared memory; everyone reads it after the
+    // barrier below)
+    if (tid == 0) {
+      int nt = 0;
+      for (int dyl = -1; dyl <= 1; ++dyl)
+        for (int dxl = -1; dxl <= 1; ++dxl) {
+          const int tx = ms_mod(ex + dxl, n_x), ty = ms_mod(ey + dyl, n_y);
+          bool dup = false;
+          for (int q = 0; q < nt; ++q) dup |= (TL[2 * q] == tx && TL[2 * q + 1] == ty);
+          if (!dup) {
+            TL[2 * nt] = tx;
+            TL[2 * nt + 1] = ty;
+            ++nt;
+          }
         }
-      }
+      TL[18] = nt;
+    }
+    __syncthreads();
+    const int nt = TL[18];
+    const int* tl = TL;
     auto du_glob = [&](int Y, int X) -> double {   // global node -> du value
       const int iy = ms_mod(Y - wy0, N_y), ix = ms_mod(X - wx0, N_x);
       return (iy < m && ix < m) ? DU[iy * m + ix] : 0.0;
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
     // du at local node (a, k) of touched element q
     auto du_at = [&](int q, int a, int k) -> double {
       if (wide) return DR[((q / 3) * p + a) * RG + (q % 3) * p + k];
-      return du_glob(ty_[q] * p + a, tx_[q] * p + k);
+      return du_glob(tl[2 * q + 1] * p + a, tl[2 * q] * p + k);
     };
     // element kernel of touched element q at local node (a, b)
     auto ekernel = [&](int q, int a, int b) -> double {
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
       // inner products G1 = nw .* (block D^T), G2 = nw .* (D block) in EO/NW
       for (int idx = tid; idx < nt * NP * NP; idx += kMsThreads) {
         const int q = idx / (NP * NP), r2 = idx - q * NP * NP, a = r2 / NP, j = r2 - a * NP;
-        const int Y0 = ty_[q] * p, X0 = tx_[q] * p;
+        const int Y0 = tl[2 * q + 1] * p, X0 = tl[2 * q] * p;
         double g1 = 0.0, g2 = 0.0;
         for (int k = 0; k < NP; ++k) {
           g1 = fma(du_at(q, a, k), L1[j * NP + k], g1);   // (block D^T)[a][j] = sum_k B[a][k] D[j][k]
@@ -197,34 +206,43 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
       return A.cx * s1 + A.cy * s2;
     };
     if (wide) {
-      // (4) every region node: subtract the outputs of the elements containing
-      //     it (fixed order: element rows, then columns), one RMW per node
+      // (4a) the nine element outputs into shared memory (EO; diffusion reads
+      //      its staged G1/G2 from EO/NW, so write to DU-free scratch RO)
+      double* RO = DR + RG * RG;
+      for (int idx = tid; idx < 9 * NP * NP; idx += kMsThreads) {
+        const int q = idx / (NP * NP), r2 = idx - q * NP * NP, a = r2 / NP, b = r2 - a * NP;
+        RO[idx] = eout(q, a, b);
+      }
+      __syncthreads();
+      // (4b) every region node: subtract the outputs of the elements containing
+      //      it (fixed order: element rows, then columns), one RMW per node
       const int ry0 = ey * p - p, rx0 = ex * p - p;
       for (int idx = tid; idx < RG * RG; idx += kMsThreads) {
         const int ry = idx / RG, rx = idx - ry * RG;
+        const int by = ry / p, bx = rx / p;          // block of the node (0..3)
+        const int ay = ry - by * p, ax = rx - bx * p;
         double acc = 0.0;
-        bool any = false;
-        for (int dyl = -1; dyl <= 1; ++dyl) {
-          const int a = ry - (dyl + 1) * p;
-          if (a < 0 || a > p) continue;
-          for (int dxl = -1; dxl <= 1; ++dxl) {
-            const int b = rx - (dxl + 1) * p;
-            if (b < 0 || b > p) continue;
-            const int q = (dyl + 1) * 3 + (dxl + 1);   // wide: the 9 elements are distinct, in (dyl, dxl) order
-            acc += eout(q, a, b);
-            any = true;
+        // element rows containing row ry: block by (local a = ay) and, when
+        // ay == 0, block by-1 (local a = p); the same for columns
+#pragma unroll
+        for (int t = 1; t >= 0; --t) {
+          const int ey_ = by - t, a = ay + t * p;
+          if (ey_ < 0 || ey_ > 2 || (t == 1 && ay != 0)) continue;
+#pragma unroll
+          for (int u_ = 1; u_ >= 0; --u_) {
+            const int ex_ = bx - u_, b = ax + u_ * p;
+            if (ex_ < 0 || ex_ > 2 || (u_ == 1 && ax != 0)) continue;
+            acc += RO[(ey_ * 3 + ex_) * NP * NP + a * NP + b];
           }
         }
-        if (any) {
-          double* rp = A.r + (size_t)ms_mod(ry0 + ry, N_y) * N_x + ms_mod(rx0 + rx, N_x);
-          __stcg(rp, __ldcg(rp) - acc);
-        }
+        double* rp = A.r + (size_t)ms_mod(ry0 + ry, N_y) * N_x + ms_mod(rx0 + rx, N_x);
+        __stcg(rp, __ldcg(rp) - acc);
       }
     } else {
       for (int q = 0; q < nt; ++q) {
         for (int idx = tid; idx < NP * NP; idx += kMsThreads) {
           const int a = idx / NP, b = idx - a * NP;
-          double* rp = A.r + (size_t)ms_mod(ty_[q] * p + a, N_y) * N_x + ms_mod(tx_[q] * p + b, N_x);
+          double* rp = A.r + (size_t)ms_mod(tl[2 * q + 1] * p + a, N_y) * N_x + ms_mod(tl[2 * q] * p + b, N_x);
           __stcg(rp, __ldcg(rp) - eout(q, a, b));
         }
         __syncthreads();
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_
 
 size_t mult_smem_bytes(int p, int m) {
   const size_t NP = p + 1;
-  return sizeof(double) * (6 * (size_t)m * m + 2 * NP * NP + 3 * NP + 18 * NP * NP + (3 * NP - 2) * (3 * NP - 2)) + 16;
+  return sizeof(double) * (6 * (size_t)m * m + 2 * NP * NP + 3 * NP + 27 * NP * NP + (3 * NP - 2) * (3 * NP - 2)) + 16;
 }
 
 int mult_sweep_launch(const MsArgs& A, cudaStream_t st) {
