@@ -246,9 +246,174 @@ int tr_launch_t(const TrArgs& A0, bool prolong, cudaStream_t st) {
   return check_launch(prolong ? "prolong_kernel" : "restrict_kernel");
 }
 
+// ---- warp-per-element transfers (power-of-two p_f <= 16) ---------------------
+// One warp owns one element and works without block-level barriers, so the
+// warps of an SM overlap their load / compute / store phases (the tiled
+// kernels above serialise them behind __syncthreads with few busy threads).
+constexpr int kTrWarps = 8;
+
+// prolongation, fine element e: u_f[e][a][b] (+)= sum J[a][ay] C[ay][ax] J[b][ax]
+template <int PC, int PF>
+__global__ void __launch_bounds__(32 * kTrWarps) prolong_warp_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
+  constexpr int NC = PC + 1;
+  static_assert(32 % PF == 0 || PF % 32 == 0, "p_f must divide the warp");
+  constexpr int LPR = PF < 32 ? 32 / PF : 1;     // output rows per warp instruction
+  __shared__ double Js[(PF + 1) * NC];
+  __shared__ double Cw[kTrWarps][NC * NC];
+  __shared__ double Tw[kTrWarps][NC * PF];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (PF + 1) * NC; i += 32 * kTrWarps) Js[i] = A.J[i];
+  const int e = blockIdx.x * kTrWarps + warp;
+  const int n_el = A.n_x * A.n_y;
+  const int ey = e / A.n_x, ex = e - ey * A.n_x;
+  const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
+  const bool act = e < n_el;
+  // coarse element values (with the high-side shared nodes)
+  if (act) {
+    for (int i = lane; i < NC * NC; i += 32) {
+      const int ay = i / NC, ax = i - ay * NC;
+      Cw[warp][i] = A.src[(size_t)wrapi(ey * PC + ay, Nyc) * Nxc + wrapi(ex * PC + ax, Nxc)];
+    }
+  }
+  // old fine values (accumulate)
+  constexpr int NO = (PF * PF + 31) / 32;
+  double old[NO];
+  const int b = lane % PF;
+#pragma unroll
+  for (int k = 0; k < NO; ++k) {
+    const int a = lane / PF + LPR * k;
+    old[k] = (act && A.accumulate && a < PF) ? A.dst[(size_t)(ey * PF + a) * Nxf + ex * PF + b] : 0.0;
+  }
+  __syncthreads();   // Js (once per block)
+  if (!act) return;
+  // x pass: Tt[ay][b] = sum_ax J[b][ax] C[ay][ax]; lane's b is fixed
+  {
+    double jb[NC];
+#pragma unroll
+    for (int ax = 0; ax < NC; ++ax) jb[ax] = Js[b * NC + ax];
+    for (int o = lane; o < NC * PF; o += 32) {
+      const int ay = o / PF;
+      const double* c = &Cw[warp][ay * NC];
+      double s = 0.0;
+#pragma unroll
+      for (int ax = 0; ax < NC; ++ax) s = fma(jb[ax], c[ax], s);
+      Tw[warp][ay * PF + b] = s;
+    }
+  }
+  __syncwarp();
+  // y pass: out[a][b] = sum_ay J[a][ay] Tt[ay][b]
+  double tb[NC];
+#pragma unroll
+  for (int ay = 0; ay < NC; ++ay) tb[ay] = Tw[warp][ay * PF + b];
+#pragma unroll
+  for (int k = 0; k < NO; ++k) {
+    const int a = lane / PF + LPR * k;
+    if (a < PF) {
+      double s = 0.0;
+#pragma unroll
+      for (int ay = 0; ay < NC; ++ay) s = fma(Js[a * NC + ay], tb[ay], s);
+      A.dst[(size_t)(ey * PF + a) * Nxf + ex * PF + b] = A.accumulate ? old[k] + s : s;
+    }
+  }
+}
+
+// restriction, coarse element e: owned coarse nodes (ay, ax < p_c) from the
+// fine blocks of elements e, e-x, e-y, e-xy (row-assigned P^T, as the tiled
+// kernel): x pass over the 2p_f fine rows, then y pass.
+template <int PF>
+constexpr int tr_rwarps() { return PF >= 16 ? 4 : kTrWarps; }
+
+template <int PC, int PF>
+__global__ void __launch_bounds__(32 * tr_rwarps<PF>()) restrict_warp_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
+  constexpr int NC = PC + 1, R2 = 2 * PF, LD = R2 + 1, RW = tr_rwarps<PF>();
+  static_assert(R2 <= 32, "fine region rows per warp");
+  __shared__ double Js[(PF + 1) * NC];
+  __shared__ double Fw[RW][R2 * LD];
+  __shared__ double Hw[RW][R2 * PC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (PF + 1) * NC; i += 32 * RW) Js[i] = A.J[i];
+  const int e = blockIdx.x * RW + warp;
+  const int n_el = A.n_x * A.n_y;
+  const int ey = e / A.n_x, ex = e - ey * A.n_x;
+  const int Nxf = A.n_x * PF, Nyf = A.n_y * PF, Nxc = A.n_x * PC;
+  const bool act = e < n_el;
+  if (act) {
+    // fine rows/cols [e*PF - PF, e*PF + PF): R2 x R2 values, lanes along rows
+    constexpr int NL = (R2 * R2 + 31) / 32;
+    double v[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const int i = lane + 32 * k, ry = i / R2, rx = i - ry * R2;
+      v[k] = i < R2 * R2 ? A.src[(size_t)wrapi(ey * PF - PF + ry, Nyf) * Nxf + wrapi(ex * PF - PF + rx, Nxf)] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const int i = lane + 32 * k, ry = i / R2, rx = i - ry * R2;
+      if (i < R2 * R2) Fw[warp][ry * LD + rx] = v[k];
+    }
+  }
+  __syncthreads();   // Js (once per block); Fw of this warp
+  if (!act) return;
+  // x pass: H[ry][ax] = sum_bx J[bx][ax] F[ry][PF+bx] (+ for ax = 0 the left
+  // element's vertex term sum_bx J[bx][PC] F[ry][bx]); lane = fine row
+  for (int ry = lane; ry < R2; ry += 32) {
+    const double* f = &Fw[warp][ry * LD];
+    double s[PC];
+#pragma unroll
+    for (int ax = 0; ax < PC; ++ax) s[ax] = 0.0;
+    double vt = 0.0;
+#pragma unroll
+    for (int bx = 0; bx < PF; ++bx) {
+      const double fo = f[PF + bx], fl = f[bx];
+#pragma unroll
+      for (int ax = 0; ax < PC; ++ax) s[ax] = fma(A.J[bx * NC + ax], fo, s[ax]);
+      vt = fma(A.J[bx * NC + PC], fl, vt);
+    }
+    s[0] += vt;
+#pragma unroll
+    for (int ax = 0; ax < PC; ++ax) Hw[warp][ry * PC + ax] = s[ax];
+  }
+  __syncwarp();
+  // y pass: f_c[ay][ax] = sum_by J[by][ay] H[PF+by][ax] (+ for ay = 0 the
+  // lower element's vertex term sum_by J[by][PC] H[by][ax])
+  for (int o = lane; o < PC * PC; o += 32) {
+    const int ay = o / PC, ax = o - ay * PC;
+    double s = 0.0, vt = 0.0;
+#pragma unroll
+    for (int by = 0; by < PF; ++by) {
+      s = fma(Js[by * NC + ay], Hw[warp][(PF + by) * PC + ax], s);
+      vt = fma(Js[by * NC + PC], Hw[warp][by * PC + ax], vt);
+    }
+    if (ay == 0) s += vt;
+    A.dst[(size_t)(ey * PC + ay) * Nxc + ex * PC + ax] = s;
+  }
+}
+
+template <int PC, int PF>
+int tr_launch_warp(const TrArgs& A, bool prolong, cudaStream_t st) {
+  if (prolong) {
+    launch(prolong_warp_kernel<PC, PF>, dim3((A.n_x * A.n_y + kTrWarps - 1) / kTrWarps), dim3(32 * kTrWarps), 0, st, A);
+  } else {
+    constexpr int RW = tr_rwarps<PF>();
+    launch(restrict_warp_kernel<PC, PF>, dim3((A.n_x * A.n_y + RW - 1) / RW), dim3(32 * RW), 0, st, A);
+  }
+  return check_launch(prolong ? "prolong_warp_kernel" : "restrict_warp_kernel");
+}
+
 // tile T (elements per side) chosen at run time from the compiled set
 template <int PC, int PF>
 int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
+  if constexpr (PF <= 16 && (PF & (PF - 1)) == 0) {
+    static const int warp = env_int("SMG_TR_WARP", 1);
+    if (warp) {
+      TrArgs B = A;
+      B.n_x = n_x;
+      B.n_y = n_y;
+      return tr_launch_warp<PC, PF>(B, prolong, st);
+    }
+  }
   constexpr int T0 = PF >= 32 ? 1 : 32 / PF;
   // largest power-of-two T <= T0 dividing the mesh that keeps >= 296 CTAs,
   // else the one with the most CTAs
