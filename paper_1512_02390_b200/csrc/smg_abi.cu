@@ -240,6 +240,10 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
   L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
+  if (!norm) {
+    const int rc = opw_launch(L, st);
+    if (rc != 1) return rc;
+  }
   return h->fn(L, st);
 }
 
