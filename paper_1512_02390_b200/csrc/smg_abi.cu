@@ -500,9 +500,10 @@ int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const dou
   // the fields allow 16-byte bulk row copies
   // measured (tools/vcycle_breakdown.py, C2): fused wins at p_f <= 8 (4.3 vs
   // 6.9 us at p_f = 2), loses at p_f = 16 (33 vs 22 us: 2.25x residual
-  // recompute, 63 KB tiles); SMG_RR_FUSED = 0 never, 1 p_f <= 8, 2 always
+  // recompute, 63 KB tiles); SMG_RR_FUSED = 0 never, 1 p_f <= 8, 2 always,
+  // 3 p_f <= 4
   static const int fused = env_int("SMG_RR_FUSED", 1);
-  if ((fused == 2 || (fused == 1 && h->pf <= 8)) && op->p == h->pf && op->n_x == h->n_x && op->n_y == h->n_y && ((long)h->n_x * h->pf) % 2 == 0) {
+  if ((fused == 2 || (fused == 1 && h->pf <= 8) || (fused == 3 && h->pf <= 4)) && op->p == h->pf && op->n_x == h->n_x && op->n_y == h->n_y && ((long)h->n_x * h->pf) % 2 == 0) {
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     RRFn fn = rr_dispatch(h->pc, h->pf, op->kind != 0, h->n_x, h->n_y);
     if (fn && al16(u) && al16(f) && (op->kind == 0 || al16(op->nu))) {

@@ -860,22 +860,38 @@ __device__ __forceinline__ void fdt_fixup_node(double* __restrict__ u, const dou
   }
   const int tx = tile % ntx, ty = tile / ntx;
   double* up = u + (size_t)(ty * OY + oy) * N_x + (tx * OX + ox);
-  double acc = *up;
+  // every ring entry this node receives is loaded before any is added (one
+  // round trip instead of a chain); added in the fixed neighbour order
+  // (dy, dx) = (-1,-1), (-1,0), ..., (1,1)
+  double val[8];
+  int nv = 0;
+  const double own = *up;
 #pragma unroll
   for (int dy = -1; dy <= 1; ++dy) {
     const int ry = oy + NO - dy * OY;
-    if (ry < 0 || ry >= RY) continue;
     const int tyn = wrapi(ty + dy, nty);
 #pragma unroll
     for (int dx = -1; dx <= 1; ++dx) {
       if (dx == 0 && dy == 0) continue;
       const int rx = ox + NO - dx * OX;
-      if (rx < 0 || rx >= RX) continue;
-      int k;  // compact ring index of region node (ry, rx) of the neighbour
+      const bool in = ry >= 0 && ry < RY && rx >= 0 && rx < RX;
+      int k = 0;  // compact ring index of region node (ry, rx) of the neighbour
       if (ry < NO || ry >= NO + OY) k = (ry < NO ? ry : ry - OY) * RX + rx;
       else k = NTB + (ry - NO) * (RX - OX) + (rx < NO ? rx : rx - OX);
-      acc += ws[(size_t)(tyn * ntx + wrapi(tx + dx, ntx)) * NRING + k];
+      const int slot = (dy + 1) * 3 + (dx + 1) - ((dy + 1) * 3 + (dx + 1) > 4 ? 1 : 0);
+      val[slot] = in ? ws[(size_t)(tyn * ntx + wrapi(tx + dx, ntx)) * NRING + k] : 0.0;
+      nv += in ? 1 : 0;
     }
+  }
+  (void)nv;
+  double acc = own;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    // absent neighbours contribute an exact 0.0 -- but x + 0.0 == x only for
+    // x != -0.0; keep the reference order and skip them explicitly
+    const int dy = (q < 4 ? q : q + 1) / 3 - 1, dx = (q < 4 ? q : q + 1) % 3 - 1;
+    const int ry = oy + NO - dy * OY, rx = ox + NO - dx * OX;
+    if (ry >= 0 && ry < RY && rx >= 0 && rx < RX) acc += val[q];
   }
   *up = acc;
 }
