@@ -477,11 +477,122 @@ pinv_cluster_kernel(int nx, int ny, const double* __restrict__ Qx, const double*
   cl.sync();  // no CTA leaves while its shared memory may still be read
 }
 
+// ---- square power-of-two coarse meshes: compile-time cluster kernel ---------
+// Same products and k order as pinv_cluster_kernel, specialised on N (n_x =
+// n_y = N) so every dot product is fully unrolled with constant strides, and
+// spread over CL = N/4 CTAs (a 16-CTA non-portable cluster at N = 64): each
+// CTA owns 4 rows, one output per thread per stage.
+template <int N>
+__device__ __forceinline__ double pc_dot(const double* __restrict__ a, int sa, const double* __restrict__ b, int sb) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; k += 4) {
+    s0 = fma(a[k * sa], b[k * sb], s0);
+    s1 = fma(a[(k + 1) * sa], b[(k + 1) * sb], s1);
+    s2 = fma(a[(k + 2) * sa], b[(k + 2) * sb], s2);
+    s3 = fma(a[(k + 3) * sa], b[(k + 3) * sb], s3);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+template <int N>
+__global__ void __launch_bounds__(4 * N) pinv_sq_kernel(const double* __restrict__ Qx, const double* __restrict__ QxT,
+                                                       const double* __restrict__ Qy,
+                                                       const double* __restrict__ Lp, const double* __restrict__ f,
+                                                       double* __restrict__ u) {
+  SMG_PDL_ENTRY();
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  constexpr int RB = 4, CLN = N / RB, NN = N * N;
+  extern __shared__ __align__(16) double smq[];
+  const int rank = (int)cl.block_rank();
+  const int i0 = rank * RB;
+  double* F = smq;          // N x N
+  double* QY = F + NN;      // N x N
+  double* QX = QY + NN;     // N x N
+  double* QXT = QX + NN;    // N x N
+  double* T2 = QXT + NN;    // N x N (own rows computed, the rest gathered)
+  double* T1 = T2 + NN;     // RB x N
+  double* LP = T1 + RB * N; // RB x N
+  uint64_t* bar = reinterpret_cast<uint64_t*>(LP + RB * N);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, (unsigned)(8 * (4 * NN + RB * N)));
+    bulk_g2s(F, f, 8u * NN, bar);
+    bulk_g2s(QY, Qy, 8u * NN, bar);
+    bulk_g2s(QX, Qx, 8u * NN, bar);
+    bulk_g2s(QXT, QxT, 8u * NN, bar);
+    bulk_g2s(LP, Lp + (size_t)i0 * N, 8u * RB * N, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const int i = tid / N, x = tid - i * N;   // one (row, column) output per thread
+  // T1[i][x] = sum_k Qy[k][i0+i] F[k][x]
+  T1[tid] = pc_dot<N>(QY + i0 + i, N, F + x, N);
+  __syncthreads();
+  // T2[i0+i][x] = (sum_j T1[i][j] Qx[j][x]) * Lp[i0+i][x]
+  T2[(i0 + i) * N + x] = pc_dot<N>(T1 + i * N, 1, QX + x, N) * LP[tid];
+  cl.sync();
+  for (int c = 0; c < CLN; ++c) {
+    if (c == rank) continue;
+    const double* rem = cl.map_shared_rank(T2, c);
+    if (tid < RB * N) T2[c * RB * N + tid] = rem[c * RB * N + tid];
+  }
+  __syncthreads();
+  // T1[i][x] = sum_k Qy[i0+i][k] T2[k][x]
+  const double t1 = pc_dot<N>(QY + (i0 + i) * N, 1, T2 + x, N);
+  __syncthreads();
+  T1[tid] = t1;
+  __syncthreads();
+  // u[i0+i][x] = sum_j T1[i][j] Qx[x][j]
+  u[(size_t)(i0 + i) * N + x] = pc_dot<N>(T1 + i * N, 1, QXT + x, N);
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+}
+
+template <int N>
+int pinv_sq_launch(const double* Qx, const double* QxT, const double* Qy, const double* Lp, const double* f,
+                   double* u, cudaStream_t st) {
+  constexpr int CLN = N / 4;
+  const size_t smem = sizeof(double) * (5 * (size_t)N * N + 8 * (size_t)N) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(pinv_sq_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && CLN > 8) e = cudaFuncSetAttribute(pinv_sq_kernel<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "pinv_sq_kernel attributes");
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CLN);
+  cfg.blockDim = dim3(4 * N);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CLN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pinv_sq_kernel<N>, Qx, QxT, Qy, Lp, f, u);
+  if (e != cudaSuccess) return cuda_fail(e, "pinv_sq_kernel launch");
+  return check_launch("pinv_sq_kernel");
+}
+
 int pinv_cluster(int nx, int ny, const double* Qx, const double* QxT, const double* Qy, const double* Lp,
                  const double* f, double* u, cudaStream_t st) {
   if (nx > kClMax || ny > kClMax || (nx * ny) % 2 || (nx * nx) % 2 || (ny * ny) % 2) return 1;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(f) || !al16(Qx) || !al16(QxT) || !al16(Qy) || !al16(Lp)) return 1;
+  static const int sq = env_int("SMG_PINV_SQ", 1);
+  if (sq && nx == ny) {
+    if (nx == 64) return pinv_sq_launch<64>(Qx, QxT, Qy, Lp, f, u, st);
+    if (nx == 32) return pinv_sq_launch<32>(Qx, QxT, Qy, Lp, f, u, st);
+    if (nx == 16) return pinv_sq_launch<16>(Qx, QxT, Qy, Lp, f, u, st);
+  }
   const int rb = (ny + kCl - 1) / kCl;
   if (((size_t)rb * nx) % 2) return 1;  // keep every row block 16-byte aligned
   const size_t smem = sizeof(double) * (2 * (size_t)ny * nx + (size_t)ny * ny + 2 * (size_t)nx * nx + 2 * (size_t)rb * nx) + 16;
