@@ -480,18 +480,18 @@ def main():
         v = [tr_all[n]["bytes_per_launch"] for n in names if n in tr_all]
         return float(sum(v)) if len(v) == len(names) else None
     kern = {
-        "residual": roofline_entry("op_kernel<16,2,2,Poisson> (r = f - A u)", t_call["residual"],
+        "residual": roofline_entry("opw_kernel<16,2,2> (r = f - A u, warp per element)", t_call["residual"],
                                    n_el * (4 * npp ** 3 + 3 * npp ** 2) + ndof, 24.0 * ndof, p64, bw * 1e9,
-                                   tb("op_kernel")),
+                                   tb("opw_kernel")),
         "schwarz": roofline_entry("fdt_kernel<16,1,4,2> + fdt_fixup (one Schwarz correction)", t_call["schwarz"],
                                   n_el * fd_eo_flops_per_element(m), 24.0 * ndof, p64, bw * 1e9,
                                   tb("fdt_kernel", "fdt_fixup"),
                                   note="even/odd flop count (SURVEY 8(d)); dense-FD equivalent "
                                        f"{n_el * fd_flops_per_element(m) / t_call['schwarz'] / 1e12:.2f} TF"),
-        "restrict": roofline_entry("restrict_kernel<8,16,2>", t_call["restrict"], f_tr, 8.0 * ndof + 8.0 * ndof_c,
-                                   p64, bw * 1e9, tb("restrict_kernel")),
-        "prolong": roofline_entry("prolong_kernel<8,16,2> (u_f += P u_c)", t_call["prolong"], f_tr,
-                                  16.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9, tb("prolong_kernel")),
+        "restrict": roofline_entry("restrict_blk_kernel<8,16>", t_call["restrict"], f_tr, 8.0 * ndof + 8.0 * ndof_c,
+                                   p64, bw * 1e9, tb("restrict_blk_kernel")),
+        "prolong": roofline_entry("prolong_warp_kernel<8,16> (u_f += P u_c)", t_call["prolong"], f_tr,
+                                  16.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9, tb("prolong_warp_kernel")),
     }
     for nm in kern:
         kern[nm]["us_per_call_flushed"] = 1e6 * t_call_flushed[nm]
