@@ -11,9 +11,9 @@ work: the top level applies A to a nonzero u).
 
 Timing: CUDA events on the launching stream around each step, L2 flushed
 (256 MiB write) before every timed step, K steps bracketed by barrier +
-synchronize, max over ranks.  N > 1: one process per GPU; the same C2 problem
-is split into element-row strips (paper_1512_02390_b200/strips.py) with NCCL
-halo exchanges and a replicated coarse solve ("scaling": "strong").
+synchronize, max over ranks.  N > 1: one process per GPU, weak scaling: each
+rank owns a C2-sized element-row strip (paper_1512_02390_b200/strips.py) of a
+64 x 64N-element mesh, NCCL halo exchanges and a replicated coarse solve.
 """
 
 from __future__ import annotations
@@ -224,8 +224,10 @@ def run_reference(args):
 
 
 def run_strips(args, world, rank, local, dev):
-    """N > 1: the C2 V-cycle strong-scaled over element-row strips (strips.py),
-    halos by NCCL send/recv, replicated coarse solve (all-gather)."""
+    """N > 1: weak scaling over element-row strips (strips.py): every rank owns
+    a C2-sized 64 x 64-element, p=16 strip of a 64 x (64 N)-element periodic
+    mesh ([0,1] x [0,N], square elements as in C2); halos by NCCL send/recv,
+    replicated global coarse solve (all-gather + pseudo-inverse)."""
     import torch
     import torch.distributed as dist
     import paper_1512_02390_b200 as P
@@ -233,7 +235,9 @@ def run_strips(args, world, rank, local, dev):
     from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, TorchTransport
 
     lib = NV.lib()
-    c = CFG
+    c = dict(CFG)
+    c["n_y"] *= world
+    c["l_y"] *= world
     plan = StripPlan(c["n_x"], c["n_y"], c["l_x"], c["l_y"], world, rank)
     rule = P.OverlapRule.parse(c["rule"])
     eng = GpuEngine(plan, c["p"], rule)
@@ -296,10 +300,11 @@ def run_strips(args, world, rank, local, dev):
         own_bytes = 8 * (own.stop - own.start) * N[1]
         line = {"metric": METRIC, "value": ndof * args.steps / t_steps, "unit": "DOF/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_steps / args.steps,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded N(0,1) RHS, mean removed)",
-                "config": {"workload": "C2: periodic Poisson [0,1]^2, 64x64 elements, p=16 (1,048,576 DOF), "
-                                       "stand-alone V-cycle (1,0), w5, fixed:1, coarse p=1 pseudo-inverse",
+                "config": {"workload": f"C2 per GPU: periodic Poisson [0,1]x[0,{world}], 64x{64 * world} elements, "
+                                       f"p=16 ({ndof:,} DOF), stand-alone V-cycle (1,0), w5, fixed:1, "
+                                       "coarse p=1 pseudo-inverse",
                            "global_dofs": ndof, "parallelism": f"{world} element-row strips "
                            f"({plan.s} rows + 2x{2} ghost rows each), NCCL halo send/recv, replicated coarse",
                            "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": False},
