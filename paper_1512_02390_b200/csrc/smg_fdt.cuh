@@ -97,7 +97,8 @@ struct FDTGeom {
   static constexpr int STR = (((RBOX > UBOX ? RBOX : UBOX) + 15) & ~15);  // 128-byte multiple
   static constexpr int NRING = RX * RY - OX * OY;    // region nodes owned by neighbour tiles
   static constexpr int KC = (M + P - 1) / P;         // max elements covering one node per direction
-  static constexpr size_t smem_for(int ns) { return sizeof(double) * ((size_t)ns * STR + (size_t)E * MM) + 16 * (size_t)ns; }
+  // nb element buffers (2: the DFMA stages ping-pong between them, no read-before-write barriers)
+  static constexpr size_t smem_for(int ns, int nb = 1) { return sizeof(double) * ((size_t)ns * STR + (size_t)nb * E * MM) + 16 * (size_t)ns; }
   static constexpr size_t HALF_SM = 112 * 1024;      // two CTAs per SM
   // stages: 4 when two CTAs still fit, else 3, else the most that fit one CTA
   static constexpr int NS = smem_for(4) <= HALF_SM ? 4 : smem_for(3) <= HALF_SM ? 3 : smem_for(4) <= 227 * 1024 ? 4 : 3;
@@ -298,9 +299,16 @@ struct FDTK {
   static constexpr int BT = (E * M + 7) / 8;                     // 8-line batches
   static constexpr int MAXB = (BT + WARPS - 1) / WARPS;
   static constexpr size_t extra = sizeof(double) * ((size_t)FRN + (DM ? E : 0));
-  static constexpr size_t smem_for(int ns) { return G::smem_for(ns) + extra; }
-  static constexpr size_t HALF_SM = 112 * 1024;
-  static constexpr int NS = smem_for(4) <= HALF_SM ? 4 : smem_for(3) <= HALF_SM ? 3 : smem_for(4) <= 227 * 1024 ? 4 : 3;
+  static constexpr size_t HALF_SM = 112 * 1024, FULL_SM = 227 * 1024;
+  static constexpr size_t sm1(int ns) { return G::smem_for(ns, 1) + extra; }
+  static constexpr size_t sm2(int ns) { return G::smem_for(ns, 2) + extra; }
+  // ping-pong element buffers (DFMA stages) when that keeps the occupancy:
+  // two CTAs per SM with 3+ stages, or one CTA per SM that one buffer needs anyway
+  static constexpr bool PP = !DM && (sm2(3) <= HALF_SM || (sm1(3) > HALF_SM && sm2(3) <= FULL_SM));
+  static constexpr size_t LIM = (PP && sm2(3) > HALF_SM) ? FULL_SM : HALF_SM;
+  static constexpr int NS = PP ? (sm2(4) <= LIM ? 4 : 3)
+                               : (sm1(4) <= HALF_SM ? 4 : sm1(3) <= HALF_SM ? 3 : sm1(4) <= FULL_SM ? 4 : 3);
+  static constexpr size_t smem_for(int ns) { return PP ? sm2(ns) : sm1(ns); }
   static constexpr size_t TSMEM = smem_for(NS);
   static constexpr int MINB = (TSMEM <= HALF_SM && NT <= 384) ? 2 : 1;
 };
@@ -372,7 +380,9 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   // this kernel); TMA boxes need 128-byte aligned destinations
   extern __shared__ __align__(1024) double sm[];
   double* EB = sm + NS * STR;  // E x M x M element buffers
-  double* FR = EB + E * MM;    // DMMA fragment table (DM only)
+  constexpr bool PP = K::PP;
+  double* EB2 = EB + (PP ? E * MM : 0);   // second element buffer (PP: DFMA stages 2 and 4 write here; else EB)
+  double* FR = EB + (PP ? 2 : 1) * E * MM; // DMMA fragment table (DM only)
   double* SN = FR + K::FRN;    // per-element 1/nu_bar of the current tile (DM only)
   uint64_t* barR = reinterpret_cast<uint64_t*>(SN + (DM ? E : 0));
   uint64_t* barU = barR + NS;
@@ -387,6 +397,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const bool act = e < E;
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
+  double* B2 = EB2 + e * MM;
   // this thread's half row of 1/(lam_y + lam_x) (L1-resident across tiles)
   const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
 
@@ -512,7 +523,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     }
 
     if (A.debug_skip) {
-      for (int idx = tid; idx < E * MM; idx += NT) EB[idx] = 0.0;
+      for (int idx = tid; idx < (PP ? 2 : 1) * E * MM; idx += NT) EB[idx] = 0.0;
       __syncthreads();
     } else if constexpr (DM) {
       double fe[K::FE], fo[K::FO];
@@ -684,14 +695,14 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           if (!odd) half_analyse<M, HE, false>(A.Sxe, in, t);
           else if (HO > 0) half_analyse<M, HOX, true>(A.Sxo, in, reinterpret_cast<double(&)[HOX]>(t));
         }
-        __syncthreads();  // every row read before the in-place writes
-        if (act) {
+        if constexpr (!PP) __syncthreads();  // every row read before the in-place writes
+        if (act) {   // PP: into the second buffer, no read-before-write barrier
           if (!odd) {
 #pragma unroll
-            for (int l = 0; l < HE; ++l) B[c * M + l] = t[l] * (__ldg(dl + l) * s);
+            for (int l = 0; l < HE; ++l) B2[c * M + l] = t[l] * (__ldg(dl + l) * s);
           } else {
 #pragma unroll
-            for (int l = 0; l < HO; ++l) B[c * M + HE + l] = t[l] * (__ldg(dl + l) * s);
+            for (int l = 0; l < HO; ++l) B2[c * M + HE + l] = t[l] * (__ldg(dl + l) * s);
           }
         }
       }
@@ -705,17 +716,17 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           if (!odd) {
             double t[HE];
 #pragma unroll
-            for (int i = 0; i < HE; ++i) t[i] = B[i * M + c];
+            for (int i = 0; i < HE; ++i) t[i] = B2[i * M + c];
             half_synth<HE>(A.SyeT, t, acc);
           } else if (HO > 0) {
             double t[HOX];
 #pragma unroll
-            for (int i = 0; i < HO; ++i) t[i] = B[(HE + i) * M + c];
+            for (int i = 0; i < HO; ++i) t[i] = B2[(HE + i) * M + c];
             half_synth<HOX>(A.SyoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
-        __syncthreads();  // every column read before the in-place writes
-        if (act) {
+        if constexpr (!PP) __syncthreads();  // every column read before the in-place writes
+        if (act) {   // PP: back into the first buffer (stage-1 data is dead)
           if (!odd) {
 #pragma unroll
             for (int k = 0; k < HE; ++k) B[k * M + c] = acc[k];
@@ -750,21 +761,22 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
             half_synth<HOX>(A.SxoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
-        __syncthreads();  // every row read before B is reused for ex / ox
+        if constexpr (!PP) __syncthreads();  // every row read before B is reused for ex / ox
         if (act) {
-          // even warps keep ex in B[c][0,HE), odd warps ox in B[c][HE,M)
+          // even warps keep ex in B2[c][0,HE), odd warps ox in B2[c][HE,M)
           if (!odd) {
 #pragma unroll
-            for (int k = 0; k < HE; ++k) B[c * M + k] = acc[k];
+            for (int k = 0; k < HE; ++k) B2[c * M + k] = acc[k];
           } else {
 #pragma unroll
-            for (int k = 0; k < HO; ++k) B[c * M + HE + k] = acc[k];
+            for (int k = 0; k < HO; ++k) B2[c * M + HE + k] = acc[k];
           }
         }
       }
       __syncthreads();
-      fdt_epilogue_fold<P, NO, TX, TY, NT>(EB);
+      fdt_epilogue_fold<P, NO, TX, TY, NT>(EB2);
     }
+    double* EF = (DM || !PP) ? EB : EB2;   // the finished element corrections
     if (!u_zero) mbar_wait(barU + b, par);
 
     // ---- gather: every region node reads ONE cell -- its home element's, or
@@ -774,7 +786,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       constexpr int NG = NT / OX;  // >= 2: NT >= 2 E M > 2 OX
       if (tid < NG * OX) {
         const int ox = tid % OX, g = tid / OX;
-        const double* cb = EB + (ox / P) * MM + (ox % P + NO);
+        const double* cb = EF + (ox / P) * MM + (ox % P + NO);
         for (int oy = g; oy < OY; oy += NG) {
           const double cor = cb[(oy / P) * (TX * MM) + (oy % P + NO) * M];
           double* uo = buf + oy * OX + ox;
@@ -800,7 +812,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
         const int ey = y < NO ? 0 : min((y - NO) / P, TY - 1);
         const int ex = x < NO ? 0 : min((x - NO) / P, TX - 1);
-        W[k] = EB[(ey * TX + ex) * MM + (y - ey * P) * M + (x - ex * P)];
+        W[k] = EF[(ey * TX + ex) * MM + (y - ey * P) * M + (x - ex * P)];
       }
     }
     fence_proxy_async_smem();
