@@ -535,10 +535,14 @@ __global__ void __launch_bounds__(4 * N) pinv_sq_kernel(const double* __restrict
   // T2[i0+i][x] = (sum_j T1[i][j] Qx[j][x]) * Lp[i0+i][x]
   T2[(i0 + i) * N + x] = pc_dot<N>(T1 + i * N, 1, QX + x, N) * LP[tid];
   cl.sync();
-  for (int c = 0; c < CLN; ++c) {
-    if (c == rank) continue;
-    const double* rem = cl.map_shared_rank(T2, c);
-    if (tid < RB * N) T2[c * RB * N + tid] = rem[c * RB * N + tid];
+  {
+    // gather the other CTAs' rows: all remote loads in flight, then stores
+    double g[CLN];
+#pragma unroll
+    for (int c = 0; c < CLN; ++c) g[c] = c == rank ? 0.0 : cl.map_shared_rank(T2, c)[c * RB * N + tid];
+#pragma unroll
+    for (int c = 0; c < CLN; ++c)
+      if (c != rank) T2[c * RB * N + tid] = g[c];
   }
   __syncthreads();
   // T1[i][x] = sum_k Qy[i0+i][k] T2[k][x]
