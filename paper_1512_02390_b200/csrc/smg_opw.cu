@@ -82,12 +82,12 @@ struct OpwGeom {
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int HX = OX + P + 1, HY = OY + P + 1;
   static constexpr int DP = (HX + 2) & ~1;
-  static constexpr int LDA = P + 1;   // per-warp AX / AY row stride
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY + 2 * (size_t)NW * P * LDA) + 16;
+  static constexpr int LDA = P + 1;   // per-warp AX row stride
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY + (size_t)NW * P * LDA) + 16;
 };
 
 template <int P, int TX, int TY>
-__global__ void __launch_bounds__(32 * TX * TY) opw_kernel(const __grid_constant__ OpwArgs<P> A) {
+__global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   SMG_PDL_ENTRY();
   using G = OpwGeom<P, TX, TY>;
   constexpr int NW = G::NW, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, DP = G::DP, LDA = G::LDA;
@@ -95,8 +95,7 @@ __global__ void __launch_bounds__(32 * TX * TY) opw_kernel(const __grid_constant
   extern __shared__ __align__(16) double smw[];
   double* U = smw;                          // HY x DP, origin (Y0-P, X0-P) at column sh
   double* AXb = U + DP * HY;                // NW x P x LDA: x-part [a][b]
-  double* AYb = AXb + NW * P * LDA;         // NW x P x LDA: y-part [b][a]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(AYb + NW * P * LDA);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(AXb + NW * P * LDA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int X0 = tx * OX, Y0 = ty * OY;
@@ -109,26 +108,16 @@ __global__ void __launch_bounds__(32 * TX * TY) opw_kernel(const __grid_constant
   }
   __syncthreads();
   if (warp == 0) pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
-  // this warp's element and output lanes; f of its outputs in flight
+  // this warp's element
   const int exl = warp % TX, eyl = warp / TX;
-  const int b = lane & 15, h = lane >> 4;
-  constexpr int APL = P / 2;                 // output rows per lane
-  const bool olane = b < P;
-  double fv[APL];
-#pragma unroll
-  for (int i = 0; i < APL; ++i) {
-    const int a = h * APL + i;
-    fv[i] = (olane && A.f != nullptr) ? __ldg(A.f + (size_t)(Y0 + eyl * P + a) * N_x + (X0 + exl * P + b)) : 0.0;
-  }
   mbar_wait(bar, 0);
   // element origin in U
   const int ur0 = P + eyl * P, uc0 = sh + P + exl * P;
   double* AX = AXb + warp * P * LDA;
-  double* AY = AYb + warp * P * LDA;
   // lanes 0..P-1: row a = lane (stride 1); lanes 16..16+P-1: column b (stride DP)
   const int li = lane & 15;
   const bool lact = li < P;
-  const bool col = h == 1;
+  const bool col = lane >= 16;
   const int st = col ? DP : 1;
   const double* xl = col ? U + ur0 * DP + uc0 + li : U + (ur0 + li) * DP + uc0;
   const double* xv = col ? xl - P * DP : xl - P;   // the neighbour element's line (vertex term)
@@ -143,22 +132,28 @@ __global__ void __launch_bounds__(32 * TX * TY) opw_kernel(const __grid_constant
       dst[0] = v[0] + vv[P];
 #pragma unroll
       for (int k = 1; k < P; ++k) dst[k] = v[k];
-    } else {
-      double* dst = AY + li * LDA;      // column b = li: line values at a, lower vertex in slot P
-#pragma unroll
-      for (int k = 0; k < P; ++k) dst[k] = v[k];
-      dst[P] = vv[P];
     }
   }
   __syncwarp();
-  if (olane) {
+  // the column lane b keeps the y-part of its column in registers and writes
+  // the column's outputs (each row of r coalesced across the half-warp)
+  if (col && lact) {
+    const int b = li;
     const double wyb = A.cy * A.wasm[b];
+    const size_t g0 = (size_t)(Y0 + eyl * P) * N_x + (X0 + exl * P + b);
+    constexpr int CH = P / 2;          // f loads in flight per chunk
 #pragma unroll
-    for (int i = 0; i < APL; ++i) {
-      const int a = h * APL + i;
-      double val = fma(A.cx * A.wasm[a], AX[a * LDA + b], wyb * AY[b * LDA + a]);
-      if (a == 0) val = fma(wyb, AY[b * LDA + P], val);
-      A.out[(size_t)(Y0 + eyl * P + a) * N_x + (X0 + exl * P + b)] = A.f != nullptr ? fv[i] - val : val;
+    for (int a0 = 0; a0 < P; a0 += CH) {
+      double fv[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) fv[i] = A.f != nullptr ? __ldg(A.f + g0 + (size_t)(a0 + i) * N_x) : 0.0;
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int a = a0 + i;
+        double val = fma(A.cx * A.wasm[a], AX[a * LDA + b], wyb * v[a]);
+        if (a == 0) val = fma(wyb, vv[P], val);
+        A.out[g0 + (size_t)a * N_x] = A.f != nullptr ? fv[i] - val : val;
+      }
     }
   }
 }
