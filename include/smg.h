@@ -45,6 +45,10 @@ int smg_version(void);
 /* Number of kernel launches libsmg has enqueued in this process (evidence
  * for the bench's gpu_launches claim; graph replays are not re-counted). */
 int64_t smg_launch_count(void);
+/* Profiling aid (SMG_FDT_PHASES=1 in the environment): copies the tiled
+ * Schwarz kernel's per-phase cycle sums (out[0] = tiles, out[1..] = cycles
+ * of thread 0 per phase, summed over CTAs) into out[0..n) and resets them. */
+int smg_debug_fdt_phases(unsigned long long* out, int n);
 /* 1 if a CUDA device is usable, else 0 (and smg_last_error says why). */
 int smg_device_ok(void);
 

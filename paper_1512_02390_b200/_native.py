@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmg.so")
+# SMG_LIB: an alternative build of the same library (e.g. the phase-profile build, tools/fdt_phases.py)
+LIB_PATH = os.environ.get("SMG_LIB") or os.path.join(_HERE, "libsmg.so")
 
 SMG_EINVAL = -1
 SMG_EUNSUPPORTED = -2
@@ -30,6 +31,7 @@ SIGNATURES = {
     "smg_version": (C.c_int, []),
     "smg_launch_count": (C.c_int64, []),
     "smg_device_ok": (C.c_int, []),
+    "smg_debug_fdt_phases": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     "smg_op_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                 C.c_double, _hp, _hp, _dp]),
     "smg_op_destroy": (C.c_int, [_vp]),

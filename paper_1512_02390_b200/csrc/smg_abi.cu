@@ -172,9 +172,30 @@ bool even_odd_split(const double* S, int m, std::vector<double>& Se, std::vector
 
 }  // namespace
 
+namespace smg {
+// Profiling aid for the tiled Schwarz kernel: per-phase clock64 sums of
+// thread 0 of every CTA, enabled by SMG_FDT_PHASES=1 (else nullptr: no cost).
+unsigned long long* fdt_phase_buffer() {
+  static unsigned long long* buf = nullptr;
+  static const int on = env_int("SMG_FDT_PHASES", 0);
+  if (on && buf == nullptr && cudaMalloc(&buf, sizeof(unsigned long long) * FDT_NPH) == cudaSuccess)
+    cudaMemset(buf, 0, sizeof(unsigned long long) * FDT_NPH);
+  return buf;
+}
+}  // namespace smg
+
 extern "C" {
 
 const char* smg_last_error(void) { return g_err; }
+
+int smg_debug_fdt_phases(unsigned long long* out, int n) {
+  unsigned long long* buf = smg::fdt_phase_buffer();
+  if (buf == nullptr) return set_error("smg_debug_fdt_phases: SMG_FDT_PHASES=1 not set"), SMG_EINVAL;
+  const int k = n < smg::FDT_NPH ? n : smg::FDT_NPH;
+  cudaError_t e = cudaMemcpy(out, buf, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(buf, 0, sizeof(unsigned long long) * smg::FDT_NPH);
+  return e == cudaSuccess ? SMG_OK : cuda_fail(e, "smg_debug_fdt_phases");
+}
 int smg_version(void) { return 1; }
 int64_t smg_launch_count(void) { return g_launches.load(); }
 

@@ -36,6 +36,10 @@ namespace smg {
 __host__ __device__ constexpr int fdt_he(int M) { return (M + 1) / 2; }  // even half (incl. centre)
 __host__ __device__ constexpr int fdt_ho(int M) { return M / 2; }        // odd half
 
+// Profiling aid: device buffer of FDT_NPH per-phase cycle sums (smg_abi.cu)
+constexpr int FDT_NPH = 10;
+unsigned long long* fdt_phase_buffer();
+
 template <int M>
 struct FDTArgs {
   CUtensorMap rmap;                   // residual (N_y, N_x), box (BRX, RY)
@@ -49,6 +53,7 @@ struct FDTArgs {
   int debug_skip;                     // profiling aid: 1 = skip the four contractions
   int u_zero;                         // 1: u holds no valid data and is treated as 0 (write, not add)
   int fused_fixup;                    // 1: cooperative launch, ring fixup after a grid barrier
+  unsigned long long* phases;         // profiling aid (SMG_FDT_PHASES=1): per-phase clock64 sums, else nullptr
   // analysis factors Se[k][i] (k physical half index); synthesis factors
   // SeT[i][k] pre-multiplied by the (mirror-symmetric) Schwarz weight w[k]
   double Sye[fdt_he(M) * fdt_he(M)], SyeT[fdt_he(M) * fdt_he(M)];
@@ -309,7 +314,12 @@ struct FDTK {
   static constexpr int NS = PP ? (sm2(4) <= LIM ? 4 : 3)
                                : (sm1(4) <= HALF_SM ? 4 : sm1(3) <= HALF_SM ? 3 : sm1(4) <= FULL_SM ? 4 : 3);
   static constexpr size_t smem_for(int ns) { return PP ? sm2(ns) : sm1(ns); }
-  static constexpr size_t TSMEM = smem_for(NS);
+  // DFMA stage 2 reads 1/(lam_y + lam_x) from shared memory when the table
+  // fits beside the chosen configuration (else from global memory through L1:
+  // those loads were the stage's long-scoreboard stalls)
+  static constexpr size_t SDB = sizeof(double) * (size_t)M * M;
+  static constexpr bool SDV = !DM && smem_for(NS) + SDB <= (smem_for(NS) <= HALF_SM ? HALF_SM : FULL_SM);
+  static constexpr size_t TSMEM = smem_for(NS) + (SDV ? SDB : 0);
   static constexpr int MINB = (TSMEM <= HALF_SM && NT <= 384) ? 2 : 1;
 };
 
@@ -384,7 +394,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   double* EB2 = EB + (PP ? E * MM : 0);   // second element buffer (PP: DFMA stages 2 and 4 write here; else EB)
   double* FR = EB + (PP ? 2 : 1) * E * MM; // DMMA fragment table (DM only)
   double* SN = FR + K::FRN;    // per-element 1/nu_bar of the current tile (DM only)
-  uint64_t* barR = reinterpret_cast<uint64_t*>(SN + (DM ? E : 0));
+  double* SD = SN + (DM ? E : 0);  // 1/(lam_y + lam_x) table (K::SDV)
+  uint64_t* barR = reinterpret_cast<uint64_t*>(SD + (K::SDV ? M * M : 0));
   uint64_t* barU = barR + NS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, t4 = lane & 3;
   const int tid = threadIdx.x;
@@ -398,8 +409,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   const int exl = e % TX, eyl = e / TX;
   double* B = EB + e * MM;
   double* B2 = EB2 + e * MM;
-  // this thread's half row of 1/(lam_y + lam_x) (L1-resident across tiles)
-  const double* dl = A.dinv + (act ? c : 0) * M + (odd ? HE : 0);
+  // this thread's half row of 1/(lam_y + lam_x) (shared memory, or L1-resident across tiles)
+  const double* dl = (K::SDV ? SD : A.dinv) + (act ? c : 0) * M + (odd ? HE : 0);
 
   if (tid == 0) {
     if (smem_u32(sm) & 127) __trap();  // alignment assumption above
@@ -407,6 +418,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     fence_mbar_init();
   }
   if constexpr (DM) dm_build_frags<M, FDTArgs<M>, K::FE, K::FO, K::KTE, K::KTO>(A, FR, NT);
+  if constexpr (K::SDV)
+    for (int idx = tid; idx < M * M; idx += NT) SD[idx] = A.dinv[idx];
   __syncthreads();
 
   // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
@@ -430,7 +443,20 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     cp_async_commit();
   }
   int tile = blockIdx.x;
+#ifdef SMG_FDT_PROFILE
+  // phase profile (build with -DSMG_FDT_PROFILE, run with SMG_FDT_PHASES=1; tools/fdt_phases.py)
+  const bool prof = A.phases != nullptr && tid == 0;
+  unsigned long long ph[FDT_NPH] = {}, tlast = 0;
+  auto mark = [&](int k) {
+    if (prof) { const unsigned long long t = clock64(); ph[k] += t - tlast; tlast = t; }
+  };
+#else
+  auto mark = [](int) {};
+#endif
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+#ifdef SMG_FDT_PROFILE
+    if (prof) { tlast = clock64(); ph[0] += 1; }
+#endif
     const int b = it % NS;
     const unsigned par = (unsigned)(it / NS) & 1u;
     double* buf = sm + b * STR;
@@ -442,6 +468,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     cp_async_wait<NS - 3>();
     mbar_wait(barR + b, par);
     __syncthreads();
+    mark(1);
 
     // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
     if constexpr (DM) {
@@ -509,6 +536,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     }
     if (tid == 0) bulk_wait_read<1>();  // the store of tile it-2 has left its buffer
     __syncthreads();
+    mark(2);
     // this buffer's residual is consumed: bring in the own block of u; and
     // refill the buffer of tile it-2 with the residual of tile it+NS-2
     if (tid == 0 && !u_zero) {
@@ -521,6 +549,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       if (nxt < ntiles) issue_r(nxt, (it + NS - 2) % NS);
       cp_async_commit();
     }
+    mark(9);
 
     if (A.debug_skip) {
       for (int idx = tid; idx < (PP ? 2 : 1) * E * MM; idx += NT) EB[idx] = 0.0;
@@ -699,14 +728,15 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         if (act) {   // PP: into the second buffer, no read-before-write barrier
           if (!odd) {
 #pragma unroll
-            for (int l = 0; l < HE; ++l) B2[c * M + l] = t[l] * (__ldg(dl + l) * s);
+            for (int l = 0; l < HE; ++l) B2[c * M + l] = t[l] * ((K::SDV ? dl[l] : __ldg(dl + l)) * s);
           } else {
 #pragma unroll
-            for (int l = 0; l < HO; ++l) B2[c * M + HE + l] = t[l] * (__ldg(dl + l) * s);
+            for (int l = 0; l < HO; ++l) B2[c * M + HE + l] = t[l] * ((K::SDV ? dl[l] : __ldg(dl + l)) * s);
           }
         }
       }
       __syncthreads();
+      mark(3);
 
       // ---- stage 3 (eigen-x columns c): even warps e = SyeT^T T2e[:, c] -> rows [0,HE),
       //      odd warps o = SyoT^T T2o[:, c] -> rows [HE, M)   (e/o recombined in stage 4)
@@ -737,6 +767,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       }
       __syncthreads();
+      mark(4);
 
       // ---- stage 4 (physical rows c): T3[c, :] = e[c'] +- o[c'] (c' = mirror-folded
       //      row), then even warps ex = SxeT^T T3e, odd warps ox = SxoT^T T3o ----
@@ -774,10 +805,13 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       }
       __syncthreads();
+      mark(5);
       fdt_epilogue_fold<P, NO, TX, TY, NT>(EB2);
+      mark(6);
     }
     double* EF = (DM || !PP) ? EB : EB2;   // the finished element corrections
     if (!u_zero) mbar_wait(barU + b, par);
+    mark(7);
 
     // ---- gather: every region node reads ONE cell -- its home element's, or
     //      for ring nodes the edge element covering it ----------------------
@@ -817,11 +851,16 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     }
     fence_proxy_async_smem();
     __syncthreads();
+    mark(8);
     if (tid == 0) {
       tma_store_2d(&A.umap, buf, X0, Y0);
       bulk_commit();
     }
   }
+#ifdef SMG_FDT_PROFILE
+  if (prof)
+    for (int k = 0; k < FDT_NPH; ++k) atomicAdd(A.phases + k, ph[k]);
+#endif
   if (tid == 0) bulk_wait0();
   cp_async_wait<0>();
   if (A.fused_fixup) {
@@ -1002,6 +1041,7 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
     A.debug_skip = (dbg && dbg[0] == '1') ? 1 : 0;
   }
   A.u_zero = L.u_zero;
+  A.phases = fdt_phase_buffer();
   // synthesis factors carry the weight of their output node: W (S t S^T) =
   // (diag(w_y) S_y) t (diag(w_x) S_x)^T, and w is mirror-symmetric, so the
   // even/odd recombination e +- o inherits it

@@ -1,0 +1,52 @@
+"""Schwarz-correction diagnostics: time one correction per (n, p) for each
+contraction engine, with and without the contractions (SMG_FD_DEBUG_SKIP=1:
+memory pipeline + epilogue only).  CUDA events, L2 flushed, median of 10.
+
+    python tools/fd_diag.py [n:p ...]      (default 256:16 256:24 256:32 128:32)
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1512_02390_b200 as P  # noqa: E402
+
+flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+cfgs = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]] or [(256, 16), (256, 24), (256, 32), (128, 32)]
+engines = os.environ.get("ENGINES", "dfma,dmma_eo").split(",")
+HBM = 6555.5e9
+P64 = 37.15e12
+
+
+def eo_flops_per_dof(p, n_o=1):
+    m = p + 1 + 2 * n_o
+    he, ho = (m + 1) // 2, m // 2
+    return (8 * m * (he * he + ho * ho) + m * m) / (p * p)
+
+
+for n, p in cfgs:
+    mesh = P.MeshConfig(n, n, 1.0, 1.0)
+    lay = P.layout_for(mesh, p)
+    r = torch.randn(lay.shape, dtype=torch.float64, device="cuda")
+    u = torch.randn(lay.shape, dtype=torch.float64, device="cuda")
+    t_roof = max(24.0 * lay.size / HBM, eo_flops_per_dof(p) * lay.size / P64) * 1e6
+    for eng in engines:
+        os.environ["SMG_FD_ENGINE"] = eng
+        sm = P.AdditiveSchwarz(P.gll_basis(p), lay, mesh.dx, mesh.dy, 1, P.WeightKind.QUINTIC)
+        for skip in ("0", "1"):
+            os.environ["SMG_FD_DEBUG_SKIP"] = skip
+            sm.correct(r, u)
+            ts = []
+            for _ in range(10):
+                flush.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                sm.correct(r, u)
+                b.record()
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            t = sorted(x.elapsed_time(y) for x, y in ts)[5] * 1e3
+            print(f"n={n} p={p} {eng:8s} skip={skip}: {t:8.1f} us  {lay.size / t / 1e3:7.2f} GDOF/s  "
+                  f"roof {t_roof:7.1f} us  frac {t_roof / t:.3f}", flush=True)
+    os.environ["SMG_FD_DEBUG_SKIP"] = "0"
