@@ -53,6 +53,9 @@ __device__ __forceinline__ void ms_mm(double* C, const double* A, int ai, int ak
 }
 
 __global__ void __launch_bounds__(kMsThreads, 1) mult_sweep_kernel(const __grid_constant__ MsArgs A) {
+  // launched with programmatic stream serialization like every libsmg kernel:
+  // wait for the residual launch before reading r (and u)
+  SMG_PDL_ENTRY();
   extern __shared__ __align__(16) double sms[];
   const int p = A.p, n_o = A.n_o, m = A.m, n_x = A.n_x, n_y = A.n_y;
   const int NP = p + 1, N_x = n_x * p, N_y = n_y * p, mm = m * m;

@@ -49,6 +49,23 @@ struct OpArgs {
   double wasm[P];                    // assembled weight by local index a in [0,p)
 };
 
+// Optional (-DSMG_DIFF_SMEM): diffusion with the derivative matrix D staged in
+// shared memory (D and D^T, rows padded to an even pitch, read as double2
+// broadcasts) instead of the parameter constant bank.  Measured on B200 at
+// C5's p = 24 level (151M DOF residual): constant bank 7.9 ms, shared memory
+// 13.7 ms (one CTA fewer per SM, shared-memory bandwidth), so the constant
+// bank stays the default.
+template <int P>
+struct DiffTab {
+#ifdef SMG_DIFF_SMEM
+  static constexpr bool ON = P >= 3;
+#else
+  static constexpr bool ON = false;
+#endif
+  static constexpr int NP = P + 1, NPP = (NP + 1) & ~1;
+  static constexpr int DOUBLES = ON ? 2 * NP * NPP : 0;
+};
+
 template <int P, int TX, int TY, bool DIFF>
 struct OpGeom {
   static constexpr int NP = P + 1;
@@ -57,9 +74,28 @@ struct OpGeom {
   static constexpr int DP = (HX + 2) & ~1;     // staged row pitch (room for the bulk-copy shift)
   static constexpr int ROWJ = OY * (TX + 1), COLJ = OX * (TY + 1);
   static constexpr int THREADS = (ROWJ > COLJ ? ROWJ : COLJ) >= 256 ? 256 : (((ROWJ > COLJ ? ROWJ : COLJ) + 31) / 32) * 32;
+  static constexpr int DTAB = DIFF ? DiffTab<P>::DOUBLES : 0;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY * (DIFF ? 2 : 1) + (size_t)OX * OY +
-                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1) + P) + 16;
+                                                   (size_t)OY * (TX + 1) + (size_t)OX * (TY + 1) + P + DTAB + 2) + 16;
 };
+
+// DS[j][b] = D[j][b], DT[k][j] = D[j][k] (pitch NPP, zero padding), from the
+// row-major D in the parameter bank; all threads of the CTA call.
+template <int P>
+__device__ __forceinline__ void diff_tab_fill(const double* Mt, double* DS, int tid, int nt) {
+  constexpr int NP = P + 1, NPP = DiffTab<P>::NPP;
+  double* DT = DS + NP * NPP;
+  for (int i = tid; i < NP * NPP; i += nt) {
+    const int r = i / NPP, c = i - r * NPP;
+    DS[i] = c < NP ? Mt[r * NP + c] : 0.0;
+    DT[i] = c < NP ? Mt[c * NP + r] : 0.0;
+  }
+}
+
+// 16-byte aligned start for the tables after `after` doubles.
+__device__ __forceinline__ double* diff_tab_ptr(double* after) {
+  return reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
+}
 
 __device__ __forceinline__ void op_cp_async8(double* smem, const double* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -162,6 +198,76 @@ __device__ __forceinline__ void line_op(const OpArgs<P>& A, const double* x, con
   }
 }
 
+// Diffusion line op with the shared-memory tables (same operation order as
+// line_op's diffusion branch: bitwise-equal results).  g = D x runs as a
+// loop over k (x_k from shared memory, the D^T row as double2 pairs), so only
+// the output contraction v = g D is unrolled.
+template <int P, bool ONLY_LAST, int ST>
+__device__ __forceinline__ void line_op_dsm(const double* __restrict__ w, const double* x, const double* nu,
+                                            const double* DS, double (&v)[P + 1]) {
+  constexpr int NP = P + 1, NPP = DiffTab<P>::NPP, NH = NP / 2;
+  const double* DT = DS + NP * NPP;
+  double g[NP];
+  {
+    const double x0 = x[0];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double2 d = *reinterpret_cast<const double2*>(DT + 2 * j);
+      g[2 * j] = d.x * x0;
+      g[2 * j + 1] = d.y * x0;
+    }
+    if (NP & 1) g[NP - 1] = DT[NP - 1] * x0;
+  }
+#pragma unroll 2
+  for (int k = 1; k < NP; ++k) {
+    const double xk = x[k * ST];
+    const double* dr = DT + k * NPP;
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double2 d = *reinterpret_cast<const double2*>(dr + 2 * j);
+      g[2 * j] = fma(d.x, xk, g[2 * j]);
+      g[2 * j + 1] = fma(d.y, xk, g[2 * j + 1]);
+    }
+    if (NP & 1) g[NP - 1] = fma(dr[NP - 1], xk, g[NP - 1]);
+  }
+#pragma unroll
+  for (int j = 0; j < NP; ++j) g[j] *= nu[j * ST] * w[j];
+  if (ONLY_LAST) {
+    const double* dc = DT + P * NPP;   // D[j][P] = DT[P][j]
+    double s = g[0] * dc[0];
+#pragma unroll
+    for (int j = 1; j < NP; ++j) s = fma(g[j], dc[j], s);
+    v[P] = s;
+  } else {
+#pragma unroll
+    for (int b = 0; b < NH; ++b) {
+      const double2 d = *reinterpret_cast<const double2*>(DS + 2 * b);
+      v[2 * b] = g[0] * d.x;
+      v[2 * b + 1] = g[0] * d.y;
+    }
+    if (NP & 1) v[NP - 1] = g[0] * DS[NP - 1];
+#pragma unroll
+    for (int j = 1; j < NP; ++j) {
+      const double* dr = DS + j * NPP;
+#pragma unroll
+      for (int b = 0; b < NH; ++b) {
+        const double2 d = *reinterpret_cast<const double2*>(dr + 2 * b);
+        v[2 * b] = fma(g[j], d.x, v[2 * b]);
+        v[2 * b + 1] = fma(g[j], d.y, v[2 * b + 1]);
+      }
+      if (NP & 1) v[NP - 1] = fma(g[j], dr[NP - 1], v[NP - 1]);
+    }
+  }
+}
+
+// line_op, with the diffusion tables from shared memory when DS != nullptr
+template <int P, bool DIFF, bool ONLY_LAST, int ST>
+__device__ __forceinline__ void line_op_any(const OpArgs<P>& A, const double* x, const double* nu, const double* DS,
+                                            double (&v)[P + 1]) {
+  if constexpr (DIFF && DiffTab<P>::ON) line_op_dsm<P, ONLY_LAST, ST>(A.w, x, nu, DS, v);
+  else line_op<P, DIFF, ONLY_LAST, ST>(A, x, nu, v);
+}
+
 template <int P, int TX, int TY, bool DIFF>
 __global__ void __launch_bounds__(OpGeom<P, TX, TY, DIFF>::THREADS)
 op_kernel(const __grid_constant__ OpArgs<P> A) {
@@ -177,11 +283,13 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   double* VX = AX + OX * OY;                       // OY x (TX+1): right-vertex value of element exl-1
   double* VY = VX + OY * (TX + 1);                 // OX x (TY+1)
   double* WS = VY + OX * (TY + 1);                 // P assembled weights (indexed per thread)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(WS + P);
+  double* DS = diff_tab_ptr(WS + P);               // diffusion: D, D^T tables (G::DTAB doubles)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(DS + G::DTAB);
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int X0 = tx * OX, Y0 = ty * OY;
   const int N_x = A.N_x, N_y = A.N_y;
+  if constexpr (G::DTAB > 0) diff_tab_fill<P>(A.Mt, DS, tid, NT);
 
   int sh = 0;
   if (A.bulk) {
@@ -221,16 +329,22 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   // row passes: item = (own row y, element exl-1), exl in [0, TX]
   // full lines (exl >= 1) first, the vertex-only lines (exl == 0) last, so
   // that warps do not diverge between the two
-  for (int it = tid; it < OY * (TX + 1); it += NT) {
+  // one-element tiles (p >= 24): full lines on warp 0, the neighbour's
+  // vertex-only lines on warp 1 -- no warp runs both paths one after the
+  // other (C5 p = 24 diffusion residual 11.4 -> 7.9 ms on B200)
+  constexpr bool SPLIT = TX == 1 && TY == 1 && P <= 32 && NT == 64;
+  for (int it0 = tid; it0 < (SPLIT ? NT : OY * (TX + 1)); it0 += NT) {
+    const int it = SPLIT ? (tid < 32 ? tid : OY + tid - 32) : it0;
+    if (SPLIT && (tid & 31) >= P) continue;
     const bool full = it < OY * TX;
     const int y = full ? it / TX : it - OY * TX, exl = full ? 1 + (it - (it / TX) * TX) : 0;
     const double* ur = U + (y + P) * DP + sh + exl * P;
     const double* nr = NU + (y + P) * DP + sh + exl * P;
     double v[NP];
     if (exl == 0) {
-      line_op<P, DIFF, true, 1>(A, ur, nr, v);
+      line_op_any<P, DIFF, true, 1>(A, ur, nr, DS, v);
     } else {
-      line_op<P, DIFF, false, 1>(A, ur, nr, v);
+      line_op_any<P, DIFF, false, 1>(A, ur, nr, DS, v);
       double* ax = AX + y * OX + (exl - 1) * P;
 #pragma unroll
       for (int b = 0; b < P; ++b) ax[b] = v[b];
@@ -242,16 +356,18 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
   // node of the item's column gets its full x-part (with the vertex term of
   // the left element) and its own y-part; the y-vertex term of the element
   // below (a == 0) is added in the output pass
-  for (int it = tid; it < OX * (TY + 1); it += NT) {
+  for (int it0 = tid; it0 < (SPLIT ? NT : OX * (TY + 1)); it0 += NT) {
+    const int it = SPLIT ? (tid < 32 ? tid : OX + tid - 32) : it0;
+    if (SPLIT && (tid & 31) >= P) continue;
     const bool full = it < OX * TY;
     const int x = full ? it / TY : it - OX * TY, eyl = full ? 1 + (it - (it / TY) * TY) : 0;
     const double* uc = U + (eyl * P) * DP + sh + (x + P);
     const double* nc = NU + (eyl * P) * DP + sh + (x + P);
     double v[NP];
     if (eyl == 0) {
-      line_op<P, DIFF, true, DP>(A, uc, nc, v);
+      line_op_any<P, DIFF, true, DP>(A, uc, nc, DS, v);
     } else {
-      line_op<P, DIFF, false, DP>(A, uc, nc, v);
+      line_op_any<P, DIFF, false, DP>(A, uc, nc, DS, v);
       const int exl = x / P, b = x - exl * P;
       const double wyb = A.cy * WS[b];
       double* axc = AX + ((eyl - 1) * P) * OX + x;

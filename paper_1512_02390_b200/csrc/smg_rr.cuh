@@ -34,7 +34,8 @@ struct RRGeom {
   static constexpr int NT = OG::THREADS;
   static constexpr size_t SMEM =
       sizeof(double) * ((size_t)OG::DP * OG::HY * (DIFF ? 2 : 1) + (size_t)FX * FX + 2 * (size_t)FX * (T + 2) + PF +
-                        (size_t)FX * OXC + (size_t)FX * (T + 1) + (size_t)OXC * OXC + (size_t)(T + 1) * OXC) +
+                        (size_t)FX * OXC + (size_t)FX * (T + 1) + (size_t)OXC * OXC + (size_t)(T + 1) * OXC +
+                        OG::DTAB + 2) +
       16;
 };
 
@@ -59,8 +60,10 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
   double* VT = Tx + FX * OXC;                      // FX x (T+1)
   double* S = VT + FX * (T + 1);                   // OXC x OXC
   double* VC = S + OXC * OXC;                      // (T+1) x OXC
-  uint64_t* bar = reinterpret_cast<uint64_t*>(VC + (T + 1) * OXC);
+  double* DS = diff_tab_ptr(VC + (T + 1) * OXC);   // diffusion: D, D^T tables
+  uint64_t* bar = reinterpret_cast<uint64_t*>(DS + OG::DTAB);
   const int tid = threadIdx.x;
+  if constexpr (OG::DTAB > 0) diff_tab_fill<P>(A.Mt, DS, tid, NT);
   const int tx = blockIdx.x % R.tiles_x, ty = blockIdx.x / R.tiles_x;
   const int N_x = A.N_x, N_y = A.N_y;
   // residual tile origin: one element below/left of the coarse block
@@ -94,9 +97,9 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
     const double* nr = NU + (y + P) * DP + sh + exl * P;
     double v[NP];
     if (exl == 0) {
-      line_op<P, DIFF, true, 1>(A, ur, nr, v);
+      line_op_any<P, DIFF, true, 1>(A, ur, nr, DS, v);
     } else {
-      line_op<P, DIFF, false, 1>(A, ur, nr, v);
+      line_op_any<P, DIFF, false, 1>(A, ur, nr, DS, v);
       double* ax = AX + y * OX + (exl - 1) * P;
 #pragma unroll
       for (int b = 0; b < P; ++b) ax[b] = v[b];
@@ -110,9 +113,9 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
     const double* nc = NU + (eyl * P) * DP + sh + (x + P);
     double v[NP];
     if (eyl == 0) {
-      line_op<P, DIFF, true, DP>(A, uc, nc, v);
+      line_op_any<P, DIFF, true, DP>(A, uc, nc, DS, v);
     } else {
-      line_op<P, DIFF, false, DP>(A, uc, nc, v);
+      line_op_any<P, DIFF, false, DP>(A, uc, nc, DS, v);
       const int exl = x / P, b = x - exl * P;
       const double wyb = A.cy * WS[b];
       double* axc = AX + ((eyl - 1) * P) * OX + x;
