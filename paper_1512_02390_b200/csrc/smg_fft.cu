@@ -54,6 +54,44 @@ __device__ __forceinline__ void fft_lines(double2* buf, int n, int logn, int lin
   }
 }
 
+// Multi-CTA variant: line-local index i stored at i + i/16 (the bit-reversed
+// scatter and the strided butterfly stages hit 16 banks otherwise) and
+// stage-major complex twiddles SW[half - 1 + pos] = W^(pos n / (2 half))
+// (consecutive threads read consecutive entries).  Same butterflies, same
+// twiddle values, same order: bitwise-equal results.
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 4); }
+
+__device__ __forceinline__ void fft_lines_p(double2* buf, int n, int logn, int lines, int ls, const double2* SW,
+                                            bool inv) {
+  const int nh = n >> 1;
+  for (int s = 0; s < logn; ++s) {
+    const int half = 1 << s;
+    for (int b = threadIdx.x; b < lines * nh; b += blockDim.x) {
+      const int l = b >> (logn - 1), j = b & (nh - 1);
+      const int grp = j >> s, pos = j & (half - 1);
+      const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+      double2* x = buf + (size_t)l * ls;
+      const double2 w = SW[half - 1 + pos];
+      const double c = w.x, sn = inv ? w.y : -w.y;
+      const double2 a = x[fpad(i0)], bb = x[fpad(i1)];
+      const double tr = bb.x * c - bb.y * sn, ti = bb.x * sn + bb.y * c;
+      x[fpad(i0)] = make_double2(a.x + tr, a.y + ti);
+      x[fpad(i1)] = make_double2(a.x - tr, a.y - ti);
+    }
+    __syncthreads();
+  }
+}
+
+// SW (n - 1 entries) from the natural table tw (cos, sin of 2 pi k / n, k < n/2)
+__device__ __forceinline__ void fft_stage_twiddles(const double* tw, int n, double2* SW) {
+  const int nh = n >> 1;
+  for (int e = threadIdx.x; e < n - 1; e += blockDim.x) {
+    const int half = 1 << (31 - __clz(e + 1));   // largest power of two <= e + 1
+    const int pos = e + 1 - half, k = pos * (nh / half);
+    SW[e] = make_double2(tw[2 * k], tw[2 * k + 1]);
+  }
+}
+
 // mu(k) = 2 - 2 cos(2 pi k / n) from the twiddle table (cos is even in k)
 __device__ __forceinline__ double mu_of(int k, int n, const double* tw) {
   const int kk = k <= n / 2 ? k : n - k;
@@ -107,62 +145,74 @@ __global__ void __launch_bounds__(1024) fft_pinv_small_kernel(int nx, int ny, in
 }
 
 // ---- three launches for larger meshes ------------------------------------------
-constexpr int kFftLines = 8;
+// `lines` FFT lines per CTA, chosen per launch so that the grid has >= 256
+// CTAs (8 lines per CTA gave 64 CTAs at 512^2: 72 us per solve on B200)
 
-// rows [r0, r0+8): forward (inv = false, real input f) or inverse (inv = true,
+// rows [r0, r0+lines): forward (inv = false, real input f) or inverse (inv = true,
 // complex input W, real output u) FFT along x
 __global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, const __grid_constant__ FftConsts C,
                                                        const double* __restrict__ f, double2* __restrict__ W,
-                                                       double* __restrict__ u, int inv) {
+                                                       double* __restrict__ u, int inv, int lines) {
   SMG_PDL_ENTRY();
   extern __shared__ __align__(16) double2 zs[];
-  double* TX = reinterpret_cast<double*>(zs + kFftLines * nx);
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
-  const int r0 = blockIdx.x * kFftLines, nr = min(kFftLines, ny - r0);
+  const int ls = fpad(nx);
+  double2* SX = zs + lines * ls;
+  const int r0 = blockIdx.x * lines, nr = min(lines, ny - r0);
+  fft_stage_twiddles(C.twx, nx, SX);
   for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) {
     const int l = i / nx, x = i - l * nx;
     const size_t g = (size_t)(r0 + l) * nx + x;
-    zs[l * nx + brev(x, lx)] = inv ? W[g] : make_double2(f[g], 0.0);
+    zs[l * ls + fpad(brev(x, lx))] = inv ? W[g] : make_double2(f[g], 0.0);
   }
   __syncthreads();
-  fft_lines(zs, nx, lx, nr, nx, 1, TX, inv != 0);
+  fft_lines_p(zs, nx, lx, nr, ls, SX, inv != 0);
   if (!inv) {
-    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) W[(size_t)r0 * nx + i] = zs[i];
+    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) {
+      const int l = i / nx, x = i - l * nx;
+      W[(size_t)r0 * nx + i] = zs[l * ls + fpad(x)];
+    }
   } else {
     const double sc = 1.0 / ((double)nx * ny);
-    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) u[(size_t)r0 * nx + i] = zs[i].x * sc;
+    for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) {
+      const int l = i / nx, x = i - l * nx;
+      u[(size_t)r0 * nx + i] = zs[l * ls + fpad(x)].x * sc;
+    }
   }
 }
 
 // columns [c0, c0+8): forward FFT along y, divide by lambda, inverse FFT along y
 __global__ void __launch_bounds__(512) fft_cols_kernel(int nx, int ny, int ly, double cx, double cy,
-                                                       const __grid_constant__ FftConsts C, double2* __restrict__ W) {
+                                                       const __grid_constant__ FftConsts C, double2* __restrict__ W,
+                                                       int lines) {
   SMG_PDL_ENTRY();
-  extern __shared__ __align__(16) double2 zs[];   // kFftLines x ny (line = column)
-  double2* Z2 = zs + kFftLines * ny;
-  double* TY = reinterpret_cast<double*>(Z2 + kFftLines * ny);
+  extern __shared__ __align__(16) double2 zs[];   // lines x fpad(ny) (line = column)
+  const int ls = fpad(ny);
+  double2* Z2 = zs + lines * ls;
+  double2* SY = Z2 + lines * ls;
+  double* TY = reinterpret_cast<double*>(SY + ny);
   double* TX = TY + ny;
   for (int i = threadIdx.x; i < ny; i += blockDim.x) TY[i] = C.twy[i];
   for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
-  const int c0 = blockIdx.x * kFftLines, nc = min(kFftLines, nx - c0);
+  fft_stage_twiddles(C.twy, ny, SY);
+  const int c0 = blockIdx.x * lines, nc = min(lines, nx - c0);
   for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
     const int y = i / nc, l = i - y * nc;
-    zs[l * ny + brev(y, ly)] = W[(size_t)y * nx + c0 + l];
+    zs[l * ls + fpad(brev(y, ly))] = W[(size_t)y * nx + c0 + l];
   }
   __syncthreads();
-  fft_lines(zs, ny, ly, nc, ny, 1, TY, false);
+  fft_lines_p(zs, ny, ly, nc, ls, SY, false);
   for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
     const int l = i / ny, ky = i - l * ny, kx = c0 + l;
     const double lam = cx * mu_of(kx, nx, TX) + cy * mu_of(ky, ny, TY);
     const double s = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
-    const double2 z = zs[i];
-    Z2[l * ny + brev(ky, ly)] = make_double2(z.x * s, z.y * s);
+    const double2 z = zs[l * ls + fpad(ky)];
+    Z2[l * ls + fpad(brev(ky, ly))] = make_double2(z.x * s, z.y * s);
   }
   __syncthreads();
-  fft_lines(Z2, ny, ly, nc, ny, 1, TY, true);
+  fft_lines_p(Z2, ny, ly, nc, ls, SY, true);
   for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
     const int y = i / nc, l = i - y * nc;
-    W[(size_t)y * nx + c0 + l] = Z2[l * ny + y];
+    W[(size_t)y * nx + c0 + l] = Z2[l * ls + fpad(y)];
   }
 }
 
@@ -206,8 +256,17 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
     return check_launch("fft_pinv_small_kernel");
   }
   double2* W = reinterpret_cast<double2*>(ws);   // the coarse ws holds 2 nx ny doubles
-  const size_t smr = sizeof(double2) * kFftLines * nx + sizeof(double) * nx;
-  const size_t smc = sizeof(double2) * 2 * kFftLines * ny + sizeof(double) * (nx + ny);
+  auto pick = [](int nlines, int n, int* threads) {
+    int lines = 8;
+    while (lines > 1 && nlines / lines < 256) lines >>= 1;
+    const int t = lines * (n / 2);
+    *threads = t >= 512 ? 512 : (t < 64 ? 64 : ((t + 31) / 32) * 32);
+    return lines;
+  };
+  int tr = 0, tc = 0;
+  const int lr = pick(ny, nx, &tr), lc = pick(nx, ny, &tc);
+  const size_t smr = sizeof(double2) * ((size_t)lr * (nx + nx / 16) + nx);
+  const size_t smc = sizeof(double2) * (2 * (size_t)lc * (ny + ny / 16) + ny) + sizeof(double) * (nx + ny);
   static size_t attr_r = 0, attr_c = 0;
   if (smr > attr_r) {
     cudaError_t e = cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
@@ -219,16 +278,14 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
     if (e != cudaSuccess) return cuda_fail(e, "fft_cols_kernel smem attribute");
     attr_c = smc;
   }
-  const int gr = (ny + kFftLines - 1) / kFftLines, gc = (nx + kFftLines - 1) / kFftLines;
-  launch(fft_rows_kernel, dim3(gr), dim3(512), sizeof(double2) * kFftLines * nx + sizeof(double) * nx, st, nx, ny, lx, C, f, W,
-         static_cast<double*>(nullptr), 0);
+  const int gr = (ny + lr - 1) / lr, gc = (nx + lc - 1) / lc;
+  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, C, f, W, static_cast<double*>(nullptr), 0, lr);
   int rc = check_launch("fft_rows_kernel");
   if (rc) return rc;
-  launch(fft_cols_kernel, dim3(gc), dim3(512), sizeof(double2) * 2 * kFftLines * ny + sizeof(double) * (nx + ny), st, nx, ny, ly, cx, cy, C, W);
+  launch(fft_cols_kernel, dim3(gc), dim3(tc), smc, st, nx, ny, ly, cx, cy, C, W, lc);
   rc = check_launch("fft_cols_kernel");
   if (rc) return rc;
-  launch(fft_rows_kernel, dim3(gr), dim3(512), sizeof(double2) * kFftLines * nx + sizeof(double) * nx, st, nx, ny, lx, C,
-         static_cast<const double*>(nullptr), W, u, 1);
+  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, C, static_cast<const double*>(nullptr), W, u, 1, lr);
   return check_launch("fft_rows_kernel");
 }
 
