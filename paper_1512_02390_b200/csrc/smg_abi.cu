@@ -87,6 +87,7 @@ struct smg_op {
   const double* nu;
   double* partials;  // device, one per CTA
   int n_ctas;
+  double* dfrag = nullptr;   // diffusion p = 24: DMMA operand fragments of D (smg_opd.cu)
 };
 
 struct smg_schwarz {
@@ -243,6 +244,13 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
   o->n_ctas = ctas;
   cudaError_t e = cudaMalloc(&o->partials, sizeof(double) * o->n_ctas);
   if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
+  if (kind == 1 && p == 24) {
+    std::vector<double> fr;
+    opd_fragments(p, mat, fr);
+    e = cudaMalloc(&o->dfrag, sizeof(double) * fr.size());
+    if (e == cudaSuccess) e = cudaMemcpy(o->dfrag, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(o->partials); delete o; return cuda_fail(e, "smg_op_create"); }
+  }
   *h = o;
   return SMG_OK;
 }
@@ -250,6 +258,7 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
 int smg_op_destroy(smg_op_t* h) {
   if (!h) return SMG_OK;
   cudaFree(h->partials);
+  if (h->dfrag) cudaFree(h->dfrag);
   delete h;
   return SMG_OK;
 }
@@ -262,7 +271,7 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
   if (!norm) {
-    const int rc = opw_launch(L, st);
+    const int rc = h->kind == 1 ? opd_launch(L, h->dfrag, st) : opw_launch(L, st);
     if (rc != 1) return rc;
   }
   return h->fn(L, st);

@@ -23,6 +23,7 @@
 // r = f - A u (f may be absent) and per-CTA partials of ||r||^2.
 #pragma once
 #include <cmath>
+#include <vector>
 #include "smg_common.cuh"
 #include "smg_tma.cuh"
 
@@ -469,6 +470,12 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   launch(op_kernel<P, TX, TY, DIFF>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(G::THREADS), G::SMEM, st, A);
   return check_launch("op_kernel");
 }
+
+// FP64 tensor-core diffusion residual for p = 24 (smg_opd.cu) without norm
+// partials; returns 1 when not applicable.  frag: device table built from D
+// by opd_fragments.
+int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st);
+void opd_fragments(int p, const double* D, std::vector<double>& out);
 
 using OpLaunchFn = int (*)(const OpLaunch&, cudaStream_t);
 // Warp-per-element Poisson residual (smg_opw.cu) for p = 8, 16 without norm

@@ -1,0 +1,232 @@
+// Diffusion residual r = f - B u on FP64 tensor cores (DMMA), one element
+// per CTA, for p = 24 (C5's top level).
+//
+// Reference: DiffusionOperator.apply (operators.py:86-92), residual (:101-103).
+// Same gather form as op_kernel (smg_op.cuh): every node row of the element
+// (and of its left neighbour, whose vertex value the element's b = 0 column
+// needs) is a line x -> v = D^T (nu w . (D x)) along x, every node column a
+// line along y, and the two parts meet in shared memory.  Here the lines are
+// batched 8 at a time into m8n8k4 DMMAs:
+//   G (8 x NP) = X (8 x NP) . D^T      (k padded to 4 KT, n to 8 NTL)
+//   G         *= nu(line, node) w(node)
+//   V (8 x NP) = G . D                 (G moved from accumulator to operand
+//                                        layout by quad shuffles)
+// The constant-coefficient-free line op stays FP64-exact per product; the
+// summation order differs from op_kernel's, so results agree to rounding
+// (the parity tests pin 1e-12 against the reference).  The row/column line
+// batches of a pass are split over three warps so that each warp holds one
+// batch of full lines and one batch of vertex-only lines.
+#include <vector>
+
+#include "smg_common.cuh"
+#include "smg_op.cuh"
+#include "smg_tma.cuh"
+
+namespace smg {
+
+template <int P>
+struct OpdGeom {
+  static constexpr int NP = P + 1;
+  static constexpr int KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
+  static constexpr int HX = 2 * P + 1, HY = 2 * P + 1, DP = (HX + 2) & ~1;
+  static constexpr int LINES = 2 * P;            // P full lines + P vertex-only lines per pass
+  static constexpr int BATCHES = LINES / 8;
+  static constexpr int WARPS = BATCHES / 2;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int FRAG = 2 * KT * NTL * 32;   // lane-ordered B fragments: D^T then D
+  static constexpr size_t SMEM =
+      sizeof(double) * ((size_t)2 * DP * HY + (size_t)P * P + 2 * (size_t)P + 2 * (size_t)P + P + NP) + 16;
+  static_assert(P % 4 == 0 && BATCHES % 2 == 0, "lines must fill whole batches");
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// One batch of 8 lines: line g (lane / 4) starts at x0 (stride ST); its nu at
+// n0.  Returns, per n-tile j, V[g][8j + 2t], V[g][8j + 2t + 1] (t = lane % 4).
+// ONLY_LAST: only the n-tile holding node P is formed in the second product.
+template <int P, bool ONLY_LAST>
+__device__ __forceinline__ void opd_batch(const double* x0, const double* n0, int st, const double* WT,
+                                          const double* __restrict__ frag, double (&V)[OpdGeom<P>::NTL][2]) {
+  using G = OpdGeom<P>;
+  constexpr int NP = G::NP, KT = G::KT, NTL = G::NTL;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double C[NTL][2];
+#pragma unroll
+  for (int j = 0; j < NTL; ++j) C[j][0] = C[j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KT; ++q) {
+    const int k = 4 * q + t;
+    const double a = k < NP ? x0[k * st] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) dmma(C[j][0], C[j][1], a, __ldg(frag + (q * NTL + j) * 32 + lane));
+  }
+  // G *= nu w (columns n = 8j + 2t + e of line g)
+#pragma unroll
+  for (int j = 0; j < NTL; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = 8 * j + 2 * t + e;
+      C[j][e] = n < NP ? C[j][e] * (n0[n * st] * WT[n]) : 0.0;
+    }
+  constexpr int J0 = ONLY_LAST ? P / 8 : 0;
+#pragma unroll
+  for (int j = J0; j < NTL; ++j) V[j][0] = V[j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KT; ++q) {
+    // operand A[g][t] = G[g][4q + t], held by lane (g, 2 (q & 1) + t / 2) at element t & 1
+    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+    const double v0 = __shfl_sync(0xffffffffu, C[q >> 1][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, C[q >> 1][1], src);
+    const double a = (t & 1) ? v1 : v0;
+#pragma unroll
+    for (int j = J0; j < NTL; ++j) dmma(V[j][0], V[j][1], a, __ldg(frag + ((KT + q) * NTL + j) * 32 + lane));
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
+                                                                  const double* __restrict__ frag) {
+  SMG_PDL_ENTRY();
+  using G = OpdGeom<P>;
+  constexpr int NP = G::NP, KT = G::KT, NTL = G::NTL, DP = G::DP, HX = G::HX, HY = G::HY;
+  constexpr int OX = P, OY = P, NT = G::THREADS;
+  extern __shared__ __align__(16) double smd[];
+  double* U = smd;                  // HY x DP window of u (column shift sh)
+  double* NU = U + DP * HY;         // same window of nu
+  double* AX = NU + DP * HY;        // OY x OX x-parts, then x+y parts
+  double* VX = AX + OX * OY;        // OY x 2: vertex value of the left element's row lines
+  double* VY = VX + 2 * OY;         // OX x 2
+  double* WS = VY + 2 * OX;         // P assembled weights
+  double* WT = WS + P;              // NP GLL weights
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WT + NP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
+  const int X0 = tx * OX, Y0 = ty * OY;
+  const int N_x = A.N_x, N_y = A.N_y;
+
+  const int sh = pwin_shift(X0 - P, N_x);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, 2u * pwin_bytes(HX, HY, sh));
+  }
+  __syncthreads();
+  if (tid < 32) {
+    pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
+    pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
+  }
+  // f while the window lands (the B fragments stream from the lane-ordered
+  // table through L1 inside the batches: 14 KB, shared by the SM's CTAs --
+  // held in registers they cost two resident CTAs per SM)
+  constexpr int KO = (OX * OY + NT - 1) / NT;
+  double fv[KO];
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int idx = tid + k * NT;
+    fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
+  }
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
+  mbar_wait(bar, 0);
+  __syncthreads();
+
+  // ---- row pass: warp w takes full-line batch w (rows 8w..8w+7 of the
+  //      element) and vertex batch w (the same rows of the left neighbour)
+  {
+    double V[NTL][2];
+    const int y = 8 * warp + g;
+    const double* ur = U + (y + P) * DP + sh;
+    const double* nr = NU + (y + P) * DP + sh;
+    opd_batch<P, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
+    if (t == 0) VX[y * 2] = V[P / 8][0];
+    opd_batch<P, false>(ur + P, nr + P, 1, WT, frag, V);
+#pragma unroll
+    for (int j = 0; j < NTL; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = 8 * j + 2 * t + e;
+        if (b < P) AX[y * OX + b] = V[j][e];
+        else if (b == P) VX[y * 2 + 1] = V[j][e];
+      }
+  }
+  __syncthreads();
+  // ---- column pass (x-part of the left element added at b == 0) -----------
+  {
+    double V[NTL][2];
+    const int x = 8 * warp + g;
+    const double* uc = U + sh + (x + P);
+    const double* nc = NU + sh + (x + P);
+    opd_batch<P, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
+    if (t == 0) VY[x * 2] = V[P / 8][0];
+    opd_batch<P, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
+    const double wyb = A.cy * WS[x];
+#pragma unroll
+    for (int j = 0; j < NTL; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int a = 8 * j + 2 * t + e;
+        if (a < P) {
+          double ax = AX[a * OX + x];
+          if (x == 0) ax += VX[a * 2];
+          AX[a * OX + x] = fma(A.cx * WS[a], ax, wyb * V[j][e]);
+        } else if (a == P) {
+          VY[x * 2 + 1] = V[j][e];
+        }
+      }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int idx = tid + k * NT;
+    if (idx < OX * OY) {
+      const int y = idx / OX, x = idx - y * OX;
+      double val = AX[idx];
+      if (y == 0) val = fma(A.cy * WS[x], VY[x * 2], val);
+      A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = A.f != nullptr ? fv[k] - val : val;
+    }
+  }
+}
+
+// Lane-ordered B fragments of D^T and D for opd_kernel (host): value for
+// (k-tile q, n-tile j, lane (g, t)) = B[4q + t][8j + g].
+void opd_fragments(int p, const double* D, std::vector<double>& out) {
+  const int NP = p + 1, KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
+  out.assign((size_t)2 * KT * NTL * 32, 0.0);
+  for (int m = 0; m < 2; ++m)
+    for (int q = 0; q < KT; ++q)
+      for (int j = 0; j < NTL; ++j)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int k = 4 * q + (lane & 3), n = 8 * j + (lane >> 2);
+          double v = 0.0;
+          if (k < NP && n < NP) v = m == 0 ? D[n * NP + k] : D[k * NP + n];   // D^T[k][n], D[k][n]
+          out[((size_t)(m * KT + q) * NTL + j) * 32 + lane] = v;
+        }
+}
+
+// 1 = not applicable (caller uses op_kernel)
+int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
+  constexpr int P = 24;
+  using G = OpdGeom<P>;
+  if (!L.diffusion || L.p != P || L.partials != nullptr || frag == nullptr || env_int("SMG_OPD", 1) == 0) return 1;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((L.n_x * P) % 2 != 0 || !al16(L.u) || !al16(L.nu)) return 1;
+  OpArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
+  op_fill_consts<P>(A, L, true);
+  A.tiles_x = L.n_x;
+  A.bulk = 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(opd_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "opd_kernel smem attribute");
+    attr = true;
+  }
+  launch(opd_kernel<P>, dim3(L.n_x * L.n_y), dim3(G::THREADS), G::SMEM, st, A, frag);
+  return check_launch("opd_kernel");
+}
+
+}  // namespace smg
