@@ -65,7 +65,9 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st);
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
-int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, cudaStream_t st);
+int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, const double* tab,
+             cudaStream_t st);
+std::vector<double> fft_table(int nx, int ny);
 int pinv_cluster(int nx, int ny, const double* Qx, const double* QxT, const double* Qy, const double* Lp,
                  const double* f, double* u, cudaStream_t st);
 int pinv_small(int nx, int ny, const double* Qx, const double* Qy, const double* Lp, const double* f,
@@ -125,6 +127,7 @@ struct smg_coarse {
   double* QxT;  // its transpose
   double* Qy;   // n_y x n_y
   double* Lp;   // n_y x n_x pseudo-inverse eigenvalues
+  double* fft = nullptr;   // FFT path table (smg_fft.cu fft_table), power-of-two meshes
 };
 
 namespace {
@@ -603,6 +606,11 @@ int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy) 
   if (e == cudaSuccess) e = cudaMemcpy(c->Qx, Qx.data(), sizeof(double) * Qx.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->Qy, Qy.data(), sizeof(double) * Qy.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->Lp, Lp.data(), sizeof(double) * Lp.size(), cudaMemcpyHostToDevice);
+  const std::vector<double> ft = fft_table(n_x, n_y);
+  if (e == cudaSuccess && !ft.empty()) {
+    e = cudaMalloc(&c->fft, sizeof(double) * ft.size());
+    if (e == cudaSuccess) e = cudaMemcpy(c->fft, ft.data(), sizeof(double) * ft.size(), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) { delete c; return cuda_fail(e, "smg_coarse_create"); }
   *h = c;
   return SMG_OK;
@@ -611,6 +619,7 @@ int smg_coarse_create(smg_coarse_t** h, int n_x, int n_y, double dx, double dy) 
 int smg_coarse_destroy(smg_coarse_t* h) {
   if (!h) return SMG_OK;
   cudaFree(h->Qx); cudaFree(h->QxT); cudaFree(h->Qy); cudaFree(h->Lp);
+  if (h->fft) cudaFree(h->fft);
   delete h;
   return SMG_OK;
 }
@@ -624,7 +633,7 @@ int smg_coarse_pinv(const smg_coarse_t* h, const double* f0, double* u0, double*
   double* T1 = ws;
   double* T2 = ws + (size_t)nx * ny;
   // power-of-two meshes: 2D FFT (one launch up to 64 x 64, three beyond)
-  int rf = pinv_fft(nx, ny, h->dx, h->dy, f0, u0, ws, st);
+  int rf = pinv_fft(nx, ny, h->dx, h->dy, f0, u0, ws, h->fft, st);
   if (rf != 1) return rf;
   // single-launch cluster variant (SMG_PINV_CLUSTER=0 selects the two-launch
   // row-block path)

@@ -16,6 +16,7 @@
 //   up to 64 x 64       : the dense two-launch path is faster; a one-CTA FFT
 //                         kernel is kept behind SMG_PINV_FFT=2.
 #include <cmath>
+#include <vector>
 
 #include "smg_common.cuh"
 
@@ -82,14 +83,13 @@ __device__ __forceinline__ void fft_lines_p(double2* buf, int n, int logn, int l
   }
 }
 
-// SW (n - 1 entries) from the natural table tw (cos, sin of 2 pi k / n, k < n/2)
-__device__ __forceinline__ void fft_stage_twiddles(const double* tw, int n, double2* SW) {
-  const int nh = n >> 1;
-  for (int e = threadIdx.x; e < n - 1; e += blockDim.x) {
-    const int half = 1 << (31 - __clz(e + 1));   // largest power of two <= e + 1
-    const int pos = e + 1 - half, k = pos * (nh / half);
-    SW[e] = make_double2(tw[2 * k], tw[2 * k + 1]);
-  }
+// Device table of the multi-CTA path (built once per coarse handle,
+// fft_table): stage-major twiddles SWx (n_x - 1 complex), SWy (n_y - 1), then
+// mu_x (n_x), mu_y (n_y) -- read coalesced instead of as divergent
+// parameter-bank loads.
+__device__ __forceinline__ void fft_load_sw(const double* __restrict__ tab, int n, double2* SW) {
+  const double2* src = reinterpret_cast<const double2*>(tab);
+  for (int e = threadIdx.x; e < n - 1; e += blockDim.x) SW[e] = __ldg(src + e);
 }
 
 // mu(k) = 2 - 2 cos(2 pi k / n) from the twiddle table (cos is even in k)
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(1024) fft_pinv_small_kernel(int nx, int ny, in
 
 // rows [r0, r0+lines): forward (inv = false, real input f) or inverse (inv = true,
 // complex input W, real output u) FFT along x
-__global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, const __grid_constant__ FftConsts C,
+__global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, const double* __restrict__ tab,
                                                        const double* __restrict__ f, double2* __restrict__ W,
                                                        double* __restrict__ u, int inv, int lines) {
   SMG_PDL_ENTRY();
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, c
   const int ls = fpad(nx);
   double2* SX = zs + lines * ls;
   const int r0 = blockIdx.x * lines, nr = min(lines, ny - r0);
-  fft_stage_twiddles(C.twx, nx, SX);
+  fft_load_sw(tab, nx, SX);
   for (int i = threadIdx.x; i < nr * nx; i += blockDim.x) {
     const int l = i / nx, x = i - l * nx;
     const size_t g = (size_t)(r0 + l) * nx + x;
@@ -182,18 +182,17 @@ __global__ void __launch_bounds__(512) fft_rows_kernel(int nx, int ny, int lx, c
 
 // columns [c0, c0+8): forward FFT along y, divide by lambda, inverse FFT along y
 __global__ void __launch_bounds__(512) fft_cols_kernel(int nx, int ny, int ly, double cx, double cy,
-                                                       const __grid_constant__ FftConsts C, double2* __restrict__ W,
+                                                       const double* __restrict__ tab, double2* __restrict__ W,
                                                        int lines) {
   SMG_PDL_ENTRY();
   extern __shared__ __align__(16) double2 zs[];   // lines x fpad(ny) (line = column)
   const int ls = fpad(ny);
   double2* Z2 = zs + lines * ls;
   double2* SY = Z2 + lines * ls;
-  double* TY = reinterpret_cast<double*>(SY + ny);
-  double* TX = TY + ny;
-  for (int i = threadIdx.x; i < ny; i += blockDim.x) TY[i] = C.twy[i];
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
-  fft_stage_twiddles(C.twy, ny, SY);
+  double* MY = reinterpret_cast<double*>(SY + ny);
+  const double* mux = tab + 2 * (nx - 1) + 2 * (ny - 1);
+  for (int i = threadIdx.x; i < ny; i += blockDim.x) MY[i] = __ldg(mux + nx + i);
+  fft_load_sw(tab + 2 * (nx - 1), ny, SY);
   const int c0 = blockIdx.x * lines, nc = min(lines, nx - c0);
   for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
     const int y = i / nc, l = i - y * nc;
@@ -203,7 +202,7 @@ __global__ void __launch_bounds__(512) fft_cols_kernel(int nx, int ny, int ly, d
   fft_lines_p(zs, ny, ly, nc, ls, SY, false);
   for (int i = threadIdx.x; i < nc * ny; i += blockDim.x) {
     const int l = i / ny, ky = i - l * ny, kx = c0 + l;
-    const double lam = cx * mu_of(kx, nx, TX) + cy * mu_of(ky, ny, TY);
+    const double lam = cx * __ldg(mux + kx) + cy * MY[ky];
     const double s = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
     const double2 z = zs[l * ls + fpad(ky)];
     Z2[l * ls + fpad(brev(ky, ly))] = make_double2(z.x * s, z.y * s);
@@ -225,7 +224,39 @@ static bool pow2(int n, int* lg) {
 }
 
 // 1 = not applicable (caller falls back to the GEMM path)
-int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, cudaStream_t st) {
+// The multi-CTA path's device table (see fft_load_sw), or an empty vector
+// when the FFT path does not apply to n_x x n_y.
+std::vector<double> fft_table(int nx, int ny) {
+  int lx = 0, ly = 0;
+  std::vector<double> t;
+  if (!pow2(nx, &lx) || !pow2(ny, &ly) || nx > kFftMax || ny > 512) return t;
+  const double pi = 3.14159265358979323846;
+  auto stage = [&](int n) {
+    const int nh = n / 2;
+    for (int e = 0; e < n - 1; ++e) {
+      int half = 1;
+      while (2 * half <= e + 1) half *= 2;
+      const int k = (e + 1 - half) * (nh / half);
+      t.push_back(std::cos(2.0 * pi * k / n));
+      t.push_back(std::sin(2.0 * pi * k / n));
+    }
+  };
+  auto mu = [&](int n) {
+    for (int k = 0; k < n; ++k) {
+      const int kk = k <= n / 2 ? k : n - k;
+      const double c = kk < n / 2 ? std::cos(2.0 * pi * kk / n) : -1.0;
+      t.push_back(2.0 - 2.0 * c);
+    }
+  };
+  stage(nx);
+  stage(ny);
+  mu(nx);
+  mu(ny);
+  return t;
+}
+
+int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, const double* tab,
+             cudaStream_t st) {
   int lx = 0, ly = 0;
   if (!pow2(nx, &lx) || !pow2(ny, &ly) || nx > kFftMax || ny > 512) return 1;
   // SMG_PINV_FFT: 0 never, 1 (default) beyond 64 x 64, 2 always.  Measured
@@ -234,16 +265,16 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
   // 0.40 -> 0.10 s, at C5 (512^2, coarse PCG) 1.61 -> 0.98 s.
   static const int mode = env_int("SMG_PINV_FFT", 1);
   if (mode == 0 || (mode == 1 && (long)nx * ny <= 64 * 64)) return 1;
-  FftConsts C;
-  const double pi = 3.14159265358979323846;
-  for (int k = 0; k < kFftMax / 2; ++k) {
-    C.twx[2 * k] = k < nx / 2 ? std::cos(2.0 * pi * k / nx) : 0.0;
-    C.twx[2 * k + 1] = k < nx / 2 ? std::sin(2.0 * pi * k / nx) : 0.0;
-    C.twy[2 * k] = k < ny / 2 ? std::cos(2.0 * pi * k / ny) : 0.0;
-    C.twy[2 * k + 1] = k < ny / 2 ? std::sin(2.0 * pi * k / ny) : 0.0;
-  }
   const double cx = dy / dx, cy = dx / dy;
   if (nx <= 64 && ny <= 64) {
+    FftConsts C;
+    const double pi = 3.14159265358979323846;
+    for (int k = 0; k < kFftMax / 2; ++k) {
+      C.twx[2 * k] = k < nx / 2 ? std::cos(2.0 * pi * k / nx) : 0.0;
+      C.twx[2 * k + 1] = k < nx / 2 ? std::sin(2.0 * pi * k / nx) : 0.0;
+      C.twy[2 * k] = k < ny / 2 ? std::cos(2.0 * pi * k / ny) : 0.0;
+      C.twy[2 * k + 1] = k < ny / 2 ? std::sin(2.0 * pi * k / ny) : 0.0;
+    }
     const size_t smem = sizeof(double2) * 2 * (size_t)(nx + 1) * ny + sizeof(double) * (nx + ny);
     static bool attr = false;
     if (!attr) {
@@ -255,6 +286,7 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
     launch(fft_pinv_small_kernel, dim3(1), dim3(1024), smem, st, nx, ny, lx, ly, cx, cy, C, f, u);
     return check_launch("fft_pinv_small_kernel");
   }
+  if (tab == nullptr) return 1;
   double2* W = reinterpret_cast<double2*>(ws);   // the coarse ws holds 2 nx ny doubles
   auto pick = [](int nlines, int n, int* threads) {
     int lines = 8;
@@ -266,7 +298,7 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
   int tr = 0, tc = 0;
   const int lr = pick(ny, nx, &tr), lc = pick(nx, ny, &tc);
   const size_t smr = sizeof(double2) * ((size_t)lr * (nx + nx / 16) + nx);
-  const size_t smc = sizeof(double2) * (2 * (size_t)lc * (ny + ny / 16) + ny) + sizeof(double) * (nx + ny);
+  const size_t smc = sizeof(double2) * (2 * (size_t)lc * (ny + ny / 16) + ny) + sizeof(double) * ny;
   static size_t attr_r = 0, attr_c = 0;
   if (smr > attr_r) {
     cudaError_t e = cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
@@ -279,13 +311,13 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
     attr_c = smc;
   }
   const int gr = (ny + lr - 1) / lr, gc = (nx + lc - 1) / lc;
-  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, C, f, W, static_cast<double*>(nullptr), 0, lr);
+  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, tab, f, W, static_cast<double*>(nullptr), 0, lr);
   int rc = check_launch("fft_rows_kernel");
   if (rc) return rc;
-  launch(fft_cols_kernel, dim3(gc), dim3(tc), smc, st, nx, ny, ly, cx, cy, C, W, lc);
+  launch(fft_cols_kernel, dim3(gc), dim3(tc), smc, st, nx, ny, ly, cx, cy, tab, W, lc);
   rc = check_launch("fft_cols_kernel");
   if (rc) return rc;
-  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, C, static_cast<const double*>(nullptr), W, u, 1, lr);
+  launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, tab, static_cast<const double*>(nullptr), W, u, 1, lr);
   return check_launch("fft_rows_kernel");
 }
 
