@@ -290,7 +290,7 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
   double2* W = reinterpret_cast<double2*>(ws);   // the coarse ws holds 2 nx ny doubles
   auto pick = [](int nlines, int n, int* threads) {
     int lines = 8;
-    while (lines > 1 && nlines / lines < 256) lines >>= 1;
+    while (lines > 1 && nlines / lines < env_int("SMG_FFT_MINCTAS", 512)) lines >>= 1;
     const int t = lines * (n / 2);
     *threads = t >= 512 ? 512 : (t < 64 ? 64 : ((t + 31) / 32) * 32);
     return lines;
