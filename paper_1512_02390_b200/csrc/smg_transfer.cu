@@ -318,6 +318,61 @@ __global__ void __launch_bounds__(32 * kTrWarps) prolong_warp_kernel(const __gri
   }
 }
 
+// prolongation for p_f that does not divide the warp (p_f = 3, 6, 12, 24):
+// lane b < p_f owns fine column b of the element (x pass over the coarse
+// rows with its J row in registers, then all p_f rows of its column; the
+// rows are written coalesced across the lanes).  Same sums as the tiled
+// kernel's gather form.
+template <int PC, int PF>
+__global__ void __launch_bounds__(32 * kTrWarps, 2) prolong_warp_g_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
+  constexpr int NC = PC + 1;
+  static_assert(PF <= 32, "one lane per fine column");
+  __shared__ double Js[(PF + 1) * NC];
+  __shared__ double Cw[kTrWarps][NC * NC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (PF + 1) * NC; i += 32 * kTrWarps) Js[i] = A.J[i];
+  const int e = blockIdx.x * kTrWarps + warp;
+  const int n_el = A.n_x * A.n_y;
+  const int ey = e / A.n_x, ex = e - ey * A.n_x;
+  const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
+  const bool act = e < n_el;
+  if (act) {
+    for (int i = lane; i < NC * NC; i += 32) {
+      const int ay = i / NC, ax = i - ay * NC;
+      Cw[warp][i] = A.src[(size_t)wrapi(ey * PC + ay, Nyc) * Nxc + wrapi(ex * PC + ax, Nxc)];
+    }
+  }
+  const int b = lane;
+  const bool lb = act && b < PF;
+  double old[PF];
+  double* out = A.dst + (size_t)(ey * PF) * Nxf + ex * PF + b;
+#pragma unroll
+  for (int a = 0; a < PF; ++a) old[a] = (lb && A.accumulate) ? out[(size_t)a * Nxf] : 0.0;
+  __syncthreads();   // Js (once per block), Cw of this warp
+  if (!lb) return;
+  // x pass: t[ay] = sum_ax J[b][ax] C[ay][ax]
+  double jb[NC], tb[NC];
+#pragma unroll
+  for (int ax = 0; ax < NC; ++ax) jb[ax] = Js[b * NC + ax];
+#pragma unroll
+  for (int ay = 0; ay < NC; ++ay) {
+    const double* c = &Cw[warp][ay * NC];
+    double s = 0.0;
+#pragma unroll
+    for (int ax = 0; ax < NC; ++ax) s = fma(jb[ax], c[ax], s);
+    tb[ay] = s;
+  }
+  // y pass: out[a][b] = sum_ay J[a][ay] t[ay]
+#pragma unroll
+  for (int a = 0; a < PF; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int ay = 0; ay < NC; ++ay) s = fma(Js[a * NC + ay], tb[ay], s);
+    out[(size_t)a * Nxf] = A.accumulate ? old[a] + s : s;
+  }
+}
+
 // restriction, coarse element e: owned coarse nodes (ay, ax < p_c) from the
 // fine blocks of elements e, e-x, e-y, e-xy (row-assigned P^T, as the tiled
 // kernel): x pass over the 2p_f fine rows, then y pass.
@@ -478,6 +533,19 @@ int tr_launch_warp(const TrArgs& A, bool prolong, cudaStream_t st) {
 // tile T (elements per side) chosen at run time from the compiled set
 template <int PC, int PF>
 int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
+  if constexpr (PF == 3 || PF == 24) {
+    // warp-per-element prolongation where it measured faster than the tiled
+    // kernel on B200 (C5 levels: p_f = 24 1272 -> 1118 us, 3: 79 -> 40 us;
+    // slower at p_f = 12: 195 -> 326, 6: 111 -> 157); restriction stays tiled
+    static const int warp = env_int("SMG_TR_WARP", 1);
+    if (prolong && warp) {
+      TrArgs B = A;
+      B.n_x = n_x;
+      B.n_y = n_y;
+      launch(prolong_warp_g_kernel<PC, PF>, dim3((n_x * n_y + kTrWarps - 1) / kTrWarps), dim3(32 * kTrWarps), 0, st, B);
+      return check_launch("prolong_warp_g_kernel");
+    }
+  }
   if constexpr (PF <= 16 && (PF & (PF - 1)) == 0) {
     static const int warp = env_int("SMG_TR_WARP", 1);
     if (warp) {
