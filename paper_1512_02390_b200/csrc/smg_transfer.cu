@@ -533,7 +533,7 @@ int tr_launch_warp(const TrArgs& A, bool prolong, cudaStream_t st) {
 // tile T (elements per side) chosen at run time from the compiled set
 template <int PC, int PF>
 int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
-  if constexpr (PF == 3 || PF == 24) {
+  if constexpr (PF == 3 || PF == 24 || PF == 32) {
     // warp-per-element prolongation where it measured faster than the tiled
     // kernel on B200 (C5 levels: p_f = 24 1272 -> 1118 us, 3: 79 -> 40 us;
     // slower at p_f = 12: 195 -> 326, 6: 111 -> 157); restriction stays tiled
