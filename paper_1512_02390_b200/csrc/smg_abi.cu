@@ -89,7 +89,7 @@ struct smg_op {
   const double* nu;
   double* partials;  // device, one per CTA
   int n_ctas;
-  double* dfrag = nullptr;   // diffusion p = 24: DMMA operand fragments of D (smg_opd.cu)
+  double* dfrag = nullptr;   // DMMA operand fragments (smg_opd.cu): diffusion p = 24, Poisson p = 32
 };
 
 struct smg_schwarz {
@@ -247,9 +247,9 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
   o->n_ctas = ctas;
   cudaError_t e = cudaMalloc(&o->partials, sizeof(double) * o->n_ctas);
   if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
-  if (kind == 1 && p == 24) {
+  if (opd_applies(p, kind == 1)) {
     std::vector<double> fr;
-    opd_fragments(p, mat, fr);
+    opd_fragments(p, kind == 1, mat, fr);
     e = cudaMalloc(&o->dfrag, sizeof(double) * fr.size());
     if (e == cudaSuccess) e = cudaMemcpy(o->dfrag, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(o->partials); delete o; return cuda_fail(e, "smg_op_create"); }
@@ -274,7 +274,8 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
   if (!norm) {
-    const int rc = h->kind == 1 ? opd_launch(L, h->dfrag, st) : opw_launch(L, st);
+    int rc = opd_launch(L, h->dfrag, st);
+    if (rc == 1 && h->kind == 0) rc = opw_launch(L, st);
     if (rc != 1) return rc;
   }
   return h->fn(L, st);

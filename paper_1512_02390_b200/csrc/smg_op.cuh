@@ -475,7 +475,8 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
 // partials; returns 1 when not applicable.  frag: device table built from D
 // by opd_fragments.
 int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st);
-void opd_fragments(int p, const double* D, std::vector<double>& out);
+bool opd_applies(int p, bool diffusion);
+void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out);
 
 using OpLaunchFn = int (*)(const OpLaunch&, cudaStream_t);
 // Warp-per-element Poisson residual (smg_opw.cu) for p = 8, 16 without norm

@@ -1,5 +1,8 @@
-// Diffusion residual r = f - B u on FP64 tensor cores (DMMA), one element
-// per CTA, for p = 24 (C5's top level).
+// Operator residuals on FP64 tensor cores (DMMA), one element per CTA:
+// diffusion at p = 24 (C5's top level) and Poisson at p = 32 (C3's).
+//
+// Poisson lines are the single product V = X . L-hat (no nu, one DMMA
+// chain); the rest of this description is the diffusion case.
 //
 // Reference: DiffusionOperator.apply (operators.py:86-92), residual (:101-103).
 // Same gather form as op_kernel (smg_op.cuh): every node row of the element
@@ -24,7 +27,7 @@
 
 namespace smg {
 
-template <int P>
+template <int P, bool DIFF>
 struct OpdGeom {
   static constexpr int NP = P + 1;
   static constexpr int KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
@@ -33,9 +36,9 @@ struct OpdGeom {
   static constexpr int BATCHES = LINES / 8;
   static constexpr int WARPS = BATCHES / 2;
   static constexpr int THREADS = 32 * WARPS;
-  static constexpr int FRAG = 2 * KT * NTL * 32;   // lane-ordered B fragments: D^T then D
+  static constexpr int FRAG = (DIFF ? 2 : 1) * KT * NTL * 32;   // lane-ordered B fragments: D^T then D (or L)
   static constexpr size_t SMEM =
-      sizeof(double) * ((size_t)2 * DP * HY + (size_t)P * P + 2 * (size_t)P + 2 * (size_t)P + P + NP) + 16;
+      sizeof(double) * ((size_t)(DIFF ? 2 : 1) * DP * HY + (size_t)P * P + 2 * (size_t)P + 2 * (size_t)P + P + NP) + 16;
   static_assert(P % 4 == 0 && BATCHES % 2 == 0, "lines must fill whole batches");
 };
 
@@ -48,12 +51,26 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // One batch of 8 lines: line g (lane / 4) starts at x0 (stride ST); its nu at
 // n0.  Returns, per n-tile j, V[g][8j + 2t], V[g][8j + 2t + 1] (t = lane % 4).
 // ONLY_LAST: only the n-tile holding node P is formed in the second product.
-template <int P, bool ONLY_LAST>
+template <int P, bool DIFF, bool ONLY_LAST>
 __device__ __forceinline__ void opd_batch(const double* x0, const double* n0, int st, const double* WT,
-                                          const double* __restrict__ frag, double (&V)[OpdGeom<P>::NTL][2]) {
-  using G = OpdGeom<P>;
+                                          const double* __restrict__ frag, double (&V)[OpdGeom<P, DIFF>::NTL][2]) {
+  using G = OpdGeom<P, DIFF>;
   constexpr int NP = G::NP, KT = G::KT, NTL = G::NTL;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int lane = threadIdx.x & 31, t = lane & 3;
+  if constexpr (!DIFF) {
+    // Poisson: V = X . L (B[k][n] = L[k][n]); vertex lines only the n-tile of node P
+    constexpr int J0 = ONLY_LAST ? P / 8 : 0;
+#pragma unroll
+    for (int j = J0; j < NTL; ++j) V[j][0] = V[j][1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      const int k = 4 * q + t;
+      const double a = k < NP ? x0[k * st] : 0.0;
+#pragma unroll
+      for (int j = J0; j < NTL; ++j) dmma(V[j][0], V[j][1], a, __ldg(frag + (q * NTL + j) * 32 + lane));
+    }
+    return;
+  }
   double C[NTL][2];
 #pragma unroll
   for (int j = 0; j < NTL; ++j) C[j][0] = C[j][1] = 0.0;
@@ -87,17 +104,17 @@ __device__ __forceinline__ void opd_batch(const double* x0, const double* n0, in
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
-                                                                  const double* __restrict__ frag) {
+template <int P, bool DIFF>
+__global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
+                                                                        const double* __restrict__ frag) {
   SMG_PDL_ENTRY();
-  using G = OpdGeom<P>;
+  using G = OpdGeom<P, DIFF>;
   constexpr int NP = G::NP, KT = G::KT, NTL = G::NTL, DP = G::DP, HX = G::HX, HY = G::HY;
   constexpr int OX = P, OY = P, NT = G::THREADS;
   extern __shared__ __align__(16) double smd[];
   double* U = smd;                  // HY x DP window of u (column shift sh)
-  double* NU = U + DP * HY;         // same window of nu
-  double* AX = NU + DP * HY;        // OY x OX x-parts, then x+y parts
+  double* NU = U + DP * HY;         // same window of nu (diffusion)
+  double* AX = NU + (DIFF ? DP * HY : 0);   // OY x OX x-parts, then x+y parts
   double* VX = AX + OX * OY;        // OY x 2: vertex value of the left element's row lines
   double* VY = VX + 2 * OY;         // OX x 2
   double* WS = VY + 2 * OX;         // P assembled weights
@@ -112,12 +129,12 @@ __global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __gri
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(bar, 2u * pwin_bytes(HX, HY, sh));
+    mbar_arrive_expect_tx(bar, (DIFF ? 2u : 1u) * pwin_bytes(HX, HY, sh));
   }
   __syncthreads();
   if (tid < 32) {
     pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
-    pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
+    if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
   }
   // f while the window lands (the B fragments stream from the lane-ordered
   // table through L1 inside the batches: 14 KB, shared by the SM's CTAs --
@@ -141,9 +158,9 @@ __global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __gri
     const int y = 8 * warp + g;
     const double* ur = U + (y + P) * DP + sh;
     const double* nr = NU + (y + P) * DP + sh;
-    opd_batch<P, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
+    opd_batch<P, DIFF, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
     if (t == 0) VX[y * 2] = V[P / 8][0];
-    opd_batch<P, false>(ur + P, nr + P, 1, WT, frag, V);
+    opd_batch<P, DIFF, false>(ur + P, nr + P, 1, WT, frag, V);
 #pragma unroll
     for (int j = 0; j < NTL; ++j)
 #pragma unroll
@@ -160,9 +177,9 @@ __global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __gri
     const int x = 8 * warp + g;
     const double* uc = U + sh + (x + P);
     const double* nc = NU + sh + (x + P);
-    opd_batch<P, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
+    opd_batch<P, DIFF, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
     if (t == 0) VY[x * 2] = V[P / 8][0];
-    opd_batch<P, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
+    opd_batch<P, DIFF, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
     const double wyb = A.cy * WS[x];
 #pragma unroll
     for (int j = 0; j < NTL; ++j)
@@ -193,40 +210,48 @@ __global__ void __launch_bounds__(OpdGeom<P>::THREADS, 5) opd_kernel(const __gri
 
 // Lane-ordered B fragments of D^T and D for opd_kernel (host): value for
 // (k-tile q, n-tile j, lane (g, t)) = B[4q + t][8j + g].
-void opd_fragments(int p, const double* D, std::vector<double>& out) {
+void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out) {
   const int NP = p + 1, KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
-  out.assign((size_t)2 * KT * NTL * 32, 0.0);
-  for (int m = 0; m < 2; ++m)
+  out.assign((size_t)(diffusion ? 2 : 1) * KT * NTL * 32, 0.0);
+  // diffusion: D^T then D; Poisson: L-hat (B[k][n] = L[k][n], the m = 1 form)
+  for (int m = diffusion ? 0 : 1; m < 2; ++m)
     for (int q = 0; q < KT; ++q)
       for (int j = 0; j < NTL; ++j)
         for (int lane = 0; lane < 32; ++lane) {
           const int k = 4 * q + (lane & 3), n = 8 * j + (lane >> 2);
           double v = 0.0;
           if (k < NP && n < NP) v = m == 0 ? D[n * NP + k] : D[k * NP + n];   // D^T[k][n], D[k][n]
-          out[((size_t)(m * KT + q) * NTL + j) * 32 + lane] = v;
+          out[((size_t)((diffusion ? m : 0) * KT + q) * NTL + j) * 32 + lane] = v;
         }
 }
 
-// 1 = not applicable (caller uses op_kernel)
-int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
-  constexpr int P = 24;
-  using G = OpdGeom<P>;
-  if (!L.diffusion || L.p != P || L.partials != nullptr || frag == nullptr || env_int("SMG_OPD", 1) == 0) return 1;
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if ((L.n_x * P) % 2 != 0 || !al16(L.u) || !al16(L.nu)) return 1;
+template <int P, bool DIFF>
+static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) {
+  using G = OpdGeom<P, DIFF>;
   OpArgs<P> A;
   A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
-  op_fill_consts<P>(A, L, true);
+  op_fill_consts<P>(A, L, DIFF);
   A.tiles_x = L.n_x;
   A.bulk = 1;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(opd_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(opd_kernel<P, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "opd_kernel smem attribute");
     attr = true;
   }
-  launch(opd_kernel<P>, dim3(L.n_x * L.n_y), dim3(G::THREADS), G::SMEM, st, A, frag);
+  launch(opd_kernel<P, DIFF>, dim3(L.n_x * L.n_y), dim3(G::THREADS), G::SMEM, st, A, frag);
   return check_launch("opd_kernel");
+}
+
+bool opd_applies(int p, bool diffusion) { return diffusion ? p == 24 : p == 32; }
+
+// 1 = not applicable (caller uses op_kernel / opw_kernel)
+int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
+  if (!opd_applies(L.p, L.diffusion != 0) || L.partials != nullptr || frag == nullptr || env_int("SMG_OPD", 1) == 0)
+    return 1;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((L.n_x * L.p) % 2 != 0 || !al16(L.u) || (L.diffusion && !al16(L.nu))) return 1;
+  return L.diffusion ? opd_launch_t<24, true>(L, frag, st) : opd_launch_t<32, false>(L, frag, st);
 }
 
 }  // namespace smg

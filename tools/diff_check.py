@@ -21,6 +21,16 @@ for n, p in [(4, 8), (8, 4), (4, 3), (8, 8), (2, 24), (4, 12), (4, 6), (16, 2)]:
     want = O.Diffusion(O.gll(p), n, n, 1.0 / n, 1.0 / n, nu).apply(u)
     print(f"n={n} p={p}: maxrel {np.abs(got - want).max() / np.abs(want).max():.2e}", flush=True)
 
+# Poisson (opd_kernel at p = 32, op/opw kernels elsewhere) vs the oracle
+for n, p in [(2, 32), (4, 32), (3, 32), (4, 16), (4, 8)]:
+    mesh = P.MeshConfig(n, n + 1, 1.0, 1.3)
+    lay = P.layout_for(mesh, p)
+    u = np.random.default_rng(1).standard_normal(lay.shape)
+    A = P.PoissonOperator(P.gll_basis(p), mesh)
+    got = A.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    want = O.Poisson(O.gll(p), n, n + 1, 1.0 / n, 1.3 / (n + 1)).apply(u)
+    print(f"poisson {n}x{n + 1} p={p}: maxrel {np.abs(got - want).max() / np.abs(want).max():.2e}", flush=True)
+
 # fused residual + restriction (rr_kernel) vs residual + restriction launches
 from paper_1512_02390_b200 import _native as NV  # noqa: E402
 lib = NV.lib()
