@@ -243,6 +243,8 @@ static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) 
   return check_launch("opd_kernel");
 }
 
+// (a p = 12 diffusion variant -- 3 warps, full and vertex lines mixed per
+// batch -- measured 1016 us vs 839 us for op_kernel<12,2,2> at C5's level 3)
 bool opd_applies(int p, bool diffusion) { return diffusion ? p == 24 : p == 32; }
 
 // 1 = not applicable (caller uses op_kernel / opw_kernel)
