@@ -65,6 +65,7 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st);
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
+int pcg_dscale(const double* in, double* out, const double* nu, int64_t n, const double* S, cudaStream_t st);
 int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, const double* tab,
              cudaStream_t st);
 std::vector<double> fft_table(int nx, int ny);
@@ -729,7 +730,20 @@ int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0,
   double* S = red + smg_reduce_ws_doubles();
   int rc;
   cudaError_t e;
+  // preconditioner: the diagonally scaled pseudo-inverse D^-1/2 A_P^+ D^-1/2
+  // (D = nodal nu; SPD on the range of A_0 -- its null space sqrt(nu) is not
+  // in it): at C5 11 iterations instead of 59 for the 1/mean(nu)-scaled A_P^+
+  // (SMG_PCG_DIAG=0), coarse solve 4.95 -> 1.32 ms on B200; q is free while
+  // the preconditioner runs
+  static const int diag = env_int("SMG_PCG_DIAG", 1);
+  const bool dsc = diag && op->kind == 1 && op->nu != nullptr;
   auto precond = [&](const double* in, double* out) -> int {
+    if (dsc) {
+      int rr = pcg_dscale(in, q, op->nu, n, S, st);
+      if (!rr) rr = smg_coarse_pinv(pc, q, out, pws, stream);
+      if (!rr) rr = pcg_dscale(out, out, op->nu, n, S, st);
+      return rr;
+    }
     int rr = smg_coarse_pinv(pc, in, out, pws, stream);
     if (rr) return rr;
     return pcg_scale(out, n, scale, S, st);

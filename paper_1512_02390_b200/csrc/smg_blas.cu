@@ -656,6 +656,16 @@ __global__ void pcg_scale_kernel(double* __restrict__ z, int64_t n, double scale
     z[i] *= scale;
 }
 
+// out = in / sqrt(nu) (the diagonal scaling of the coarse PCG preconditioner
+// D^-1/2 A_P^+ D^-1/2), skipped once converged
+__global__ void pcg_dscale_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ nu,
+                                  int64_t n, const double* S) {
+  SMG_PDL_ENTRY();
+  if (S[4] != 0.0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] / sqrt(nu[i]);
+}
+
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st) {
   launch(pcg_update_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, st, x, r, p, q, n, S, ro, tol, it, ws);
@@ -664,6 +674,10 @@ int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st) {
   launch(pcg_scale_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, st, z, n, scale, S);
   return check_launch("pcg_scale_kernel");
+}
+int pcg_dscale(const double* in, double* out, const double* nu, int64_t n, const double* S, cudaStream_t st) {
+  launch(pcg_dscale_kernel, dim3(grid_for(n)), dim3(kReduceThreads), 0, st, in, out, nu, n, S);
+  return check_launch("pcg_dscale_kernel");
 }
 }  // namespace smg
 
