@@ -533,10 +533,11 @@ int tr_launch_warp(const TrArgs& A, bool prolong, cudaStream_t st) {
 // tile T (elements per side) chosen at run time from the compiled set
 template <int PC, int PF>
 int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
-  if constexpr (PF == 3 || PF == 24 || PF == 32) {
+  if constexpr (PF == 3 || PF == 32) {
     // warp-per-element prolongation where it measured faster than the tiled
-    // kernel on B200 (C5 levels: p_f = 24 1272 -> 1118 us, 3: 79 -> 40 us;
-    // slower at p_f = 12: 195 -> 326, 6: 111 -> 157); restriction stays tiled
+    // kernel on B200 (C5 p_f = 3: 79 -> 40 us, C3 p_f = 32: 152 -> 136 us;
+    // slower at p_f = 12: 195 -> 326, 6: 111 -> 157, and at 24 than the
+    // two-element tiles below: 1118 vs 584 us); restriction stays tiled
     static const int warp = env_int("SMG_TR_WARP", 1);
     if (prolong && warp) {
       TrArgs B = A;
@@ -555,7 +556,9 @@ int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) 
       return tr_launch_warp<PC, PF>(B, prolong, st);
     }
   }
-  constexpr int T0 = PF >= 32 ? 1 : 32 / PF;
+  // (p_f = 24: two coarse elements per side -- 2.25x the window of one, a
+  // quarter of the CTAs; one-element CTAs were latency-bound)
+  constexpr int T0 = PF >= 32 ? 1 : (PF > 16 ? 2 : 32 / PF);
   // largest power-of-two T <= T0 dividing the mesh that keeps >= 296 CTAs,
   // else the one with the most CTAs
   int best = 1;
