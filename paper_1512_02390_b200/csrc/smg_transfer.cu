@@ -533,11 +533,11 @@ int tr_launch_warp(const TrArgs& A, bool prolong, cudaStream_t st) {
 // tile T (elements per side) chosen at run time from the compiled set
 template <int PC, int PF>
 int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) {
-  if constexpr (PF == 3 || PF == 32) {
+  if constexpr (PF == 3) {
     // warp-per-element prolongation where it measured faster than the tiled
-    // kernel on B200 (C5 p_f = 3: 79 -> 40 us, C3 p_f = 32: 152 -> 136 us;
-    // slower at p_f = 12: 195 -> 326, 6: 111 -> 157, and at 24 than the
-    // two-element tiles below: 1118 vs 584 us); restriction stays tiled
+    // kernel on B200 (C5 p_f = 3: 79 -> 40 us; slower at p_f = 12: 195 ->
+    // 326, 6: 111 -> 157, and at 24 / 32 than the two-element tiles below:
+    // 1118 vs 584 us, 136 vs 89 us); restriction stays tiled
     static const int warp = env_int("SMG_TR_WARP", 1);
     if (prolong && warp) {
       TrArgs B = A;
@@ -556,13 +556,17 @@ int tr_launch(const TrArgs& A, int n_x, int n_y, bool prolong, cudaStream_t st) 
       return tr_launch_warp<PC, PF>(B, prolong, st);
     }
   }
-  // (p_f = 24: two coarse elements per side -- 2.25x the window of one, a
-  // quarter of the CTAs; one-element CTAs were latency-bound)
-  constexpr int T0 = PF >= 32 ? 1 : (PF > 16 ? 2 : 32 / PF);
-  // largest power-of-two T <= T0 dividing the mesh that keeps >= 296 CTAs,
+  // p_f > 16: two coarse elements per side (2.25x the window of one, a
+  // quarter of the CTAs; one-element CTAs were latency-bound) -- except the
+  // p_f = 32 restriction, measured slower that way (C3: 172 -> 201 us;
+  // prolongation 136 -> 89 us, p_f = 24: restrict 1437 -> 834, prolong
+  // 1118 -> 584 us)
+  constexpr int T0 = PF > 16 ? 2 : 32 / PF;
+  const int t0 = (PF >= 32 && !prolong) ? 1 : T0;
+  // largest power-of-two T <= t0 dividing the mesh that keeps >= 296 CTAs,
   // else the one with the most CTAs
   int best = 1;
-  for (int t = T0; t >= 1; t /= 2) {
+  for (int t = t0; t >= 1; t /= 2) {
     if (n_x % t || n_y % t) continue;
     best = t;
     static const int min_ctas = env_int("SMG_TR_MIN_CTAS", 296);
