@@ -104,6 +104,84 @@ __device__ __forceinline__ void opd_batch(const double* x0, const double* n0, in
   }
 }
 
+// Diffusion batch with the symmetry of the GLL derivative matrix,
+// D[P-i][P-j] = -D[i][j]: in terms of a_k = x_k + x_{P-k}, d_k = x_k - x_{P-k}
+// (k < H = P/2) and the centre c = x_H,
+//   G[n]   = (E a + D[n][H] c) + O d,   G[P-n] = O d - (E a + D[n][H] c),
+//   E[n][k] = (D[n][k] + D[n][P-k]) / 2,  O[n][k] = (D[n][k] - D[n][P-k]) / 2
+// for n <= H -- two (H+1) x (H+1) products instead of one (P+1) x (P+1), i.e.
+// 2 x 16 x 16 instead of 32 x 28 DMMA slots at p = 24; the second product
+// (V = g D) splits the same way with a' = g_j + g_{P-j}, d' = g_j - g_{P-j}.
+// Returns, for node n = 8j + 2t + e <= H of line g, Vb = V[n] and Vm = V[P-n].
+// ONLY_LAST: only the n-tile holding n = 0 (V[P] = Vm[0][0] at t = 0).
+template <int P, bool ONLY_LAST>
+__device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0, int st, const double* WT,
+                                             const double* __restrict__ frag, double (&Vb)[2][2], double (&Vm)[2][2]) {
+  constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+  static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
+  const int lane = threadIdx.x & 31, t = lane & 3;
+  const double* BE = frag;
+  const double* BO = frag + KH * NH * 32;
+  const double* BE2 = frag + 2 * KH * NH * 32;
+  const double* BO2 = frag + 3 * KH * NH * 32;
+  double W[NH][2], U[NH][2];
+#pragma unroll
+  for (int j = 0; j < NH; ++j) W[j][0] = W[j][1] = U[j][0] = U[j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int k = 4 * q + t;
+    const double xa = k <= H ? x0[k * st] : 0.0;
+    const double xb = k < H ? x0[(P - k) * st] : 0.0;
+    const double a = xa + xb, d = k < H ? xa - xb : 0.0;
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      dmma(W[j][0], W[j][1], a, __ldg(BE + (q * NH + j) * 32 + lane));
+      dmma(U[j][0], U[j][1], d, __ldg(BO + (q * NH + j) * 32 + lane));
+    }
+  }
+  // g = G nu w at nodes n and P - n, then a' (centre: g_H) and d'
+#pragma unroll
+  for (int j = 0; j < NH; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = 8 * j + 2 * t + e;
+      double ga = 0.0, gd = 0.0;
+      if (n <= H) {
+        const double gn = (U[j][e] + W[j][e]) * (n0[n * st] * WT[n]);
+        const double gm = (U[j][e] - W[j][e]) * (n0[(P - n) * st] * WT[P - n]);
+        ga = n < H ? gn + gm : gn;
+        gd = n < H ? gn - gm : 0.0;
+      }
+      W[j][e] = ga;
+      U[j][e] = gd;
+    }
+  constexpr int J0 = 0, J1 = ONLY_LAST ? 1 : NH;
+  double W2[NH][2], U2[NH][2];
+#pragma unroll
+  for (int j = J0; j < J1; ++j) W2[j][0] = W2[j][1] = U2[j][0] = U2[j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+    const double a0 = __shfl_sync(0xffffffffu, W[q >> 1][0], src);
+    const double a1 = __shfl_sync(0xffffffffu, W[q >> 1][1], src);
+    const double d0 = __shfl_sync(0xffffffffu, U[q >> 1][0], src);
+    const double d1 = __shfl_sync(0xffffffffu, U[q >> 1][1], src);
+    const double a = (t & 1) ? a1 : a0, d = (t & 1) ? d1 : d0;
+#pragma unroll
+    for (int j = J0; j < J1; ++j) {
+      dmma(W2[j][0], W2[j][1], a, __ldg(BE2 + (q * NH + j) * 32 + lane));
+      dmma(U2[j][0], U2[j][1], d, __ldg(BO2 + (q * NH + j) * 32 + lane));
+    }
+  }
+#pragma unroll
+  for (int j = J0; j < J1; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      Vb[j][e] = U2[j][e] + W2[j][e];
+      Vm[j][e] = U2[j][e] - W2[j][e];
+    }
+}
+
 template <int P, bool DIFF>
 __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
                                                                         const double* __restrict__ frag) {
@@ -158,17 +236,35 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
     const int y = 8 * warp + g;
     const double* ur = U + (y + P) * DP + sh;
     const double* nr = NU + (y + P) * DP + sh;
-    opd_batch<P, DIFF, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
-    if (t == 0) VX[y * 2] = V[P / 8][0];
-    opd_batch<P, DIFF, false>(ur + P, nr + P, 1, WT, frag, V);
+    if constexpr (DIFF) {
+      double Vb[2][2], Vm[2][2];
+      opd_batch_eo<P, true>(ur, nr, 1, WT, frag, Vb, Vm);   // left neighbour: its node P only
+      if (t == 0) VX[y * 2] = Vm[0][0];
+      opd_batch_eo<P, false>(ur + P, nr + P, 1, WT, frag, Vb, Vm);
 #pragma unroll
-    for (int j = 0; j < NTL; ++j)
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int b = 8 * j + 2 * t + e;
-        if (b < P) AX[y * OX + b] = V[j][e];
-        else if (b == P) VX[y * 2 + 1] = V[j][e];
-      }
+        for (int e = 0; e < 2; ++e) {
+          const int b = 8 * j + 2 * t + e;
+          if (b <= P / 2) {
+            AX[y * OX + b] = Vb[j][e];
+            if (b == 0) VX[y * 2 + 1] = Vm[j][e];
+            else if (b < P / 2) AX[y * OX + (P - b)] = Vm[j][e];
+          }
+        }
+    } else {
+      opd_batch<P, DIFF, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
+      if (t == 0) VX[y * 2] = V[P / 8][0];
+      opd_batch<P, DIFF, false>(ur + P, nr + P, 1, WT, frag, V);
+#pragma unroll
+      for (int j = 0; j < NTL; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int b = 8 * j + 2 * t + e;
+          if (b < P) AX[y * OX + b] = V[j][e];
+          else if (b == P) VX[y * 2 + 1] = V[j][e];
+        }
+    }
   }
   __syncthreads();
   // ---- column pass (x-part of the left element added at b == 0) -----------
@@ -177,23 +273,43 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
     const int x = 8 * warp + g;
     const double* uc = U + sh + (x + P);
     const double* nc = NU + sh + (x + P);
-    opd_batch<P, DIFF, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
-    if (t == 0) VY[x * 2] = V[P / 8][0];
-    opd_batch<P, DIFF, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
     const double wyb = A.cy * WS[x];
-#pragma unroll
-    for (int j = 0; j < NTL; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int a = 8 * j + 2 * t + e;
-        if (a < P) {
-          double ax = AX[a * OX + x];
-          if (x == 0) ax += VX[a * 2];
-          AX[a * OX + x] = fma(A.cx * WS[a], ax, wyb * V[j][e]);
-        } else if (a == P) {
-          VY[x * 2 + 1] = V[j][e];
-        }
+    auto put = [&](int a, double v) {   // y-part v at node a of column x
+      if (a < P) {
+        double ax = AX[a * OX + x];
+        if (x == 0) ax += VX[a * 2];
+        AX[a * OX + x] = fma(A.cx * WS[a], ax, wyb * v);
+      } else {
+        VY[x * 2 + 1] = v;
       }
+    };
+    if constexpr (DIFF) {
+      double Vb[2][2], Vm[2][2];
+      opd_batch_eo<P, true>(uc, nc, DP, WT, frag, Vb, Vm);   // lower neighbour: its node P only
+      if (t == 0) VY[x * 2] = Vm[0][0];
+      opd_batch_eo<P, false>(uc + P * DP, nc + P * DP, DP, WT, frag, Vb, Vm);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int a = 8 * j + 2 * t + e;
+          if (a <= P / 2) {
+            put(a, Vb[j][e]);
+            if (a < P / 2) put(P - a, Vm[j][e]);
+          }
+        }
+    } else {
+      opd_batch<P, DIFF, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
+      if (t == 0) VY[x * 2] = V[P / 8][0];
+      opd_batch<P, DIFF, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
+#pragma unroll
+      for (int j = 0; j < NTL; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int a = 8 * j + 2 * t + e;
+          if (a <= P) put(a, V[j][e]);
+        }
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -212,6 +328,31 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
 // (k-tile q, n-tile j, lane (g, t)) = B[4q + t][8j + g].
 void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out) {
   const int NP = p + 1, KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
+  if (diffusion) {
+    // even/odd halves (opd_batch_eo): B[k][n] for k, n <= H
+    //   E [k][n] = (D[n][k] + D[n][P-k]) / 2 (k < H), E [H][n] = D[n][H]
+    //   O [k][n] = (D[n][k] - D[n][P-k]) / 2 (k < H)
+    //   E2[k][n] = (D[k][n] + D[P-k][n]) / 2 (k < H), E2[H][n] = D[H][n]
+    //   O2[k][n] = (D[k][n] - D[P-k][n]) / 2 (k < H)
+    const int H = p / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+    auto d = [&](int i, int j) { return D[i * NP + j]; };
+    out.assign((size_t)4 * KH * NH * 32, 0.0);
+    for (int m = 0; m < 4; ++m)
+      for (int q = 0; q < KH; ++q)
+        for (int j = 0; j < NH; ++j)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int k = 4 * q + (lane & 3), n = 8 * j + (lane >> 2);
+            double v = 0.0;
+            if (k <= H && n <= H) {
+              if (m == 0) v = k < H ? 0.5 * (d(n, k) + d(n, p - k)) : d(n, H);
+              else if (m == 1) v = k < H ? 0.5 * (d(n, k) - d(n, p - k)) : 0.0;
+              else if (m == 2) v = k < H ? 0.5 * (d(k, n) + d(p - k, n)) : d(H, n);
+              else v = k < H ? 0.5 * (d(k, n) - d(p - k, n)) : 0.0;
+            }
+            out[((size_t)(m * KH + q) * NH + j) * 32 + lane] = v;
+          }
+    return;
+  }
   out.assign((size_t)(diffusion ? 2 : 1) * KT * NTL * 32, 0.0);
   // diffusion: D^T then D; Poisson: L-hat (B[k][n] = L[k][n], the m = 1 form)
   for (int m = diffusion ? 0 : 1; m < 2; ++m)
