@@ -182,6 +182,42 @@ __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0,
     }
 }
 
+// Poisson batch with the centro-symmetry L[P-i][P-j] = L[i][j] of L-hat:
+//   v[n] = (Ee a + L[H][n] c) + Oo d,   v[P-n] = (Ee a + L[H][n] c) - Oo d,
+//   Ee[k][n] = (L[k][n] + L[P-k][n]) / 2,  Oo[k][n] = (L[k][n] - L[P-k][n]) / 2
+// (n <= H = P/2): 2 x 20 x 24 DMMA slots per batch instead of 36 x 40 at p = 32.
+template <int P, bool ONLY_LAST>
+__device__ __forceinline__ void opd_batch_pe(const double* x0, int st, const double* __restrict__ frag,
+                                             double (&Vb)[(P / 2 + 8) / 8][2], double (&Vm)[(P / 2 + 8) / 8][2]) {
+  constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+  const int lane = threadIdx.x & 31, t = lane & 3;
+  const double* BE = frag;
+  const double* BO = frag + KH * NH * 32;
+  constexpr int J1 = ONLY_LAST ? 1 : NH;
+  double W[NH][2], U[NH][2];
+#pragma unroll
+  for (int j = 0; j < J1; ++j) W[j][0] = W[j][1] = U[j][0] = U[j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int k = 4 * q + t;
+    const double xa = k <= H ? x0[k * st] : 0.0;
+    const double xb = k < H ? x0[(P - k) * st] : 0.0;
+    const double a = xa + xb, d = k < H ? xa - xb : 0.0;
+#pragma unroll
+    for (int j = 0; j < J1; ++j) {
+      dmma(W[j][0], W[j][1], a, __ldg(BE + (q * NH + j) * 32 + lane));
+      dmma(U[j][0], U[j][1], d, __ldg(BO + (q * NH + j) * 32 + lane));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J1; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      Vb[j][e] = W[j][e] + U[j][e];
+      Vm[j][e] = W[j][e] - U[j][e];
+    }
+}
+
 template <int P, bool DIFF>
 __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
                                                                         const double* __restrict__ frag) {
@@ -253,16 +289,21 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
           }
         }
     } else {
-      opd_batch<P, DIFF, true>(ur, nr, 1, WT, frag, V);   // left neighbour: its node P only
-      if (t == 0) VX[y * 2] = V[P / 8][0];
-      opd_batch<P, DIFF, false>(ur + P, nr + P, 1, WT, frag, V);
+      constexpr int NHO = (P / 2 + 8) / 8;
+      double Vb[NHO][2], Vm[NHO][2];
+      opd_batch_pe<P, true>(ur, 1, frag, Vb, Vm);   // left neighbour: its node P only
+      if (t == 0) VX[y * 2] = Vm[0][0];
+      opd_batch_pe<P, false>(ur + P, 1, frag, Vb, Vm);
 #pragma unroll
-      for (int j = 0; j < NTL; ++j)
+      for (int j = 0; j < NHO; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int b = 8 * j + 2 * t + e;
-          if (b < P) AX[y * OX + b] = V[j][e];
-          else if (b == P) VX[y * 2 + 1] = V[j][e];
+          if (b <= P / 2) {
+            AX[y * OX + b] = Vb[j][e];
+            if (b == 0) VX[y * 2 + 1] = Vm[j][e];
+            else if (b < P / 2) AX[y * OX + (P - b)] = Vm[j][e];
+          }
         }
     }
   }
@@ -299,15 +340,20 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
           }
         }
     } else {
-      opd_batch<P, DIFF, true>(uc, nc, DP, WT, frag, V);   // lower neighbour: its node P only
-      if (t == 0) VY[x * 2] = V[P / 8][0];
-      opd_batch<P, DIFF, false>(uc + P * DP, nc + P * DP, DP, WT, frag, V);
+      constexpr int NHO = (P / 2 + 8) / 8;
+      double Vb[NHO][2], Vm[NHO][2];
+      opd_batch_pe<P, true>(uc, DP, frag, Vb, Vm);   // lower neighbour: its node P only
+      if (t == 0) VY[x * 2] = Vm[0][0];
+      opd_batch_pe<P, false>(uc + P * DP, DP, frag, Vb, Vm);
 #pragma unroll
-      for (int j = 0; j < NTL; ++j)
+      for (int j = 0; j < NHO; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int a = 8 * j + 2 * t + e;
-          if (a <= P) put(a, V[j][e]);
+          if (a <= P / 2) {
+            put(a, Vb[j][e]);
+            if (a < P / 2) put(P - a, Vm[j][e]);
+          }
         }
     }
   }
@@ -348,6 +394,26 @@ void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& 
               else if (m == 1) v = k < H ? 0.5 * (d(n, k) - d(n, p - k)) : 0.0;
               else if (m == 2) v = k < H ? 0.5 * (d(k, n) + d(p - k, n)) : d(H, n);
               else v = k < H ? 0.5 * (d(k, n) - d(p - k, n)) : 0.0;
+            }
+            out[((size_t)(m * KH + q) * NH + j) * 32 + lane] = v;
+          }
+    return;
+  }
+  {
+    // Poisson even/odd halves (opd_batch_pe): Ee[k][n] = (L[k][n] + L[P-k][n]) / 2
+    // (k < H), Ee[H][n] = L[H][n]; Oo[k][n] = (L[k][n] - L[P-k][n]) / 2
+    const int H = p / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+    auto l = [&](int i, int j) { return D[i * NP + j]; };
+    out.assign((size_t)2 * KH * NH * 32, 0.0);
+    for (int m = 0; m < 2; ++m)
+      for (int q = 0; q < KH; ++q)
+        for (int j = 0; j < NH; ++j)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int k = 4 * q + (lane & 3), n = 8 * j + (lane >> 2);
+            double v = 0.0;
+            if (k <= H && n <= H) {
+              if (m == 0) v = k < H ? 0.5 * (l(k, n) + l(p - k, n)) : l(H, n);
+              else v = k < H ? 0.5 * (l(k, n) - l(p - k, n)) : 0.0;
             }
             out[((size_t)(m * KH + q) * NH + j) * 32 + lane] = v;
           }
