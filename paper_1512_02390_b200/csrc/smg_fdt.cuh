@@ -319,7 +319,18 @@ struct FDTK {
   // those loads were the stage's long-scoreboard stalls)
   static constexpr size_t SDB = sizeof(double) * (size_t)M * M;
   static constexpr bool SDV = !DM && smem_for(NS) + SDB <= (smem_for(NS) <= HALF_SM ? HALF_SM : FULL_SM);
-  static constexpr size_t TSMEM = smem_for(NS) + (SDV ? SDB : 0);
+  // SMG_FDT_SMEMF build: the eight DFMA factor halves are staged in shared
+  // memory (broadcast LDS) instead of read from the parameter constant bank
+  // (LDCU + uniform-register operand), when that keeps the occupancy
+#ifdef SMG_FDT_SMEMF
+  static constexpr size_t FSMB = sizeof(double) * (4 * (size_t)HE * HE + 4 * (size_t)HO * HO + 2);
+  static constexpr size_t T0 = smem_for(NS) + (SDV ? SDB : 0);
+  static constexpr bool SMF = !DM && (T0 > HALF_SM || T0 + FSMB <= HALF_SM) && T0 + FSMB <= FULL_SM;
+#else
+  static constexpr size_t FSMB = 0;
+  static constexpr bool SMF = false;
+#endif
+  static constexpr size_t TSMEM = smem_for(NS) + (SDV ? SDB : 0) + (SMF ? FSMB : 0);
   static constexpr int MINB = (TSMEM <= HALF_SM && NT <= 384) ? 2 : 1;
 };
 
@@ -397,6 +408,16 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   double* SD = SN + (DM ? E : 0);  // 1/(lam_y + lam_x) table (K::SDV)
   uint64_t* barR = reinterpret_cast<uint64_t*>(SD + (K::SDV ? M * M : 0));
   uint64_t* barU = barR + NS;
+  // factor halves (K::SMF: shared-memory copies; else the parameter bank)
+  double* SF = reinterpret_cast<double*>(barU + NS + ((NS & 1) ? 1 : 0));
+  const double* FSye = K::SMF ? SF : A.Sye;
+  const double* FSyeT = K::SMF ? SF + HE * HE : A.SyeT;
+  const double* FSxe = K::SMF ? SF + 2 * HE * HE : A.Sxe;
+  const double* FSxeT = K::SMF ? SF + 3 * HE * HE : A.SxeT;
+  const double* FSyo = K::SMF ? SF + 4 * HE * HE : A.Syo;
+  const double* FSyoT = K::SMF ? SF + 4 * HE * HE + HO * HO : A.SyoT;
+  const double* FSxo = K::SMF ? SF + 4 * HE * HE + 2 * HO * HO : A.Sxo;
+  const double* FSxoT = K::SMF ? SF + 4 * HE * HE + 3 * HO * HO : A.SxoT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, t4 = lane & 3;
   const int tid = threadIdx.x;
   const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
@@ -420,6 +441,20 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   if constexpr (DM) dm_build_frags<M, FDTArgs<M>, K::FE, K::FO, K::KTE, K::KTO>(A, FR, NT);
   if constexpr (K::SDV)
     for (int idx = tid; idx < M * M; idx += NT) SD[idx] = A.dinv[idx];
+  if constexpr (K::SMF) {
+    for (int idx = tid; idx < HE * HE; idx += NT) {
+      SF[idx] = A.Sye[idx];
+      SF[HE * HE + idx] = A.SyeT[idx];
+      SF[2 * HE * HE + idx] = A.Sxe[idx];
+      SF[3 * HE * HE + idx] = A.SxeT[idx];
+    }
+    for (int idx = tid; idx < HO * HO; idx += NT) {
+      SF[4 * HE * HE + idx] = A.Syo[idx];
+      SF[4 * HE * HE + HO * HO + idx] = A.SyoT[idx];
+      SF[4 * HE * HE + 2 * HO * HO + idx] = A.Sxo[idx];
+      SF[4 * HE * HE + 3 * HO * HO + idx] = A.SxoT[idx];
+    }
+  }
   __syncthreads();
 
   // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
@@ -524,12 +559,12 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       auto in = [&](int k) { return col[k * BRX]; };
       if (!odd) {
         double t[HE];
-        half_analyse<M, HE, false>(A.Sye, in, t);
+        half_analyse<M, HE, false>(FSye, in, t);
 #pragma unroll
         for (int i = 0; i < HE; ++i) B[i * M + c] = t[i];
       } else if (HO > 0) {
         double t[HOX];
-        half_analyse<M, HOX, true>(A.Syo, in, t);
+        half_analyse<M, HOX, true>(FSyo, in, t);
 #pragma unroll
         for (int i = 0; i < HO; ++i) B[(HE + i) * M + c] = t[i];
       }
@@ -721,8 +756,8 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         const double* row = B + c * M;
         auto in = [&](int k) { return row[k]; };
         if (act) {
-          if (!odd) half_analyse<M, HE, false>(A.Sxe, in, t);
-          else if (HO > 0) half_analyse<M, HOX, true>(A.Sxo, in, reinterpret_cast<double(&)[HOX]>(t));
+          if (!odd) half_analyse<M, HE, false>(FSxe, in, t);
+          else if (HO > 0) half_analyse<M, HOX, true>(FSxo, in, reinterpret_cast<double(&)[HOX]>(t));
         }
         if constexpr (!PP) __syncthreads();  // every row read before the in-place writes
         if (act) {   // PP: into the second buffer, no read-before-write barrier
@@ -747,12 +782,12 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
             double t[HE];
 #pragma unroll
             for (int i = 0; i < HE; ++i) t[i] = B2[i * M + c];
-            half_synth<HE>(A.SyeT, t, acc);
+            half_synth<HE>(FSyeT, t, acc);
           } else if (HO > 0) {
             double t[HOX];
 #pragma unroll
             for (int i = 0; i < HO; ++i) t[i] = B2[(HE + i) * M + c];
-            half_synth<HOX>(A.SyoT, t, reinterpret_cast<double(&)[HOX]>(acc));
+            half_synth<HOX>(FSyoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
         if constexpr (!PP) __syncthreads();  // every column read before the in-place writes
@@ -784,12 +819,12 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
             double t[HE];
 #pragma unroll
             for (int i = 0; i < HE; ++i) t[i] = t3(i);
-            half_synth<HE>(A.SxeT, t, acc);
+            half_synth<HE>(FSxeT, t, acc);
           } else if (HO > 0) {
             double t[HOX];
 #pragma unroll
             for (int i = 0; i < HO; ++i) t[i] = t3(HE + i);
-            half_synth<HOX>(A.SxoT, t, reinterpret_cast<double(&)[HOX]>(acc));
+            half_synth<HOX>(FSxoT, t, reinterpret_cast<double(&)[HOX]>(acc));
           }
         }
         if constexpr (!PP) __syncthreads();  // every row read before B is reused for ex / ox
