@@ -299,7 +299,10 @@ struct FDTK {
   static constexpr int MTO = (HO + 7) / 8, KTO = (HO + 3) / 4;   // odd half
   static constexpr int FE = MTE * KTE, FO = MTO * KTO;
   static constexpr int FRN = DM ? 4 * (FE + FO) * 32 : 0;        // fragment table (doubles)
-  static constexpr int WARPS = 8;
+#ifndef SMG_FDT_DMW
+#define SMG_FDT_DMW 8   // warps per CTA of the DMMA variant (alternative builds: -DSMG_FDT_DMW=16)
+#endif
+  static constexpr int WARPS = DM ? SMG_FDT_DMW : 8;
   static constexpr int NT = DM ? 32 * WARPS : G::THREADS;
   static constexpr int BT = (E * M + 7) / 8;                     // 8-line batches
   static constexpr int MAXB = (BT + WARPS - 1) / WARPS;
