@@ -401,6 +401,98 @@ def mult():
             out[f"mv{j}_{solver}_res"] = np.array(rep.residuals)
     save("mult", **out)
 
+
+def c5full():
+    """BASELINE configs[4] (C5) at full size: 512x512 elements, p=24, levels
+    (1,3,6,12,24), nu_hat=0.9, nu_shift=0 (== [0,2pi]^2, nu = 1+0.9 sin x sin y),
+    seeded mean-zero Gaussian f, zero start, MGCG to 1e10 (krylov.py:70-115).
+    About 2-4 h and ~18 GB RSS in this container; run once in the background."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    t = time.time()
+    msh = mesh.MeshConfig(512, 512, 1.0, 1.0)
+    h = _hand_hierarchy(multigrid, basis, mesh, operators, schwarz, msh, [1, 3, 6, 12, 24], 0.9, 0.0)
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    print(f"C5 build {time.time() - t:.1f}s", flush=True)
+    u, rep = krylov.solve(h, f, krylov.SolveConfig(solver="mgcg", tol_reduction=1e10), u0=np.zeros_like(f))
+    out["c5_mgcg_res"] = np.array(rep.residuals)
+    out["c5_mgcg_sample"] = u[::192, ::192].copy()
+    out["c5_mgcg_norm"] = np.array(np.linalg.norm(u))
+    out["c5_breakdown"] = np.array(rep.breakdown)
+    out["c5_wall"] = np.array(time.time() - t)
+    print(f"C5 full done in {time.time() - t:.1f}s, {rep.cycles} cycles", flush=True)
+    save("xlarge_c5", **out)
+
+
+def c3full():
+    """BASELINE configs[2] (C3): 128x128, p=32, fixed:1, full MG history to 1e10
+    (krylov.py:49-67) from a zero start, seed 0."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    t = time.time()
+    msh = mesh.MeshConfig(128, 128, 1.0, 1.0)
+    h = multigrid.build_hierarchy(msh, 32, multigrid.OverlapRule("fixed", 1))
+    lay = h.top.op.layout
+    f = operators.project_mean(np.random.default_rng(0).standard_normal((lay.N_y, lay.N_x)))
+    u, rep = krylov.solve(h, f, krylov.SolveConfig(solver="mg", tol_reduction=1e10), u0=np.zeros_like(f))
+    out["c3_mg_res"] = np.array(rep.residuals)
+    out["c3_mg_sample"] = u[::64, ::64].copy()
+    print(f"C3 full MG done in {time.time() - t:.1f}s, {rep.cycles} cycles", flush=True)
+    save("xlarge_c3_mg", **out)
+
+
+def ceilp8():
+    """The paper's recommended overlap rule ceil(p/8) (multigrid.py:28-54) at the
+    BASELINE top orders: additive sweeps at p=16/24/32 (n_o=2/3/4, m=21/31/41,
+    schwarz.py:255-275), Poisson and diffusion, ragged meshes; one ceilp8
+    V-cycle at p=32 (multigrid.py:231-251); coarse solves of p=1 meshes above
+    64^2 (multigrid.py:196-228: plain CG to 1e-12), Poisson and diffusion.
+    Inputs are regenerated from per-case seeds by the tests (ceilp8_inputs)
+    instead of stored, to keep the fixture small."""
+    basis, krylov, mesh, multigrid, operators, schwarz = _ref()
+    out = {}
+    for i, (nx, ny, lx, ly, p, n_o, nu_hat) in enumerate(CEILP8_SWEEPS):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        b = basis.gll_basis(p)
+        lay = mesh.layout_for(msh, p)
+        if nu_hat is None:
+            op, nb = operators.PoissonOperator(b, msh), None
+        else:
+            op = operators.DiffusionOperator(b, msh, operators.diffusivity_field(msh, b, nu_hat, 0.2))
+            nb = op.element_mean_nu()
+        sm = schwarz.AdditiveSchwarz(b, lay, msh.dx, msh.dy, n_o, schwarz.WeightKind.QUINTIC, nu_bar=nb)
+        u0, f = ceilp8_inputs(800 + i, (lay.N_y, lay.N_x))
+        out[f"sw{i}_u1"] = sm.smooth(op, u0.copy(), f, 1)
+        out[f"sw{i}_in_sample"] = np.array([u0[0, 0], f[-1, -1]])
+    for i, (nx, ny, p) in enumerate(CEILP8_VCYCLES):
+        msh = mesh.MeshConfig(nx, ny, 1.0, 1.0)
+        h = multigrid.build_hierarchy(msh, p, multigrid.OverlapRule.parse("ceilp8"))
+        lay = h.top.op.layout
+        u, f = ceilp8_inputs(900 + i, (lay.N_y, lay.N_x))
+        f = operators.project_mean(f)
+        out[f"vc{i}_uout"] = multigrid.v_cycle(h, u.copy(), f)
+    for i, (nx, ny, lx, ly, nu_hat) in enumerate(CEILP8_COARSE):
+        msh = mesh.MeshConfig(nx, ny, lx, ly)
+        h = multigrid.build_hierarchy(msh, 2, multigrid.OverlapRule("fixed", 1), nu_hat=nu_hat, nu_shift=0.0)
+        _, f0 = ceilp8_inputs(950 + i, (ny, nx))
+        out[f"cs{i}_u0"] = multigrid.coarse_solve(h, f0)
+    save("ceilp8", **out)
+
+
+# (n_x, n_y, l_x, l_y, p, n_o = ceil(p/8), nu_hat or None)
+CEILP8_SWEEPS = [(6, 5, 1.0, 1.0, 16, 2, None), (5, 4, 1.0, 1.0, 24, 3, None), (5, 6, 2.0, 1.0, 32, 4, None),
+                 (4, 4, 1.0, 1.0, 24, 3, 0.9), (4, 5, 1.0, 1.0, 32, 4, 0.5), (9, 7, 1.0, 1.0, 16, 2, None)]
+CEILP8_VCYCLES = [(8, 8, 32)]
+# p = 1 coarse meshes above 64^2 (n_x, n_y, l_x, l_y, nu_hat or None; nu_shift 0)
+CEILP8_COARSE = [(128, 128, 1.0, 1.0, None), (128, 128, 1.0, 1.0, 0.9), (256, 128, 2.0, 1.0, 0.9)]
+
+
+def ceilp8_inputs(seed, shape):
+    """(u0 in [0,1), f ~ N(0,1)) for one ceilp8 fixture case."""
+    rng = np.random.default_rng(seed)
+    return rng.random(shape), rng.standard_normal(shape)
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
@@ -408,7 +500,19 @@ if __name__ == "__main__":
     ap.add_argument("--xlarge", action="store_true")
     ap.add_argument("--harness", action="store_true", help="only the f1/f2 harness fixtures")
     ap.add_argument("--mult", action="store_true", help="only the f3 multiplicative fixtures")
+    ap.add_argument("--c5full", action="store_true", help="only the full-size C5 MGCG history (hours)")
+    ap.add_argument("--c3full", action="store_true", help="only the full C3 MG history")
+    ap.add_argument("--ceilp8", action="store_true", help="only the ceil(p/8) sweeps / V-cycles / coarse solves")
     a = ap.parse_args()
+    if a.c5full:
+        c5full()
+        sys.exit(0)
+    if a.c3full:
+        c3full()
+        sys.exit(0)
+    if a.ceilp8:
+        ceilp8()
+        sys.exit(0)
     if a.mult:
         mult()
         sys.exit(0)
