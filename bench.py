@@ -442,7 +442,7 @@ def main():
         "residual": (lambda S: NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(S["u"]), NV.ptr(S["r"]),
                                                             NV.ptr(S["o"]), st)), 2),
         "schwarz": (lambda S: NV.check(lib.smg_schwarz_correct(top.smoother._h.raw, NV.ptr(S["r"]), NV.ptr(S["o"]),
-                                                              st)), 1),
+                                                              NV.ptr(top.smoother.ring), st)), 1),
         "restrict": (lambda S: NV.check(lib.smg_restrict(top.transfer.handle.raw, NV.ptr(S["r"]), NV.ptr(S["fc"]),
                                                          st)), 1),
         "prolong": (lambda S: NV.check(lib.smg_prolongate(top.transfer.handle.raw, NV.ptr(S["uc"]), NV.ptr(S["o"]), 1,

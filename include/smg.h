@@ -13,7 +13,10 @@
  *   - Every launch is enqueued on the caller's stream (a cudaStream_t passed
  *     as void*); nothing synchronizes except where documented.
  *   - Host arrays (factors, matrices) are copied at create time; handles own
- *     only immutable per-level constants.  Workspaces are caller-owned.
+ *     only immutable per-level constants, so one handle may serve several
+ *     streams at once.  Every scratch buffer a call writes (ring workspace,
+ *     reduction partials) is caller-owned and passed in; calls running
+ *     concurrently need distinct workspaces.
  *   - Return value: 0 on success, <0 on error; smg_last_error() explains.
  *     No CPU fallback exists: without a CUDA device every compute call fails.
  */
@@ -37,7 +40,6 @@ typedef struct smg_op smg_op_t;             /* one level's operator          */
 typedef struct smg_schwarz smg_schwarz_t;   /* one level's additive smoother */
 typedef struct smg_transfer smg_transfer_t; /* level l-1 <-> l transfers     */
 typedef struct smg_coarse smg_coarse_t;     /* p=1 pseudo-inverse            */
-typedef struct smg_vtail smg_vtail_t;       /* V-cycle levels 1..K + coarse  */
 typedef struct smg_mult smg_mult_t;         /* multiplicative smoother       */
 
 const char* smg_last_error(void);
@@ -65,7 +67,9 @@ int smg_op_destroy(smg_op_t* h);
 int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out,
                     void* stream);
 /* Like smg_op_residual, and also *norm2_out (device double) = ||out||^2
- * summed deterministically; ws must hold smg_reduce_ws_doubles() doubles. */
+ * summed deterministically; ws (device) must hold smg_op_ws_doubles(h)
+ * doubles (the per-CTA partials) and must not overlap norm2_out. */
+size_t smg_op_ws_doubles(const smg_op_t* h);
 int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
                           double* norm2_out, double* ws, void* stream);
 
@@ -79,14 +83,20 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y,
                        const double* lam_y, const double* w_x, const double* w_y,
                        const double* inv_nu_dev);
 int smg_schwarz_destroy(smg_schwarz_t* h);
+/* Ring workspace of the tiled kernel (doubles, device): the overlap-region
+ * contributions one tile hands to its neighbours within a correction.  0 for
+ * the coloured dense path.  One workspace per concurrently running call. */
+size_t smg_schwarz_ws_doubles(const smg_schwarz_t* h);
 /* u += sum_s R_s^T W A_s^-1 R_s r (/ nu_bar): the additive correction of one
- * sweep given the residual r.  Deterministic (no atomics). */
-int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream);
-/* One or more full sweeps: r = f - A u; u += correction.  work: N_y*N_x.
- * u_is_zero != 0 declares u == 0 on entry: the first sweep skips A u and
- * WRITES u = correction (u's prior contents are never read). */
+ * sweep given the residual r.  ws: smg_schwarz_ws_doubles(h) doubles.
+ * Deterministic (no atomics). */
+int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, double* ws, void* stream);
+/* One or more full sweeps: r = f - A u; u += correction.  work: N_y*N_x,
+ * ws as smg_schwarz_correct.  u_is_zero != 0 declares u == 0 on entry: the
+ * first sweep skips A u and WRITES u = correction (u's prior contents are
+ * never read). */
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
-                       double* work, int n_it, int u_is_zero, void* stream);
+                       double* work, double* ws, int n_it, int u_is_zero, void* stream);
 /* FastDiagSolver.solve on nb independent (m,m) blocks: out = W*(S_y(S_y^T B S_x ./ L)S_x^T).
  * apply_weight=0 skips W (the multiplicative / kind=None solver). */
 int smg_fd_solve_blocks(const smg_schwarz_t* h, const double* blocks, double* out, int nb,
@@ -130,24 +140,6 @@ int smg_mult_destroy(smg_mult_t* h);
  * Sequential by construction (one CTA walks the chain). */
 int smg_mult_sweep(const smg_mult_t* h, const smg_op_t* op, double* u, double* r, int forward,
                    void* stream);
-
-/* ---- V-cycle tail (replaces the lower part of multigrid.py:231-251 v_cycle:
- *      levels K..1 smoothing from zero, residual, restriction, the p=1
- *      pseudo-inverse and the prolongations back up to level K) as ONE
- *      cooperative launch.  Poisson, additive smoother, n_pre=1, n_post=0 on
- *      levels 1..K (K <= 3) of orders p_l = 2^l with one overlap layer,
- *      coarse mesh <= 64 x 64.
- * ops/sm/tr/f/u: K+1 entries indexed by level (sm[0], tr[0] unused); f[K]
- * is the input, u[K] the output (overwritten, u[K] = V-cycle correction);
- * f[l], u[l] for l < K are level work fields.  All pointers must outlive h. */
-int smg_vtail_create(smg_vtail_t** h, int K, const smg_op_t* const* ops, const smg_schwarz_t* const* sm,
-                     const smg_transfer_t* const* tr, const smg_coarse_t* coarse, double* const* f,
-                     double* const* u);
-int smg_vtail_destroy(smg_vtail_t* h);
-int smg_vtail_run(const smg_vtail_t* h, void* stream);
-/* Debug aid: globaltimer (ns) at the phase boundaries of the last run, CTA 0
- * (handle created with SMG_VTAIL_PROF=1; synchronous copy of n entries). */
-int smg_vtail_profile(const smg_vtail_t* h, int64_t* out, int n);
 
 /* Parity mode: the reference's plain CG (multigrid.py:196-228) on the device:
  * u0 = mean0(CG(A0, f0 - mean f0)) to ||r|| <= tol ||b||, at most max_iter

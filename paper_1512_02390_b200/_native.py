@@ -36,12 +36,14 @@ SIGNATURES = {
                                 C.c_double, _hp, _hp, _dp]),
     "smg_op_destroy": (C.c_int, [_vp]),
     "smg_op_residual": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
+    "smg_op_ws_doubles": (C.c_size_t, [_vp]),
     "smg_op_residual_norm2": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _vp]),
     "smg_schwarz_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, _hp, _hp,
                                      _hp, _hp, _hp, _hp, _dp]),
     "smg_schwarz_destroy": (C.c_int, [_vp]),
-    "smg_schwarz_correct": (C.c_int, [_vp, _dp, _dp, _vp]),
-    "smg_schwarz_smooth": (C.c_int, [_vp, _vp, _dp, _dp, _dp, C.c_int, C.c_int, _vp]),
+    "smg_schwarz_ws_doubles": (C.c_size_t, [_vp]),
+    "smg_schwarz_correct": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
+    "smg_schwarz_smooth": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, C.c_int, C.c_int, _vp]),
     "smg_fd_solve_blocks": (C.c_int, [_vp, _dp, _dp, C.c_int, C.c_int, _vp]),
     "smg_transfer_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, _hp]),
     "smg_transfer_destroy": (C.c_int, [_vp]),
@@ -55,11 +57,6 @@ SIGNATURES = {
     "smg_mult_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, _hp, _hp, _hp, _hp, _dp]),
     "smg_mult_destroy": (C.c_int, [_vp]),
     "smg_mult_sweep": (C.c_int, [_vp, _vp, _dp, _dp, C.c_int, _vp]),
-    "smg_vtail_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _vp,
-                                   C.POINTER(_vp), C.POINTER(_vp)]),
-    "smg_vtail_destroy": (C.c_int, [_vp]),
-    "smg_vtail_run": (C.c_int, [_vp, _vp]),
-    "smg_vtail_profile": (C.c_int, [_vp, C.POINTER(_i64), C.c_int]),
     "smg_coarse_cg": (C.c_int, [_vp, _dp, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int), _vp]),
     "smg_coarse_cg_ws_doubles": (C.c_size_t, [_i64]),
     "smg_coarse_pcg_ws_doubles": (C.c_size_t, [_vp]),

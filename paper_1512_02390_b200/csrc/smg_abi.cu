@@ -11,11 +11,10 @@
 
 #include "smg_common.cuh"
 #include "smg_fd.cuh"
-#include "smg_fdm.cuh"
+#include "smg_fdt.cuh"
 #include "smg_op.cuh"
 #include "smg_transfer.cuh"
 #include "smg_rr.cuh"
-#include "smg_vtail.cuh"
 #include "smg_mult.cuh"
 
 namespace smg {
@@ -88,7 +87,7 @@ struct smg_op {
   double dx, dy;
   std::vector<double> Mt, w, wasm;
   const double* nu;
-  double* partials;  // device, one per CTA
+  // norm partials (one per CTA) live in the caller's workspace (smg_op_ws_doubles)
   int n_ctas;
   double* dfrag = nullptr;   // DMMA operand fragments (smg_opd.cu): diffusion p = 24, Poisson p = 32
 };
@@ -106,12 +105,7 @@ struct smg_schwarz {
   int TX, TY, ntx, nty;
   std::vector<double> Sye, Syo, Sxe, Sxo;
   double* dinv_perm;
-  double* ws;
-  unsigned int* ctr;
-  double* Sx_dev;
-  double* Sy_dev;
-  double* frag_dev;
-  bool dmma;      // block-level dense DMMA kernel (smg_fdm.cuh)
+  size_t ws_doubles;  // ring workspace the caller passes to correct / smooth
   bool eo_dmma;   // even/odd DMMA stages inside the TMA-pipelined tiled kernel
 };
 
@@ -133,11 +127,6 @@ struct smg_coarse {
 
 namespace {
 
-// Measured per-m choice of the contraction engine (profiles/: DMMA vs DFMA).
-bool fd_prefers_dmma(int m) {
-  (void)m;
-  return false;
-}
 // tools/time_fd1.py on B200 (us, DFMA vs even/odd DMMA): 256^2 p=16 230 / 286,
 // p=24 585 / 593, 128^2 p=32 401 / 372 -> DMMA from m = 35 (p = 32) up
 bool fd_prefers_eo_dmma(int m) { return m >= 33; }
@@ -246,14 +235,29 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
   o->nu = nu_dev;
   o->fn = fn;
   o->n_ctas = ctas;
-  cudaError_t e = cudaMalloc(&o->partials, sizeof(double) * o->n_ctas);
-  if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
-  if (opd_applies(p, kind == 1)) {
+  cudaError_t e = cudaSuccess;
+  // The tensor-core path builds its fragments from averaged halves of `mat`:
+  // exact only if L-hat is centro-symmetric (Poisson) or D anti-centro-
+  // symmetric (diffusion), as the reference's GLL matrices are.  Any other
+  // matrix keeps the CUDA-core kernels (dfrag stays null -> opd_launch declines).
+  bool sym_ok = true;
+  {
+    const int NP = p + 1;
+    double mmax = 0.0, dev = 0.0;
+    for (int i = 0; i < NP * NP; ++i) mmax = std::fmax(mmax, std::fabs(mat[i]));
+    for (int i = 0; i < NP; ++i)
+      for (int j = 0; j < NP; ++j) {
+        const double a = mat[i * NP + j], b = mat[(p - i) * NP + (p - j)];
+        dev = std::fmax(dev, std::fabs(kind == 1 ? a + b : a - b));
+      }
+    sym_ok = dev <= 1e-14 * (mmax > 0.0 ? mmax : 1.0);
+  }
+  if (sym_ok && opd_applies(p, kind == 1)) {
     std::vector<double> fr;
     opd_fragments(p, kind == 1, mat, fr);
     e = cudaMalloc(&o->dfrag, sizeof(double) * fr.size());
     if (e == cudaSuccess) e = cudaMemcpy(o->dfrag, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) { cudaFree(o->partials); delete o; return cuda_fail(e, "smg_op_create"); }
+    if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }
   }
   *h = o;
   return SMG_OK;
@@ -261,16 +265,16 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
 
 int smg_op_destroy(smg_op_t* h) {
   if (!h) return SMG_OK;
-  cudaFree(h->partials);
   if (h->dfrag) cudaFree(h->dfrag);
   delete h;
   return SMG_OK;
 }
 
-static int op_run(const smg_op_t* h, const double* u, const double* f, double* out, bool norm,
+static int op_run(const smg_op_t* h, const double* u, const double* f, double* out, double* partials,
                   cudaStream_t st) {
+  const bool norm = partials != nullptr;
   OpLaunch L;
-  L.u = u; L.f = f; L.out = out; L.nu = h->nu; L.partials = norm ? h->partials : nullptr;
+  L.u = u; L.f = f; L.out = out; L.nu = h->nu; L.partials = partials;
   L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
@@ -284,21 +288,22 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
 
 int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out, void* stream) {
   if (!h || !u || !out || u == out) { set_error("smg_op_residual: bad argument"); return SMG_EINVAL; }
-  return op_run(h, u, f, out, false, as_stream(stream));
+  return op_run(h, u, f, out, nullptr, as_stream(stream));
 }
 
 int smg_sum_partials(const double* part, int nb, double* out, void* stream);
 
+size_t smg_op_ws_doubles(const smg_op_t* h) { return h ? (size_t)h->n_ctas : 0; }
+
 int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
                           double* norm2_out, double* ws, void* stream) {
-  (void)ws;
-  if (!h || !u || !out || u == out || !norm2_out) {
+  if (!h || !u || !out || u == out || !norm2_out || !ws) {
     set_error("smg_op_residual_norm2: bad argument");
     return SMG_EINVAL;
   }
-  int rc = op_run(h, u, f, out, true, as_stream(stream));
+  int rc = op_run(h, u, f, out, ws, as_stream(stream));
   if (rc) return rc;
-  return smg_sum_partials(h->partials, h->n_ctas, norm2_out, stream);
+  return smg_sum_partials(ws, h->n_ctas, norm2_out, stream);
 }
 
 // ---- additive Schwarz ---------------------------------------------------------
@@ -350,15 +355,13 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   colour_classes(n_y, c > n_y ? n_y : c, s->cy);
   // tiled even/odd path
   s->tiled = false;
-  s->dinv_perm = nullptr; s->ws = nullptr; s->ctr = nullptr;
+  s->dinv_perm = nullptr; s->ws_doubles = 0;
   std::vector<int> px, py;
   const char* force = getenv("SMG_FD_DENSE");
   s->fdt = nullptr;
-  s->Sx_dev = s->Sy_dev = s->frag_dev = nullptr;
-  // contraction engine: FP64 tensor cores (DMMA) or CUDA-core DFMA even/odd;
-  // SMG_FD_ENGINE=dmma|dfma overrides the per-m default
+  // contraction engine: even/odd FP64 tensor cores (DMMA) or CUDA-core DFMA;
+  // SMG_FD_ENGINE=dmma_eo|dfma overrides the per-m default
   const char* eng = getenv("SMG_FD_ENGINE");
-  s->dmma = eng ? (std::strcmp(eng, "dmma") == 0) : fd_prefers_dmma(m);
   s->eo_dmma = eng ? (std::strcmp(eng, "dmma_eo") == 0) : fd_prefers_eo_dmma(m);
   // the tiled kernel folds the weights into its synthesis factors, which needs
   // mirror-symmetric weights (true for every reference weight kind, to 1 ulp)
@@ -368,14 +371,10 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
     wmax = std::fmax(wmax, std::fmax(std::fabs(w_x[k]), std::fabs(w_y[k])));
   }
   const bool w_sym = wasym <= 1e-14 * (wmax > 0.0 ? wmax : 1.0);
-  const bool eo_ok = s->dmma || (w_sym && even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
-                                 even_odd_split(S_y, m, s->Sye, s->Syo, py));
-  if (s->dmma) {
-    px.resize(m); py.resize(m);
-    for (int i = 0; i < m; ++i) px[i] = py[i] = i;
-  }
+  const bool eo_ok = w_sym && even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
+                     even_odd_split(S_y, m, s->Sye, s->Syo, py);
   if (!(force && force[0] == '1') && eo_ok &&
-      (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY, s->dmma)) != nullptr) {
+      (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY, s->eo_dmma)) != nullptr) {
     s->ntx = n_x / s->TX; s->nty = n_y / s->TY;
     const int nt = s->ntx * s->nty;
     const size_t RX = (size_t)s->TX * p + 2 * n_o + 1, RY = (size_t)s->TY * p + 2 * n_o + 1;
@@ -384,19 +383,7 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
       for (int j = 0; j < m; ++j) dp[i * m + j] = 1.0 / (lam_y[py[i]] + lam_x[px[j]]);
     e = cudaMalloc(&s->dinv_perm, sizeof(double) * m * m);
     if (e == cudaSuccess) e = cudaMemcpy(s->dinv_perm, dp.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&s->ws, sizeof(double) * nt * RX * RY);
-    if (e == cudaSuccess) e = cudaMalloc(&s->ctr, sizeof(unsigned int) * 3 * nt);
-    if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, sizeof(unsigned int) * 3 * nt);
-    if (e == cudaSuccess) e = cudaMalloc(&s->Sx_dev, sizeof(double) * m * m);
-    if (e == cudaSuccess) e = cudaMalloc(&s->Sy_dev, sizeof(double) * m * m);
-    if (e == cudaSuccess) e = cudaMemcpy(s->Sx_dev, S_x, sizeof(double) * m * m, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(s->Sy_dev, S_y, sizeof(double) * m * m, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) {
-      std::vector<double> fr;
-      fdm_fragments(m, S_x, S_y, fr);
-      e = cudaMalloc(&s->frag_dev, sizeof(double) * fr.size());
-      if (e == cudaSuccess) e = cudaMemcpy(s->frag_dev, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
-    }
+    s->ws_doubles = (size_t)nt * (RX * RY - (size_t)s->TX * p * s->TY * p);  // ring nodes per tile
     if (e != cudaSuccess) { smg_schwarz_destroy(s); return cuda_fail(e, "smg_schwarz_create (tiles)"); }
     s->tiled = true;
   }
@@ -408,11 +395,6 @@ int smg_schwarz_destroy(smg_schwarz_t* h) {
   if (!h) return SMG_OK;
   cudaFree(h->dinv);
   if (h->dinv_perm) cudaFree(h->dinv_perm);
-  if (h->ws) cudaFree(h->ws);
-  if (h->ctr) cudaFree(h->ctr);
-  if (h->Sx_dev) cudaFree(h->Sx_dev);
-  if (h->Sy_dev) cudaFree(h->Sy_dev);
-  if (h->frag_dev) cudaFree(h->frag_dev);
   delete h;
   return SMG_OK;
 }
@@ -427,15 +409,17 @@ static FDLaunch fd_base(const smg_schwarz_t* h) {
   return L;
 }
 
-static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, int u_zero, void* stream) {
+size_t smg_schwarz_ws_doubles(const smg_schwarz_t* h) { return h ? h->ws_doubles : 0; }
+
+static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, double* ws, int u_zero,
+                           void* stream) {
   if (h->tiled) {
     FDTLaunch T;
     T.r = r; T.u = u; T.u_zero = u_zero;
-    T.dinv_dense = h->dinv; T.Sx_dev = h->Sx_dev; T.Sy_dev = h->Sy_dev; T.frag_dev = h->frag_dev; T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = h->ws; T.ctr = h->ctr;
+    T.inv_nu = h->inv_nu; T.dinv = h->dinv_perm; T.ws = ws;
     T.N_x = h->p * h->n_x; T.N_y = h->p * h->n_y; T.n_x = h->n_x; T.ntx = h->ntx; T.nty = h->nty;
     T.Sye = h->Sye.data(); T.Syo = h->Syo.data(); T.Sxe = h->Sxe.data(); T.Sxo = h->Sxo.data();
     T.wx = h->wx.data(); T.wy = h->wy.data();
-    T.eo_dmma = h->eo_dmma ? 1 : 0;
     const int rc = h->fdt(T, as_stream(stream));
     if (rc != SMG_EUNSUPPORTED) return rc;
     // TMA cannot describe these buffers (odd row length or unaligned base):
@@ -458,14 +442,18 @@ static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, i
   return SMG_OK;
 }
 
-int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, void* stream) {
-  if (!h || !r || !u || r == u) { set_error("smg_schwarz_correct: bad argument"); return SMG_EINVAL; }
-  return schwarz_correct(h, r, u, 0, stream);
+int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, double* ws, void* stream) {
+  if (!h || !r || !u || r == u || (h->ws_doubles && !ws)) {
+    set_error("smg_schwarz_correct: bad argument");
+    return SMG_EINVAL;
+  }
+  return schwarz_correct(h, r, u, ws, 0, stream);
 }
 
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
-                       double* work, int n_it, int u_is_zero, void* stream) {
-  if (!h || !op || !u || !f || !work || n_it < 0 || op->p != h->p || op->n_x != h->n_x || op->n_y != h->n_y) {
+                       double* work, double* ws, int n_it, int u_is_zero, void* stream) {
+  if (!h || !op || !u || !f || !work || n_it < 0 || op->p != h->p || op->n_x != h->n_x || op->n_y != h->n_y ||
+      (h->ws_doubles && !ws)) {
     set_error("smg_schwarz_smooth: bad argument");
     return SMG_EINVAL;
   }
@@ -476,7 +464,7 @@ int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, co
       if (rc) return rc;
       r = work;
     }
-    int rc = schwarz_correct(h, r, u, (it == 0 && u_is_zero) ? 1 : 0, stream);
+    int rc = schwarz_correct(h, r, u, ws, (it == 0 && u_is_zero) ? 1 : 0, stream);
     if (rc) return rc;
   }
   return SMG_OK;
@@ -783,140 +771,6 @@ int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0,
   return smg_project_mean(u0, n, red, stream);
 }
 
-// ---- V-cycle tail (smg_vtail.cu): levels 1..K + coarse pinv in one launch ----
-struct smg_vtail {
-  int K, n_x, n_y, grid;
-  VtArgs* dev;                 // device copy of the launch arguments
-  long long* prof = nullptr;   // SMG_VTAIL_PROF=1: phase timestamps
-  std::vector<void*> owned;    // device buffers owned by the handle
-};
-
-int smg_vtail_destroy(smg_vtail_t* h) {
-  if (!h) return SMG_OK;
-  for (void* p : h->owned) cudaFree(p);
-  delete h;
-  return SMG_OK;
-}
-
-int smg_vtail_create(smg_vtail_t** out, int K, const smg_op_t* const* ops, const smg_schwarz_t* const* sm,
-                     const smg_transfer_t* const* tr, const smg_coarse_t* coarse, double* const* f,
-                     double* const* u) {
-  if (!out || K < 1 || K > kVtMaxLevels || !ops || !sm || !tr || !coarse || !f || !u) {
-    set_error("smg_vtail_create: bad argument");
-    return SMG_EINVAL;
-  }
-  const int n_x = coarse->n_x, n_y = coarse->n_y;
-  if (n_x > kVtMaxN0 || n_y > kVtMaxN0) {
-    set_error("smg_vtail_create: coarse mesh %dx%d exceeds %d^2", n_x, n_y, kVtMaxN0);
-    return SMG_EUNSUPPORTED;
-  }
-  for (int l = 0; l <= K; ++l) {
-    if (!f[l] || !u[l] || !ops[l] || ops[l]->kind != 0 || ops[l]->n_x != n_x || ops[l]->n_y != n_y) {
-      set_error("smg_vtail_create: level %d: needs a Poisson operator on the %dx%d mesh and its fields", l, n_x, n_y);
-      return SMG_EINVAL;
-    }
-  }
-  if (ops[0]->p != 1) { set_error("smg_vtail_create: level 0 must be p = 1"); return SMG_EINVAL; }
-  for (int l = 1; l <= K; ++l) {
-    const smg_schwarz_t* s = sm[l];
-    const smg_transfer_t* t = tr[l];
-    if (!s || !t || s->p != ops[l]->p || s->n_x != n_x || s->n_y != n_y || s->inv_nu != nullptr ||
-        t->pf != ops[l]->p || t->pc != ops[l - 1]->p) {
-      set_error("smg_vtail_create: level %d: inconsistent smoother / transfer", l);
-      return SMG_EINVAL;
-    }
-    if (s->p != (1 << l) || s->n_o != 1 || l > 3) {
-      set_error("smg_vtail_create: level %d: p=%d, n_o=%d not compiled into the tail kernel (orders 2, 4, 8 "
-                "with one overlap layer)", l, s->p, s->n_o);
-      return SMG_EUNSUPPORTED;
-    }
-  }
-  const int grid = vtail_grid();
-  if (grid <= 0) { set_error("smg_vtail_create: cooperative grid unavailable"); return SMG_EUNSUPPORTED; }
-  smg_vtail* h = new (std::nothrow) smg_vtail();
-  if (!h) return SMG_ENOMEM;
-  h->K = K; h->n_x = n_x; h->n_y = n_y; h->grid = grid;
-  auto upload = [&](const double* src, size_t n, const double** dst) -> cudaError_t {
-    void* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, sizeof(double) * (n ? n : 1));
-    if (e != cudaSuccess) return e;
-    h->owned.push_back(d);
-    *dst = static_cast<const double*>(d);
-    return n ? cudaMemcpy(d, src, sizeof(double) * n, cudaMemcpyHostToDevice) : cudaSuccess;
-  };
-  VtArgs A;
-  std::memset(&A, 0, sizeof(A));
-  A.K = K; A.n_x = n_x; A.n_y = n_y;
-  A.Qx = coarse->Qx; A.Qy = coarse->Qy; A.Lp = coarse->Lp;
-  A.lv[0].p = 1; A.lv[0].f = f[0]; A.lv[0].u = u[0];
-  cudaError_t e = cudaSuccess;
-  // the EF tile edge (the level-K tiling) and the BC tile edges: largest of
-  // 4, 2, 1 elements that still gives every SM a tile
-  // tile edge of the BC / EF phases: the smallest that gives every CTA at
-  // most one tile (one round), capped at kVtTE and at the mesh
-  auto tile_edge = [&](void) {
-    int te = 1;
-    while (te < kVtTE && te < n_x && te < n_y && ((n_x + te - 1) / te) * ((n_y + te - 1) / te) > grid) ++te;
-    return te;
-  };
-  const int te = tile_edge();
-  for (int l = 1; l <= K && e == cudaSuccess; ++l) {
-    const smg_schwarz_t* s = sm[l];
-    const smg_op_t* o = ops[l];
-    VtLevel& L = A.lv[l];
-    L.p = s->p; L.n_o = s->n_o; L.m = s->m; L.te = te;
-    L.cx = o->dy / o->dx; L.cy = o->dx / o->dy;
-    L.f = f[l]; L.u = u[l];
-    const int m = s->m;
-    e = upload(s->Sx.data(), (size_t)m * m, &L.Sx);
-    if (e == cudaSuccess) e = upload(s->Sy.data(), (size_t)m * m, &L.Sy);
-    if (e == cudaSuccess) { L.dinv = s->dinv; }
-    if (e == cudaSuccess) e = upload(s->wx.data(), m, &L.wx);
-    if (e == cudaSuccess) e = upload(s->wy.data(), m, &L.wy);
-    if (e == cudaSuccess) e = upload(o->Mt.data(), o->Mt.size(), &L.L);
-    if (e == cudaSuccess) e = upload(o->wasm.data(), o->wasm.size(), &L.wasm);
-    if (e == cudaSuccess) e = upload(tr[l]->J.data(), tr[l]->J.size(), &L.J);
-    if (e == cudaSuccess) {
-      void* d = nullptr;
-      e = cudaMalloc(&d, sizeof(double) * (size_t)n_x * n_y * m * m);
-      if (e == cudaSuccess) { h->owned.push_back(d); L.corr = static_cast<double*>(d); }
-    }
-  }
-  if (e == cudaSuccess) {
-    void* d = nullptr;
-    e = cudaMalloc(&d, sizeof(double) * (size_t)n_x * n_y);
-    if (e == cudaSuccess) { h->owned.push_back(d); A.T2 = static_cast<double*>(d); }
-  }
-  if (e == cudaSuccess && env_int("SMG_VTAIL_PROF", 0)) {
-    void* d = nullptr;
-    e = cudaMalloc(&d, sizeof(long long) * 64);
-    if (e == cudaSuccess) { h->owned.push_back(d); A.prof = static_cast<long long*>(d); h->prof = A.prof; }
-  }
-  if (e == cudaSuccess) {
-    void* d = nullptr;
-    e = cudaMalloc(&d, sizeof(VtArgs));
-    if (e == cudaSuccess) {
-      h->owned.push_back(d);
-      h->dev = static_cast<VtArgs*>(d);
-      e = cudaMemcpy(d, &A, sizeof(VtArgs), cudaMemcpyHostToDevice);
-    }
-  }
-  if (e != cudaSuccess) { smg_vtail_destroy(h); return cuda_fail(e, "smg_vtail_create"); }
-  *out = h;
-  return SMG_OK;
-}
-
-int smg_vtail_profile(const smg_vtail_t* h, int64_t* out, int n) {
-  if (!h || !out || n < 1 || n > 64) { set_error("smg_vtail_profile: bad argument"); return SMG_EINVAL; }
-  if (!h->prof) { set_error("smg_vtail_profile: create the handle with SMG_VTAIL_PROF=1"); return SMG_EUNSUPPORTED; }
-  cudaError_t e = cudaMemcpy(out, h->prof, sizeof(long long) * n, cudaMemcpyDeviceToHost);
-  return e == cudaSuccess ? SMG_OK : cuda_fail(e, "smg_vtail_profile");
-}
-
-int smg_vtail_run(const smg_vtail_t* h, void* stream) {
-  if (!h) { set_error("smg_vtail_run: bad argument"); return SMG_EINVAL; }
-  return vtail_launch(h->dev, 1 << h->K, h->grid, as_stream(stream));
-}
 
 }  // extern "C"
 

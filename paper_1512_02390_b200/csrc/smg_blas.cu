@@ -560,7 +560,7 @@ int pinv_sq_launch(const double* Qx, const double* QxT, const double* Qy, const 
                    double* u, cudaStream_t st) {
   constexpr int CLN = N / 4;
   const size_t smem = sizeof(double) * (5 * (size_t)N * N + 8 * (size_t)N) + 16;
-  static bool attr = false;
+  static DeviceFlag attr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(pinv_sq_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess && CLN > 8) e = cudaFuncSetAttribute(pinv_sq_kernel<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

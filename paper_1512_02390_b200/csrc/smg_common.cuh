@@ -1,6 +1,7 @@
 // Shared helpers for libsmg (sm_100a only).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -29,6 +30,29 @@ inline int check_launch(const char* where) {
   if (e != cudaSuccess) return cuda_fail(e, where);
   return SMG_OK;
 }
+
+// Per-device one-time state.  Kernel attributes (max dynamic shared memory,
+// cluster permissions) and occupancy-derived grid caps belong to a device, so
+// a process that drives several GPUs through the ABI keeps one slot per
+// device ordinal; the slots are atomics, so host threads may race on them
+// (every writer stores the same value).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+template <class T>
+struct PerDevice {
+  std::atomic<T> v[kMaxDevices]{};
+  operator T() const { return v[current_device()].load(std::memory_order_acquire); }
+  PerDevice& operator=(T x) {
+    v[current_device()].store(x, std::memory_order_release);
+    return *this;
+  }
+};
+using DeviceFlag = PerDevice<bool>;
+using DeviceInt = PerDevice<int>;
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

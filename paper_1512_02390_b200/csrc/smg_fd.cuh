@@ -187,7 +187,7 @@ struct FDLaunch {
 
 template <int M>
 int fd_launch(const FDLaunch& L, cudaStream_t st) {
-  static bool attr_done = false;
+  static DeviceFlag attr_done;
   if (!attr_done) {
     if (fd_smem<M>() > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fd_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,

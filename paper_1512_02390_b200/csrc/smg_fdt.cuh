@@ -25,7 +25,6 @@
 //    second kernel adds the band contributions to u in a fixed tile order.
 //    Bitwise reproducible, no atomics, no inter-CTA waiting.
 #pragma once
-#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "smg_common.cuh"
@@ -50,9 +49,7 @@ struct FDTArgs {
   const double* __restrict__ dinv;    // (M,M), [even | odd] eigen order in both dims
   double* __restrict__ ws;            // ring workspace: ntiles * RY * RX
   int N_x, N_y, n_x, ntx, nty;
-  int debug_skip;                     // profiling aid: 1 = skip the four contractions
   int u_zero;                         // 1: u holds no valid data and is treated as 0 (write, not add)
-  int fused_fixup;                    // 1: cooperative launch, ring fixup after a grid barrier
   unsigned long long* phases;         // profiling aid (SMG_FDT_PHASES=1): per-phase clock64 sums, else nullptr
   // analysis factors Se[k][i] (k physical half index); synthesis factors
   // SeT[i][k] pre-multiplied by the (mirror-symmetric) Schwarz weight w[k]
@@ -299,10 +296,7 @@ struct FDTK {
   static constexpr int MTO = (HO + 7) / 8, KTO = (HO + 3) / 4;   // odd half
   static constexpr int FE = MTE * KTE, FO = MTO * KTO;
   static constexpr int FRN = DM ? 4 * (FE + FO) * 32 : 0;        // fragment table (doubles)
-#ifndef SMG_FDT_DMW
-#define SMG_FDT_DMW 8   // warps per CTA of the DMMA variant (alternative builds: -DSMG_FDT_DMW=16)
-#endif
-  static constexpr int WARPS = DM ? SMG_FDT_DMW : 8;
+  static constexpr int WARPS = 8;
   static constexpr int NT = DM ? 32 * WARPS : G::THREADS;
   static constexpr int BT = (E * M + 7) / 8;                     // 8-line batches
   static constexpr int MAXB = (BT + WARPS - 1) / WARPS;
@@ -322,18 +316,7 @@ struct FDTK {
   // those loads were the stage's long-scoreboard stalls)
   static constexpr size_t SDB = sizeof(double) * (size_t)M * M;
   static constexpr bool SDV = !DM && smem_for(NS) + SDB <= (smem_for(NS) <= HALF_SM ? HALF_SM : FULL_SM);
-  // SMG_FDT_SMEMF build: the eight DFMA factor halves are staged in shared
-  // memory (broadcast LDS) instead of read from the parameter constant bank
-  // (LDCU + uniform-register operand), when that keeps the occupancy
-#ifdef SMG_FDT_SMEMF
-  static constexpr size_t FSMB = sizeof(double) * (4 * (size_t)HE * HE + 4 * (size_t)HO * HO + 2);
-  static constexpr size_t T0 = smem_for(NS) + (SDV ? SDB : 0);
-  static constexpr bool SMF = !DM && (T0 > HALF_SM || T0 + FSMB <= HALF_SM) && T0 + FSMB <= FULL_SM;
-#else
-  static constexpr size_t FSMB = 0;
-  static constexpr bool SMF = false;
-#endif
-  static constexpr size_t TSMEM = smem_for(NS) + (SDV ? SDB : 0) + (SMF ? FSMB : 0);
+  static constexpr size_t TSMEM = smem_for(NS) + (SDV ? SDB : 0);
   static constexpr int MINB = (TSMEM <= HALF_SM && NT <= 384) ? 2 : 1;
 };
 
@@ -389,6 +372,14 @@ constexpr long fdt_fixup_per_tile() {
   return (long)(2 * NO + 1) * G::OX + (long)(G::OY - 2 * NO - 1) * (2 * NO + 1);
 }
 
+// Profiling aid: -DSMG_FDT_DEBUG_SKIP builds skip the four contractions (the
+// memory pipeline and epilogue alone; tools/fd_diag.py).  Never in the default build.
+#ifdef SMG_FDT_DEBUG_SKIP
+constexpr bool kFdtSkip = true;
+#else
+constexpr bool kFdtSkip = false;
+#endif
+
 template <int P, int NO, int TX, int TY, bool DM>
 __global__ void __launch_bounds__(FDTK<P, NO, TX, TY, DM>::NT, FDTK<P, NO, TX, TY, DM>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
@@ -411,16 +402,14 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   double* SD = SN + (DM ? E : 0);  // 1/(lam_y + lam_x) table (K::SDV)
   uint64_t* barR = reinterpret_cast<uint64_t*>(SD + (K::SDV ? M * M : 0));
   uint64_t* barU = barR + NS;
-  // factor halves (K::SMF: shared-memory copies; else the parameter bank)
-  double* SF = reinterpret_cast<double*>(barU + NS + ((NS & 1) ? 1 : 0));
-  const double* FSye = K::SMF ? SF : A.Sye;
-  const double* FSyeT = K::SMF ? SF + HE * HE : A.SyeT;
-  const double* FSxe = K::SMF ? SF + 2 * HE * HE : A.Sxe;
-  const double* FSxeT = K::SMF ? SF + 3 * HE * HE : A.SxeT;
-  const double* FSyo = K::SMF ? SF + 4 * HE * HE : A.Syo;
-  const double* FSyoT = K::SMF ? SF + 4 * HE * HE + HO * HO : A.SyoT;
-  const double* FSxo = K::SMF ? SF + 4 * HE * HE + 2 * HO * HO : A.Sxo;
-  const double* FSxoT = K::SMF ? SF + 4 * HE * HE + 3 * HO * HO : A.SxoT;
+  const double* FSye = A.Sye;
+  const double* FSyeT = A.SyeT;
+  const double* FSxe = A.Sxe;
+  const double* FSxeT = A.SxeT;
+  const double* FSyo = A.Syo;
+  const double* FSyoT = A.SyoT;
+  const double* FSxo = A.Sxo;
+  const double* FSxoT = A.SxoT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g8 = lane >> 2, t4 = lane & 3;
   const int tid = threadIdx.x;
   const int N_x = A.N_x, N_y = A.N_y, ntx = A.ntx, nty = A.nty, ntiles = ntx * nty;
@@ -444,20 +433,6 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   if constexpr (DM) dm_build_frags<M, FDTArgs<M>, K::FE, K::FO, K::KTE, K::KTO>(A, FR, NT);
   if constexpr (K::SDV)
     for (int idx = tid; idx < M * M; idx += NT) SD[idx] = A.dinv[idx];
-  if constexpr (K::SMF) {
-    for (int idx = tid; idx < HE * HE; idx += NT) {
-      SF[idx] = A.Sye[idx];
-      SF[HE * HE + idx] = A.SyeT[idx];
-      SF[2 * HE * HE + idx] = A.Sxe[idx];
-      SF[3 * HE * HE + idx] = A.SxeT[idx];
-    }
-    for (int idx = tid; idx < HO * HO; idx += NT) {
-      SF[4 * HE * HE + idx] = A.Syo[idx];
-      SF[4 * HE * HE + HO * HO + idx] = A.SyoT[idx];
-      SF[4 * HE * HE + 2 * HO * HO + idx] = A.Sxo[idx];
-      SF[4 * HE * HE + 3 * HO * HO + idx] = A.SxoT[idx];
-    }
-  }
   __syncthreads();
 
   // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
@@ -510,7 +485,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 
     // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
     if constexpr (DM) {
-      if (!A.debug_skip) {
+      if (!kFdtSkip) {
         const double* R0 = buf + fdt_box_shift(X0, NO);
         double fe[K::FE], fo[K::FO];
         dm_load_frags<K::FE, K::FO>(FR, 0, lane, fe, fo);
@@ -557,7 +532,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           }
         }
       }
-    } else if (!A.debug_skip && act) {
+    } else if (!kFdtSkip && act) {
       const double* col = buf + fdt_box_shift(X0, NO) + (eyl * P) * BRX + exl * P + c;
       auto in = [&](int k) { return col[k * BRX]; };
       if (!odd) {
@@ -589,7 +564,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     }
     mark(9);
 
-    if (A.debug_skip) {
+    if (kFdtSkip) {
       for (int idx = tid; idx < (PP ? 2 : 1) * E * MM; idx += NT) EB[idx] = 0.0;
       __syncthreads();
     } else if constexpr (DM) {
@@ -901,15 +876,6 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 #endif
   if (tid == 0) bulk_wait0();
   cp_async_wait<0>();
-  if (A.fused_fixup) {
-    // cooperative launch: every tile's own block (TMA store, complete) and
-    // ring entries are written before any CTA applies the ring fixup
-    if (tid == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    cooperative_groups::this_grid().sync();
-    const long nb = fdt_fixup_per_tile<P, NO, TX, TY>() * ntiles;
-    for (long gid = (long)blockIdx.x * NT + tid; gid < nb; gid += (long)gridDim.x * NT)
-      fdt_fixup_node<P, NO, TX, TY>(A.u, A.ws, N_x, ntx, nty, gid);
-  }
 }
 
 // Ring fixup (second launch): an own node within n_o (+1) of its tile's edge
@@ -992,66 +958,13 @@ __global__ void __launch_bounds__(256) fdt_fixup(double* __restrict__ u, const d
   fdt_fixup_node<P, NO, TX, TY>(u, ws, N_x, ntx, nty, (long)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
-// Band fixup of the DMMA variant (smg_fdm.cuh), which writes every band node
-// of its region to the workspace: u = (((u + c_lo,lo) + c_hi,lo) + c_lo,hi) + c_hi,hi.
-template <int P, int NO, int TX, int TY>
-__global__ void __launch_bounds__(256) fdm_fixup(double* __restrict__ u, const double* __restrict__ ws, int N_x,
-                                                 int N_y, int ntx, int nty, int u_zero) {
-  SMG_PDL_ENTRY();
-  using G = FDTGeom<P, NO, TX, TY>;
-  constexpr int OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY, BW = G::BW;
-  constexpr size_t RS = (size_t)RX * RY;
-  constexpr int NXE = BW * (OY - BW), NYE = (OX - BW) * BW, NCO = BW * BW;
-  constexpr int PER = NXE + NYE + NCO;
-  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int ntiles = ntx * nty;
-  if (gid >= (long)ntiles * PER) return;
-  const int tile = (int)(gid / PER);
-  int k = (int)(gid - (long)tile * PER);
-  const int tx = tile % ntx, ty = tile / ntx;
-  const int txm = (tx + ntx - 1) % ntx, tym = (ty + nty - 1) % nty;
-  const int X0 = tx * OX, Y0 = ty * OY;
-  if (k < NXE) {
-    const int yy = BW + k / BW, d = k % BW - NO;
-    const double cl = ws[(size_t)(ty * ntx + txm) * RS + (size_t)yy * RX + (OX + NO + d)];
-    const double cr = ws[(size_t)(ty * ntx + tx) * RS + (size_t)yy * RX + (NO + d)];
-    double* up = u + (size_t)(Y0 - NO + yy) * N_x + wrapi(X0 + d, N_x);
-    *up = ((u_zero ? 0.0 : *up) + cl) + cr;
-    return;
-  }
-  k -= NXE;
-  if (k < NYE) {
-    const int d = k / (OX - BW) - NO, xx = BW + k % (OX - BW);
-    const double cb = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + d) * RX + xx];
-    const double ct = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + d) * RX + xx];
-    double* up = u + (size_t)wrapi(Y0 + d, N_y) * N_x + (X0 - NO + xx);
-    *up = ((u_zero ? 0.0 : *up) + cb) + ct;
-    return;
-  }
-  k -= NYE;
-  {
-    const int dy = k / BW - NO, dx = k % BW - NO;
-    const double c00 = ws[(size_t)(tym * ntx + txm) * RS + (size_t)(OY + NO + dy) * RX + (OX + NO + dx)];
-    const double c10 = ws[(size_t)(tym * ntx + tx) * RS + (size_t)(OY + NO + dy) * RX + (NO + dx)];
-    const double c01 = ws[(size_t)(ty * ntx + txm) * RS + (size_t)(NO + dy) * RX + (OX + NO + dx)];
-    const double c11 = ws[(size_t)(ty * ntx + tx) * RS + (size_t)(NO + dy) * RX + (NO + dx)];
-    double* up = u + (size_t)wrapi(Y0 + dy, N_y) * N_x + wrapi(X0 + dx, N_x);
-    *up = ((((u_zero ? 0.0 : *up) + c00) + c10) + c01) + c11;
-  }
-}
-
 struct FDTLaunch {
   const double* r;
   double* u;
   int u_zero;
   const double* inv_nu;
   const double* dinv;        // permuted (even/odd) 1/(lam_y + lam_x)
-  const double* dinv_dense;  // natural order (DMMA variant)
-  const double* Sx_dev;      // device factors (DMMA variant)
-  const double* Sy_dev;
-  const double* frag_dev;    // lane-ordered DMMA fragments (fdm_fragments)
   double* ws;
-  unsigned int* ctr;
   int N_x, N_y, n_x, ntx, nty;
   const double* Sye;   // host, HE*HE row-major [k][i]
   const double* Syo;   // host, HO*HO
@@ -1059,7 +972,6 @@ struct FDTLaunch {
   const double* Sxo;
   const double* wx;
   const double* wy;
-  int eo_dmma;         // 1: even/odd DMMA contraction stages
 };
 
 template <int P, int NO, int TX, int TY, bool DM>
@@ -1074,10 +986,6 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
     return SMG_EUNSUPPORTED;
   A.r = L.r; A.u = L.u; A.inv_nu = L.inv_nu; A.dinv = L.dinv; A.ws = L.ws;
   A.N_x = L.N_x; A.N_y = L.N_y; A.n_x = L.n_x; A.ntx = L.ntx; A.nty = L.nty;
-  {
-    const char* dbg = getenv("SMG_FD_DEBUG_SKIP");
-    A.debug_skip = (dbg && dbg[0] == '1') ? 1 : 0;
-  }
   A.u_zero = L.u_zero;
   A.phases = fdt_phase_buffer();
   // synthesis factors carry the weight of their output node: W (S t S^T) =
@@ -1094,7 +1002,7 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
       A.Sxo[k * HO + i] = L.Sxo[k * HO + i]; A.SxoT[i * HO + k] = L.Sxo[k * HO + i] * L.wx[k];
     }
   A.Syo[HO * HO] = A.SyoT[HO * HO] = A.Sxo[HO * HO] = A.SxoT[HO * HO] = 0.0;
-  static int grid_cap = 0;
+  static DeviceInt grid_cap;
   if (grid_cap == 0) {
     if (K::TSMEM > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fdt_kernel<P, NO, TX, TY, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1109,27 +1017,6 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
   }
   const int ntiles = L.ntx * L.nty;
   const int grid = ntiles < grid_cap ? ntiles : grid_cap;
-  // SMG_FDT_FUSED=1: one cooperative launch with the ring fixup after a grid
-  // barrier.  Measured slower on B200 at C2 (V-cycle 145.6 vs 135.2 us: the
-  // barrier and the lost PDL overlap cost more than the second launch), so
-  // the fixup stays a second (PDL) launch by default.
-  static const int fused = env_int("SMG_FDT_FUSED", 0);
-  A.fused_fixup = fused;
-  if (fused) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(K::NT);
-    cfg.dynamicSmemBytes = K::TSMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, fdt_kernel<P, NO, TX, TY, DM>, A);
-    if (e != cudaSuccess) return cuda_fail(e, "fdt_kernel (cooperative) launch");
-    return check_launch("fdt_kernel");
-  }
   launch(fdt_kernel<P, NO, TX, TY, DM>, dim3(grid), dim3(K::NT), K::TSMEM, st, A);
   int rc = check_launch("fdt_kernel");
   if (rc) return rc;
@@ -1139,16 +1026,10 @@ int fdt_launch_k(const FDTLaunch& L, cudaStream_t st) {
   return check_launch("fdt_fixup");
 }
 
-// Contraction engine per launch: DFMA stages, or the even/odd DMMA stages
-// (FDTLaunch::eo_dmma) -- same pipeline, epilogue and results to rounding.
-template <int P, int NO, int TX, int TY>
-int fdt_launch(const FDTLaunch& L, cudaStream_t st) {
-  return L.eo_dmma ? fdt_launch_k<P, NO, TX, TY, true>(L, st) : fdt_launch_k<P, NO, TX, TY, false>(L, st);
-}
-
 using FDTLaunchFn = int (*)(const FDTLaunch&, cudaStream_t);
 // Tiled kernel for (p, n_o) on an n_x x n_y mesh, or nullptr; sets TX, TY.
-// dmma selects the FP64 tensor-core variant (smg_fdm.cuh) of the same tiling.
+// dmma selects the even/odd FP64 tensor-core (DMMA) contraction engine of the
+// same kernel where it is compiled (m >= 27), else the DFMA engine.
 FDTLaunchFn fdt_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY, bool dmma);
 
 }  // namespace smg

@@ -276,7 +276,7 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
       C.twy[2 * k + 1] = k < ny / 2 ? std::sin(2.0 * pi * k / ny) : 0.0;
     }
     const size_t smem = sizeof(double2) * 2 * (size_t)(nx + 1) * ny + sizeof(double) * (nx + ny);
-    static bool attr = false;
+    static DeviceFlag attr;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(fft_pinv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(double2) * 2 * 65 * 64 + sizeof(double) * 128));

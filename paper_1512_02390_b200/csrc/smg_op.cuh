@@ -458,7 +458,7 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
   A.tiles_x = L.n_x / TX;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   A.bulk = (A.N_x % 2 == 0) && al16(L.u) && (!DIFF || al16(L.nu)) ? 1 : 0;
-  static bool attr = false;
+  static DeviceFlag attr;
   if (!attr) {
     {  // always: static shared memory adds to the dynamic size
       cudaError_t e = cudaFuncSetAttribute(op_kernel<P, TX, TY, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,

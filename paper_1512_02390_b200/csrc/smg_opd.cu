@@ -440,7 +440,7 @@ static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) 
   op_fill_consts<P>(A, L, DIFF);
   A.tiles_x = L.n_x;
   A.bulk = 1;
-  static bool attr = false;
+  static DeviceFlag attr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(opd_kernel<P, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "opd_kernel smem attribute");
@@ -455,8 +455,14 @@ static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) 
 bool opd_applies(int p, bool diffusion) { return diffusion ? p == 24 : p == 32; }
 
 // 1 = not applicable (caller uses op_kernel / opw_kernel)
+// SMG_OPD=0 disables the tensor-core operator path (read once).
+static bool opd_enabled() {
+  static const bool on = env_int("SMG_OPD", 1) != 0;
+  return on;
+}
+
 int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
-  if (!opd_applies(L.p, L.diffusion != 0) || L.partials != nullptr || frag == nullptr || env_int("SMG_OPD", 1) == 0)
+  if (!opd_applies(L.p, L.diffusion != 0) || L.partials != nullptr || frag == nullptr || !opd_enabled())
     return 1;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if ((L.n_x * L.p) % 2 != 0 || !al16(L.u) || (L.diffusion && !al16(L.nu))) return 1;

@@ -190,7 +190,7 @@ int opw_launch_t(const OpLaunch& L, cudaStream_t st) {
     A.Lo[H * H] = 0.0;
   }
   for (int i = 0; i < P; ++i) A.wasm[i] = L.wasm[i];
-  static bool attr = false;
+  static DeviceFlag attr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(opw_kernel<P, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G::SMEM);

@@ -220,7 +220,7 @@ int rr_launch_t(const RRLaunch& L, cudaStream_t st) {
   R.fc = L.fc;
   R.tiles_x = L.op.n_x / T;
   for (int i = 0; i < (PF + 1) * (PC + 1); ++i) R.J[i] = L.J[i];
-  static bool attr = false;
+  static DeviceFlag attr;
   if (!attr) {
     {  // always: static shared memory adds to the dynamic size
       cudaError_t e = cudaFuncSetAttribute(rr_kernel<PC, PF, T, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -231,13 +231,13 @@ int tr_launch_t(const TrArgs& A0, bool prolong, cudaStream_t st) {
   }
   const int grid = (A.n_x / T) * (A.n_y / T);
   if (prolong) {
-    static bool attr = false;
+    static DeviceFlag attr;
     if (!attr && G::SMEM_P > 48 * 1024)
       cudaFuncSetAttribute(prolong_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_P);
     attr = true;
     launch(prolong_kernel<PC, PF, T>, dim3(grid), dim3(G::NT), G::SMEM_P, st, A);
   } else {
-    static bool attr = false;
+    static DeviceFlag attr;
     if (!attr && G::SMEM_R > 48 * 1024)
       cudaFuncSetAttribute(restrict_kernel<PC, PF, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_R);
     attr = true;

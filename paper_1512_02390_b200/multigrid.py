@@ -22,7 +22,6 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -137,52 +136,6 @@ class MultigridHierarchy:
         self._cg_ws = None
         self._n0 = n0
         self.reduce_ws = torch.zeros(N.lib().smg_reduce_ws_doubles(), dtype=torch.float64, device="cuda")
-        self._tail = None          # V-cycle tail handle (levels 1..tail_levels + coarse, one launch)
-        self.tail_levels = 0
-        self._tail_checked = False
-
-    def _setup_tail(self):
-        """Fuse the small bottom levels of the V-cycle into one cooperative
-        launch (smg_vtail_*): Poisson + pinv coarse, levels 1..K with
-        n_pre = 1, n_post = 0, orders p_l = 2^l <= 8 with one overlap layer, N_l <= SMG_VTAIL_MAXDOF
-        (default 2^18), coarse mesh <= 64^2, K below the top level.
-        Opt-in (SMG_VTAIL=1): measured on B200 at C2 it is not yet faster
-        than the per-kernel path (82 vs 75 us for levels p <= 8 + coarse;
-        DESIGN.md section 3.3), so the per-kernel path stays the default."""
-        self._tail_checked = True
-        if os.environ.get("SMG_VTAIL", "0") != "1" or self.coarse != "pinv" or self.depth < 2:
-            return
-        if not isinstance(self.levels[0].op, PoissonOperator):
-            return
-        if self.mesh.n_x > 64 or self.mesh.n_y > 64:
-            return
-        maxdof = int(os.environ.get("SMG_VTAIL_MAXDOF", str(1 << 18)))
-        K = 0
-        for l in range(1, self.depth):
-            lv = self.levels[l]
-            p = lv.basis.p
-            if (lv.n_pre != 1 or lv.n_post != 0 or p != (1 << l) or p > 8 or lv.n_o != 1
-                    or not isinstance(lv.smoother, AdditiveSchwarz) or lv.smoother._inv_nu is not None
-                    or lv.op.layout.size > maxdof):
-                break
-            K = l
-        if K == 0:
-            return
-        lib = N.lib()
-        n = K + 1
-        ops = (C.c_void_p * n)(*[self.levels[l].op._handle.raw.value for l in range(n)])
-        sms = (C.c_void_p * n)(None, *[self.levels[l].smoother._h.raw.value for l in range(1, n)])
-        trs = (C.c_void_p * n)(None, *[self.levels[l].transfer.handle.raw.value for l in range(1, n)])
-        fs = (C.c_void_p * n)(*[self.levels[l].f.data_ptr() for l in range(n)])
-        us = (C.c_void_p * n)(*[self.levels[l].u.data_ptr() for l in range(n)])
-        raw = C.c_void_p()
-        rc = lib.smg_vtail_create(C.byref(raw), K, ops, sms, trs, self._pinv.handle.raw, fs, us)
-        if rc == N.SMG_EUNSUPPORTED:
-            log.info("V-cycle tail unavailable: %s", lib.smg_last_error().decode())
-            return
-        N.check(rc, "vtail_create")
-        self._tail = N.Handle(raw, "smg_vtail_destroy")
-        self.tail_levels = K
 
     def reset_smoothers(self):
         if self.sweep_counter is not None:
@@ -322,10 +275,7 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
     L = h.depth
     top = h.top
     top.u, top.f = u, f
-    if not h._tail_checked:
-        h._setup_tail()
-    K = h.tail_levels if h._tail is not None else 0
-    for l in range(L, K, -1):
+    for l in range(L, 0, -1):
         lv = h.levels[l]
         zero = u_zero if l == L else True
         if zero and not lv.n_pre:
@@ -337,7 +287,8 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
                 lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_pre)
             else:
                 N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                               N.ptr(lv.work), lv.n_pre, int(zero), st), "smooth")
+                                               N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_pre, int(zero), st),
+                        "smooth")
             zero = False
         fc = h.levels[l - 1].f
         if zero:
@@ -345,12 +296,8 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
         else:
             N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
                                               N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st), "residual_restrict")
-    if K:
-        # levels K..1 and the coarse solve in one cooperative launch; writes u_K
-        N.check(lib.smg_vtail_run(h._tail.raw, st), "vtail_run")
-    else:
-        _coarse_into(h, h.levels[0].f, h.levels[0].u)
-    for l in range(K + 1, L + 1):
+    _coarse_into(h, h.levels[0].f, h.levels[0].u)
+    for l in range(1, L + 1):
         lv = h.levels[l]
         N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
                 "prolongate")
@@ -359,7 +306,8 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
                 lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)
             else:
                 N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                               N.ptr(lv.work), lv.n_post, 0, st), "smooth")
+                                               N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_post, 0, st),
+                        "smooth")
     return u
 
 

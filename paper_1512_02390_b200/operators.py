@@ -53,6 +53,8 @@ class _DeviceOperator:
                 "op_create")
         self._handle = N.Handle(raw, "smg_op_destroy")
         self._norm_buf = None
+        # per-CTA norm partials (caller-owned scratch of smg_op_residual_norm2)
+        self.partials = torch.empty(max(1, int(lib.smg_op_ws_doubles(raw))), dtype=torch.float64, device="cuda")
 
     def apply(self, u) -> torch.Tensor:
         """A u as a new device field (operators.py:49-54 / 86-92)."""
@@ -69,7 +71,7 @@ class _DeviceOperator:
             N.check(lib.smg_op_residual(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.stream()), "residual")
         else:
             N.check(lib.smg_op_residual_norm2(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.ptr(norm2),
-                                              None, N.stream()), "residual")
+                                              N.ptr(self.partials), N.stream()), "residual")
         return out
 
 

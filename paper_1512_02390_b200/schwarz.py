@@ -271,6 +271,10 @@ class AdditiveSchwarz:
         self._h = _make_schwarz(layout.p, n_o, layout.n_x, layout.n_y, self.solver.S_x, self.solver.S_y,
                                 self.solver.lam_x, self.solver.lam_y, w1, self._inv_nu)
         self._work = None
+        # ring workspace of the tiled kernel (caller-owned scratch, include/smg.h);
+        # one per smoother: calls on one smoother are stream-ordered
+        self.ring = torch.empty(max(1, int(N.lib().smg_schwarz_ws_doubles(self._h.raw))), dtype=torch.float64,
+                                device="cuda")
 
     def _workspace(self):
         if self._work is None:
@@ -279,7 +283,8 @@ class AdditiveSchwarz:
 
     def correct(self, r, u):
         """u += sum_s R_s^T W A_s^-1 R_s r (/nu_bar), in place (device)."""
-        N.check(N.lib().smg_schwarz_correct(self._h.raw, N.ptr(r), N.ptr(u), N.stream()), "schwarz_correct")
+        N.check(N.lib().smg_schwarz_correct(self._h.raw, N.ptr(r), N.ptr(u), N.ptr(self.ring), N.stream()),
+                "schwarz_correct")
         return u
 
     def smooth(self, op, u, f, n_it: int, u_is_zero: bool = False):
@@ -288,7 +293,8 @@ class AdditiveSchwarz:
             raise TypeError("AdditiveSchwarz.smooth mutates u in place: pass a CUDA float64 tensor")
         f = _as_device(f)
         N.check(N.lib().smg_schwarz_smooth(self._h.raw, op._handle.raw, N.ptr(u), N.ptr(f),
-                                           N.ptr(self._workspace()), int(n_it), int(bool(u_is_zero)),
+                                           N.ptr(self._workspace()), N.ptr(self.ring), int(n_it),
+                                           int(bool(u_is_zero)),
                                            N.stream()), "schwarz_smooth")
         return u
 

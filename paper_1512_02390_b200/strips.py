@@ -438,8 +438,10 @@ class GpuEngine:
         from . import _native as N
         lv = self.h.levels[l]
         N.check(N.lib().smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(u), N.ptr(r),
-                                           N.ptr(self._work[l]), 1, 1 if zero else 0, N.stream())
-                if zero else N.lib().smg_schwarz_correct(lv.smoother._h.raw, N.ptr(r), N.ptr(u), N.stream()),
+                                           N.ptr(self._work[l]), N.ptr(lv.smoother.ring), 1, 1 if zero else 0,
+                                           N.stream())
+                if zero else N.lib().smg_schwarz_correct(lv.smoother._h.raw, N.ptr(r), N.ptr(u),
+                                                         N.ptr(lv.smoother.ring), N.stream()),
                 "strip correct")
 
     def restrict(self, l, fine, out):

@@ -37,7 +37,7 @@ for l in range(h.depth, 0, -1):
     lv.f.normal_()
     st = N.stream()
     t_res = timeit(lambda: N.check(lib.smg_op_residual(lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f), N.ptr(lv.work), st)))
-    t_fd = timeit(lambda: N.check(lib.smg_schwarz_correct(lv.smoother._h.raw, N.ptr(lv.work), N.ptr(lv.u), st)))
+    t_fd = timeit(lambda: N.check(lib.smg_schwarz_correct(lv.smoother._h.raw, N.ptr(lv.work), N.ptr(lv.u), N.ptr(lv.smoother.ring), st)))
     fc = h.levels[l - 1].f
     t_rs = timeit(lambda: N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.work), N.ptr(fc), st)))
     uc = h.levels[l - 1].u
