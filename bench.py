@@ -11,9 +11,17 @@ work: the top level applies A to a nonzero u).
 
 Timing: CUDA events on the launching stream around each step, L2 flushed
 (256 MiB write) before every timed step, K steps bracketed by barrier +
-synchronize, max over ranks.  N > 1: one process per GPU, weak scaling: each
-rank owns a C2-sized element-row strip (paper_1512_02390_b200/strips.py) of a
-64 x 64N-element mesh, NCCL halo exchanges and a replicated coarse solve.
+synchronize, max over ranks.  N > 1 (torchrun, one process per GPU): BASELINE
+configs[2] (C3: 128x128 elements, p = 32, 16.8M DOF) STRONG-scaled over
+element-row strips (paper_1512_02390_b200/strips.py: 128/N element rows per
+rank, NCCL halo send/recv on device buffers, device-side dot products
+all-reduced by NCCL, replicated coarse solve), plus one C4 MGCG solve; the
+N = 1 line carries the single-GPU C3 V-cycle as the strong-scaling reference.
+
+--impl reference times the UNMODIFIED reference package (pip-installed into
+baseline/_ref from /root/reference, pure Python + NumPy/OpenBLAS on every host
+core) through its own v_cycle on the same C2 workload; if baseline/_ref is
+missing it falls back to the numpy restatement in oracle/ and says so.
 """
 
 from __future__ import annotations
@@ -33,6 +41,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(n_x=64, n_y=64, l_x=1.0, l_y=1.0, p=16, rule="fixed:1", seed=0)
+C3 = dict(n_x=128, n_y=128, l_x=1.0, l_y=1.0, p=32, rule="fixed:1", seed=0)
+C4 = dict(n_x=256, n_y=256, l_x=8.0, l_y=1.0, p=16, rule="fixed:1", seed=0)
+# one workload string for both arms (the driver compares the config of the two lines)
+WORKLOAD_C2 = ("C2: periodic Poisson [0,1]^2, 64x64 elements, p=16 (1,048,576 DOF), stand-alone V-cycle "
+               "(1 pre-, 0 post-smoothing), w5, fixed:1")
+WORKLOAD_C3 = ("C3: periodic Poisson [0,1]^2, 128x128 elements, p=32 (16,777,216 DOF), V-cycle (1,0), w5, "
+               "fixed:1, element-row strips")
 METRIC = "weighted-Schwarz smoother + V-cycle DOF/s, fraction of FP64/HBM roofline"
 FP64_PEAK_TFLOPS = 37.15   # measured: DMMA m8n8k4 on this pool's B200 (tools/peaks, profiles/fp64_peaks.txt)
 FP64_DFMA_TFLOPS = 34.2    # measured: DFMA register-operand peak
@@ -186,69 +201,107 @@ def oracle_problem():
     return O, h, f
 
 
+def reference_problem():
+    """The unmodified reference (baseline/_ref, pip-installed from
+    /root/reference) on the C2 workload, or None when it is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "schwarzmg")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from schwarzmg import mesh, multigrid, operators
+    except Exception:
+        return None
+    c = CFG
+    msh = mesh.MeshConfig(c["n_x"], c["n_y"], c["l_x"], c["l_y"])
+    h = multigrid.build_hierarchy(msh, c["p"], multigrid.OverlapRule.parse(c["rule"]))
+    N = (c["p"] * c["n_y"], c["p"] * c["n_x"])
+    f = operators.project_mean(np.random.default_rng(c["seed"]).standard_normal(N))
+    return multigrid.v_cycle, h, f
+
+
 def time_cpu_vcycles(budget_s: float, max_steps: int | None = None, warmup: int = 0):
-    """The oracle port (numpy restatement of the reference, all host threads)."""
-    O, h, f = oracle_problem()
+    """The reference's own v_cycle (multigrid.py:231-251) from baseline/_ref on
+    all host threads; the oracle port if the reference is not installed.
+    Returns (per-step seconds, DOF, kind)."""
+    rp = reference_problem()
+    if rp is not None:
+        vcyc, h, f = rp
+        kind = "reference"
+    else:
+        O, h, f = oracle_problem()
+        vcyc = O.v_cycle
+        kind = "port"
     u = np.zeros_like(f)
     for _ in range(warmup):
-        u = O.v_cycle(h, u, f)
+        u = vcyc(h, u, f)
     times = []
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        u = O.v_cycle(h, u, f)
+        u = vcyc(h, u, f)
         times.append(time.perf_counter() - t0)
         if max_steps is not None and len(times) >= max_steps:
             break
         if max_steps is None and time.perf_counter() - t_start > budget_s:
             break
-    return times, f.size
+    return times, f.size, kind
+
+
+def _cpu_sample(kind, n):
+    if kind == "reference":
+        return (f"{n} C2 V-cycles of the unmodified reference (schwarzmg.multigrid.v_cycle from baseline/_ref, "
+                "coarse plain CG as the reference does), NumPy/OpenBLAS on every host core")
+    return (f"{n} C2 V-cycles of the numpy restatement (oracle/smg_oracle.py; baseline/_ref not installed)")
 
 
 def run_reference(args):
-    times, ndof = time_cpu_vcycles(0.0, max_steps=args.steps, warmup=args.warmup)
+    times, ndof, kind = time_cpu_vcycles(0.0, max_steps=args.steps, warmup=min(args.warmup, 3))
     t = float(np.sum(times))
     value = ndof * len(times) / t
     cores = cpu_threads()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": args.gpus,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1), mean removed)",
-            "config": {"workload": "C2: periodic Poisson 64x64 elements, p=16 (1,048,576 DOF), stand-alone "
-                                   "V-cycle (1,0), w5, fixed:1", "parallelism": "cpu"},
-            "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
-                             "sample": f"{len(times)} V-cycles of the numpy restatement (oracle/smg_oracle.py) "
-                                       f"of the reference on the C2 workload"},
+            "data": "synthetic (seeded N(0,1) RHS, mean removed)",
+            "config": {"workload": WORKLOAD_C2, "coarse": "plain CG to 1e-12 (the reference's)",
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": kind,
+                             "sample": _cpu_sample(kind, len(times))},
             "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def _strip_setup(cfg, world, rank, dev):
+    import torch
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, TorchTransport
+    plan = StripPlan(cfg["n_x"], cfg["n_y"], cfg["l_x"], cfg["l_y"], world, rank)
+    eng = GpuEngine(plan, cfg["p"], P.OverlapRule.parse(cfg["rule"]))
+    sol = StripSolver(plan, eng, TorchTransport(plan))
+    p = cfg["p"]
+    N = (p * cfg["n_y"], p * cfg["n_x"])
+    f_host = P.project_mean(np.random.default_rng(cfg["seed"]).standard_normal(N))
+    rows = plan.global_rows(p)
+    f = torch.from_numpy(f_host[rows].copy()).to(dev)
+    return plan, sol, f, f_host, rows, N
+
+
 def run_strips(args, world, rank, local, dev):
-    """N > 1: weak scaling over element-row strips (strips.py): every rank owns
-    a C2-sized 64 x 64-element, p=16 strip of a 64 x (64 N)-element periodic
-    mesh ([0,1] x [0,N], square elements as in C2); halos by NCCL send/recv,
-    replicated global coarse solve (all-gather + pseudo-inverse)."""
+    """N > 1: BASELINE configs[2] (C3, 128x128 elements, p = 32) STRONG-scaled
+    over element-row strips (strips.py): 128/N element rows per rank, one ghost
+    element row each side, NCCL halo send/recv on device buffers, replicated
+    coarse pseudo-inverse.  A step is one V-cycle of the MG iteration.  Then
+    one C4 MGCG solve on the same ranks (device dots all-reduced by NCCL)."""
     import torch
     import torch.distributed as dist
-    import paper_1512_02390_b200 as P
     from paper_1512_02390_b200 import _native as NV
-    from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, TorchTransport
 
     lib = NV.lib()
-    c = dict(CFG)
-    c["n_y"] *= world
-    c["l_y"] *= world
-    plan = StripPlan(c["n_x"], c["n_y"], c["l_x"], c["l_y"], world, rank)
-    rule = P.OverlapRule.parse(c["rule"])
-    eng = GpuEngine(plan, c["p"], rule)
-    sol = StripSolver(plan, eng, TorchTransport(plan))
-    p = c["p"]
-    N = (p * c["n_y"], p * c["n_x"])
+    plan, sol, f, f_host, rows, N = _strip_setup(C3, world, rank, dev)
+    own = plan.own(C3["p"])
     ndof = N[0] * N[1]
-    f_host = P.project_mean(np.random.default_rng(c["seed"]).standard_normal(N))
-    rows = plan.global_rows(p)
-    own = plan.own(p)
-    f = torch.from_numpy(f_host[rows].copy()).to(dev)
     u = torch.zeros_like(f)
     sol.v_cycle(u, f)
     torch.cuda.synchronize()
@@ -279,7 +332,7 @@ def run_strips(args, world, rank, local, dev):
     tt = torch.tensor([t_steps], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_steps = float(tt.item())
-    # end to end: own rows of f from pinned host, own rows of u back
+    # end to end: the rank's rows of f from pinned host, its owned rows of u back
     f_pin = torch.from_numpy(f_host[rows].copy()).pin_memory()
     u_pin = torch.empty(f.shape, dtype=torch.float64).pin_memory()
     dist.barrier()
@@ -296,23 +349,81 @@ def run_strips(args, world, rank, local, dev):
     tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_e2e = float(tt.item())
+    # C4 MGCG on the same ranks (time to solution, max over ranks)
+    c4 = None
+    if not args.no_c4:
+        plan4, sol4, f4, _, _, N4 = _strip_setup(C4, world, rank, dev)
+        sol4.solve_mgcg(f4.clone(), torch.zeros_like(f4), max_cycles=2)   # warm-up (handles, attributes)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep = sol4.solve_mgcg(f4.clone(), torch.zeros_like(f4))
+        torch.cuda.synchronize()
+        tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        c4 = {"workload": "C4: [0,8]x[0,1], 256x256 elements (AR 8), p=16 (16,777,216 DOF), MGCG to 1e10",
+              "cycles": rep.cycles, "converged": rep.converged, "breakdown": rep.breakdown,
+              "rbar": rep.rbar, "time_to_solution_s": float(tt.item()),
+              "dof_cycles_per_s": N4[0] * N4[1] * rep.cycles / float(tt.item()),
+              "timing": "host wall clock around solve_mgcg (one sync per cycle for the convergence test), "
+                        "max over ranks"}
     if rank == 0:
         own_bytes = 8 * (own.stop - own.start) * N[1]
         line = {"metric": METRIC, "value": ndof * args.steps / t_steps, "unit": "DOF/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_steps / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded N(0,1) RHS, mean removed)",
-                "config": {"workload": f"C2 per GPU: periodic Poisson [0,1]x[0,{world}], 64x{64 * world} elements, "
-                                       f"p=16 ({ndof:,} DOF), stand-alone V-cycle (1,0), w5, fixed:1, "
-                                       "coarse p=1 pseudo-inverse",
+                "config": {"workload": WORKLOAD_C3, "coarse": "p=1 pseudo-inverse, replicated",
                            "global_dofs": ndof, "parallelism": f"{world} element-row strips "
-                           f"({plan.s} rows + 2x{2} ghost rows each), NCCL halo send/recv, replicated coarse",
-                           "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": False},
+                           f"({plan.s} rows + 1 ghost row each side), NCCL halo send/recv, NCCL all-gather + "
+                           "replicated coarse solve",
+                           "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": False,
+                           "strong_scaling_reference": "the N=1 line's c3_single_gpu"},
                 "e2e": {"value": ndof * args.steps / t_e2e, "unit": "DOF/s",
                         "h2d_bytes_per_step": 8 * f.numel() * world, "d2h_bytes_per_step": own_bytes * world},
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+        if c4 is not None:
+            line["c4_mgcg"] = c4
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def c3_single_gpu(args, dev, flush):
+    """Strong-scaling reference for the N > 1 lines: the C3 V-cycle on one GPU
+    (graph replay of the public path, L2 flushed before each step)."""
+    import torch
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200.multigrid import _v_cycle
+    c = C3
+    h = P.build_hierarchy(P.MeshConfig(c["n_x"], c["n_y"], c["l_x"], c["l_y"]), c["p"], P.OverlapRule.parse(c["rule"]))
+    shape = h.top.op.layout.shape
+    f = torch.from_numpy(P.project_mean(np.random.default_rng(c["seed"]).standard_normal(shape))).to(dev)
+    u = torch.zeros_like(f)
+    _v_cycle(h, u, f)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        _v_cycle(h, u, f)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        _v_cycle(h, u, f)
+    for _ in range(3):
+        g.replay()
+    evs = []
+    n = max(5, min(args.steps, 20))
+    for _ in range(n):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    t = float(sum(a.elapsed_time(b) for a, b in evs)) / 1e3 / n
+    del g
+    return {"workload": WORKLOAD_C3.replace(", element-row strips", ", one GPU"), "value": shape[0] * shape[1] / t,
+            "unit": "DOF/s", "ms_per_step": 1e3 * t, "steps": n}
 
 
 def main():
@@ -324,6 +435,7 @@ def main():
     ap.add_argument("--no-micro", action="store_true", help="skip the smoother microbenchmark")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-c4", action="store_true", help="N > 1: skip the C4 MGCG solve")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -339,6 +451,7 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver counts ranks / sees NVLS in the log
         ngpu = torch.cuda.device_count()
         local = local % max(ngpu, 1)
         torch.cuda.set_device(local)
@@ -619,22 +732,65 @@ def main():
                     "tflops_dense_equiv": msh.n_el * fd_flops_per_element(mm) / tt / 1e12}
                 del sm2, rr, uu
 
+    # ---- the same V-cycle with the reference's own coarse solver (plain CG to
+    # 1e-12 on the device, coarse="cg"; not graph-capturable: it tests
+    # convergence on the host every 32 iterations) -- the like-for-like
+    # companion of the reference arm, whose V-cycle runs that CG on the CPU
+    hcg = P.build_hierarchy(mesh, c["p"], rule, coarse="cg")
+    ucg = torch.zeros_like(u)
+    _v_cycle(hcg, ucg, f)
+    evs = []
+    for _ in range(max(5, min(args.steps, 20))):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _v_cycle(hcg, ucg, f)
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    t_cg = float(np.mean([a.elapsed_time(b) for a, b in evs])) / 1e3
+    vc_cg = {"value": ndof / t_cg, "unit": "DOF/s", "ms_per_step": 1e3 * t_cg,
+             "coarse": "plain CG to 1e-12 on the device (the reference's coarse solver)",
+             "coarse_iterations": hcg.coarse_iterations[-1] if hcg.coarse_iterations else None,
+             "timing": "eager launches, CUDA events, L2 flushed before each step"}
+    del hcg, ucg
+
+    # ---- solve-level end to end through the public API: solve(h, f_host, cfg,
+    # u0) with numpy f (H2D inside), MG to 1e10 (13 cycles), u read back to the
+    # host; value = DOF x V-cycles / wall time
+    sols = []
+    for k in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        us_, rep = P.solve(h, f_host, P.SolveConfig(solver="mg"), u0=np.zeros_like(f_host))
+        u_host = us_.cpu().numpy()
+        t1 = time.perf_counter() - t0
+        if k:
+            sols.append((t1, rep.cycles))
+    t_sol = float(np.median([t for t, _ in sols]))
+    e2e_solve = {"value": ndof * sols[-1][1] / t_sol, "unit": "DOF/s", "cycles": sols[-1][1],
+                 "time_to_solution_ms": 1e3 * t_sol, "converged": bool(rep.converged),
+                 "h2d_bytes": 8 * ndof * 2, "d2h_bytes": 8 * ndof,
+                 "path": "solve(h, f_host (numpy), SolveConfig('mg'), u0=zeros (numpy)) -> u.cpu(); host wall "
+                         "clock, median of 3 after one warm-up; one host sync per cycle (convergence test)"}
+    assert np.isfinite(u_host).all()
+
+    c3 = c3_single_gpu(args, dev, flush)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        times, _ = time_cpu_vcycles(args.cpu_budget)
+        times, _, kind = time_cpu_vcycles(args.cpu_budget)
         tc = float(np.sum(times))
-        cpu = {"value": ndof * len(times) / tc, "unit": "DOF/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"{len(times)} C2 V-cycles of the numpy restatement of the reference "
-                         "(oracle/smg_oracle.py), OpenBLAS threads = cores"}
+        cpu = {"value": ndof * len(times) / tc, "unit": "DOF/s", "cores": cpu_threads(), "kind": kind,
+               "sample": _cpu_sample(kind, len(times))}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded N(0,1) RHS, mean removed)",
-                "config": {"workload": "C2: periodic Poisson [0,1]^2, 64x64 elements, p=16 (1,048,576 DOF), "
-                                       "stand-alone V-cycle (1 pre-, 0 post-smoothing), w5, fixed:1, "
-                                       "coarse p=1 pseudo-inverse",
+                "config": {"workload": WORKLOAD_C2, "coarse": "p=1 pseudo-inverse (exact; vcycle_coarse_cg: "
+                                                              "the reference's CG)",
                            "global_dofs": ndof * world, "levels": orders,
                            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
                            "l2": "flushed (256 MiB write) before every timed step",
@@ -643,7 +799,8 @@ def main():
                                     "frac": t_roof_vc / (ms_per_step / 1e3),
                                     "model": "SURVEY.md §8(d) sum of max(F/P64, B/BW) over levels, "
                                              f"P64={FP64_PEAK_TFLOPS} TF, BW={bw} GB/s ({bw_src}), coarse excluded"},
-                "roofline": roofline, "top_level_kernels": kern, "e2e": e2e,
+                "roofline": roofline, "top_level_kernels": kern, "e2e": e2e, "e2e_solve": e2e_solve,
+                "vcycle_coarse_cg": vc_cg, "c3_single_gpu": c3,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks, "wall_s_timed_region": t_wall}
         if cpu is not None:

@@ -109,6 +109,15 @@ int smg_transfer_destroy(smg_transfer_t* h);
 /* uf = P uc (accumulate=0) or uf += P uc (accumulate=1). */
 int smg_prolongate(const smg_transfer_t* h, const double* uc, double* uf, int accumulate,
                    void* stream);
+/* The ascending half of a V-cycle without post-smoothing (multigrid.py:
+ * 247-248, n_post = 0) in ONE launch: for l = 1..K, u_l += P_l u_{l-1},
+ * u_0 = the coarse solution.  tr[l-1] is the p = 2^(l-1) -> 2^l transfer of
+ * level l, u[l-1] its field (K <= 4, p_K <= 16).  Only u[K-1] (level K) is
+ * written -- bitwise what K smg_prolongate(..., accumulate=1) calls leave
+ * there; the intermediate fields are read, not updated.  SMG_EUNSUPPORTED
+ * for other chains (the caller then prolongates level by level). */
+int smg_prolongate_chain(const smg_transfer_t* const* tr, int K, const double* u0, double* const* u,
+                         void* stream);
 /* fc = P^T ff (P's rows are assigned, not summed: owner-computes). */
 int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* stream);
 /* fc = P^T (f - A u): residual fused with restriction (multigrid.py:244). */
@@ -180,6 +189,10 @@ int smg_cg_update2(double* u, const double* r_in, double* r_out, const double* p
  * be NULL = zeros), s2 = z.r; scal[5] = s1 / scal[0] (beta); scal[0] = s2. */
 int smg_cg_beta(const double* z, const double* r, const double* r_old, int64_t n, double* scal,
                 double* ws, void* stream);
+/* The same bookkeeping from sums already reduced across ranks (strip-
+ * parallel MGCG: smg_dot2 on each rank's owned rows into scal[3..4], an
+ * all-reduce, then this): scal[5] = scal[3] / scal[0]; scal[0] = scal[4]. */
+int smg_cg_beta_finish(double* scal, void* stream);
 /* p = z + scal[5] p  (krylov.py:109) */
 int smg_cg_direction(double* p, const double* z, int64_t n, double* scal, void* stream);
 /* f -= mean(f) (operators.py:138-140) */

@@ -48,6 +48,7 @@ SIGNATURES = {
     "smg_transfer_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_int, _hp]),
     "smg_transfer_destroy": (C.c_int, [_vp]),
     "smg_prolongate": (C.c_int, [_vp, _dp, _dp, C.c_int, _vp]),
+    "smg_prolongate_chain": (C.c_int, [C.POINTER(_vp), C.c_int, _dp, C.POINTER(_vp), _vp]),
     "smg_restrict": (C.c_int, [_vp, _dp, _dp, _vp]),
     "smg_residual_restrict": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _vp]),
     "smg_coarse_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double]),
@@ -68,6 +69,7 @@ SIGNATURES = {
     "smg_cg_update": (C.c_int, [_dp, _dp, _dp, _dp, _i64, _dp, _dp, _dp, _vp]),
     "smg_cg_update2": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _i64, _dp, _dp, _dp, _vp]),
     "smg_cg_beta": (C.c_int, [_dp, _dp, _dp, _i64, _dp, _dp, _vp]),
+    "smg_cg_beta_finish": (C.c_int, [_dp, _vp]),
     "smg_cg_direction": (C.c_int, [_dp, _dp, _i64, _dp, _vp]),
     "smg_project_mean": (C.c_int, [_dp, _i64, _dp, _vp]),
     "smg_sum": (C.c_int, [_dp, _i64, _dp, _dp, _vp]),

@@ -125,6 +125,11 @@ struct smg_coarse {
   double* fft = nullptr;   // FFT path table (smg_fft.cu fft_table), power-of-two meshes
 };
 
+namespace smg {
+int prolong_chain_run(int K, int n_x, int n_y, const double* const* J, const double* u0, double* const* u,
+                      cudaStream_t st);
+}
+
 namespace {
 
 // tools/time_fd1.py on B200 (us, DFMA vs even/odd DMMA): 256^2 p=16 230 / 286,
@@ -509,6 +514,26 @@ static int tr_run(const smg_transfer_t* h, const double* src, double* dst, int a
 int smg_prolongate(const smg_transfer_t* h, const double* uc, double* uf, int accumulate, void* stream) {
   if (!h || !uc || !uf) { set_error("smg_prolongate: bad argument"); return SMG_EINVAL; }
   return tr_run(h, uc, uf, accumulate, true, as_stream(stream));
+}
+
+int smg_prolongate_chain(const smg_transfer_t* const* tr, int K, const double* u0, double* const* u,
+                         void* stream) {
+  if (!tr || !u0 || !u || K < 1) { set_error("smg_prolongate_chain: bad argument"); return SMG_EINVAL; }
+  if (K > 4) { set_error("smg_prolongate_chain: chains up to p = 16"); return SMG_EUNSUPPORTED; }
+  const double* J[5] = {nullptr};
+  double* uu[5] = {nullptr};
+  for (int l = 1; l <= K; ++l) {
+    const smg_transfer_t* t = tr[l - 1];
+    if (!t || !u[l - 1] || t->pc != (1 << (l - 1)) || t->pf != (1 << l) || t->n_x != tr[0]->n_x ||
+        t->n_y != tr[0]->n_y) {
+      set_error("smg_prolongate_chain: level %d is not the p = %d -> %d transfer of one mesh", l, 1 << (l - 1),
+                1 << l);
+      return SMG_EUNSUPPORTED;
+    }
+    J[l] = t->J.data();
+    uu[l] = u[l - 1];
+  }
+  return prolong_chain_run(K, tr[0]->n_x, tr[0]->n_y, J, u0, uu, as_stream(stream));
 }
 
 int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* stream) {

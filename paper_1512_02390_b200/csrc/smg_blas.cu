@@ -150,6 +150,16 @@ __global__ void cg_direction_kernel(double* __restrict__ p, const double* __rest
     p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
 
+// Polak-Ribiere bookkeeping from all-reduced dot2 sums (strip-parallel MGCG):
+// scal[5] = scal[3] / scal[0] (beta), scal[0] = scal[4] (delta).
+__global__ void cg_beta_finish_kernel(double* scal) {
+  SMG_PDL_ENTRY();
+  if (threadIdx.x == 0) {
+    scal[5] = scal[3] / scal[0];
+    scal[0] = scal[4];
+  }
+}
+
 __global__ void axpby_kernel(double a, const double* __restrict__ x, double b, double* __restrict__ y, int64_t n) {
   SMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -732,6 +742,12 @@ int smg_cg_update2(double* u, const double* r_in, double* r_out, const double* p
 int smg_cg_update(double* u, double* r, const double* p, const double* q, int64_t n, double* scal,
                   int* flag, double* ws, void* stream) {
   return smg_cg_update2(u, r, r, p, q, n, scal, flag, ws, stream);
+}
+
+int smg_cg_beta_finish(double* scal, void* stream) {
+  if (!scal) { set_error("smg_cg_beta_finish: bad argument"); return SMG_EINVAL; }
+  launch(cg_beta_finish_kernel, dim3(1), dim3(32), 0, as_stream(stream), scal);
+  return check_launch("cg_beta_finish_kernel");
 }
 
 int smg_cg_direction(double* p, const double* z, int64_t n, double* scal, void* stream) {

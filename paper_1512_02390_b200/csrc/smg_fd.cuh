@@ -9,6 +9,11 @@
 // in one launch.  Elements of one colour have disjoint windows, so the
 // scatter-add is a plain read-modify-write: deterministic, no atomics.
 //
+// This is the fallback / blocks-mode path (FastDiagSolver.solve, factors that
+// are not even/odd, TMA-incompatible fields); the tiled kernel (smg_fdt.cuh)
+// is the production sweep.  Its outer contraction loops are only partially
+// unrolled (compiled for every window size m = 2..41, code size matters more).
+//
 // Work mapping: a CTA owns E elements; their m x m residual windows are
 // staged in shared memory.  The four contractions alternate between
 // "column" threads (thread = (element, column)) and "row" threads; every
@@ -84,7 +89,7 @@ fd_kernel(const __grid_constant__ FDArgs<M> A) {
     double x = B[c];
 #pragma unroll
     for (int i = 0; i < M; ++i) acc[i] = A.Sy[i] * x;
-#pragma unroll
+#pragma unroll 2
     for (int k = 1; k < M; ++k) {
       x = B[k * M + c];
 #pragma unroll
@@ -100,7 +105,7 @@ fd_kernel(const __grid_constant__ FDArgs<M> A) {
     double x = B[c * M];
 #pragma unroll
     for (int l = 0; l < M; ++l) acc[l] = A.Sx[l] * x;
-#pragma unroll
+#pragma unroll 2
     for (int j = 1; j < M; ++j) {
       x = B[c * M + j];
 #pragma unroll
@@ -125,7 +130,7 @@ fd_kernel(const __grid_constant__ FDArgs<M> A) {
     double x[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) x[k] = B[k * M + c];
-#pragma unroll
+#pragma unroll 2
     for (int i = 0; i < M; ++i) {
       double a = A.Sy[i * M] * x[0];
 #pragma unroll
@@ -141,7 +146,7 @@ fd_kernel(const __grid_constant__ FDArgs<M> A) {
 #pragma unroll
     for (int l = 0; l < M; ++l) x[l] = B[c * M + l];
     const double wyc = A.apply_weight ? A.wy[c] : 1.0;
-#pragma unroll
+#pragma unroll 2
     for (int j = 0; j < M; ++j) {
       double a = A.Sx[j * M] * x[0];
 #pragma unroll

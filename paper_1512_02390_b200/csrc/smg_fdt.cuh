@@ -281,7 +281,7 @@ __device__ __forceinline__ void fdt_epilogue_fold(double* EB) {
 // FP64 tensor-core MMA, m8n8k4: lane (g = lane/4, t = lane%4) holds A[g][t],
 // B[t][g] and accumulates C[g][2t], C[g][2t+1].
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -296,10 +296,22 @@ struct FDTK {
   static constexpr int MTO = (HO + 7) / 8, KTO = (HO + 3) / 4;   // odd half
   static constexpr int FE = MTE * KTE, FO = MTO * KTO;
   static constexpr int FRN = DM ? 4 * (FE + FO) * 32 : 0;        // fragment table (doubles)
-  static constexpr int WARPS = 8;
-  static constexpr int NT = DM ? 32 * WARPS : G::THREADS;
   static constexpr int BT = (E * M + 7) / 8;                     // 8-line batches
-  static constexpr int MAXB = (BT + WARPS - 1) / WARPS;
+  // DMMA stages: each warp iteration carries DMB batches whose accumulator
+  // chains interleave (2 (MTE + MTO) independent DMMAs per k-step: the chains
+  // were latency-bound with one batch, ncu stall_wait); the warp count is the
+  // smallest that keeps the fewest iterations per warp (balanced batches)
+  static constexpr int DMB = 2;
+  static constexpr int dm_warps() {
+    int it_min = (BT + DMB * 12 - 1) / (DMB * 12);
+    for (int w = 4; w <= 12; ++w)
+      if ((BT + DMB * w - 1) / (DMB * w) == it_min) return w;
+    return 12;
+  }
+  static constexpr int WARPS = DM ? dm_warps() : 8;
+  static constexpr int NT = DM ? 32 * WARPS : G::THREADS;
+  static constexpr int DMIT = (BT + DMB * WARPS - 1) / (DMB * WARPS);   // iterations per warp
+  static constexpr int MAXB = DMB * DMIT;
   static constexpr size_t extra = sizeof(double) * ((size_t)FRN + (DM ? E : 0));
   static constexpr size_t HALF_SM = 112 * 1024, FULL_SM = 227 * 1024;
   static constexpr size_t sm1(int ns) { return G::smem_for(ns, 1) + extra; }
@@ -486,50 +498,69 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     // ---- stage 1 (physical columns c): [T1e; T1o][:, c] = [Se; So]^T fold_y(R_e[:, c])
     if constexpr (DM) {
       if (!kFdtSkip) {
+        constexpr int DMB = K::DMB;
         const double* R0 = buf + fdt_box_shift(X0, NO);
         double fe[K::FE], fo[K::FO];
         dm_load_frags<K::FE, K::FO>(FR, 0, lane, fe, fo);
-        for (int bt = warp; bt < K::BT; bt += K::WARPS) {
-          const int n = 8 * bt + g8;
-          const bool vn = n < E * M;
-          const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
-          const double* col = R0 + ((en / TX) * P) * BRX + (en % TX) * P + cn;
-          double ae[K::MTE][2], ao[K::MTO][2];
+        for (int b0 = DMB * warp; b0 < K::BT; b0 += DMB * K::WARPS) {
+          const double* col[DMB];
+          bool vn[DMB];
 #pragma unroll
-          for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+          for (int q = 0; q < DMB; ++q) {
+            const int n = 8 * (b0 + q) + g8;
+            vn[q] = n < E * M;
+            const int en = vn[q] ? n / M : 0, cn = vn[q] ? n - en * M : 0;
+            col[q] = R0 + ((en / TX) * P) * BRX + (en % TX) * P + cn;
+          }
+          double ae[DMB][K::MTE][2], ao[DMB][K::MTO][2];
 #pragma unroll
-          for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+          for (int q = 0; q < DMB; ++q) {
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m) ae[q][m][0] = ae[q][m][1] = 0.0;
+#pragma unroll
+            for (int m = 0; m < K::MTO; ++m) ao[q][m][0] = ao[q][m][1] = 0.0;
+          }
 #pragma unroll
           for (int kt = 0; kt < K::KTE; ++kt) {
             const int k = 4 * kt + t4;
-            double x0 = 0.0, x1 = 0.0;
-            if (vn && k < HE) {
-              x0 = col[k * BRX];
-              if (k < HO) x1 = col[(M - 1 - k) * BRX];
-            }
-            const double be = x0 + x1, bo = (k < HO) ? x0 - x1 : 0.0;
+            double be[DMB], bo[DMB];
 #pragma unroll
-            for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], fe[m * K::KTE + kt], be);
+            for (int q = 0; q < DMB; ++q) {
+              double x0 = 0.0, x1 = 0.0;
+              if (vn[q] && k < HE) {
+                x0 = col[q][k * BRX];
+                if (k < HO) x1 = col[q][(M - 1 - k) * BRX];
+              }
+              be[q] = x0 + x1;
+              bo[q] = (k < HO) ? x0 - x1 : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+              for (int q = 0; q < DMB; ++q) dmma884(ae[q][m][0], ae[q][m][1], fe[m * K::KTE + kt], be[q]);
             if (kt < K::KTO) {
 #pragma unroll
               for (int m = 0; m < K::MTO; ++m)
-                dmma884(ao[m][0], ao[m][1], fo[m * K::KTO + kt], bo);
+#pragma unroll
+                for (int q = 0; q < DMB; ++q) dmma884(ao[q][m][0], ao[q][m][1], fo[m * K::KTO + kt], bo[q]);
             }
           }
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int n2 = 8 * bt + 2 * t4 + j;
-            if (n2 < E * M) {
-              const int e2 = n2 / M, c2 = n2 - e2 * M;
-              double* o = EB + e2 * MM + c2;
+          for (int q = 0; q < DMB; ++q)
 #pragma unroll
-              for (int m = 0; m < K::MTE; ++m)
-                if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[m][j];
+            for (int j = 0; j < 2; ++j) {
+              const int n2 = 8 * (b0 + q) + 2 * t4 + j;
+              if (n2 < E * M) {
+                const int e2 = n2 / M, c2 = n2 - e2 * M;
+                double* o = EB + e2 * MM + c2;
 #pragma unroll
-              for (int m = 0; m < K::MTO; ++m)
-                if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[m][j];
+                for (int m = 0; m < K::MTE; ++m)
+                  if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[q][m][j];
+#pragma unroll
+                for (int m = 0; m < K::MTO; ++m)
+                  if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[q][m][j];
+              }
             }
-          }
         }
       }
     } else if (!kFdtSkip && act) {
@@ -568,38 +599,59 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       for (int idx = tid; idx < (PP ? 2 : 1) * E * MM; idx += NT) EB[idx] = 0.0;
       __syncthreads();
     } else if constexpr (DM) {
+      constexpr int DMB = K::DMB;
       double fe[K::FE], fo[K::FO];
       // ---- stage 2 (rows n = (e, c)): T2[n][l] = fold_x(T1[n][:]) . [Se | So] * dinv * (1/nu_bar);
       //      a batch's 8 rows are read and rewritten by one warp only
       dm_load_frags<K::FE, K::FO>(FR, 1, lane, fe, fo);
-      for (int bt = warp; bt < K::BT; bt += K::WARPS) {
-        const int n = 8 * bt + g8;
-        const bool vn = n < E * M;
-        const double* row = EB + (vn ? n : 0) * M;
-        double ae[K::MTE][2], ao[K::MTO][2];
+      for (int b0 = DMB * warp; b0 < K::BT; b0 += DMB * K::WARPS) {
+        const double* row[DMB];
+        bool vn[DMB];
+        int nq[DMB];
 #pragma unroll
-        for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+        for (int q = 0; q < DMB; ++q) {
+          nq[q] = 8 * (b0 + q) + g8;
+          vn[q] = nq[q] < E * M;
+          row[q] = EB + (vn[q] ? nq[q] : 0) * M;
+        }
+        double ae[DMB][K::MTE][2], ao[DMB][K::MTO][2];
 #pragma unroll
-        for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+        for (int q = 0; q < DMB; ++q) {
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m) ae[q][m][0] = ae[q][m][1] = 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m) ao[q][m][0] = ao[q][m][1] = 0.0;
+        }
 #pragma unroll
         for (int kt = 0; kt < K::KTE; ++kt) {
           const int k = 4 * kt + t4;
-          double x0 = 0.0, x1 = 0.0;
-          if (vn && k < HE) {
-            x0 = row[k];
-            if (k < HO) x1 = row[M - 1 - k];
-          }
-          const double a_e = x0 + x1, a_o = (k < HO) ? x0 - x1 : 0.0;
+          double a_e[DMB], a_o[DMB];
 #pragma unroll
-          for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], a_e, fe[m * K::KTE + kt]);
+          for (int q = 0; q < DMB; ++q) {
+            double x0 = 0.0, x1 = 0.0;
+            if (vn[q] && k < HE) {
+              x0 = row[q][k];
+              if (k < HO) x1 = row[q][M - 1 - k];
+            }
+            a_e[q] = x0 + x1;
+            a_o[q] = (k < HO) ? x0 - x1 : 0.0;
+          }
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+            for (int q = 0; q < DMB; ++q) dmma884(ae[q][m][0], ae[q][m][1], a_e[q], fe[m * K::KTE + kt]);
           if (kt < K::KTO) {
 #pragma unroll
             for (int m = 0; m < K::MTO; ++m)
-              dmma884(ao[m][0], ao[m][1], a_o, fo[m * K::KTO + kt]);
+#pragma unroll
+              for (int q = 0; q < DMB; ++q) dmma884(ao[q][m][0], ao[q][m][1], a_o[q], fo[m * K::KTO + kt]);
           }
         }
         __syncwarp();
-        if (vn) {
+#pragma unroll
+        for (int q = 0; q < DMB; ++q) {
+          if (!vn[q]) continue;
+          const int n = nq[q];
           const int en = n / M, cn = n - en * M;
           const double sc = SN[en];
           double* w = EB + n * M;
@@ -609,14 +661,14 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int l = 8 * m + 2 * t4 + j;
-              if (l < HE) w[l] = ae[m][j] * (__ldg(dn + l) * sc);
+              if (l < HE) w[l] = ae[q][m][j] * (__ldg(dn + l) * sc);
             }
 #pragma unroll
           for (int m = 0; m < K::MTO; ++m)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int l = 8 * m + 2 * t4 + j;
-              if (l < HO) w[HE + l] = ao[m][j] * (__ldg(dn + HE + l) * sc);
+              if (l < HO) w[HE + l] = ao[q][m][j] * (__ldg(dn + HE + l) * sc);
             }
         }
         __syncwarp();
@@ -624,44 +676,61 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       __syncthreads();
       // ---- stage 3 (columns n = (e, c)): e = SyeT' T2e[:, c] (rows [0,HE)), o = SyoT' T2o[:, c]
       dm_load_frags<K::FE, K::FO>(FR, 2, lane, fe, fo);
-      for (int bt = warp; bt < K::BT; bt += K::WARPS) {
-        const int n = 8 * bt + g8;
-        const bool vn = n < E * M;
-        const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
-        const double* col = EB + en * MM + cn;
-        double ae[K::MTE][2], ao[K::MTO][2];
+      for (int b0 = DMB * warp; b0 < K::BT; b0 += DMB * K::WARPS) {
+        const double* col[DMB];
+        bool vn[DMB];
 #pragma unroll
-        for (int m = 0; m < K::MTE; ++m) ae[m][0] = ae[m][1] = 0.0;
+        for (int q = 0; q < DMB; ++q) {
+          const int n = 8 * (b0 + q) + g8;
+          vn[q] = n < E * M;
+          const int en = vn[q] ? n / M : 0, cn = vn[q] ? n - en * M : 0;
+          col[q] = EB + en * MM + cn;
+        }
+        double ae[DMB][K::MTE][2], ao[DMB][K::MTO][2];
 #pragma unroll
-        for (int m = 0; m < K::MTO; ++m) ao[m][0] = ao[m][1] = 0.0;
+        for (int q = 0; q < DMB; ++q) {
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m) ae[q][m][0] = ae[q][m][1] = 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m) ao[q][m][0] = ao[q][m][1] = 0.0;
+        }
 #pragma unroll
         for (int kt = 0; kt < K::KTE; ++kt) {
           const int i = 4 * kt + t4;
-          const double be = (vn && i < HE) ? col[i * M] : 0.0;
-          const double bo = (vn && i < HO) ? col[(HE + i) * M] : 0.0;
+          double be[DMB], bo[DMB];
 #pragma unroll
-          for (int m = 0; m < K::MTE; ++m) dmma884(ae[m][0], ae[m][1], fe[m * K::KTE + kt], be);
+          for (int q = 0; q < DMB; ++q) {
+            be[q] = (vn[q] && i < HE) ? col[q][i * M] : 0.0;
+            bo[q] = (vn[q] && i < HO) ? col[q][(HE + i) * M] : 0.0;
+          }
+#pragma unroll
+          for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+            for (int q = 0; q < DMB; ++q) dmma884(ae[q][m][0], ae[q][m][1], fe[m * K::KTE + kt], be[q]);
           if (kt < K::KTO) {
 #pragma unroll
             for (int m = 0; m < K::MTO; ++m)
-              dmma884(ao[m][0], ao[m][1], fo[m * K::KTO + kt], bo);
+#pragma unroll
+              for (int q = 0; q < DMB; ++q) dmma884(ao[q][m][0], ao[q][m][1], fo[m * K::KTO + kt], bo[q]);
           }
         }
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int n2 = 8 * bt + 2 * t4 + j;
-          if (n2 < E * M) {
-            const int e2 = n2 / M, c2 = n2 - e2 * M;
-            double* o = EB + e2 * MM + c2;
+        for (int q = 0; q < DMB; ++q)
 #pragma unroll
-            for (int m = 0; m < K::MTE; ++m)
-              if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[m][j];
+          for (int j = 0; j < 2; ++j) {
+            const int n2 = 8 * (b0 + q) + 2 * t4 + j;
+            if (n2 < E * M) {
+              const int e2 = n2 / M, c2 = n2 - e2 * M;
+              double* o = EB + e2 * MM + c2;
 #pragma unroll
-            for (int m = 0; m < K::MTO; ++m)
-              if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[m][j];
+              for (int m = 0; m < K::MTE; ++m)
+                if (8 * m + g8 < HE) o[(8 * m + g8) * M] = ae[q][m][j];
+#pragma unroll
+              for (int m = 0; m < K::MTO; ++m)
+                if (8 * m + g8 < HO) o[(HE + 8 * m + g8) * M] = ao[q][m][j];
+            }
           }
-        }
         __syncwarp();
       }
       __syncthreads();
@@ -671,60 +740,79 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       double re[K::MAXB][K::MTE][2], ro[K::MAXB][K::MTO][2];
       dm_load_frags<K::FE, K::FO>(FR, 3, lane, fe, fo);
 #pragma unroll
-      for (int q = 0; q < K::MAXB; ++q) {
-        const int bt = warp + q * K::WARPS;
-        const int n = 8 * bt + g8;
-        const bool vn = bt < K::BT && n < E * M;
-        const int en = vn ? n / M : 0, cn = vn ? n - en * M : 0;
-        const int cf = cn < HE ? cn : M - 1 - cn;
-        const double sg = cn < HE ? 1.0 : -1.0;
-        const bool centre = (M & 1) && cn == HO;
-        const double* er = EB + en * MM + cf * M;
-        const double* orow = EB + en * MM + (HE + (cf < HO ? cf : 0)) * M;
+      for (int it2 = 0; it2 < K::DMIT; ++it2) {
+        const double* er[DMB];
+        const double* orow[DMB];
+        double sg[DMB];
+        bool ctr[DMB], vn[DMB];
 #pragma unroll
-        for (int m = 0; m < K::MTE; ++m) re[q][m][0] = re[q][m][1] = 0.0;
+        for (int q = 0; q < DMB; ++q) {
+          const int bt = DMB * (warp + it2 * K::WARPS) + q;
+          const int n = 8 * bt + g8;
+          vn[q] = bt < K::BT && n < E * M;
+          const int en = vn[q] ? n / M : 0, cn = vn[q] ? n - en * M : 0;
+          const int cf = cn < HE ? cn : M - 1 - cn;
+          sg[q] = cn < HE ? 1.0 : -1.0;
+          ctr[q] = (M & 1) && cn == HO;
+          er[q] = EB + en * MM + cf * M;
+          orow[q] = EB + en * MM + (HE + (cf < HO ? cf : 0)) * M;
 #pragma unroll
-        for (int m = 0; m < K::MTO; ++m) ro[q][m][0] = ro[q][m][1] = 0.0;
-        if (bt < K::BT) {
+          for (int m = 0; m < K::MTE; ++m) re[it2 * DMB + q][m][0] = re[it2 * DMB + q][m][1] = 0.0;
+#pragma unroll
+          for (int m = 0; m < K::MTO; ++m) ro[it2 * DMB + q][m][0] = ro[it2 * DMB + q][m][1] = 0.0;
+        }
+        if (DMB * (warp + it2 * K::WARPS) < K::BT) {
 #pragma unroll
           for (int kt = 0; kt < K::KTE; ++kt) {
             const int i = 4 * kt + t4;
-            double a_e = 0.0, a_o = 0.0;
-            if (vn && i < HE) a_e = centre ? er[i] : fma(sg, orow[i], er[i]);
-            if (vn && i < HO) a_o = centre ? er[HE + i] : fma(sg, orow[HE + i], er[HE + i]);
+            double a_e[DMB], a_o[DMB];
 #pragma unroll
-            for (int m = 0; m < K::MTE; ++m) dmma884(re[q][m][0], re[q][m][1], a_e, fe[m * K::KTE + kt]);
+            for (int q = 0; q < DMB; ++q) {
+              a_e[q] = 0.0;
+              a_o[q] = 0.0;
+              if (vn[q] && i < HE) a_e[q] = ctr[q] ? er[q][i] : fma(sg[q], orow[q][i], er[q][i]);
+              if (vn[q] && i < HO) a_o[q] = ctr[q] ? er[q][HE + i] : fma(sg[q], orow[q][HE + i], er[q][HE + i]);
+            }
+#pragma unroll
+            for (int m = 0; m < K::MTE; ++m)
+#pragma unroll
+              for (int q = 0; q < DMB; ++q)
+                dmma884(re[it2 * DMB + q][m][0], re[it2 * DMB + q][m][1], a_e[q], fe[m * K::KTE + kt]);
             if (kt < K::KTO) {
 #pragma unroll
               for (int m = 0; m < K::MTO; ++m)
-                dmma884(ro[q][m][0], ro[q][m][1], a_o, fo[m * K::KTO + kt]);
+#pragma unroll
+                for (int q = 0; q < DMB; ++q)
+                  dmma884(ro[it2 * DMB + q][m][0], ro[it2 * DMB + q][m][1], a_o[q], fo[m * K::KTO + kt]);
             }
           }
         }
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < K::MAXB; ++q) {
-        const int bt = warp + q * K::WARPS;
-        const int n = 8 * bt + g8;
-        if (bt < K::BT && n < E * M) {
-          double* w = EB + n * M;
+      for (int it2 = 0; it2 < K::DMIT; ++it2)
 #pragma unroll
-          for (int m = 0; m < K::MTE; ++m)
+        for (int q = 0; q < DMB; ++q) {
+          const int bt = DMB * (warp + it2 * K::WARPS) + q;
+          const int n = 8 * bt + g8;
+          if (bt < K::BT && n < E * M) {
+            double* w = EB + n * M;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int k = 8 * m + 2 * t4 + j;
-              if (k < HE) w[k] = re[q][m][j];
-            }
+            for (int m = 0; m < K::MTE; ++m)
 #pragma unroll
-          for (int m = 0; m < K::MTO; ++m)
+              for (int j = 0; j < 2; ++j) {
+                const int k = 8 * m + 2 * t4 + j;
+                if (k < HE) w[k] = re[it2 * DMB + q][m][j];
+              }
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int k = 8 * m + 2 * t4 + j;
-              if (k < HO) w[HE + k] = ro[q][m][j];
-            }
+            for (int m = 0; m < K::MTO; ++m)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int k = 8 * m + 2 * t4 + j;
+                if (k < HO) w[HE + k] = ro[it2 * DMB + q][m][j];
+              }
+          }
         }
-      }
       __syncthreads();
       fdt_epilogue_fold<P, NO, TX, TY, NT>(EB);
     } else {

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -264,6 +265,36 @@ def coarse_solve(h: MultigridHierarchy, f0) -> torch.Tensor:
     return u0
 
 
+def _chain_levels(h: MultigridHierarchy) -> int:
+    """Levels 1..K whose prolongations run as one launch (smg_prolongate_chain):
+    orders 2^l up to p = 16 and no post-smoothing below level K.  Cached per
+    hierarchy together with the ctypes argument arrays (pointers into the
+    level fields, which the V-cycle keeps, except the caller's top u)."""
+    import ctypes as C
+    top_ptr = h.top.u.data_ptr() if h.top.u is not None else 0
+    # opt-in (SMG_CHAIN=1): bitwise equal, but measured no faster than the
+    # per-level launches with PDL on B200 (C2 V-cycle 110.6 vs 110.6 us, C3
+    # 1231 vs 1216 us; DESIGN.md section 3.3)
+    key = (top_ptr, os.environ.get("SMG_CHAIN", "0"))
+    if getattr(h, "_chain_key", None) == key:
+        return h._chain_K
+    K = 0
+    if key[1] == "1":
+        for l in range(1, min(h.depth, 4) + 1):
+            lv = h.levels[l]
+            if lv.basis.p != (1 << l) or h.levels[l - 1].basis.p != (1 << (l - 1)):
+                break
+            K = l
+            if lv.n_post:
+                break
+    h._chain_K = K
+    h._chain_key = key
+    if K >= 2:
+        h._chain_tr = (C.c_void_p * K)(*[h.levels[l].transfer.handle.raw.value for l in range(1, K + 1)])
+        h._chain_u = (C.c_void_p * K)(*[h.levels[l].u.data_ptr() for l in range(1, K + 1)])
+    return K
+
+
 def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bool = False) -> torch.Tensor:
     """Algorithm 3 on device buffers; u is updated in place.  u_zero declares
     the initial guess to be 0 (MGCG preconditioning): u's prior contents are
@@ -297,10 +328,17 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
             N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
                                               N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st), "residual_restrict")
     _coarse_into(h, h.levels[0].f, h.levels[0].u)
-    for l in range(1, L + 1):
+    K = _chain_levels(h)
+    if K >= 2:
+        # levels 1..K prolongated in one launch (n_post = 0 below level K)
+        N.check(lib.smg_prolongate_chain(h._chain_tr, K, N.ptr(h.levels[0].u), h._chain_u, st), "prolongate_chain")
+    else:
+        K = 0
+    for l in range(max(K, 1), L + 1):
         lv = h.levels[l]
-        N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
-                "prolongate")
+        if l > K:
+            N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
+                    "prolongate")
         if lv.n_post:
             if isinstance(lv.smoother, MultiplicativeSchwarz):
                 lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)

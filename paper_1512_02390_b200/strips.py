@@ -1,29 +1,39 @@
 """Element-row strip decomposition of the V-cycle and the outer solvers
 across ranks (one process per GPU).
 
-Rank g owns element rows [g s, (g+1) s) (s = n_y / world) and keeps G = 2
-ghost element rows on each side.  Its local arrays are the (p (s + 2G), N_x)
-row window of the global (N_y, N_x) field, and every per-level operator,
-smoother and transfer runs UNCHANGED on the local mesh
-``MeshConfig(n_x, s + 2G, l_x, dy (s + 2G))`` treated as periodic: outputs on
-owned rows are exact as long as the ghost rows hold the neighbours' data,
-because
+Rank g owns element rows [g s, (g+1) s) (s = n_y / world) and keeps ONE ghost
+element row on each side.  Its local arrays are the (p (s + 2), N_x) row window
+of the global (N_y, N_x) field; every per-level operator, smoother and
+transfer runs UNCHANGED on the local mesh ``MeshConfig(n_x, s + 2, l_x,
+dy (s + 2))`` treated as periodic.  Outputs on owned rows are exact because
 
-* ``r = f - A u`` on owned rows reads u one element row beyond them;
-* the Schwarz windows of the first ghost element row reach n_o < p rows into
-  the strip and read r up to n_o rows beyond it, i.e. inside the second
-  ghost row -- so with two ghost rows of r, every correction landing on an
-  owned row is exact (the outer ghost row's windows wrap onto garbage, but
-  they only touch ghost rows);
-* restriction of owned coarse rows reads the element row below; the
-  prolongation of owned fine rows reads the coarse vertex row above.
+* ``r = f - A u`` on owned node rows reads u on the ghost element row below
+  (p node rows) and on the first node row above -- the forward halo of u;
+* the Schwarz correction is computed only for OWNED elements: the ghost
+  elements' windows are switched off through the smoother's per-element
+  scale 1/nu_bar = 0 (nu_bar = inf on the ghost rows; exact, bitwise the
+  unscaled arithmetic elsewhere since 1/1.0 = 1.0).  An owned window reads r
+  on n_o rows below the strip and n_o + 1 rows above it (the forward halo of
+  r), and its correction lands on n_o ghost rows below and n_o + 1 above:
+  those rows start from zero and are sent back to the neighbour that owns
+  them, which adds them to its owned rows (the reverse halo);
+* restriction of the owned coarse rows reads the fine ghost element row below
+  (p rows of r); prolongation of the owned fine rows reads the first coarse
+  node row above.
 
-Ghost rows are refreshed by row-slab exchanges with the two neighbours (the
-layout is row-major, so a slab is contiguous: no packing), inner products
-are summed over owned rows and all-reduced, and the singular p = 1 coarse
-problem is all-gathered and solved redundantly on every rank (it is tiny),
-each rank keeping its window of the solution.  Redundant work: 2G/s extra
-element rows per strip (12% at s = 32).
+Ghost slabs are contiguous in the row-major layout (no packing).  Inner
+products are summed over owned rows on the device (smg_dot / smg_dot2 /
+smg_cg_update2 into a device scalar block) and all-reduced in place on the
+device -- the host reads ||r|| and the breakdown flag once per cycle, as the
+single-GPU solver does.  The singular p = 1 coarse problem is all-gathered
+into a preallocated global array and solved redundantly on every rank.
+
+Halo traffic per level of order p and overlap n_o (rows of N_x = p n_x
+doubles): u forward p + 1, r forward (2 n_o + 1) + correction reverse
+(2 n_o + 1), r forward p before the restriction, 1 coarse row before the
+prolongation -- e.g. C3 at p = 32, n_o = 1: 33 + 3 + 3 + 32 rows of 32 KB.
+Redundant work: the ghost element rows of the operator and transfer kernels,
+2/s of a strip (the masked Schwarz windows still cost their contractions).
 
 The driver is written against two small interfaces so the same code runs
 (a) one process per GPU over NCCL (``TorchTransport``), (b) CPU gloo ranks
@@ -42,7 +52,7 @@ import numpy as np
 
 from .metrics import ConvergenceReport
 
-G = 2  # ghost element rows on each side
+G = 1  # ghost element rows on each side
 
 
 @dataclass(frozen=True)
@@ -55,6 +65,8 @@ class StripPlan:
     rank: int
 
     def __post_init__(self):
+        if self.world < 1 or not 0 <= self.rank < self.world:
+            raise ValueError(f"bad rank {self.rank} of {self.world}")
         if self.n_y % self.world:
             raise ValueError(f"{self.n_y} element rows do not split into {self.world} strips")
         if self.n_y // self.world < 1:
@@ -88,6 +100,18 @@ class StripPlan:
         N_y = p * self.n_y
         return (np.arange(p * self.local_ny) + (self.ey0 - G) * p) % N_y
 
+    def ghost_mask(self) -> np.ndarray:
+        """(local_ny, n_x) bool: element rows whose Schwarz windows are off."""
+        m = np.zeros((self.local_ny, self.n_x), dtype=bool)
+        m[:G] = True
+        m[G + self.s:] = True
+        return m
+
+    def check_level(self, p: int, n_o: int):
+        """The reverse halo of a strip must not overlap itself."""
+        if self.s * p < 2 * n_o + 1:
+            raise ValueError(f"strip of {self.s} element rows too thin for p={p}, n_o={n_o}")
+
     def below(self) -> int:
         return (self.rank - 1) % self.world
 
@@ -99,61 +123,109 @@ class StripPlan:
 # transports
 
 
+def _rows(plan, p):
+    own = plan.own(p)
+    return own.start, own.stop
+
+
 class TorchTransport:
-    """torch.distributed point-to-point + collectives (NCCL for CUDA tensors,
-    gloo for CPU tensors)."""
+    """torch.distributed point-to-point + collectives (NCCL on device buffers;
+    gloo for CPU tensors, or host-staged when given CUDA tensors)."""
 
     def __init__(self, plan: StripPlan, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.plan = plan
         self.group = group
-        # gloo cannot move CUDA tensors point-to-point: stage through the host
         self.host_staged = dist.get_backend(group) != "nccl"
 
-    def exchange(self, t, p: int, k: int):
-        """Fill k ghost element rows on each side of t (level p) from the neighbours."""
+    def _p2p(self, send_down, send_up, recv_from_above, recv_from_below):
+        """send_down -> rank below, send_up -> rank above; receive the
+        matching messages (fixed op order: deterministic, deadlock-free)."""
+        import torch
+        dist, pl = self.dist, self.plan
+        stage = self.host_staged and send_down.is_cuda
+        sd, su = (send_down.cpu(), send_up.cpu()) if stage else (send_down, send_up)
+        ra = torch.empty_like(sd) if stage else recv_from_above
+        rb = torch.empty_like(su) if stage else recv_from_below
+        ops = []
+        if sd.numel():
+            ops += [dist.P2POp(dist.isend, sd, pl.below(), self.group),
+                    dist.P2POp(dist.irecv, ra, pl.above(), self.group)]
+        if su.numel():
+            ops += [dist.P2POp(dist.isend, su, pl.above(), self.group),
+                    dist.P2POp(dist.irecv, rb, pl.below(), self.group)]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if stage:
+            recv_from_above.copy_(ra)
+            recv_from_below.copy_(rb)
+
+    def exchange(self, t, p: int, below: int, above: int):
+        """Forward halo: `below` ghost rows under the strip and `above` over it
+        from the neighbours' owned rows."""
+        pl = self.plan
+        lo, hi = _rows(pl, p)
+        if pl.world == 1:
+            if above:
+                t[hi:hi + above] = t[lo:lo + above]
+            if below:
+                t[lo - below:lo] = t[hi - below:hi]
+            return
+        # my bottom `above` rows are the lower neighbour's top ghost rows, and
+        # my top `below` rows its upper neighbour's bottom ghost rows
+        self._p2p(t[lo:lo + above], t[hi - below:hi], t[hi:hi + above], t[lo - below:lo])
+
+    def exchange_add(self, t, p: int, below: int, above: int):
+        """Reverse halo: the contributions in the ghost rows go to the owners,
+        which add them to their boundary rows (from below first, then above)."""
         import torch
         pl = self.plan
-        own = pl.own(p)
-        lo, hi = own.start, own.stop
-        R = k * p
+        lo, hi = _rows(pl, p)
         if pl.world == 1:
-            t[lo - R:lo] = t[hi - R:hi]
-            t[hi:hi + R] = t[lo:lo + R]
+            if above:
+                t[lo:lo + above] += t[hi:hi + above]
+            if below:
+                t[hi - below:hi] += t[lo - below:lo]
             return
-        dist = self.dist
-        send_down = t[lo:lo + R].contiguous()
-        send_up = t[hi - R:hi].contiguous()
-        if self.host_staged and t.is_cuda:
-            send_down, send_up = send_down.cpu(), send_up.cpu()
-        recv_top = torch.empty_like(send_down)
-        recv_bot = torch.empty_like(send_down)
-        ops = [dist.P2POp(dist.isend, send_down, pl.below(), self.group),
-               dist.P2POp(dist.isend, send_up, pl.above(), self.group),
-               dist.P2POp(dist.irecv, recv_top, pl.above(), self.group),
-               dist.P2POp(dist.irecv, recv_bot, pl.below(), self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-        t[hi:hi + R] = recv_top
-        t[lo - R:lo] = recv_bot
+        from_above = torch.empty_like(t[lo - below:lo])
+        from_below = torch.empty_like(t[hi:hi + above])
+        self._p2p(t[lo - below:lo], t[hi:hi + above], from_above, from_below)
+        if above:
+            t[lo:lo + above] += from_below
+        if below:
+            t[hi - below:hi] += from_above
 
-    def allreduce(self, x: float) -> float:
-        import torch
-        dev = "cpu" if self.host_staged else "cuda"
-        v = torch.tensor([x], dtype=torch.float64, device=dev)
-        self.dist.all_reduce(v, group=self.group)
-        return float(v.item())
+    def allreduce_(self, x):
+        """In-place sum of a (device) tensor over the ranks."""
+        if self.plan.world == 1:
+            return x
+        if self.host_staged and x.is_cuda:
+            h = x.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            x.copy_(h)
+        else:
+            self.dist.all_reduce(x, group=self.group)
+        return x
 
     def allgather_rows(self, own, full):
-        """full[(N_y, N_x)] <- concatenation of every rank's owned rows `own`."""
-        import torch
+        """full (N_y, N_x) <- every rank's owned rows `own`, in rank order,
+        gathered straight into the preallocated array."""
+        if self.plan.world == 1:
+            full.copy_(own)
+            return
         src = own.contiguous()
         if self.host_staged and src.is_cuda:
-            src = src.cpu()
-        parts = [torch.empty_like(src) for _ in range(self.plan.world)]
-        self.dist.all_gather(parts, src, group=self.group)
-        full.copy_(torch.cat(parts, 0))
+            import torch
+            parts = [torch.empty_like(src.cpu()) for _ in range(self.plan.world)]
+            self.dist.all_gather(parts, src.cpu(), group=self.group)
+            full.copy_(torch.cat(parts, 0))
+        elif src.is_cuda:
+            self.dist.all_gather_into_tensor(full, src, group=self.group)
+        else:
+            parts = list(full.chunk(self.plan.world, 0))
+            self.dist.all_gather(parts, src, group=self.group)
 
 
 class ThreadTransport:
@@ -169,28 +241,44 @@ class ThreadTransport:
         torch.cuda.synchronize()
         self.sh["barrier"].wait()
 
-    def exchange(self, t, p: int, k: int):
-        pl = self.plan
-        own = pl.own(p)
-        lo, hi = own.start, own.stop
-        R = k * p
-        self.sh["slots"][pl.rank] = t
+    def _neighbours(self, t):
+        self.sh["slots"][self.plan.rank] = t
         self._sync()
-        below = self.sh["slots"][pl.below()]
-        above = self.sh["slots"][pl.above()]
-        top = above[lo:lo + R].clone()
-        bot = below[hi - R:hi].clone()
+        return self.sh["slots"][self.plan.below()], self.sh["slots"][self.plan.above()]
+
+    def exchange(self, t, p: int, below: int, above: int):
+        lo, hi = _rows(self.plan, p)
+        bel, abv = self._neighbours(t)
+        top = abv[lo:lo + above].clone()
+        bot = bel[hi - below:hi].clone()
         self._sync()
-        t[hi:hi + R] = top
-        t[lo - R:lo] = bot
+        t[hi:hi + above] = top
+        t[lo - below:lo] = bot
         self._sync()
 
-    def allreduce(self, x: float) -> float:
-        self.sh["slots"][self.plan.rank] = x
+    def exchange_add(self, t, p: int, below: int, above: int):
+        lo, hi = _rows(self.plan, p)
+        bel, abv = self._neighbours(t)
+        from_below = bel[hi:hi + above].clone()
+        from_above = abv[lo - below:lo].clone()
         self._sync()
-        v = math.fsum(self.sh["slots"][r] for r in range(self.plan.world))
+        if above:
+            t[lo:lo + above] += from_below
+        if below:
+            t[hi - below:hi] += from_above
         self._sync()
-        return v
+
+    def allreduce_(self, x):
+        import torch
+        self.sh["slots"][self.plan.rank] = x.clone()
+        self._sync()
+        parts = [self.sh["slots"][r] for r in range(self.plan.world)]
+        acc = parts[0].clone()
+        for q in parts[1:]:
+            acc += q.to(acc.device)
+        self._sync()
+        x.copy_(acc)
+        return x
 
     def allgather_rows(self, own, full):
         import torch
@@ -232,45 +320,57 @@ class StripSolver:
     """V-cycle, MG and MGCG on one rank's strip.
 
     ``engine`` provides, per level l (0 = p=1 coarse), on LOCAL arrays:
-      orders            list of level orders
-      n_pre, n_post     smoothing counts per level
-      zeros(l)          new local array
-      residual(l, u, f, out)   out = f - A u     (f None: out = A u)
-      correct(l, r, u, zero)   u += M r  (zero: u := M r)
-      restrict(l, fine, out)   out (level l-1) = P^T fine
+      orders, n_o, n_pre, n_post        per-level lists
+      us, fs                            per-level solution / right-hand side
+      zeros(l), work(l), clone(a), copy(dst, src), fill_zero(a)
+      residual(l, u, f, out)            out = f - A u     (f None: out = A u)
+      correct(l, r, u, zero)            u += M r (zero: u := M r), ghost windows off
+      restrict(l, fine, out)            out (level l-1) = P^T fine
       prolong_add(l, coarse, fine)
-      coarse_full(f0_full) -> u0_full            (global p=1 solve)
-      full_zeros0()     new global p=1 array
-      local_dot(a, b)   sum over owned rows (caller passes own slices)
-      copy(dst, src)
+      coarse_full(f0_full) -> u0_full   global p=1 solve
+      full_zeros0()                     new global p=1 array
+      scalars()                         (scal[8], flag) device block
+      dot(a, b, out)                    out[0] = a . b   (owned slices)
+      dot2(z, r, r_old, out)            out[0] = z.(r - r_old), out[1] = z.r
+      cg_update(u, r, r_new, d, q, scal, flag)   krylov.py:95-103 on owned slices
+      cg_beta_finish(scal), cg_direction(d, z, scal)
+      read(scal, flag) -> (host floats, int)    the per-cycle sync
     """
 
     def __init__(self, plan: StripPlan, engine, transport):
         self.plan, self.eng, self.tr = plan, engine, transport
         self.L = len(engine.orders) - 1
+        for l in range(1, self.L + 1):
+            plan.check_level(engine.orders[l], engine.n_o[l])
 
-    # -- helpers
     def own(self, l):
         return self.plan.own(self.eng.orders[l])
 
-    def dot(self, a, b, l=None):
-        l = self.L if l is None else l
-        o = self.own(l)
-        return self.tr.allreduce(self.eng.local_dot(a[o], b[o]))
+    # -- halos per stage (rows below, rows above)
+    def _residual(self, l, u, f, out):
+        p = self.eng.orders[l]
+        self.tr.exchange(u, p, p, 1)
+        self.eng.residual(l, u, f, out)
+
+    def _correct(self, l, r, u, zero):
+        e, p = self.eng, self.eng.orders[l]
+        n_o = e.n_o[l]
+        self.tr.exchange(r, p, n_o, n_o + 1)
+        if not zero:
+            own = self.own(l)
+            u[:own.start] = 0.0
+            u[own.stop:] = 0.0
+        e.correct(l, r, u, zero)
+        self.tr.exchange_add(u, p, n_o, n_o + 1)
 
     def _smooth(self, l, u, f, n_it, zero):
-        e, p = self.eng, self.eng.orders[l]
         for it in range(n_it):
-            z = zero and it == 0
-            if z:
-                self.tr.exchange(f, p, G)          # r = f needs 2 ghost rows for the windows
-                e.correct(l, f, u, True)
+            if zero and it == 0:
+                self._correct(l, f, u, True)
             else:
-                r = e.work(l)
-                self.tr.exchange(u, p, 1)
-                e.residual(l, u, f, r)
-                self.tr.exchange(r, p, G)
-                e.correct(l, r, u, False)
+                r = self.eng.work(l)
+                self._residual(l, u, f, r)
+                self._correct(l, r, u, False)
 
     def v_cycle(self, u, f, u_zero=False):
         """Algorithm 3 (multigrid.py:231-251) on the strip; u updated in place."""
@@ -290,92 +390,98 @@ class StripSolver:
             if zero:
                 e.copy(r, fs[l])
             else:
-                self.tr.exchange(us[l], p, 1)
-                e.residual(l, us[l], fs[l], r)
-            self.tr.exchange(r, p, 1)
+                self._residual(l, us[l], fs[l], r)
+            self.tr.exchange(r, p, p, 0)
             e.restrict(l, r, fs[l - 1])
         # replicated coarse solve
         p0 = e.orders[0]
-        f0_full = e.full_zeros0()
+        f0_full = e.full0
         self.tr.allgather_rows(fs[0][self.own(0)], f0_full)
         u0_full = e.coarse_full(f0_full)
         e.copy(us[0], u0_full[self.plan.global_rows(p0)])
         for l in range(1, L + 1):
-            self.tr.exchange(us[l - 1], e.orders[l - 1], 1)
+            self.tr.exchange(us[l - 1], e.orders[l - 1], 0, 1)
             e.prolong_add(l, us[l - 1], us[l])
             if e.n_post[l]:
                 self._smooth(l, us[l], fs[l], e.n_post[l], False)
         return u
 
-    def _norm(self, r):
-        return math.sqrt(self.dot(r, r))
-
     def solve_mg(self, f, u, tol=1e10, max_cycles=200):
         """krylov.py:49-67 on strips; f, u local (u = initial guess, updated)."""
         t0 = time.perf_counter()
         e, L = self.eng, self.L
+        o = self.own(L)
         r = e.zeros(L)
-        p = e.orders[L]
-        self.tr.exchange(u, p, 1)
-        e.residual(L, u, f, r)
-        res = [self._norm(r)]
+        scal, flag = e.scalars()
+
+        def norm():
+            self._residual(L, u, f, r)
+            e.dot(r[o], r[o], scal[2:3])
+            self.tr.allreduce_(scal[2:3])
+            host, _ = e.read(scal, flag)
+            return math.sqrt(host[2])
+
+        res = [norm()]
         r_max = res[0] / tol
         ok = res[0] <= r_max
         cycles = 0
         while not ok and cycles < max_cycles:
             self.v_cycle(u, f)
             cycles += 1
-            self.tr.exchange(u, p, 1)
-            e.residual(L, u, f, r)
-            res.append(self._norm(r))
+            res.append(norm())
             ok = res[-1] <= r_max
         return u, ConvergenceReport(res, ok, cycles, time.perf_counter() - t0)
 
     def solve_mgcg(self, f, u, tol=1e10, max_cycles=200):
-        """krylov.py:70-115 on strips (beta = z^T (r - r_old) / delta as coded)."""
+        """krylov.py:70-115 on strips (beta = z^T (r - r_old) / delta as coded),
+        every scalar on the device: scal[0] delta, [1] p.q, [2] ||r||^2,
+        [3:5] the dot2 sums, [5] beta, [6] alpha."""
         t0 = time.perf_counter()
         e, L = self.eng, self.L
-        p_ = e.orders[L]
+        o = self.own(L)
+        scal, flag = e.scalars()
+        tr = self.tr
         r = e.zeros(L)
-        self.tr.exchange(u, p_, 1)
-        e.residual(L, u, f, r)
-        res = [self._norm(r)]
+        self._residual(L, u, f, r)
+        e.dot(r[o], r[o], scal[2:3])
+        tr.allreduce_(scal[2:3])
+        host, _ = e.read(scal, flag)
+        res = [math.sqrt(host[2])]
         r_max = res[0] / tol
         ok = res[0] <= r_max
         broke = False
         cycles = 0
         if not ok:
             d = e.zeros(L)
-            self.v_cycle(d, e.clone(r), u_zero=True)
-            delta = self.dot(d, r)
-            r_old = None
             q = e.zeros(L)
+            z = e.zeros(L)
+            r_new = e.zeros(L)
+            self.v_cycle(d, e.clone(r), u_zero=True)
+            e.dot(d[o], r[o], scal[0:1])
+            tr.allreduce_(scal[0:1])
+            first = True
             for _ in range(max_cycles):
-                self.tr.exchange(d, p_, 1)
-                e.residual(L, d, None, q)
-                pq = self.dot(d, q)
-                if pq <= 0.0:
+                self._residual(L, d, None, q)
+                e.dot(d[o], q[o], scal[1:2])
+                tr.allreduce_(scal[1:2])
+                e.cg_update(u[o], r[o], r_new[o], d[o], q[o], scal, flag)
+                tr.allreduce_(scal[2:3])
+                host, brk = e.read(scal, flag)
+                if brk:
                     broke = True
                     break
-                alpha = delta / pq
-                e.axpy(alpha, d, u)
-                r_new = e.clone(r)
-                e.axpy(-alpha, q, r_new)
-                r_prev, r = r, r_new
                 cycles += 1
-                res.append(self._norm(r))
+                res.append(math.sqrt(host[2]))
                 if res[-1] <= r_max:
                     ok = True
                     break
-                z = e.zeros(L)
-                self.v_cycle(z, e.clone(r), u_zero=True)
-                diff = e.clone(r)
-                if r_old is not None:
-                    e.axpy(-1.0, r_old, diff)
-                beta = self.dot(z, diff) / delta
-                e.xpby(z, beta, d)              # d = z + beta d
-                delta = self.dot(z, r)
-                r_old = r
+                self.v_cycle(z, e.clone(r_new), u_zero=True)
+                e.dot2(z[o], r_new[o], None if first else r[o], scal[3:5])
+                tr.allreduce_(scal[3:5])
+                e.cg_beta_finish(scal)
+                e.cg_direction(d[o], z[o], scal)
+                r, r_new = r_new, r
+                first = False
         rep = ConvergenceReport(res, ok, cycles, time.perf_counter() - t0)
         rep.breakdown = broke
         return u, rep
@@ -386,28 +492,26 @@ class StripSolver:
 
 
 class GpuEngine:
-    """Per-level device handles built on the rank's local (strip + ghosts) mesh."""
+    """Per-level device handles built on the rank's local (strip + ghosts)
+    mesh, the Schwarz windows of the ghost element rows switched off."""
 
     def __init__(self, plan: StripPlan, p: int, rule, kind="w5", n_pre=1, n_post=0, orders=None,
                  nu_hat=None, nu_shift=0.2, coarse=None, coarse_tol=1e-12):
         import torch
-        from . import multigrid as MG
+        from . import _native as N
         from .mesh import MeshConfig
-        from .operators import diffusivity_field
+        from .schwarz import WeightKind
         self.torch = torch
+        self.N = N
         self.plan = plan
         lm = MeshConfig(*plan.local_mesh_args())
         gm = MeshConfig(plan.n_x, plan.n_y, plan.l_x, plan.l_y)
-        # the local hierarchy: same kernels on the local periodic mesh (its own
-        # coarse level is never used: the coarse problem is solved globally)
-        if nu_hat is None:
-            self.h = MG.build_hierarchy(lm, p, rule, weight=kind, n_pre=n_pre, n_post=n_post, orders=orders,
-                                        coarse="cg", coarse_tol=coarse_tol)
-        else:  # nu sampled at GLOBAL coordinates
-            self.h = _local_diffusion_hierarchy(plan, lm, gm, p, rule, kind, n_pre, n_post, orders, nu_hat,
-                                                nu_shift, coarse_tol, diffusivity_field)
+        kind = WeightKind(kind) if isinstance(kind, str) else kind
+        self.h = _local_hierarchy(plan, lm, gm, p, rule, kind, n_pre, n_post, orders, nu_hat, nu_shift,
+                                  coarse_tol)
         levels = self.h.levels
         self.orders = [lv.basis.p for lv in levels]
+        self.n_o = [lv.n_o for lv in levels]
         self.n_pre = [lv.n_pre for lv in levels]
         self.n_post = [lv.n_post for lv in levels]
         self.us = [lv.u for lv in levels]
@@ -415,6 +519,12 @@ class GpuEngine:
         self._work = [lv.work for lv in levels]
         # global p=1 coarse problem, replicated on every rank
         self.hc = _coarse_only(gm, nu_hat, nu_shift, coarse, coarse_tol)
+        self.full0 = torch.zeros((plan.n_y, plan.n_x), dtype=torch.float64, device="cuda")
+        self.ws = torch.zeros(N.lib().smg_reduce_ws_doubles(), dtype=torch.float64, device="cuda")
+        self._scal = torch.zeros(8, dtype=torch.float64, device="cuda")
+        self._flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._hscal = torch.zeros(8, dtype=torch.float64).pin_memory()
+        self._hflag = torch.zeros(1, dtype=torch.int32).pin_memory()
 
     def zeros(self, l):
         return self.torch.zeros(self.h.levels[l].op.layout.shape, dtype=self.torch.float64, device="cuda")
@@ -435,71 +545,103 @@ class GpuEngine:
         self.h.levels[l].op.residual_into(u, f, out)
 
     def correct(self, l, r, u, zero):
-        from . import _native as N
+        N = self.N
         lv = self.h.levels[l]
-        N.check(N.lib().smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(u), N.ptr(r),
-                                           N.ptr(self._work[l]), N.ptr(lv.smoother.ring), 1, 1 if zero else 0,
-                                           N.stream())
-                if zero else N.lib().smg_schwarz_correct(lv.smoother._h.raw, N.ptr(r), N.ptr(u),
-                                                         N.ptr(lv.smoother.ring), N.stream()),
-                "strip correct")
+        if zero:
+            rc = N.lib().smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(u), N.ptr(r),
+                                            N.ptr(self._work[l]), N.ptr(lv.smoother.ring), 1, 1, N.stream())
+        else:
+            rc = N.lib().smg_schwarz_correct(lv.smoother._h.raw, N.ptr(r), N.ptr(u), N.ptr(lv.smoother.ring),
+                                             N.stream())
+        N.check(rc, "strip correct")
 
     def restrict(self, l, fine, out):
-        from . import _native as N
+        N = self.N
         N.check(N.lib().smg_restrict(self.h.levels[l].transfer.handle.raw, N.ptr(fine), N.ptr(out), N.stream()),
                 "strip restrict")
 
     def prolong_add(self, l, coarse, fine):
-        from . import _native as N
+        N = self.N
         N.check(N.lib().smg_prolongate(self.h.levels[l].transfer.handle.raw, N.ptr(coarse), N.ptr(fine), 1,
                                        N.stream()), "strip prolong")
-
-    def full_zeros0(self):
-        return self.torch.zeros((self.plan.n_y, self.plan.n_x), dtype=self.torch.float64, device="cuda")
 
     def coarse_full(self, f0_full):
         from .multigrid import coarse_solve
         return coarse_solve(self.hc, f0_full)
 
-    def local_dot(self, a, b):
-        return float(self.torch.sum(a * b).item())
+    # -- BLAS-1 on owned slices, device scalars
+    def scalars(self):
+        self._scal.zero_()
+        self._flag.zero_()
+        return self._scal, self._flag
 
-    def axpy(self, alpha, x, y):
-        y.add_(x, alpha=alpha)
+    def dot(self, a, b, out):
+        N = self.N
+        N.check(N.lib().smg_dot(N.ptr(a), N.ptr(b), a.numel(), N.ptr(out), N.ptr(self.ws), N.stream()), "strip dot")
 
-    def xpby(self, x, beta, y):
-        y.mul_(beta).add_(x)
+    def dot2(self, z, r, r_old, out):
+        N = self.N
+        N.check(N.lib().smg_dot2(N.ptr(z), N.ptr(r), N.ptr(r_old) if r_old is not None else None, z.numel(),
+                                 N.ptr(out), N.ptr(self.ws), N.stream()), "strip dot2")
+
+    def cg_update(self, u, r, r_new, d, q, scal, flag):
+        N = self.N
+        N.check(N.lib().smg_cg_update2(N.ptr(u), N.ptr(r), N.ptr(r_new), N.ptr(d), N.ptr(q), u.numel(), N.ptr(scal),
+                                       N.ptr(flag), N.ptr(self.ws), N.stream()), "strip cg_update")
+
+    def cg_beta_finish(self, scal):
+        N = self.N
+        N.check(N.lib().smg_cg_beta_finish(N.ptr(scal), N.stream()), "strip cg_beta_finish")
+
+    def cg_direction(self, d, z, scal):
+        N = self.N
+        N.check(N.lib().smg_cg_direction(N.ptr(d), N.ptr(z), d.numel(), N.ptr(scal), N.stream()),
+                "strip cg_direction")
+
+    def read(self, scal, flag):
+        self._hscal.copy_(scal, non_blocking=True)
+        self._hflag.copy_(flag, non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+        return [float(v) for v in self._hscal], int(self._hflag[0])
 
 
-def _local_diffusion_hierarchy(plan, lm, gm, p, rule, kind, n_pre, n_post, orders, nu_hat, nu_shift,
-                               coarse_tol, diffusivity_field):
-    """Diffusion hierarchy on the local mesh with nu sampled at GLOBAL coordinates."""
+def _local_hierarchy(plan, lm, gm, p, rule, kind, n_pre, n_post, orders, nu_hat, nu_shift, coarse_tol):
+    """The rank's levels on the local mesh: operators (nu sampled at GLOBAL
+    coordinates for diffusion), transfers, and smoothers whose ghost-row
+    windows are off (nu_bar = inf there)."""
     import torch
     from . import multigrid as MG
     from .basis import gll_basis, interp_matrix
     from .mesh import layout_for
-    from .operators import DiffusionOperator
+    from .operators import DiffusionOperator, PoissonOperator, diffusivity_field
     from .schwarz import AdditiveSchwarz
     if orders is None:
+        if p < 2 or (p & (p - 1)) != 0:
+            raise ValueError(f"top-level order must be a power of two >= 2, got {p}")
         orders = [1 << l for l in range(p.bit_length())]
+    ghost = plan.ghost_mask()
     levels = []
-    depth = len(orders) - 1
     for l, p_l in enumerate(orders):
         b = gll_basis(p_l)
-        nu_g = diffusivity_field(gm, b, nu_hat, nu_shift)
-        nu_l = nu_g[plan.global_rows(p_l)]
-        op = DiffusionOperator(b, lm, nu_l)
+        if nu_hat is None:
+            op = PoissonOperator(b, lm)
+            nb = np.ones((plan.local_ny, plan.n_x))
+        else:
+            nu_l = diffusivity_field(gm, b, nu_hat, nu_shift)[plan.global_rows(p_l)]
+            op = DiffusionOperator(b, lm, nu_l)
+            nb = np.array(op.element_mean_nu(), dtype=np.float64)
+        nb = np.where(ghost, np.inf, nb)
         lay = layout_for(lm, p_l)
         if l == 0:
             lv = MG.Level(l, b, op, None, 0, 0, 0)
         else:
             n_o = rule.layers(p_l)
-            sm = AdditiveSchwarz(b, lay, lm.dx, lm.dy, n_o, kind, nu_bar=op.element_mean_nu())
+            sm = AdditiveSchwarz(b, lay, lm.dx, lm.dy, n_o, kind, nu_bar=nb)
             lv = MG.Level(l, b, op, sm, n_pre, n_post, n_o)
             lv.transfer = MG._Transfer(orders[l - 1], p_l, lm.n_x, lm.n_y, interp_matrix(levels[-1].basis, b).matrix)
         lv.u = torch.zeros(lay.shape, dtype=torch.float64, device="cuda")
         lv.f = torch.zeros(lay.shape, dtype=torch.float64, device="cuda")
-        lv.work = torch.empty(lay.shape, dtype=torch.float64, device="cuda")
+        lv.work = torch.zeros(lay.shape, dtype=torch.float64, device="cuda")
         levels.append(lv)
     return MG.MultigridHierarchy(lm, levels, coarse_tol=coarse_tol, coarse="cg")
 

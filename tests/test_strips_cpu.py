@@ -18,19 +18,28 @@ from paper_1512_02390_b200.strips import G, StripPlan, StripSolver, TorchTranspo
 
 class OracleEngine:
     """Engine interface of StripSolver implemented with the numpy oracle on
-    the rank's local periodic mesh (torch CPU tensors at the boundary)."""
+    the rank's local periodic mesh (torch CPU tensors at the boundary); the
+    ghost element rows' Schwarz windows are off (nu_bar = inf there), as in
+    the GPU engine."""
 
     def __init__(self, plan, p, rule="fixed:1", nu_hat=None):
         self.plan = plan
         nx, nyl, lx, lyl = plan.local_mesh_args()
         self.h = O.Hierarchy(nx, nyl, lx, lyl, p, rule=rule, nu_hat=None)
+        ghost = plan.ghost_mask()
+        for l in range(1, len(self.h.levels)):
+            lv = self.h.levels[l]
+            nb = np.where(ghost, np.inf, 1.0)
+            lv.sm = O.AdditiveSweep(lv.b, nx, nyl, lx / nx, lyl / nyl, lv.n_o, "w5", nu_bar=nb)
         self.hg = O.Hierarchy(plan.n_x, plan.n_y, plan.l_x, plan.l_y, 2, rule=rule)
         self.orders = [lv.p for lv in self.h.levels]
+        self.n_o = [lv.n_o for lv in self.h.levels]
         self.n_pre = [lv.n_pre for lv in self.h.levels]
         self.n_post = [lv.n_post for lv in self.h.levels]
         self.us = [self.zeros(l) for l in range(len(self.orders))]
         self.fs = [self.zeros(l) for l in range(len(self.orders))]
         self._work = [self.zeros(l) for l in range(len(self.orders))]
+        self.full0 = torch.zeros((plan.n_y, plan.n_x), dtype=torch.float64)
 
     def zeros(self, l):
         return torch.zeros(self.h.levels[l].op.shape, dtype=torch.float64)
@@ -64,20 +73,39 @@ class OracleEngine:
     def prolong_add(self, l, coarse, fine):
         fine.add_(torch.from_numpy(O.prolongate(self.h, l, coarse.numpy())))
 
-    def full_zeros0(self):
-        return torch.zeros((self.plan.n_y, self.plan.n_x), dtype=torch.float64)
-
     def coarse_full(self, f0):
         return torch.from_numpy(O.coarse_solve(self.hg, f0.numpy()))
 
-    def local_dot(self, a, b):
-        return float(torch.sum(a * b))
+    # device-scalar BLAS-1 restated on host tensors (krylov.py:91-111)
+    def scalars(self):
+        return torch.zeros(8, dtype=torch.float64), torch.zeros(1, dtype=torch.int32)
 
-    def axpy(self, alpha, x, y):
-        y.add_(x, alpha=alpha)
+    def dot(self, a, b, out):
+        out[0] = float(torch.sum(a * b))
 
-    def xpby(self, x, beta, y):
-        y.mul_(beta).add_(x)
+    def dot2(self, z, r, r_old, out):
+        out[0] = float(torch.sum(z * (r if r_old is None else r - r_old)))
+        out[1] = float(torch.sum(z * r))
+
+    def cg_update(self, u, r, r_new, d, q, scal, flag):
+        if not scal[1] > 0.0:
+            flag[0] = 1
+            return
+        alpha = float(scal[0] / scal[1])
+        u.add_(d, alpha=alpha)
+        r_new.copy_(r - alpha * q)
+        scal[2] = float(torch.sum(r_new * r_new))
+        scal[6] = alpha
+
+    def cg_beta_finish(self, scal):
+        scal[5] = scal[3] / scal[0]
+        scal[0] = scal[4]
+
+    def cg_direction(self, d, z, scal):
+        d.mul_(float(scal[5])).add_(z)
+
+    def read(self, scal, flag):
+        return [float(v) for v in scal], int(flag[0])
 
 
 def _free_port():
@@ -148,11 +176,15 @@ def test_strip_decomposition_gloo(world):
 
 def test_strip_plan_geometry():
     pl = StripPlan(4, 8, 2.0, 2.0, 4, 1)
-    assert pl.s == 2 and pl.ey0 == 2 and pl.local_ny == 2 + 2 * G
+    assert G == 1 and pl.s == 2 and pl.ey0 == 2 and pl.local_ny == 2 + 2 * G
     rows = pl.global_rows(4)
     assert rows[0] == (2 - G) * 4 and len(rows) == 4 * pl.local_ny
     own = pl.own(4)
     assert list(rows[own]) == list(range(8, 16))
+    m = pl.ghost_mask()
+    assert m.shape == (4, 4) and m[0].all() and m[3].all() and not m[1:3].any()
+    with pytest.raises(ValueError):
+        StripPlan(4, 8, 2.0, 2.0, 8, 0).check_level(2, 1)   # one element row at p=2 < 2 n_o + 1
     with pytest.raises(ValueError):
         StripPlan(4, 6, 2.0, 2.0, 4, 0)
     assert StripPlan(4, 8, 2.0, 2.0, 4, 0).below() == 3
