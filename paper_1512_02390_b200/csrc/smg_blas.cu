@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(4 * N) pinv_sq_kernel(const double* __restrict
                                                        const double* __restrict__ Qy,
                                                        const double* __restrict__ Lp, const double* __restrict__ f,
                                                        double* __restrict__ u) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();
   namespace cgx = cooperative_groups;
   cgx::cluster_group cl = cgx::this_cluster();
   constexpr int RB = 4, CLN = N / RB, NN = N * N;
@@ -527,17 +527,25 @@ __global__ void __launch_bounds__(4 * N) pinv_sq_kernel(const double* __restrict
   uint64_t* bar = reinterpret_cast<uint64_t*>(LP + RB * N);
   const int tid = threadIdx.x;
   if (tid == 0) {
+    // the eigenbasis tables are per-handle constants: in flight while the
+    // preceding grid (which writes f) drains; f itself after the wait
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(bar, (unsigned)(8 * (4 * NN + RB * N)));
-    bulk_g2s(F, f, 8u * NN, bar);
+    mbar_arrive_expect_tx(bar, (unsigned)(8 * (3 * NN + RB * N)));
     bulk_g2s(QY, Qy, 8u * NN, bar);
     bulk_g2s(QX, Qx, 8u * NN, bar);
     bulk_g2s(QXT, QxT, 8u * NN, bar);
     bulk_g2s(LP, Lp + (size_t)i0 * N, 8u * RB * N, bar);
   }
+  SMG_PDL_WAIT();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar + 1, 8u * NN);
+    bulk_g2s(F, f, 8u * NN, bar + 1);
+  }
   __syncthreads();
   mbar_wait(bar, 0);
+  mbar_wait(bar + 1, 0);
   const int i = tid / N, x = tid - i * N;   // one (row, column) output per thread
   // T1[i][x] = sum_k Qy[k][i0+i] F[k][x]
   T1[tid] = pc_dot<N>(QY + i0 + i, N, F + x, N);
@@ -569,7 +577,7 @@ template <int N>
 int pinv_sq_launch(const double* Qx, const double* QxT, const double* Qy, const double* Lp, const double* f,
                    double* u, cudaStream_t st) {
   constexpr int CLN = N / 4;
-  const size_t smem = sizeof(double) * (5 * (size_t)N * N + 8 * (size_t)N) + 16;
+  const size_t smem = sizeof(double) * (5 * (size_t)N * N + 8 * (size_t)N) + 32;
   static DeviceFlag attr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(pinv_sq_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

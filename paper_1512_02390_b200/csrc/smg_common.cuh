@@ -100,6 +100,13 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double* sbuf /*32*
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
   } while (0)
 
+// Split form for kernels with a prologue that reads nothing the preceding
+// grid writes (constant tables, mbarrier setup): SMG_PDL_TRIGGER() first, the
+// prologue, then SMG_PDL_WAIT() before the first dependent global access --
+// the prologue overlaps the previous kernel's tail.
+#define SMG_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory")
+#define SMG_PDL_WAIT() asm volatile("griddepcontrol.wait;\n" ::: "memory")
+
 bool pdl_enabled();
 // Integer tuning knob from the environment (read once per name by the caller).
 int env_int(const char* name, int def);

@@ -395,7 +395,10 @@ constexpr bool kFdtSkip = false;
 template <int P, int NO, int TX, int TY, bool DM>
 __global__ void __launch_bounds__(FDTK<P, NO, TX, TY, DM>::NT, FDTK<P, NO, TX, TY, DM>::MINB)
 fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
-  SMG_PDL_ENTRY();
+  // PDL: the prologue below (barriers, factor fragments, the 1/(lam_y+lam_x)
+  // table -- all per-level constants) overlaps the preceding grid; the wait
+  // sits before the first read of r / u
+  SMG_PDL_TRIGGER();
   using G = FDTGeom<P, NO, TX, TY>;
   using K = FDTK<P, NO, TX, TY, DM>;
   constexpr int M = G::M, MM = G::MM, E = G::E, OX = G::OX, OY = G::OY, RX = G::RX, RY = G::RY;
@@ -446,6 +449,7 @@ fdt_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   if constexpr (K::SDV)
     for (int idx = tid; idx < M * M; idx += NT) SD[idx] = A.dinv[idx];
   __syncthreads();
+  SMG_PDL_WAIT();
 
   // residual box of tile t into buffer b (all threads call; thread 0 owns TMA).
   // The caller guarantees the buffer is free (its last store has been read).

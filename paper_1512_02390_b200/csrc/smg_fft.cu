@@ -103,7 +103,7 @@ __device__ __forceinline__ double mu_of(int k, int n, const double* tw) {
 __global__ void __launch_bounds__(1024) fft_pinv_small_kernel(int nx, int ny, int lx, int ly, double cx, double cy,
                                                               const __grid_constant__ FftConsts C,
                                                               const double* __restrict__ f, double* __restrict__ u) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();
   extern __shared__ __align__(16) double2 zs[];
   const int PX = nx + 1;      // padded row pitch: column FFTs are bank-conflict free
   double2* Z = zs;            // ny x PX
@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(1024) fft_pinv_small_kernel(int nx, int ny, in
   const int n = nx * ny;
   for (int i = threadIdx.x; i < nx; i += blockDim.x) TX[i] = C.twx[i];
   for (int i = threadIdx.x; i < ny; i += blockDim.x) TY[i] = C.twy[i];
+  SMG_PDL_WAIT();   // the twiddles (parameters) are staged while the preceding grid drains
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int y = i >> lx, x = i & (nx - 1);
     Z[y * PX + brev(x, lx)] = make_double2(f[i], 0.0);

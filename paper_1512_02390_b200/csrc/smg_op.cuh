@@ -272,7 +272,7 @@ __device__ __forceinline__ void line_op_any(const OpArgs<P>& A, const double* x,
 template <int P, int TX, int TY, bool DIFF>
 __global__ void __launch_bounds__(OpGeom<P, TX, TY, DIFF>::THREADS)
 op_kernel(const __grid_constant__ OpArgs<P> A) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();   // the tables and barrier below are set up while the preceding grid drains
   using G = OpGeom<P, TX, TY, DIFF>;
   constexpr int NP = G::NP, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, NT = G::THREADS;
   extern __shared__ __align__(16) double smo[];
@@ -301,12 +301,14 @@ op_kernel(const __grid_constant__ OpArgs<P> A) {
       fence_mbar_init();
       mbar_arrive_expect_tx(bar, pwin_bytes(HX, HY, sh) * (DIFF ? 2u : 1u));
     }
+    SMG_PDL_WAIT();
     __syncthreads();
     if (tid < 32) {
       pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
       if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0 - P, Y0 - P, HX, HY, NU, DP, bar);
     }
   } else {
+    SMG_PDL_WAIT();
     for (int idx = tid; idx < HX * HY; idx += NT) {
       const int hy = idx / HX, hx = idx - hy * HX;
       const size_t g = (size_t)wrapi(Y0 - P + hy, N_y) * N_x + wrapi(X0 - P + hx, N_x);

@@ -43,7 +43,7 @@ struct OpdGeom {
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -182,6 +182,108 @@ __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0,
     }
 }
 
+// The vertex-only batch (the neighbour's node P) and the full batch of one
+// warp in lockstep: their DMMA chains interleave (8 independent accumulator
+// chains in the first product instead of 4 -- ncu put the opd warps on
+// DMMA-dependency and fragment-load stalls), each fragment load feeds both.
+// Same arithmetic as two opd_batch_eo calls.
+template <int P>
+__device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double* nv, const double* xf,
+                                                  const double* nf, int st, const double* WT,
+                                                  const double* __restrict__ frag, double& vlast,
+                                                  double (&Vb)[2][2], double (&Vm)[2][2]) {
+  constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+  static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
+  const int lane = threadIdx.x & 31, t = lane & 3;
+  const double* BE = frag;
+  const double* BO = frag + KH * NH * 32;
+  const double* BE2 = frag + 2 * KH * NH * 32;
+  const double* BO2 = frag + 3 * KH * NH * 32;
+  double W[2][NH][2], U[2][NH][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j = 0; j < NH; ++j) W[s][j][0] = W[s][j][1] = U[s][j][0] = U[s][j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int k = 4 * q + t;
+    double a[2], d[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double* x0 = s ? xf : xv;
+      const double xa = k <= H ? x0[k * st] : 0.0;
+      const double xb = k < H ? x0[(P - k) * st] : 0.0;
+      a[s] = xa + xb;
+      d[s] = k < H ? xa - xb : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double be = __ldg(BE + (q * NH + j) * 32 + lane), bo = __ldg(BO + (q * NH + j) * 32 + lane);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        dmma(W[s][j][0], W[s][j][1], a[s], be);
+        dmma(U[s][j][0], U[s][j][1], d[s], bo);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const double* n0 = s ? nf : nv;
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 8 * j + 2 * t + e;
+        double ga = 0.0, gd = 0.0;
+        if (n <= H) {
+          const double gn = (U[s][j][e] + W[s][j][e]) * (n0[n * st] * WT[n]);
+          const double gm = (U[s][j][e] - W[s][j][e]) * (n0[(P - n) * st] * WT[P - n]);
+          ga = n < H ? gn + gm : gn;
+          gd = n < H ? gn - gm : 0.0;
+        }
+        W[s][j][e] = ga;
+        U[s][j][e] = gd;
+      }
+  }
+  double W2[2][NH][2], U2[2][NH][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j = 0; j < NH; ++j) W2[s][j][0] = W2[s][j][1] = U2[s][j][0] = U2[s][j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+    double a[2], d[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double a0 = __shfl_sync(0xffffffffu, W[s][q >> 1][0], src);
+      const double a1 = __shfl_sync(0xffffffffu, W[s][q >> 1][1], src);
+      const double d0 = __shfl_sync(0xffffffffu, U[s][q >> 1][0], src);
+      const double d1 = __shfl_sync(0xffffffffu, U[s][q >> 1][1], src);
+      a[s] = (t & 1) ? a1 : a0;
+      d[s] = (t & 1) ? d1 : d0;
+    }
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double be = __ldg(BE2 + (q * NH + j) * 32 + lane), bo = __ldg(BO2 + (q * NH + j) * 32 + lane);
+      if (j == 0) {   // the vertex batch needs only the n-tile holding node 0 (its V[P])
+        dmma(W2[0][j][0], W2[0][j][1], a[0], be);
+        dmma(U2[0][j][0], U2[0][j][1], d[0], bo);
+      }
+      dmma(W2[1][j][0], W2[1][j][1], a[1], be);
+      dmma(U2[1][j][0], U2[1][j][1], d[1], bo);
+    }
+  }
+  vlast = U2[0][0][0] - W2[0][0][0];
+#pragma unroll
+  for (int j = 0; j < NH; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      Vb[j][e] = U2[1][j][e] + W2[1][j][e];
+      Vm[j][e] = U2[1][j][e] - W2[1][j][e];
+    }
+}
+
 // Poisson batch with the centro-symmetry L[P-i][P-j] = L[i][j] of L-hat:
 //   v[n] = (Ee a + L[H][n] c) + Oo d,   v[P-n] = (Ee a + L[H][n] c) - Oo d,
 //   Ee[k][n] = (L[k][n] + L[P-k][n]) / 2,  Oo[k][n] = (L[k][n] - L[P-k][n]) / 2
@@ -221,7 +323,7 @@ __device__ __forceinline__ void opd_batch_pe(const double* x0, int st, const dou
 template <int P, bool DIFF>
 __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const __grid_constant__ OpArgs<P> A,
                                                                         const double* __restrict__ frag) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();   // barrier + weight tables overlap the preceding grid; wait before u / nu / f
   using G = OpdGeom<P, DIFF>;
   constexpr int NP = G::NP, KT = G::KT, NTL = G::NTL, DP = G::DP, HX = G::HX, HY = G::HY;
   constexpr int OX = P, OY = P, NT = G::THREADS;
@@ -240,11 +342,14 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
   const int N_x = A.N_x, N_y = A.N_y;
 
   const int sh = pwin_shift(X0 - P, N_x);
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(bar, (DIFF ? 2u : 1u) * pwin_bytes(HX, HY, sh));
   }
+  SMG_PDL_WAIT();
   __syncthreads();
   if (tid < 32) {
     pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
@@ -260,8 +365,6 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
     const int idx = tid + k * NT;
     fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
   }
-  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
-  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
   mbar_wait(bar, 0);
   __syncthreads();
 
@@ -273,10 +376,10 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
     const double* ur = U + (y + P) * DP + sh;
     const double* nr = NU + (y + P) * DP + sh;
     if constexpr (DIFF) {
-      double Vb[2][2], Vm[2][2];
-      opd_batch_eo<P, true>(ur, nr, 1, WT, frag, Vb, Vm);   // left neighbour: its node P only
-      if (t == 0) VX[y * 2] = Vm[0][0];
-      opd_batch_eo<P, false>(ur + P, nr + P, 1, WT, frag, Vb, Vm);
+      double Vb[2][2], Vm[2][2], vl;
+      // left neighbour (its node P only) and the element's own row lines
+      opd_batch_eo_pair<P>(ur, nr, ur + P, nr + P, 1, WT, frag, vl, Vb, Vm);
+      if (t == 0) VX[y * 2] = vl;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -325,10 +428,10 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
       }
     };
     if constexpr (DIFF) {
-      double Vb[2][2], Vm[2][2];
-      opd_batch_eo<P, true>(uc, nc, DP, WT, frag, Vb, Vm);   // lower neighbour: its node P only
-      if (t == 0) VY[x * 2] = Vm[0][0];
-      opd_batch_eo<P, false>(uc + P * DP, nc + P * DP, DP, WT, frag, Vb, Vm);
+      double Vb[2][2], Vm[2][2], vl;
+      // lower neighbour (its node P only) and the element's own column lines
+      opd_batch_eo_pair<P>(uc, nc, uc + P * DP, nc + P * DP, DP, WT, frag, vl, Vb, Vm);
+      if (t == 0) VY[x * 2] = vl;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll

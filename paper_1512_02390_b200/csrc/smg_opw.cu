@@ -88,7 +88,7 @@ struct OpwGeom {
 
 template <int P, int TX, int TY>
 __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel(const __grid_constant__ OpwArgs<P> A) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();
   using G = OpwGeom<P, TX, TY>;
   constexpr int NW = G::NW, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, DP = G::DP, LDA = G::LDA;
   static_assert(2 * P <= 32, "row and column lines share one warp");
@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
     fence_mbar_init();
     mbar_arrive_expect_tx(bar, pwin_bytes(HX, HY, sh));
   }
+  SMG_PDL_WAIT();   // barrier set up while the preceding grid drains; u after it
   __syncthreads();
   if (warp == 0) pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
   // this warp's element

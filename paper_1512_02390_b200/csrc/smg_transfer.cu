@@ -255,7 +255,7 @@ constexpr int kTrWarps = 8;
 // prolongation, fine element e: u_f[e][a][b] (+)= sum J[a][ay] C[ay][ax] J[b][ax]
 template <int PC, int PF>
 __global__ void __launch_bounds__(32 * kTrWarps) prolong_warp_kernel(const __grid_constant__ TrArgs A) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();
   constexpr int NC = PC + 1;
   static_assert(32 % PF == 0 || PF % 32 == 0, "p_f must divide the warp");
   constexpr int LPR = PF < 32 ? 32 / PF : 1;     // output rows per warp instruction
@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(32 * kTrWarps) prolong_warp_kernel(const __gri
   const int ey = e / A.n_x, ex = e - ey * A.n_x;
   const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
   const bool act = e < n_el;
+  SMG_PDL_WAIT();   // J (a parameter) is staged above while the preceding grid drains
   // coarse element values (with the high-side shared nodes)
   if (act) {
     for (int i = lane; i < NC * NC; i += 32) {
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(32 * kTrWarps, 2) prolong_warp_g_kernel(const 
   const int ey = e / A.n_x, ex = e - ey * A.n_x;
   const int Nxc = A.n_x * PC, Nyc = A.n_y * PC, Nxf = A.n_x * PF;
   const bool act = e < n_el;
+  SMG_PDL_WAIT();   // J (a parameter) is staged above while the preceding grid drains
   if (act) {
     for (int i = lane; i < NC * NC; i += 32) {
       const int ay = i / NC, ax = i - ay * NC;
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(32 * tr_rwarps<PF>()) restrict_warp_kernel(con
 // restrict_warp_kernel's.
 template <int PC, int PF>
 __global__ void __launch_bounds__(128) restrict_blk_kernel(const __grid_constant__ TrArgs A) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();
   constexpr int NC = PC + 1, R3 = 3 * PF, LD = R3 + 1, R2 = 2 * PF;
   static_assert(R2 <= 32, "fine rows per warp");
   __shared__ double Js[(PF + 1) * NC];
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(128) restrict_blk_kernel(const __grid_constant
   const int bx = blockIdx.x % A.tiles_x, by = blockIdx.x / A.tiles_x;
   const int Nxf = A.n_x * PF, Nyf = A.n_y * PF, Nxc = A.n_x * PC;
   const int Y0 = (2 * by - 1) * PF, X0 = (2 * bx - 1) * PF;   // region origin (fine)
+  SMG_PDL_WAIT();
   {
     constexpr int NL = (R3 * R3 + 127) / 128;
     double v[NL];

@@ -106,11 +106,42 @@ class _Segment:
         self.g.replay()
 
 
+class _SolveState:
+    """Per-hierarchy solver workspace: the iterate, right-hand side and CG
+    vectors live in fixed buffers across solve() calls, so the cycle segments
+    are captured as CUDA graphs once per hierarchy and replayed by every later
+    solve (the caller gets a copy of the iterate)."""
+
+    def __init__(self, h: MultigridHierarchy):
+        shape = h.top.op.layout.shape
+        mk = lambda: torch.zeros(shape, dtype=torch.float64, device="cuda")  # noqa: E731
+        self.u, self.f, self.r_cur, self.r_new, self.p, self.q, self.z = (mk() for _ in range(7))
+        self.s = _Scalars()
+        self.graph = _graphable(h)
+        self.segs = {}
+
+    def seg(self, key, fn):
+        if key not in self.segs:
+            self.segs[key] = _Segment(fn, self.graph)
+        return self.segs[key]
+
+
+def _state(h: MultigridHierarchy) -> _SolveState:
+    st = getattr(h, "_solve_state", None)
+    if st is None or st.graph != _graphable(h):
+        st = _SolveState(h)
+        h._solve_state = st
+    return st
+
+
 def _start(h, f, cfg, u0):
     shape = h.top.op.layout.shape
-    f = to_device(f, shape)
-    u = to_device(random_initial_guess(h, cfg.seed) if u0 is None else u0, shape).clone()
-    return f, u
+    ws = _state(h)
+    ws.f.copy_(to_device(f, shape))
+    ws.u.copy_(to_device(random_initial_guess(h, cfg.seed) if u0 is None else u0, shape))
+    ws.s.dev.zero_()
+    ws.s.flag.zero_()
+    return ws.f, ws.u
 
 
 def solve_mg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
@@ -119,25 +150,27 @@ def solve_mg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
     h.reset_smoothers()
     op = h.top.op
     f, u = _start(h, f, cfg, u0)
-    r = torch.empty_like(u)
-    s = _Scalars()
+    ws = _state(h)
+    r = ws.r_cur
+    s = ws.s
     op.residual_into(u, f, r, norm2=s.dev[2:3])
     host, _ = s.read()
     res = [math.sqrt(float(host[2]))]
     r_max = res[0] / cfg.tol_reduction
     converged = res[0] <= r_max
     cycles = 0
+
     def cycle():
         _v_cycle(h, u, f)
         op.residual_into(u, f, r, norm2=s.dev[2:3])
-    seg = _Segment(cycle, _graphable(h))
+    seg = ws.seg("mg", cycle)
     while not converged and cycles < cfg.max_cycles:
         seg()
         cycles += 1
         host, _ = s.read()
         res.append(math.sqrt(float(host[2])))
         converged = res[-1] <= r_max
-    return u, ConvergenceReport(res, converged, cycles, time.perf_counter() - t0)
+    return u.clone(), ConvergenceReport(res, converged, cycles, time.perf_counter() - t0)
 
 
 def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
@@ -148,14 +181,11 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
     lib = N.lib()
     op = h.top.op
     f, u = _start(h, f, cfg, u0)
+    W = _state(h)
     n = u.numel()
-    r_cur = torch.empty_like(u)
-    r_new = torch.empty_like(u)
-    p = torch.empty_like(u)
-    q = torch.empty_like(u)
-    z = torch.empty_like(u)
+    r_cur, r_new, p, q, z = W.r_cur, W.r_new, W.p, W.q, W.z
     ws = h.reduce_ws
-    s = _Scalars()
+    s = W.s
     st = N.stream()
     op.residual_into(u, f, r_cur, norm2=s.dev[2:3])
     host, _ = s.read()
@@ -165,8 +195,6 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
     converged = res[0] <= r_max
     cycles = 0
     if not converged:
-        graph = _graphable(h)
-
         def step(ra, rb):
             # krylov.py:91-103: q = A p, alpha = delta / p.q, u += alpha p, rb = ra - alpha q
             def run():
@@ -187,16 +215,19 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
                 N.check(lib.smg_cg_direction(N.ptr(p), N.ptr(z), n, N.ptr(s.dev), st), "cg_direction")
             return run
 
-        bufs = (r_cur, r_new)
-        # segments between two host reads: the first (r_old = 0) and the two
-        # buffer parities of the steady state
-        first = step(bufs[0], bufs[1])
-        seg = {0: _Segment(lambda: (precond(bufs[1], None)(), step(bufs[1], bufs[0])()), graph),
-               1: _Segment(lambda: (precond(bufs[0], bufs[1])(), step(bufs[0], bufs[1])()), graph),
-               2: _Segment(lambda: (precond(bufs[1], bufs[0])(), step(bufs[1], bufs[0])()), graph)}
-        _v_cycle(h, p, r_cur, u_zero=True)
-        N.check(lib.smg_dot(N.ptr(p), N.ptr(r_cur), n, N.ptr(s.dev[0:1]), N.ptr(ws), st), "dot")
-        first()
+        def start():
+            # p = V(r0), delta = p.r0, then the first step
+            st = N.stream()
+            _v_cycle(h, p, r_cur, u_zero=True)
+            N.check(lib.smg_dot(N.ptr(p), N.ptr(r_cur), n, N.ptr(s.dev[0:1]), N.ptr(ws), st), "dot")
+            step(r_cur, r_new)()
+
+        # segments between two host reads: the start, the first precondition
+        # (r_old = 0) and the two buffer parities of the steady state
+        seg = [W.seg("cg0", lambda: (precond(r_new, None)(), step(r_new, r_cur)())),
+               W.seg("cg1", lambda: (precond(r_cur, r_new)(), step(r_cur, r_new)())),
+               W.seg("cg2", lambda: (precond(r_new, r_cur)(), step(r_new, r_cur)()))]
+        W.seg("cgs", start)()
         for it in range(cfg.max_cycles):
             host, flag = s.read()
             if flag:
@@ -210,4 +241,4 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
             seg[0 if it == 0 else (1 if it % 2 == 1 else 2)]()
     report = ConvergenceReport(res, converged, cycles, time.perf_counter() - t0)
     report.breakdown = breakdown
-    return u, report
+    return u.clone(), report

@@ -265,6 +265,26 @@ def coarse_solve(h: MultigridHierarchy, f0) -> torch.Tensor:
     return u0
 
 
+_NVTX = os.environ.get("SMG_NVTX", "0") == "1"
+
+
+class _Range:
+    """NVTX range (SMG_NVTX=1; a no-op otherwise) so that nsys / ncu --nvtx
+    timelines show the V-cycle's levels and phases by name."""
+    __slots__ = ("name",)
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX:
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
+
+
 def _chain_levels(h: MultigridHierarchy) -> int:
     """Levels 1..K whose prolongations run as one launch (smg_prolongate_chain):
     orders 2^l up to p = 16 and no post-smoothing below level K.  Cached per
@@ -307,27 +327,29 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
     top = h.top
     top.u, top.f = u, f
     for l in range(L, 0, -1):
-        lv = h.levels[l]
-        zero = u_zero if l == L else True
-        if zero and not lv.n_pre:
-            lv.u.zero_()
-        if lv.n_pre:
-            if isinstance(lv.smoother, MultiplicativeSchwarz):
-                if zero:
-                    lv.u.zero_()
-                lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_pre)
+        with _Range(f"down p={h.levels[l].basis.p}"):
+            lv = h.levels[l]
+            zero = u_zero if l == L else True
+            if zero and not lv.n_pre:
+                lv.u.zero_()
+            if lv.n_pre:
+                if isinstance(lv.smoother, MultiplicativeSchwarz):
+                    if zero:
+                        lv.u.zero_()
+                    lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_pre)
+                else:
+                    N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
+                                                   N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_pre, int(zero), st),
+                            "smooth")
+                zero = False
+            fc = h.levels[l - 1].f
+            if zero:
+                N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.f), N.ptr(fc), st), "restrict")
             else:
-                N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                               N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_pre, int(zero), st),
-                        "smooth")
-            zero = False
-        fc = h.levels[l - 1].f
-        if zero:
-            N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.f), N.ptr(fc), st), "restrict")
-        else:
-            N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
-                                              N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st), "residual_restrict")
-    _coarse_into(h, h.levels[0].f, h.levels[0].u)
+                N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                  N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st), "residual_restrict")
+    with _Range("coarse"):
+        _coarse_into(h, h.levels[0].f, h.levels[0].u)
     K = _chain_levels(h)
     if K >= 2:
         # levels 1..K prolongated in one launch (n_post = 0 below level K)
@@ -335,17 +357,18 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
     else:
         K = 0
     for l in range(max(K, 1), L + 1):
-        lv = h.levels[l]
-        if l > K:
-            N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
-                    "prolongate")
-        if lv.n_post:
-            if isinstance(lv.smoother, MultiplicativeSchwarz):
-                lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)
-            else:
-                N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                               N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_post, 0, st),
-                        "smooth")
+        with _Range(f"up p={h.levels[l].basis.p}"):
+            lv = h.levels[l]
+            if l > K:
+                N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(h.levels[l - 1].u), N.ptr(lv.u), 1, st),
+                        "prolongate")
+            if lv.n_post:
+                if isinstance(lv.smoother, MultiplicativeSchwarz):
+                    lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)
+                else:
+                    N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
+                                                   N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_post, 0, st),
+                            "smooth")
     return u
 
 
