@@ -273,7 +273,7 @@ class AdditiveSchwarz:
         self._work = None
         # ring workspace of the tiled kernel (caller-owned scratch, include/smg.h);
         # one per smoother: calls on one smoother are stream-ordered
-        self.ring = torch.empty(max(1, int(N.lib().smg_schwarz_ws_doubles(self._h.raw))), dtype=torch.float64,
+        self.ring = torch.zeros(max(1, int(N.lib().smg_schwarz_ws_doubles(self._h.raw))), dtype=torch.float64,
                                 device="cuda")
 
     def _workspace(self):
