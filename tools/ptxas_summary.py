@@ -1,11 +1,12 @@
 """Summarise ptxas -v logs: registers and spills per kernel (demangled-ish)."""
 import glob
+import os
 import re
 import sys
 
 pat = sys.argv[1] if len(sys.argv) > 1 else "fdt_kernel"
 rows = {}
-for f in glob.glob("build/smg/*.ptxas.log"):
+for f in glob.glob(os.environ.get("PTXAS_GLOB", "build/smg/*.ptxas.log")):
     name = None
     for line in open(f):
         m = re.search(r"Compiling entry function '(\S+)'", line)
