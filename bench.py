@@ -310,9 +310,13 @@ def run_strips(args, world, rank, local, dev):
     torch.cuda.synchronize()
     launches_per_step = lib.smg_launch_count() - n0
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    # SMG_STRIP_GRAPH=1: replay the strip V-cycle (NCCL halos and all-gather
+    # included) as one captured CUDA graph -- opt-in: validated on one GPU only
+    use_graph = os.environ.get("SMG_STRIP_GRAPH", "0") == "1"
+    step = (lambda: sol.v_cycle_graph(u, f)) if use_graph else (lambda: sol.v_cycle(u, f))
     for _ in range(args.warmup):
         flush.fill_(1.0)
-        sol.v_cycle(u, f)
+        step()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -323,7 +327,7 @@ def run_strips(args, world, rank, local, dev):
         flush.fill_(1.0)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        sol.v_cycle(u, f)
+        step()
         b.record()
         torch.cuda.synchronize()
         t_steps += a.elapsed_time(b) / 1e3
@@ -377,7 +381,7 @@ def run_strips(args, world, rank, local, dev):
                            "global_dofs": ndof, "parallelism": f"{world} element-row strips "
                            f"({plan.s} rows + 1 ghost row each side), NCCL halo send/recv, NCCL all-gather + "
                            "replicated coarse solve",
-                           "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": False,
+                           "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": use_graph,
                            "strong_scaling_reference": "the N=1 line's c3_single_gpu"},
                 "e2e": {"value": ndof * args.steps / t_e2e, "unit": "DOF/s",
                         "h2d_bytes_per_step": 8 * f.numel() * world, "d2h_bytes_per_step": own_bytes * world},

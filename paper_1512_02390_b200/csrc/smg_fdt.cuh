@@ -288,6 +288,10 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 
 // Kernel-level constants: DM selects the even/odd DMMA contraction stages
 // (8 warps; factor fragments in shared memory) instead of the DFMA stages.
+#ifndef SMG_FDT_DMB
+#define SMG_FDT_DMB 2   // 8-line batches per warp iteration of the DMMA stages
+#endif
+
 template <int P, int NO, int TX, int TY, bool DM>
 struct FDTK {
   using G = FDTGeom<P, NO, TX, TY>;
@@ -301,7 +305,7 @@ struct FDTK {
   // chains interleave (2 (MTE + MTO) independent DMMAs per k-step: the chains
   // were latency-bound with one batch, ncu stall_wait); the warp count is the
   // smallest that keeps the fewest iterations per warp (balanced batches)
-  static constexpr int DMB = 2;
+  static constexpr int DMB = SMG_FDT_DMB;
   static constexpr int dm_warps() {
     int it_min = (BT + DMB * 12 - 1) / (DMB * 12);
     for (int w = 4; w <= 12; ++w)

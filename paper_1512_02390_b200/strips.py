@@ -327,8 +327,8 @@ class StripSolver:
       correct(l, r, u, zero)            u += M r (zero: u := M r), ghost windows off
       restrict(l, fine, out)            out (level l-1) = P^T fine
       prolong_add(l, coarse, fine)
-      coarse_full(f0_full) -> u0_full   global p=1 solve
-      full_zeros0()                     new global p=1 array
+      coarse_local(f0_full, u0)         global p=1 solve, the rank's rows into u0
+      full0                             preallocated global p=1 array
       scalars()                         (scal[8], flag) device block
       dot(a, b, out)                    out[0] = a . b   (owned slices)
       dot2(z, r, r_old, out)            out[0] = z.(r - r_old), out[1] = z.r
@@ -394,16 +394,34 @@ class StripSolver:
             self.tr.exchange(r, p, p, 0)
             e.restrict(l, r, fs[l - 1])
         # replicated coarse solve
-        p0 = e.orders[0]
         f0_full = e.full0
         self.tr.allgather_rows(fs[0][self.own(0)], f0_full)
-        u0_full = e.coarse_full(f0_full)
-        e.copy(us[0], u0_full[self.plan.global_rows(p0)])
+        e.coarse_local(f0_full, us[0])
         for l in range(1, L + 1):
             self.tr.exchange(us[l - 1], e.orders[l - 1], 0, 1)
             e.prolong_add(l, us[l - 1], us[l])
             if e.n_post[l]:
                 self._smooth(l, us[l], fs[l], e.n_post[l], False)
+        return u
+
+    def v_cycle_graph(self, u, f):
+        """The strip V-cycle captured once as a CUDA graph for fixed (u, f)
+        buffers and replayed (opt-in: the NCCL point-to-point and all-gather
+        are captured with it -- validated on one GPU only, with the world-1
+        transport, since the pool has one GPU per call)."""
+        import torch
+        key = (u.data_ptr(), f.data_ptr())
+        if getattr(self, "_graph_key", None) != key:
+            self.v_cycle(u, f)                      # this call's cycle, eagerly (sets kernel attributes)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):  # recorded, not executed
+                self.v_cycle(u, f)
+            torch.cuda.current_stream().wait_stream(side)
+            self._graph, self._graph_key = g, key
+            return u
+        self._graph.replay()
         return u
 
     def solve_mg(self, f, u, tol=1e10, max_cycles=200):
@@ -520,6 +538,8 @@ class GpuEngine:
         # global p=1 coarse problem, replicated on every rank
         self.hc = _coarse_only(gm, nu_hat, nu_shift, coarse, coarse_tol)
         self.full0 = torch.zeros((plan.n_y, plan.n_x), dtype=torch.float64, device="cuda")
+        self.u0_full = torch.zeros_like(self.full0)
+        self.rows0 = torch.as_tensor(plan.global_rows(self.orders[0]), dtype=torch.long, device="cuda")
         self.ws = torch.zeros(N.lib().smg_reduce_ws_doubles(), dtype=torch.float64, device="cuda")
         self._scal = torch.zeros(8, dtype=torch.float64, device="cuda")
         self._flag = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -565,9 +585,13 @@ class GpuEngine:
         N.check(N.lib().smg_prolongate(self.h.levels[l].transfer.handle.raw, N.ptr(coarse), N.ptr(fine), 1,
                                        N.stream()), "strip prolong")
 
-    def coarse_full(self, f0_full):
-        from .multigrid import coarse_solve
-        return coarse_solve(self.hc, f0_full)
+    def coarse_local(self, f0_full, u0):
+        """The replicated global p=1 solve into preallocated buffers (graph-
+        capturable for the pseudo-inverse), the rank's rows gathered by a
+        device index."""
+        from .multigrid import _coarse_into
+        _coarse_into(self.hc, f0_full, self.u0_full)
+        self.torch.index_select(self.u0_full, 0, self.rows0, out=u0)
 
     # -- BLAS-1 on owned slices, device scalars
     def scalars(self):

@@ -70,3 +70,47 @@ def test_strip_diffusion_mg(cuda_device):
     for _, res in out:
         assert len(res) == len(rep.residuals)
         assert np.max(np.abs(np.log10(np.asarray(res) / np.asarray(rep.residuals)))) < 1e-6
+
+
+def test_strip_vcycle_graph_world1(cuda_device):
+    """The strip V-cycle captured as a CUDA graph (StripSolver.v_cycle_graph)
+    equals the eager strip V-cycle bitwise; world-1 TorchTransport (its halo
+    copies are device ops, so the capture covers the whole cycle)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1512_02390_b200.strips import TorchTransport
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        n, p = 16, 8
+        N = n * p
+        f = O.project_mean(np.random.default_rng(5).standard_normal((N, N)))
+        u0 = np.random.default_rng(6).random((N, N))
+        plan = StripPlan(n, n, 1.0, 1.0, 1, 0)
+        rows = plan.global_rows(p)
+        outs = []
+        for graph in (False, True):
+            eng = GpuEngine(plan, p, P.OverlapRule("fixed", 1))
+            sol = StripSolver(plan, eng, TorchTransport(plan))
+            fl = torch.from_numpy(f[rows].copy()).cuda()
+            u = torch.from_numpy(u0[rows].copy()).cuda()
+            for _ in range(3):
+                if graph:
+                    sol.v_cycle_graph(u, fl)
+                else:
+                    sol.v_cycle(u, fl)
+            torch.cuda.synchronize()
+            outs.append(u[plan.own(p)].cpu().numpy())
+        assert np.array_equal(outs[0], outs[1])
+        h = P.build_hierarchy(P.MeshConfig(n, n, 1.0, 1.0), p, P.OverlapRule("fixed", 1))
+        want = torch.from_numpy(u0).cuda()
+        for _ in range(3):
+            P.v_cycle(h, want, f)
+        assert maxrel(outs[1], want.cpu().numpy()) < 1e-11
+    finally:
+        dist.destroy_process_group()

@@ -73,8 +73,9 @@ class OracleEngine:
     def prolong_add(self, l, coarse, fine):
         fine.add_(torch.from_numpy(O.prolongate(self.h, l, coarse.numpy())))
 
-    def coarse_full(self, f0):
-        return torch.from_numpy(O.coarse_solve(self.hg, f0.numpy()))
+    def coarse_local(self, f0, u0):
+        full = O.coarse_solve(self.hg, f0.numpy())
+        u0.copy_(torch.from_numpy(full[self.plan.global_rows(self.orders[0])]))
 
     # device-scalar BLAS-1 restated on host tensors (krylov.py:91-111)
     def scalars(self):
