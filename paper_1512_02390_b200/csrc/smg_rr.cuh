@@ -41,7 +41,7 @@ struct RRGeom {
 
 template <int PC, int PF, int T, bool DIFF>
 __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const __grid_constant__ RRArgs<PF> R) {
-  SMG_PDL_ENTRY();
+  SMG_PDL_TRIGGER();   // tables and barrier set up while the preceding grid drains; wait before u / nu / f
   using G = RRGeom<PC, PF, T, DIFF>;
   using OG = typename G::OG;
   constexpr int P = PF, TX = T + 1, TY = T + 1, NP = P + 1;
@@ -70,11 +70,13 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
   const int X0 = (tx * T - 1) * P, Y0 = (ty * T - 1) * P;
 
   const int sh = pwin_shift(X0 - P, N_x);
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(bar, pwin_bytes(HX, HY, sh) * (DIFF ? 2u : 1u));
   }
+  SMG_PDL_WAIT();
   __syncthreads();
   if (tid < 32) {
     pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
@@ -86,7 +88,6 @@ __global__ void __launch_bounds__(RRGeom<PC, PF, T, DIFF>::NT) rr_kernel(const _
     const int idx = tid + k * NT;
     fv[k] = idx < OX * OY ? __ldg(A.f + (size_t)wrapi(Y0 + idx / OX, N_y) * N_x + wrapi(X0 + idx % OX, N_x)) : 0.0;
   }
-  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
   mbar_wait(bar, 0);
   __syncthreads();
 
