@@ -456,6 +456,7 @@ def main():
     import torch.distributed as dist
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver counts ranks / sees NVLS in the log
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # ... on stderr: stdout carries only the JSON line
         ngpu = torch.cuda.device_count()
         local = local % max(ngpu, 1)
         torch.cuda.set_device(local)
