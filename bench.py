@@ -276,10 +276,10 @@ def run_reference(args):
 def _strip_setup(cfg, world, rank, dev):
     import torch
     import paper_1512_02390_b200 as P
-    from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, TorchTransport
+    from paper_1512_02390_b200.strips import GpuEngine, StripPlan, StripSolver, make_transport
     plan = StripPlan(cfg["n_x"], cfg["n_y"], cfg["l_x"], cfg["l_y"], world, rank)
     eng = GpuEngine(plan, cfg["p"], P.OverlapRule.parse(cfg["rule"]))
-    sol = StripSolver(plan, eng, TorchTransport(plan))
+    sol = StripSolver(plan, eng, make_transport(plan))
     p = cfg["p"]
     N = (p * cfg["n_y"], p * cfg["n_x"])
     f_host = P.project_mean(np.random.default_rng(cfg["seed"]).standard_normal(N))

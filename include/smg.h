@@ -215,6 +215,46 @@ int smg_problem_field(int kind, int p, int n_x, int n_y, double dx, double dy, c
 int smg_element_mean(int p, int n_x, int n_y, const double* weights, const double* nu, double* out,
                      void* stream);
 
+/* ---- strip halos and strip collectives over NCCL -------
+ * The reference runs in one process; at a strip boundary these replace the
+ * periodic wrap of its windows and element gathers (mesh.py:97-105, 124-139)
+ * and the global sums of its inner products (krylov.py:91-111).  Rank g of
+ * nranks owns element rows [g s, (g+1) s); its neighbours are g-1 (below) and
+ * g+1 (above) mod nranks, so one rank wraps onto itself (NCCL self send/recv).
+ * A field t is (rows, row_len) row-major on the device; rows [lo, hi) are
+ * owned, ghost rows lie below lo and at/above hi (lo >= below and
+ * hi + above <= rows, else SMG_EINVAL).  NCCL is loaded at run time
+ * (libnccl.so.2); without it these return SMG_EUNSUPPORTED.  All calls enqueue
+ * on the caller's stream (graph-capturable), none synchronizes. */
+typedef struct smg_halo smg_halo_t;
+/* 1 if NCCL could be loaded. */
+int smg_halo_available(void);
+/* NCCL version code of the loaded library (0 if none). */
+int smg_halo_nccl_version(void);
+/* Rank 0 draws the communicator id (n_bytes >= 128) and sends it to the
+ * others out of band (torch.distributed broadcast, a file, MPI ...). */
+int smg_halo_unique_id(unsigned char* out, int n_bytes);
+/* Join the communicator on `device` (collective over the nranks ranks). */
+int smg_halo_create(const unsigned char* id, int n_bytes, int nranks, int rank, int device, smg_halo_t** out);
+int smg_halo_destroy(smg_halo_t* h);
+/* Forward halo: ghost rows [lo - below, lo) <- the lower neighbour's top
+ * `below` owned rows, ghost rows [hi, hi + above) <- the upper neighbour's
+ * bottom `above` owned rows. */
+int smg_halo_exchange(const smg_halo_t* h, double* t, int64_t rows, int64_t row_len, int64_t lo, int64_t hi,
+                      int below, int above, void* stream);
+/* Reverse halo: the contributions in ghost rows [lo - below, lo) go to the
+ * lower neighbour and those in [hi, hi + above) to the upper one; each rank
+ * adds what it receives to its owned rows -- rows [lo, lo + above) first,
+ * then rows [hi - below, hi) (a fixed order, deterministic).  ws: caller-owned,
+ * smg_halo_ws_doubles(row_len, below, above) doubles. */
+int64_t smg_halo_ws_doubles(int64_t row_len, int below, int above);
+int smg_halo_exchange_add(const smg_halo_t* h, double* t, int64_t rows, int64_t row_len, int64_t lo, int64_t hi,
+                          int below, int above, double* ws, void* stream);
+/* In-place sum of x[0..n) over the ranks (the strip-parallel dots). */
+int smg_halo_allreduce(const smg_halo_t* h, double* x, int64_t n, void* stream);
+/* full[r n_per_rank + i] <- rank r's own[i] (the replicated p = 1 coarse RHS). */
+int smg_halo_allgather(const smg_halo_t* h, const double* own, double* full, int64_t n_per_rank, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,16 @@ SIGNATURES = {
     "smg_cg_update2": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _i64, _dp, _dp, _dp, _vp]),
     "smg_cg_beta": (C.c_int, [_dp, _dp, _dp, _i64, _dp, _dp, _vp]),
     "smg_cg_beta_finish": (C.c_int, [_dp, _vp]),
+    "smg_halo_available": (C.c_int, []),
+    "smg_halo_nccl_version": (C.c_int, []),
+    "smg_halo_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "smg_halo_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "smg_halo_destroy": (C.c_int, [_vp]),
+    "smg_halo_exchange": (C.c_int, [_vp, _dp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _vp]),
+    "smg_halo_ws_doubles": (_i64, [_i64, C.c_int, C.c_int]),
+    "smg_halo_exchange_add": (C.c_int, [_vp, _dp, _i64, _i64, _i64, _i64, C.c_int, C.c_int, _dp, _vp]),
+    "smg_halo_allreduce": (C.c_int, [_vp, _dp, _i64, _vp]),
+    "smg_halo_allgather": (C.c_int, [_vp, _dp, _dp, _i64, _vp]),
     "smg_cg_direction": (C.c_int, [_dp, _dp, _i64, _dp, _vp]),
     "smg_project_mean": (C.c_int, [_dp, _i64, _dp, _vp]),
     "smg_sum": (C.c_int, [_dp, _i64, _dp, _dp, _vp]),

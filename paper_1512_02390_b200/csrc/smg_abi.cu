@@ -126,6 +126,8 @@ struct smg_coarse {
 };
 
 namespace smg {
+int ccg_cta_run(int nx, int ny, double cx, double cy, const double* f0, double* u0, double tol, int max_iter,
+                double* S, cudaStream_t st);
 int prolong_chain_run(int K, int n_x, int n_y, const double* const* J, const double* u0, double* const* u,
                       cudaStream_t st);
 }
@@ -684,6 +686,20 @@ int smg_coarse_cg(const smg_op_t* op, const double* f0, double* u0, double* ws, 
   double* S = red + smg_reduce_ws_doubles();
   int rc;
   cudaError_t e;
+  // Poisson meshes up to 64 x 64: the whole CG in one CTA (smg_blas.cu
+  // ccg_cta_kernel), one host read for the iteration count
+  static const int cta = env_int("SMG_CCG_CTA", 1);
+  if (cta && op->kind == 0 && n <= 4096) {
+    rc = ccg_cta_run(op->n_x, op->n_y, op->dy / op->dx, op->dx / op->dy, f0, u0, tol, max_iter, S, st);
+    if (rc != SMG_EUNSUPPORTED) {
+      if (rc) return rc;
+      double hs[6];
+      if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 6, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_cg");
+      if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_cg");
+      *iters_out = hs[4] != 0.0 ? (int)hs[5] : -max_iter;
+      return SMG_OK;
+    }
+  }
   // b = f0 - mean(f0); x = 0; r = b; p = r
   if ((e = cudaMemcpyAsync(b, f0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st))) return cuda_fail(e, "smg_coarse_cg");
   if ((rc = smg_project_mean(b, n, red, stream))) return rc;

@@ -282,6 +282,115 @@ __global__ void ccg_dot_kernel(const double* __restrict__ x, const double* __res
   reset_counter(ws);
 }
 
+// ---- the whole coarse CG in ONE CTA (Poisson, n_x n_y <= 4096) -------------
+// The p = 1 Poisson operator is the periodic 5-point stencil
+//   (A u)_ij = cx (2 u - u_W - u_E) + cy (2 u - u_S - u_N),  cx = dy/dx, cy = dx/dy
+// (PoissonOperator with the GLL p = 1 mass and stiffness, operators.py:30-54,
+// assembled).  x, r, p, q live in shared memory; every dot product is a fixed-
+// order block reduction (deterministic); the iteration is the reference's
+// plain CG (multigrid.py:196-228) with b = f0 - mean(f0), tol on ||r|| /
+// ||b||, at most max_iter steps, u0 = x - mean(x).  One launch replaces the
+// ~4 launches per iteration and the host polls of the grid-wide path.
+__device__ __forceinline__ double cta_sum(double v, double* sred) {
+  // fixed tree: warp shuffles, then warp 0 over the per-warp partials; broadcast
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();                  // sred free (previous broadcast consumed)
+  if (lane == 0) sred[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < nw ? sred[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sred[32] = t;
+  }
+  __syncthreads();
+  return sred[32];
+}
+
+__global__ void __launch_bounds__(1024) ccg_cta_kernel(int nx, int ny, double cx, double cy,
+                                                      const double* __restrict__ f0, double* __restrict__ u0,
+                                                      double tol, int max_iter, double* S) {
+  SMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double csm[];
+  const int n = nx * ny, tid = threadIdx.x, NT = blockDim.x;
+  double* x = csm;
+  double* r = x + n;
+  double* p = r + n;
+  double* q = p + n;
+  double* sred = q + n;   // 33 doubles
+  double v = 0.0;
+  for (int i = tid; i < n; i += NT) {
+    const double fi = f0[i];
+    r[i] = fi;
+    v += fi;
+  }
+  const double mean = cta_sum(v, sred) / (double)n;
+  v = 0.0;
+  for (int i = tid; i < n; i += NT) {
+    const double bi = r[i] - mean;
+    r[i] = bi;
+    p[i] = bi;
+    x[i] = 0.0;
+    v = fma(bi, bi, v);
+  }
+  const double bb = cta_sum(v, sred);
+  int it = 0;
+  bool ok = bb == 0.0;
+  double rho = bb;
+  const double thr = tol * sqrt(bb);
+  while (!ok && it < max_iter) {
+    ++it;
+    v = 0.0;
+    for (int i = tid; i < n; i += NT) {
+      const int iy = i / nx, ix = i - iy * nx;
+      const double c = p[i];
+      const double w = p[iy * nx + (ix == 0 ? nx - 1 : ix - 1)], e = p[iy * nx + (ix == nx - 1 ? 0 : ix + 1)];
+      const double so = p[(iy == 0 ? ny - 1 : iy - 1) * nx + ix], no = p[(iy == ny - 1 ? 0 : iy + 1) * nx + ix];
+      const double qi = cx * ((c + c) - w - e) + cy * ((c + c) - so - no);
+      q[i] = qi;
+      v = fma(c, qi, v);
+    }
+    const double alpha = rho / cta_sum(v, sred);
+    v = 0.0;
+    for (int i = tid; i < n; i += NT) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+      r[i] = ri;
+      v = fma(ri, ri, v);
+    }
+    const double rr = cta_sum(v, sred);
+    if (sqrt(rr) <= thr) { ok = true; break; }
+    const double beta = rr / rho;
+    rho = rr;
+    for (int i = tid; i < n; i += NT) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+    __syncthreads();
+  }
+  v = 0.0;
+  for (int i = tid; i < n; i += NT) v += x[i];
+  const double xm = cta_sum(v, sred) / (double)n;
+  for (int i = tid; i < n; i += NT) u0[i] = x[i] - xm;
+  if (tid == 0) {
+    S[4] = ok ? 1.0 : 0.0;
+    S[5] = (double)it;
+  }
+}
+
+int ccg_cta_run(int nx, int ny, double cx, double cy, const double* f0, double* u0, double tol, int max_iter,
+                double* S, cudaStream_t st) {
+  const long n = (long)nx * ny;
+  if (n > 4096 || n < 1) return SMG_EUNSUPPORTED;
+  const size_t smem = sizeof(double) * (4 * (size_t)n + 33);
+  static DeviceFlag attr;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ccg_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(double) * (4 * 4096 + 33)));
+    if (e != cudaSuccess) return cuda_fail(e, "ccg_cta_kernel smem attribute");
+    attr = true;
+  }
+  launch(ccg_cta_kernel, dim3(1), dim3(1024), smem, st, nx, ny, cx, cy, f0, u0, tol, max_iter, S);
+  return check_launch("ccg_cta_kernel");
+}
+
 int ccg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro,
                int rn, double tol, int it, double* ws, cudaStream_t st) {
   launch(ccg_update_kernel, dim3(grid_for_reduce(n)), dim3(kReduceThreads), 0, st, x, r, p, q, n, S, ro, rn, tol, it, ws);

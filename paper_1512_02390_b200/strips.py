@@ -36,7 +36,9 @@ Redundant work: the ghost element rows of the operator and transfer kernels,
 2/s of a strip (the masked Schwarz windows still cost their contractions).
 
 The driver is written against two small interfaces so the same code runs
-(a) one process per GPU over NCCL (``TorchTransport``), (b) CPU gloo ranks
+(a) one process per GPU over NCCL -- libsmg's own halo and collective entry
+points (``NcclHaloTransport``, smg_halo_* in include/smg.h) or
+torch.distributed's (``TorchTransport``), (b) CPU gloo ranks
 in the tests with an oracle engine, and (c) several ranks emulated by
 threads on one GPU (``ThreadTransport``) for single-device validation.
 """
@@ -226,6 +228,105 @@ class TorchTransport:
         else:
             parts = list(full.chunk(self.plan.world, 0))
             self.dist.all_gather(parts, src, group=self.group)
+
+
+class NcclHaloTransport:
+    """The strip halos and collectives through libsmg's own NCCL entry points
+    (``smg_halo_*``, include/smg.h): device buffers, the caller's stream, no
+    host round trip -- a strip V-cycle with its halos captures into one CUDA
+    graph.  The communicator id is drawn by rank 0 and broadcast over the
+    torch.distributed group (any backend); one rank needs no process group
+    and exchanges with itself (NCCL self send/recv).  Same semantics and the
+    same fixed addition order as ``TorchTransport``."""
+
+    def __init__(self, plan: StripPlan, group=None, device=None):
+        import ctypes as C
+        import torch
+        from . import _native as NV
+        self.plan = plan
+        self.NV = NV
+        lib = NV.lib()
+        if not lib.smg_halo_available():
+            raise RuntimeError("smg_halo: NCCL could not be loaded")
+        uid = C.create_string_buffer(128)
+        if plan.rank == 0:
+            NV.check(lib.smg_halo_unique_id(uid, 128), "smg_halo_unique_id")
+        raw = uid.raw
+        if plan.world > 1:
+            import torch.distributed as dist
+            box = [raw if plan.rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            raw = box[0]
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        h = C.c_void_p()
+        NV.check(lib.smg_halo_create(raw, 128, plan.world, plan.rank, self.device, C.byref(h)), "smg_halo_create")
+        self.h = h
+        self._ws = {}
+
+    def close(self):
+        """Destroy the communicator.  Release every CUDA graph that captured
+        this transport's calls first (StripSolver.release_graph): NCCL keeps
+        captured work alive and ncclCommDestroy waits for it."""
+        if self.h is not None and self.h.value:
+            self.NV.check(self.NV.lib().smg_halo_destroy(self.h), "smg_halo_destroy")
+        self.h = None
+
+    @staticmethod
+    def _field(t):
+        if t.dim() != 2 or not t.is_contiguous() or not t.is_cuda:
+            raise ValueError("halo fields are contiguous 2-D device arrays")
+        return t.shape[1]
+
+    def exchange(self, t, p: int, below: int, above: int):
+        lo, hi = _rows(self.plan, p)
+        NV = self.NV
+        NV.check(NV.lib().smg_halo_exchange(self.h, t.data_ptr(), t.shape[0], self._field(t), lo, hi, below, above,
+                                            NV.stream()), "smg_halo_exchange")
+
+    def exchange_add(self, t, p: int, below: int, above: int):
+        import torch
+        lo, hi = _rows(self.plan, p)
+        NV = self.NV
+        row_len = self._field(t)
+        key = (row_len, below, above)
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = self._ws[key] = torch.empty(max(1, NV.lib().smg_halo_ws_doubles(*key)), dtype=torch.float64,
+                                             device=t.device)
+        NV.check(NV.lib().smg_halo_exchange_add(self.h, t.data_ptr(), t.shape[0], row_len, lo, hi, below, above,
+                                                ws.data_ptr(), NV.stream()), "smg_halo_exchange_add")
+
+    def allreduce_(self, x):
+        if not x.is_contiguous():
+            raise ValueError("allreduce_ needs a contiguous tensor")
+        NV = self.NV
+        NV.check(NV.lib().smg_halo_allreduce(self.h, x.data_ptr(), x.numel(), NV.stream()), "smg_halo_allreduce")
+        return x
+
+    def allgather_rows(self, own, full):
+        if not own.is_contiguous() or not full.is_contiguous() or full.numel() != own.numel() * self.plan.world:
+            raise ValueError("allgather_rows: contiguous own rows and a (world x own) full array")
+        NV = self.NV
+        NV.check(NV.lib().smg_halo_allgather(self.h, own.data_ptr(), full.data_ptr(), own.numel(), NV.stream()),
+                 "smg_halo_allgather")
+
+
+def make_transport(plan: StripPlan, group=None):
+    """The transport for a GPU strip solver: libsmg's NCCL halos
+    (``NcclHaloTransport``) unless SMG_HALO=torch selects torch.distributed's
+    point-to-point (``TorchTransport``; also the choice for non-NCCL groups)."""
+    import os
+    choice = os.environ.get("SMG_HALO", "nccl")
+    if choice == "torch":
+        return TorchTransport(plan, group)
+    if choice != "nccl":
+        raise ValueError(f"SMG_HALO must be 'nccl' or 'torch', not {choice!r}")
+    if plan.world > 1:
+        import torch.distributed as dist
+        if dist.get_backend(group) != "nccl":
+            return TorchTransport(plan, group)
+    return NcclHaloTransport(plan, group)
 
 
 class ThreadTransport:
@@ -423,6 +524,12 @@ class StripSolver:
             return u
         self._graph.replay()
         return u
+
+    def release_graph(self):
+        """Drop the captured V-cycle graph (before closing an NCCL transport)."""
+        import torch
+        torch.cuda.synchronize()
+        self._graph, self._graph_key = None, None
 
     def solve_mg(self, f, u, tol=1e10, max_cycles=200):
         """krylov.py:49-67 on strips; f, u local (u = initial guess, updated)."""

@@ -189,3 +189,27 @@ def test_strip_plan_geometry():
     with pytest.raises(ValueError):
         StripPlan(4, 6, 2.0, 2.0, 4, 0)
     assert StripPlan(4, 8, 2.0, 2.0, 4, 0).below() == 3
+
+
+def test_make_transport_choice(monkeypatch):
+    """SMG_HALO selects the strip transport; unknown values fail loudly."""
+    from paper_1512_02390_b200.strips import StripPlan, TorchTransport, make_transport
+    import socket
+    import torch.distributed as dist
+    plan = StripPlan(4, 4, 1.0, 1.0, 1, 0)
+    monkeypatch.setenv("SMG_HALO", "mpi")
+    with pytest.raises(ValueError):
+        make_transport(plan)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        monkeypatch.setenv("SMG_HALO", "torch")
+        assert isinstance(make_transport(plan), TorchTransport)
+        # a two-rank plan over a non-NCCL group keeps torch.distributed's transport
+        monkeypatch.setenv("SMG_HALO", "nccl")
+        assert isinstance(make_transport(StripPlan(4, 4, 1.0, 1.0, 2, 0)), TorchTransport)
+    finally:
+        dist.destroy_process_group()
