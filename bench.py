@@ -270,7 +270,26 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": kind,
                              "sample": _cpu_sample(kind, len(times))},
             "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    """Keep stdout for the one JSON line: native libraries (NCCL prints its
+    version banner on fd 1) write to stderr from here on."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def _strip_setup(cfg, world, rank, dev):
@@ -310,9 +329,13 @@ def run_strips(args, world, rank, local, dev):
     torch.cuda.synchronize()
     launches_per_step = lib.smg_launch_count() - n0
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    # SMG_STRIP_GRAPH=1: replay the strip V-cycle (NCCL halos and all-gather
-    # included) as one captured CUDA graph -- opt-in: validated on one GPU only
-    use_graph = os.environ.get("SMG_STRIP_GRAPH", "0") == "1"
+    # replay the strip V-cycle (NCCL halos and all-gather included) as one
+    # captured CUDA graph: the default with libsmg's own halos (smg_halo_*,
+    # every call on the compute stream; the capture is tested on one GPU through
+    # NCCL self send/recv, tests/test_gpu_halo.py); SMG_STRIP_GRAPH=0/1 overrides
+    from paper_1512_02390_b200.strips import NcclHaloTransport
+    native = isinstance(sol.tr, NcclHaloTransport)
+    use_graph = os.environ.get("SMG_STRIP_GRAPH", "1" if native else "0") == "1"
     step = (lambda: sol.v_cycle_graph(u, f)) if use_graph else (lambda: sol.v_cycle(u, f))
     for _ in range(args.warmup):
         flush.fill_(1.0)
@@ -381,6 +404,8 @@ def run_strips(args, world, rank, local, dev):
                            "global_dofs": ndof, "parallelism": f"{world} element-row strips "
                            f"({plan.s} rows + 1 ghost row each side), NCCL halo send/recv, NCCL all-gather + "
                            "replicated coarse solve",
+                           "halo": ("libsmg smg_halo_* (NCCL, compute stream)" if native
+                                    else "torch.distributed point-to-point"),
                            "l2": "flushed (256 MiB write) before every timed step", "cuda_graph": use_graph,
                            "strong_scaling_reference": "the N=1 line's c3_single_gpu"},
                 "e2e": {"value": ndof * args.steps / t_e2e, "unit": "DOF/s",
@@ -388,7 +413,7 @@ def run_strips(args, world, rank, local, dev):
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
         if c4 is not None:
             line["c4_mgcg"] = c4
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -454,6 +479,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    _claim_stdout()
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver counts ranks / sees NVLS in the log
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # ... on stderr: stdout carries only the JSON line
@@ -473,6 +499,17 @@ def main():
     from paper_1512_02390_b200.multigrid import _v_cycle
 
     lib = NV.lib()
+    if world == 1 and os.environ.get("SMG_BENCH_STRIPS") == "1":
+        # testing aid: the N > 1 code path (strips, NCCL halos, graph) on one
+        # rank, its halos wrapping onto itself
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=dev)
+        return run_strips(args, world, rank, local, dev)
     if world > 1:
         return run_strips(args, world, rank, local, dev)
     c = CFG
@@ -812,7 +849,7 @@ def main():
             line["cpu_baseline"] = cpu
         if micro is not None:
             line["smoother_microbench"] = micro
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
