@@ -1127,5 +1127,7 @@ using FDTLaunchFn = int (*)(const FDTLaunch&, cudaStream_t);
 // dmma selects the even/odd FP64 tensor-core (DMMA) contraction engine of the
 // same kernel where it is compiled (m >= 27), else the DFMA engine.
 FDTLaunchFn fdt_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY, bool dmma);
+// Paired-line engine (smg_fdp.cuh) for (p, n_o) on this mesh, or nullptr; sets TX, TY.
+FDTLaunchFn fdp_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY);
 
 }  // namespace smg
