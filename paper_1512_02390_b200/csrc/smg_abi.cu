@@ -380,8 +380,9 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   const bool w_sym = wasym <= 1e-14 * (wmax > 0.0 ? wmax : 1.0);
   const bool eo_ok = w_sym && even_odd_split(S_x, m, s->Sxe, s->Sxo, px) &&
                      even_odd_split(S_y, m, s->Sye, s->Syo, py);
-  // SMG_FD_ENGINE=pair: the paired-line kernel (smg_fdp.cuh) where it is compiled
-  const bool want_pair = eng && std::strcmp(eng, "pair") == 0;
+  // the paired-line kernel (smg_fdp.cuh) where it is compiled, unless
+  // SMG_FD_ENGINE names one of the fdt_kernel engines
+  const bool want_pair = !eng || std::strcmp(eng, "pair") == 0;
   if (!(force && force[0] == '1') && eo_ok && want_pair)
     s->fdt = fdp_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY);
   if (!(force && force[0] == '1') && eo_ok &&

@@ -3,20 +3,36 @@
 namespace smg {
 namespace {
 struct Cfg { int p, n_o, tx, ty; FDTLaunchFn fn; };
+// per order: largest tile first (B200, 256^2 elements, us per correction: p = 16 4x4 175.0 /
+// 4x2 205.7; p = 24 4x2 441.4 / 2x2 509.0; p = 32 4x2 871.3 / 2x2 1055.8)
 const Cfg kCfgs[] = {
+  {8, 1, 4, 4, &fdp_launch_k<8, 1, 4, 4>},
+  {12, 1, 4, 4, &fdp_launch_k<12, 1, 4, 4>},
   {16, 1, 4, 4, &fdp_launch_k<16, 1, 4, 4>},
   {16, 1, 4, 2, &fdp_launch_k<16, 1, 4, 2>},
+  {24, 1, 4, 2, &fdp_launch_k<24, 1, 4, 2>},
+  {24, 1, 2, 2, &fdp_launch_k<24, 1, 2, 2>},
+  {32, 1, 4, 2, &fdp_launch_k<32, 1, 4, 2>},
+  {32, 1, 2, 2, &fdp_launch_k<32, 1, 2, 2>},
 };
 }  // namespace
 FDTLaunchFn fdp_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY) {
+  // the first (largest) tile that divides the mesh and still gives every SM a
+  // tile, else the divisible one with most tiles
+  static const int min_tiles = env_int("SMG_FDT_MIN_TILES", 148);
   static const int force_all = env_int("SMG_FDP_TILE", 0);  // TX*10+TY (tuning aid)
+  const Cfg* best = nullptr;
+  long best_tiles = -1;
   for (const Cfg& c : kCfgs) {
     if (c.p != p || c.n_o != n_o || n_x % c.tx || n_y % c.ty) continue;
     if (force_all && c.tx * 10 + c.ty != force_all) continue;
-    *TX = c.tx;
-    *TY = c.ty;
-    return c.fn;
+    const long tiles = (long)(n_x / c.tx) * (n_y / c.ty);
+    if (tiles >= min_tiles) { best = &c; break; }
+    if (tiles > best_tiles) { best = &c; best_tiles = tiles; }
   }
-  return nullptr;
+  if (!best) return nullptr;
+  *TX = best->tx;
+  *TY = best->ty;
+  return best->fn;
 }
 }  // namespace smg

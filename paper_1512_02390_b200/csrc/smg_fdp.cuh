@@ -55,7 +55,8 @@ struct FDPK {
   static constexpr int USZ = (UB + 15) & ~15;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)USZ + MM) + 16;
   static constexpr int by_smem = (int)((227 * 1024) / (SMEM + 1024));
-  static constexpr int by_regs = 65536 / (NT * 64);
+  static constexpr int REGS = 4 * HE + 24 < 64 ? 64 : ((4 * HE + 24 + 7) / 8) * 8;   // two lines of HE accumulators + addressing
+  static constexpr int by_regs = 65536 / (NT * REGS);
 #ifdef SMG_FDP_MINB
   static constexpr int MINB = SMG_FDP_MINB;   // tuning aid
 #else
@@ -65,17 +66,32 @@ struct FDPK {
   __host__ __device__ static constexpr int ry(int y) { return y < HE ? y : HE + (M - 1 - y); }
 };
 
-// out1[j], out2[j] = sum_l F[l*H + j] * in{1,2}(l): two lines share every factor entry
+// out1[j], out2[j] = sum_l F[l*H + j] * in{1,2}(l): two lines share every factor entry.
+// The l loop stays a loop (the j loop is unrolled: accumulators in registers): the
+// fully unrolled kernel was 100 KB of code at p = 32 and ncu's top stall was
+// instruction fetch (no_instruction 3.7 warps per issue at p = 32, 1.05 at p = 16).
+// Measured on B200 at 256^2 elements (tools/gpu/r2_pair_unr.sh, us per correction, unroll
+// 1 / 2 / 3 / 4 / full): p = 8: 66.5 62.5 62.3 60.4 62.5; p = 12: 115.6 111.6 109.6 109.6
+// 117.8; p = 16: 191.4 183.3 181.0 185.3 175.0; p = 24: 453.9 441.4 478.1 523.3 513.1;
+// p = 32: 1055.8 1204.3 1472.6 1298.4 1303.6.
+#ifdef SMG_FDP_UNR
+__host__ __device__ constexpr int fdp_unroll(int) { return SMG_FDP_UNR; }   // tuning aid
+#else
+__host__ __device__ constexpr int fdp_unroll(int H) { return H >= 16 ? 1 : H >= 12 ? 2 : H >= 9 ? H : 4; }
+#endif
 template <int H, class In1, class In2>
 __device__ __forceinline__ void fdp_contract2(const double* __restrict__ F, In1 in1, In2 in2, double (&o1)[H],
                                               double (&o2)[H]) {
 #pragma unroll
+  for (int j = 0; j < H; ++j) o1[j] = o2[j] = 0.0;
+  constexpr int UNR = fdp_unroll(H);
+#pragma unroll UNR
   for (int l = 0; l < H; ++l) {
     const double x1 = in1(l), x2 = in2(l);
 #pragma unroll
     for (int j = 0; j < H; ++j) {
-      o1[j] = l == 0 ? F[j] * x1 : fma(F[l * H + j], x1, o1[j]);
-      o2[j] = l == 0 ? F[j] * x2 : fma(F[l * H + j], x2, o2[j]);
+      o1[j] = fma(F[l * H + j], x1, o1[j]);
+      o2[j] = fma(F[l * H + j], x2, o2[j]);
     }
   }
 }
@@ -165,30 +181,40 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
     //      every thread has read the box
     double tA[HE], tD[HE];
     {
+      constexpr int UNR1 = fdp_unroll(HE);
       const int exl = e1 % TX, eyl = e1 / TX;
       const double* c1 = U + shift + (eyl * P) * BRX + exl * P + p1;
       const double* c2 = U + shift + (eyl * P) * BRX + exl * P + (M - 1 - p1);
       if (!odd) {
 #pragma unroll
-        for (int k = 0; k < HE; ++k) {
-          double s1, s2;
-          if (k < HO) {
-            s1 = c1[k * BRX] + c1[(M - 1 - k) * BRX];
-            s2 = c2[k * BRX] + c2[(M - 1 - k) * BRX];
-          } else {
-            s1 = c1[k * BRX];
-            s2 = c2[k * BRX];
-          }
+        for (int i = 0; i < HE; ++i) tA[i] = tD[i] = 0.0;
+#pragma unroll UNR1
+        for (int k = 0; k < HO; ++k) {
+          const double s1 = c1[k * BRX] + c1[(M - 1 - k) * BRX];
+          double s2 = c2[k * BRX] + c2[(M - 1 - k) * BRX];
           if (sg1) s2 = 0.0;
           const double a = s1 + s2, d = s1 - s2;
 #pragma unroll
           for (int i = 0; i < HE; ++i) {
-            tA[i] = k == 0 ? FSye[i] * a : fma(FSye[k * HE + i], a, tA[i]);
-            tD[i] = k == 0 ? FSye[i] * d : fma(FSye[k * HE + i], d, tD[i]);
+            tA[i] = fma(FSye[k * HE + i], a, tA[i]);
+            tD[i] = fma(FSye[k * HE + i], d, tD[i]);
+          }
+        }
+        if (CEN) {   // centre row of the window
+          const double s1 = c1[HO * BRX];
+          double s2 = c2[HO * BRX];
+          if (sg1) s2 = 0.0;
+          const double a = s1 + s2, d = s1 - s2;
+#pragma unroll
+          for (int i = 0; i < HE; ++i) {
+            tA[i] = fma(FSye[HO * HE + i], a, tA[i]);
+            tD[i] = fma(FSye[HO * HE + i], d, tD[i]);
           }
         }
       } else {
 #pragma unroll
+        for (int i = 0; i < HO; ++i) tA[i] = tD[i] = 0.0;
+#pragma unroll UNR1
         for (int k = 0; k < HO; ++k) {
           const double s1 = c1[k * BRX] - c1[(M - 1 - k) * BRX];
           double s2 = c2[k * BRX] - c2[(M - 1 - k) * BRX];
@@ -196,8 +222,8 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           const double a = s1 + s2, d = s1 - s2;
 #pragma unroll
           for (int i = 0; i < HO; ++i) {
-            tA[i] = k == 0 ? FSyo[i] * a : fma(FSyo[k * HO + i], a, tA[i]);
-            tD[i] = k == 0 ? FSyo[i] * d : fma(FSyo[k * HO + i], d, tD[i]);
+            tA[i] = fma(FSyo[k * HO + i], a, tA[i]);
+            tD[i] = fma(FSyo[k * HO + i], d, tD[i]);
           }
         }
       }
