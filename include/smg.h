@@ -87,6 +87,11 @@ int smg_schwarz_destroy(smg_schwarz_t* h);
  * contributions one tile hands to its neighbours within a correction.  0 for
  * the coloured dense path.  One workspace per concurrently running call. */
 size_t smg_schwarz_ws_doubles(const smg_schwarz_t* h);
+/* Which kernel the handle dispatches to (diagnostics, bench labels, tests):
+ * *engine = 0 coloured dense kernel, 1 tiled even/odd DFMA, 2 tiled even/odd
+ * DMMA, 3 paired-line tiled kernel; *tx, *ty = elements per tile (0 for the
+ * dense kernel).  Any pointer may be NULL. */
+int smg_schwarz_info(const smg_schwarz_t* h, int* engine, int* tx, int* ty);
 /* u += sum_s R_s^T W A_s^-1 R_s r (/ nu_bar): the additive correction of one
  * sweep given the residual r.  ws: smg_schwarz_ws_doubles(h) doubles.
  * Deterministic (no atomics). */

@@ -42,6 +42,7 @@ SIGNATURES = {
                                      _hp, _hp, _hp, _hp, _dp]),
     "smg_schwarz_destroy": (C.c_int, [_vp]),
     "smg_schwarz_ws_doubles": (C.c_size_t, [_vp]),
+    "smg_schwarz_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "smg_schwarz_correct": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
     "smg_schwarz_smooth": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, C.c_int, C.c_int, _vp]),
     "smg_fd_solve_blocks": (C.c_int, [_vp, _dp, _dp, C.c_int, C.c_int, _vp]),

@@ -107,6 +107,7 @@ struct smg_schwarz {
   double* dinv_perm;
   size_t ws_doubles;  // ring workspace the caller passes to correct / smooth
   bool eo_dmma;   // even/odd DMMA stages inside the TMA-pipelined tiled kernel
+  bool pair;      // paired-line kernel (smg_fdp.cuh)
 };
 
 struct smg_transfer {
@@ -383,8 +384,11 @@ int smg_schwarz_create(smg_schwarz_t** h, int p, int n_o, int n_x, int n_y, cons
   // the paired-line kernel (smg_fdp.cuh) where it is compiled, unless
   // SMG_FD_ENGINE names one of the fdt_kernel engines
   const bool want_pair = !eng || std::strcmp(eng, "pair") == 0;
-  if (!(force && force[0] == '1') && eo_ok && want_pair)
+  s->pair = false;
+  if (!(force && force[0] == '1') && eo_ok && want_pair) {
     s->fdt = fdp_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY);
+    s->pair = s->fdt != nullptr;
+  }
   if (!(force && force[0] == '1') && eo_ok &&
       (s->fdt != nullptr || (s->fdt = fdt_dispatch(p, n_o, n_x, n_y, &s->TX, &s->TY, s->eo_dmma)) != nullptr)) {
     s->ntx = n_x / s->TX; s->nty = n_y / s->TY;
@@ -422,6 +426,19 @@ static FDLaunch fd_base(const smg_schwarz_t* h) {
 }
 
 size_t smg_schwarz_ws_doubles(const smg_schwarz_t* h) { return h ? h->ws_doubles : 0; }
+
+int smg_schwarz_info(const smg_schwarz_t* h, int* engine, int* tx, int* ty) {
+  if (!h) return set_error("smg_schwarz_info: null handle"), SMG_EINVAL;
+  if (engine) {
+    int tx0 = 0, ty0 = 0;
+    const bool dm = h->tiled && !h->pair && h->eo_dmma &&
+                    h->fdt != fdt_dispatch(h->p, h->n_o, h->n_x, h->n_y, &tx0, &ty0, false);
+    *engine = !h->tiled ? 0 : h->pair ? 3 : dm ? 2 : 1;
+  }
+  if (tx) *tx = h->tiled ? h->TX : 0;
+  if (ty) *ty = h->tiled ? h->TY : 0;
+  return SMG_OK;
+}
 
 static int schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, double* ws, int u_zero,
                            void* stream) {

@@ -6,14 +6,21 @@ struct Cfg { int p, n_o, tx, ty; FDTLaunchFn fn; };
 // per order: largest tile first (B200, 256^2 elements, us per correction: p = 16 4x4 175.0 /
 // 4x2 205.7; p = 24 4x2 441.4 / 2x2 509.0; p = 32 4x2 871.3 / 2x2 1055.8)
 const Cfg kCfgs[] = {
+  {6, 1, 4, 4, &fdp_launch_k<6, 1, 4, 4>},
   {8, 1, 4, 4, &fdp_launch_k<8, 1, 4, 4>},
   {12, 1, 4, 4, &fdp_launch_k<12, 1, 4, 4>},
+  {12, 2, 4, 4, &fdp_launch_k<12, 2, 4, 4>},
   {16, 1, 4, 4, &fdp_launch_k<16, 1, 4, 4>},
   {16, 1, 4, 2, &fdp_launch_k<16, 1, 4, 2>},
+  {16, 2, 4, 4, &fdp_launch_k<16, 2, 4, 4>},
+  {16, 2, 4, 2, &fdp_launch_k<16, 2, 4, 2>},
   {24, 1, 4, 2, &fdp_launch_k<24, 1, 4, 2>},
   {24, 1, 2, 2, &fdp_launch_k<24, 1, 2, 2>},
+  {24, 3, 4, 2, &fdp_launch_k<24, 3, 4, 2>},
+  {24, 3, 2, 2, &fdp_launch_k<24, 3, 2, 2>},
   {32, 1, 4, 2, &fdp_launch_k<32, 1, 4, 2>},
   {32, 1, 2, 2, &fdp_launch_k<32, 1, 2, 2>},
+  {32, 4, 2, 2, &fdp_launch_k<32, 4, 2, 2>},
 };
 }  // namespace
 FDTLaunchFn fdp_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY) {

@@ -27,9 +27,38 @@
 //   * Stages 2-4 map lanes to ELEMENTS (element stride odd): every shared
 //     memory access of a half-warp hits 16 distinct banks.
 #pragma once
+#include <cstring>
+
 #include "smg_fdt.cuh"
 
 namespace smg {
+
+// Kernel arguments: as FDTArgs, with every factor row padded to an even
+// length and 16-byte aligned so that a uniform load brings two entries
+// (LDCU.128: one factor load per four DFMAs with two lines per thread).
+constexpr int fdp_pad(int h) { return (h + 1) & ~1; }
+template <int M>
+struct FDPArgs {
+  static constexpr int HE = fdt_he(M), HO = fdt_ho(M), HEP = fdp_pad(HE), HOP = fdp_pad(HO > 0 ? HO : 1);
+  CUtensorMap rmap;                   // residual (N_y, N_x), box (BRX, RY)
+  CUtensorMap umap;                   // u (N_y, N_x), box (OX, OY): L2 prefetch only
+  const double* __restrict__ r;
+  double* __restrict__ u;
+  const double* __restrict__ inv_nu;  // (n_y, n_x) or nullptr
+  const double* __restrict__ dinv;    // (M,M), [even | odd] eigen order in both dims
+  double* __restrict__ ws;            // ring workspace: ntiles * NRING
+  int N_x, N_y, n_x, ntx, nty;
+  int u_zero;
+  // analysis factors S[k][i] (row k padded), synthesis factors ST[i][k] times the weight w[k]
+  alignas(16) double Sye[HE * HEP];
+  alignas(16) double SyeT[HE * HEP];
+  alignas(16) double Sxe[HE * HEP];
+  alignas(16) double SxeT[HE * HEP];
+  alignas(16) double Syo[(HO > 0 ? HO : 1) * HOP];
+  alignas(16) double SyoT[(HO > 0 ? HO : 1) * HOP];
+  alignas(16) double Sxo[(HO > 0 ? HO : 1) * HOP];
+  alignas(16) double SxoT[(HO > 0 ? HO : 1) * HOP];
+};
 
 template <int P, int NO, int TX, int TY>
 struct FDPK {
@@ -79,26 +108,38 @@ __host__ __device__ constexpr int fdp_unroll(int) { return SMG_FDP_UNR; }   // t
 #else
 __host__ __device__ constexpr int fdp_unroll(int H) { return H >= 16 ? 1 : H >= 12 ? 2 : H >= 9 ? H : 4; }
 #endif
-template <int H, class In1, class In2>
+template <int H, int HP, class In1, class In2>
 __device__ __forceinline__ void fdp_contract2(const double* __restrict__ F, In1 in1, In2 in2, double (&o1)[H],
                                               double (&o2)[H]) {
 #pragma unroll
   for (int j = 0; j < H; ++j) o1[j] = o2[j] = 0.0;
   constexpr int UNR = fdp_unroll(H);
+  // the next step's inputs are loaded before this step's FMAs (a rolled loop is not
+  // software-pipelined by the compiler: short-scoreboard stalls at the loop top)
+  double x1 = in1(0), x2 = in2(0);
 #pragma unroll UNR
   for (int l = 0; l < H; ++l) {
-    const double x1 = in1(l), x2 = in2(l);
+    const double2* __restrict__ F2 = reinterpret_cast<const double2*>(F + l * HP);   // 16-byte aligned rows
+    const int ln = l + 1 < H ? l + 1 : l;
+    const double n1 = in1(ln), n2 = in2(ln);
 #pragma unroll
-    for (int j = 0; j < H; ++j) {
-      o1[j] = fma(F[l * H + j], x1, o1[j]);
-      o2[j] = fma(F[l * H + j], x2, o2[j]);
+    for (int j = 0; j < H; j += 2) {
+      const double2 fj = F2[j / 2];
+      o1[j] = fma(fj.x, x1, o1[j]);
+      o2[j] = fma(fj.x, x2, o2[j]);
+      if (j + 1 < H) {
+        o1[j + 1] = fma(fj.y, x1, o1[j + 1]);
+        o2[j + 1] = fma(fj.y, x2, o2[j + 1]);
+      }
     }
+    x1 = n1;
+    x2 = n2;
   }
 }
 
 template <int P, int NO, int TX, int TY>
 __global__ void __launch_bounds__(FDPK<P, NO, TX, TY>::NT, FDPK<P, NO, TX, TY>::MINB)
-fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
+fdp_kernel(const __grid_constant__ FDPArgs<P + 1 + 2 * NO> A) {
   SMG_PDL_TRIGGER();
   using G = FDTGeom<P, NO, TX, TY>;
   using K = FDPK<P, NO, TX, TY>;
@@ -106,6 +147,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
   constexpr int HE = G::HE, HO = G::HO, HOX = G::HOX, BRX = G::BRX, NRING = G::NRING;
   constexpr int NT = K::NT, NH = K::NH, NR = K::NR, ES = K::ES;
   constexpr bool CEN = K::CEN;
+  constexpr int HEP = fdp_pad(HE), HOP = fdp_pad(HOX);
   static_assert(K::SMEM <= 227 * 1024, "tile does not fit in shared memory");
   extern __shared__ __align__(1024) double sm[];
   double* U = sm;                  // residual box (row pitch BRX), then E element windows (stride ES, pitch M)
@@ -185,20 +227,33 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       const int exl = e1 % TX, eyl = e1 / TX;
       const double* c1 = U + shift + (eyl * P) * BRX + exl * P + p1;
       const double* c2 = U + shift + (eyl * P) * BRX + exl * P + (M - 1 - p1);
+      // one step = the four box values of rows k and m-1-k in the two columns; the next
+      // step's values are loaded before this step's FMAs (software pipelining by hand)
+      double v1a = c1[0], v1b = c1[(M - 1) * BRX], v2a = c2[0], v2b = c2[(M - 1) * BRX];
       if (!odd) {
 #pragma unroll
         for (int i = 0; i < HE; ++i) tA[i] = tD[i] = 0.0;
 #pragma unroll UNR1
         for (int k = 0; k < HO; ++k) {
-          const double s1 = c1[k * BRX] + c1[(M - 1 - k) * BRX];
-          double s2 = c2[k * BRX] + c2[(M - 1 - k) * BRX];
+          const int kn = k + 1 < HO ? k + 1 : k;
+          const double n1a = c1[kn * BRX], n1b = c1[(M - 1 - kn) * BRX];
+          const double n2a = c2[kn * BRX], n2b = c2[(M - 1 - kn) * BRX];
+          const double s1 = v1a + v1b;
+          double s2 = v2a + v2b;
           if (sg1) s2 = 0.0;
           const double a = s1 + s2, d = s1 - s2;
+          const double2* __restrict__ F2 = reinterpret_cast<const double2*>(FSye + k * HEP);
 #pragma unroll
-          for (int i = 0; i < HE; ++i) {
-            tA[i] = fma(FSye[k * HE + i], a, tA[i]);
-            tD[i] = fma(FSye[k * HE + i], d, tD[i]);
+          for (int i = 0; i < HE; i += 2) {
+            const double2 fi = F2[i / 2];
+            tA[i] = fma(fi.x, a, tA[i]);
+            tD[i] = fma(fi.x, d, tD[i]);
+            if (i + 1 < HE) {
+              tA[i + 1] = fma(fi.y, a, tA[i + 1]);
+              tD[i + 1] = fma(fi.y, d, tD[i + 1]);
+            }
           }
+          v1a = n1a; v1b = n1b; v2a = n2a; v2b = n2b;
         }
         if (CEN) {   // centre row of the window
           const double s1 = c1[HO * BRX];
@@ -207,8 +262,8 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
           const double a = s1 + s2, d = s1 - s2;
 #pragma unroll
           for (int i = 0; i < HE; ++i) {
-            tA[i] = fma(FSye[HO * HE + i], a, tA[i]);
-            tD[i] = fma(FSye[HO * HE + i], d, tD[i]);
+            tA[i] = fma(FSye[HO * HEP + i], a, tA[i]);
+            tD[i] = fma(FSye[HO * HEP + i], d, tD[i]);
           }
         }
       } else {
@@ -216,15 +271,25 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         for (int i = 0; i < HO; ++i) tA[i] = tD[i] = 0.0;
 #pragma unroll UNR1
         for (int k = 0; k < HO; ++k) {
-          const double s1 = c1[k * BRX] - c1[(M - 1 - k) * BRX];
-          double s2 = c2[k * BRX] - c2[(M - 1 - k) * BRX];
+          const int kn = k + 1 < HO ? k + 1 : k;
+          const double n1a = c1[kn * BRX], n1b = c1[(M - 1 - kn) * BRX];
+          const double n2a = c2[kn * BRX], n2b = c2[(M - 1 - kn) * BRX];
+          const double s1 = v1a - v1b;
+          double s2 = v2a - v2b;
           if (sg1) s2 = 0.0;
           const double a = s1 + s2, d = s1 - s2;
+          const double2* __restrict__ F2 = reinterpret_cast<const double2*>(FSyo + k * HOP);
 #pragma unroll
-          for (int i = 0; i < HO; ++i) {
-            tA[i] = fma(FSyo[k * HO + i], a, tA[i]);
-            tD[i] = fma(FSyo[k * HO + i], d, tD[i]);
+          for (int i = 0; i < HO; i += 2) {
+            const double2 fi = F2[i / 2];
+            tA[i] = fma(fi.x, a, tA[i]);
+            tD[i] = fma(fi.x, d, tD[i]);
+            if (i + 1 < HO) {
+              tA[i + 1] = fma(fi.y, a, tA[i + 1]);
+              tD[i + 1] = fma(fi.y, d, tD[i + 1]);
+            }
           }
+          v1a = n1a; v1b = n1b; v2a = n2a; v2b = n2b;
         }
       }
     }
@@ -256,7 +321,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       const double* d2 = SD + q2 * M + (odd ? HE : 0);
       if (!odd) {
         double t1[HE], t2[HE];
-        fdp_contract2<HE>(FSxe, [&](int l) { return r1[l]; }, [&](int l) { return r2[l]; }, t1, t2);
+        fdp_contract2<HE, HEP>(FSxe, [&](int l) { return r1[l]; }, [&](int l) { return r2[l]; }, t1, t2);
 #pragma unroll
         for (int j = 0; j < HE; ++j) {
           r1[j] = t1[j] * (d1[j] * s);
@@ -264,7 +329,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       } else {
         double t1[HOX], t2[HOX];
-        fdp_contract2<HOX>(FSxo, [&](int l) { return r1[l]; }, [&](int l) { return r2[l]; }, t1, t2);
+        fdp_contract2<HOX, HOP>(FSxo, [&](int l) { return r1[l]; }, [&](int l) { return r2[l]; }, t1, t2);
 #pragma unroll
         for (int j = 0; j < HO; ++j) {
           r1[j] = t1[j] * (d1[j] * s);
@@ -281,7 +346,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       double* c2 = B + q2 + (odd ? HE * M : 0);
       if (!odd) {
         double o1[HE], o2[HE];
-        fdp_contract2<HE>(FSyeT, [&](int i) { return c1[i * M]; }, [&](int i) { return c2[i * M]; }, o1, o2);
+        fdp_contract2<HE, HEP>(FSyeT, [&](int i) { return c1[i * M]; }, [&](int i) { return c2[i * M]; }, o1, o2);
 #pragma unroll
         for (int k = 0; k < HE; ++k) {
           c1[k * M] = o1[k];
@@ -289,7 +354,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       } else {
         double o1[HOX], o2[HOX];
-        fdp_contract2<HOX>(FSyoT, [&](int i) { return c1[i * M]; }, [&](int i) { return c2[i * M]; }, o1, o2);
+        fdp_contract2<HOX, HOP>(FSyoT, [&](int i) { return c1[i * M]; }, [&](int i) { return c2[i * M]; }, o1, o2);
 #pragma unroll
         for (int k = 0; k < HO; ++k) {
           c1[k * M] = o1[k];
@@ -307,7 +372,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
       double* r2 = B + q2 * M + (odd ? HE : 0);
       if (!odd) {
         double g1[HE], g2[HE];
-        fdp_contract2<HE>(FSxeT, [&](int j) { return r1[j]; }, [&](int j) { return r2[j]; }, g1, g2);
+        fdp_contract2<HE, HEP>(FSxeT, [&](int j) { return r1[j]; }, [&](int j) { return r2[j]; }, g1, g2);
 #pragma unroll
         for (int l = 0; l < HE; ++l) {
           if (sg2) {
@@ -319,7 +384,7 @@ fdp_kernel(const __grid_constant__ FDTArgs<P + 1 + 2 * NO> A) {
         }
       } else {
         double g1[HOX], g2[HOX];
-        fdp_contract2<HOX>(FSxoT, [&](int j) { return r1[j]; }, [&](int j) { return r2[j]; }, g1, g2);
+        fdp_contract2<HOX, HOP>(FSxoT, [&](int j) { return r1[j]; }, [&](int j) { return r2[j]; }, g1, g2);
 #pragma unroll
         for (int l = 0; l < HO; ++l) {
           if (sg2) {
@@ -445,26 +510,29 @@ int fdp_launch_k(const FDTLaunch& L, cudaStream_t st) {
   using G = FDTGeom<P, NO, TX, TY>;
   using K = FDPK<P, NO, TX, TY>;
   constexpr int M = G::M, HE = fdt_he(M), HO = fdt_ho(M);
-  FDTArgs<M> A;
+  FDPArgs<M> A;
+  constexpr int HEP = FDPArgs<M>::HEP, HOP = FDPArgs<M>::HOP;
   // umap only feeds the L2 prefetch of the tile's block of u (updated in place in global memory)
   if (!tmap_2d(&A.rmap, L.r, L.N_x, L.N_y, G::BRX, G::RY) || !tmap_2d(&A.umap, L.u, L.N_x, L.N_y, G::OX, G::OY))
     return SMG_EUNSUPPORTED;
   A.r = L.r; A.u = L.u; A.inv_nu = L.inv_nu; A.dinv = L.dinv; A.ws = L.ws;
   A.N_x = L.N_x; A.N_y = L.N_y; A.n_x = L.n_x; A.ntx = L.ntx; A.nty = L.nty;
   A.u_zero = L.u_zero;
-  A.phases = nullptr;
+  std::memset(A.Sye, 0, sizeof(A.Sye)); std::memset(A.SyeT, 0, sizeof(A.SyeT));
+  std::memset(A.Sxe, 0, sizeof(A.Sxe)); std::memset(A.SxeT, 0, sizeof(A.SxeT));
+  std::memset(A.Syo, 0, sizeof(A.Syo)); std::memset(A.SyoT, 0, sizeof(A.SyoT));
+  std::memset(A.Sxo, 0, sizeof(A.Sxo)); std::memset(A.SxoT, 0, sizeof(A.SxoT));
   // synthesis factors carry the (mirror-symmetric) weight of their output node
   for (int k = 0; k < HE; ++k)
     for (int i = 0; i < HE; ++i) {
-      A.Sye[k * HE + i] = L.Sye[k * HE + i]; A.SyeT[i * HE + k] = L.Sye[k * HE + i] * L.wy[k];
-      A.Sxe[k * HE + i] = L.Sxe[k * HE + i]; A.SxeT[i * HE + k] = L.Sxe[k * HE + i] * L.wx[k];
+      A.Sye[k * HEP + i] = L.Sye[k * HE + i]; A.SyeT[i * HEP + k] = L.Sye[k * HE + i] * L.wy[k];
+      A.Sxe[k * HEP + i] = L.Sxe[k * HE + i]; A.SxeT[i * HEP + k] = L.Sxe[k * HE + i] * L.wx[k];
     }
   for (int k = 0; k < HO; ++k)
     for (int i = 0; i < HO; ++i) {
-      A.Syo[k * HO + i] = L.Syo[k * HO + i]; A.SyoT[i * HO + k] = L.Syo[k * HO + i] * L.wy[k];
-      A.Sxo[k * HO + i] = L.Sxo[k * HO + i]; A.SxoT[i * HO + k] = L.Sxo[k * HO + i] * L.wx[k];
+      A.Syo[k * HOP + i] = L.Syo[k * HO + i]; A.SyoT[i * HOP + k] = L.Syo[k * HO + i] * L.wy[k];
+      A.Sxo[k * HOP + i] = L.Sxo[k * HO + i]; A.SxoT[i * HOP + k] = L.Sxo[k * HO + i] * L.wx[k];
     }
-  A.Syo[HO * HO] = A.SyoT[HO * HO] = A.Sxo[HO * HO] = A.SxoT[HO * HO] = 0.0;
   static DeviceInt grid_cap;
   if (grid_cap == 0) {
     if (K::SMEM > 48 * 1024) {

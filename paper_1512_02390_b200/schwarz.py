@@ -276,6 +276,14 @@ class AdditiveSchwarz:
         self.ring = torch.zeros(max(1, int(N.lib().smg_schwarz_ws_doubles(self._h.raw))), dtype=torch.float64,
                                 device="cuda")
 
+    def kernel_info(self):
+        """(engine, tile_x, tile_y) of the device kernel behind this smoother: engine is
+        'dense', 'tiled-dfma', 'tiled-dmma' or 'pair' (diagnostics and bench labels)."""
+        import ctypes as C
+        e, tx, ty = C.c_int(0), C.c_int(0), C.c_int(0)
+        N.check(N.lib().smg_schwarz_info(self._h.raw, C.byref(e), C.byref(tx), C.byref(ty)), "schwarz_info")
+        return ("dense", "tiled-dfma", "tiled-dmma", "pair")[e.value], tx.value, ty.value
+
     def _workspace(self):
         if self._work is None:
             self._work = torch.empty(self.layout.shape, dtype=torch.float64, device="cuda")

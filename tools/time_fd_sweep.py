@@ -19,6 +19,7 @@ cfgs = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]] or \
     [(256, 8), (256, 12), (256, 16), (256, 24), (256, 32), (128, 32), (64, 16)]
 engines = os.environ.get("ENGINES", "dfma").split(",")
 tag = os.environ.get("TAG", "lc" + os.environ.get("SMG_FDT_LC", "2"))
+NO = int(os.environ.get("NO", "1"))   # overlap layers
 
 
 def eo_flops_per_dof(p, n_o=1):
@@ -32,10 +33,10 @@ for n, p in cfgs:
     lay = P.layout_for(mesh, p)
     r = torch.randn(lay.shape, dtype=torch.float64, device="cuda")
     u = torch.zeros(lay.shape, dtype=torch.float64, device="cuda")
-    t_roof = max(24.0 * lay.size / HBM, eo_flops_per_dof(p) * lay.size / P64) * 1e6
+    t_roof = max(24.0 * lay.size / HBM, eo_flops_per_dof(p, NO) * lay.size / P64) * 1e6
     for eng in engines:
         os.environ["SMG_FD_ENGINE"] = eng
-        sm = P.AdditiveSchwarz(P.gll_basis(p), lay, mesh.dx, mesh.dy, 1, P.WeightKind.QUINTIC)
+        sm = P.AdditiveSchwarz(P.gll_basis(p), lay, mesh.dx, mesh.dy, NO, P.WeightKind.QUINTIC)
         for _ in range(3):
             sm.correct(r, u)
         ts = []
@@ -48,5 +49,5 @@ for n, p in cfgs:
             ts.append((a, b))
         torch.cuda.synchronize()
         t = sorted(x.elapsed_time(y) for x, y in ts)[10] * 1e3
-        print(f"{tag} {eng:8s} n={n:3d} p={p:2d}: {t:8.1f} us  {lay.size / t / 1e3:7.2f} GDOF/s  "
+        print(f"{tag} {eng:8s} {sm.kernel_info()} n_o={NO} n={n:3d} p={p:2d}: {t:8.1f} us  {lay.size / t / 1e3:7.2f} GDOF/s  "
               f"roof {t_roof:7.1f} us  frac {t_roof / t:.3f}", flush=True)
