@@ -128,6 +128,15 @@ int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* st
 /* fc = P^T (f - A u): residual fused with restriction (multigrid.py:244). */
 int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const double* u,
                           const double* f, double* fc, double* work, void* stream);
+/* Restriction with a caller-owned ring workspace: where the halo-free kernel
+ * is compiled (p_f = 16, 24, 32: one warp per fine element, high-side
+ * vertex rows handed over through the ring, a fixup launch adds them in a
+ * fixed order) smg_transfer_ws_doubles(h) > 0 and the _ws calls use it; with
+ * ws == NULL or 0 doubles they are smg_restrict / smg_residual_restrict. */
+size_t smg_transfer_ws_doubles(const smg_transfer_t* h);
+int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, double* ws, void* stream);
+int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const double* u,
+                             const double* f, double* fc, double* work, double* ws, void* stream);
 
 /* ---- p=1 coarse problem (replaces multigrid.py:196-228 coarse CG)
  * Poisson: exact pseudo-inverse by global fast diagonalization (zero mode

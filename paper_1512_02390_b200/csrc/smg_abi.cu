@@ -114,6 +114,7 @@ struct smg_transfer {
   int pc, pf, n_x, n_y;
   std::vector<double> J;
   smg::TrFn fn;
+  smg::RwFn rw;   // halo-free restriction (smg_rw.cu) or nullptr
 };
 
 struct smg_coarse {
@@ -520,6 +521,13 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   smg_transfer* t = new (std::nothrow) smg_transfer();
   if (!t) return SMG_ENOMEM;
   t->pc = p_c; t->pf = p_f; t->n_x = n_x; t->n_y = n_y; t->fn = fn;
+  // SMG_RW=0 keeps the tiled kernels (B200, us per restriction, tiled -> halo-free: C3 p_f = 32
+  // 176 -> 77; 256^2 p_f = 24 208 -> 157, p_f = 16 110 -> 69; C2 15.4 -> 13.3)
+  const int rw_mode = env_int("SMG_RW", 1);   // read per handle (create time only)
+  // p_f = 16 on small meshes (C2): the extra fixup launch costs more inside the V-cycle's
+  // dependent chain than the kernel gains (C2 V-cycle 105.2 -> 107.8 us with it)
+  const bool big = p_f >= 24 || (long)n_x * n_y >= 16384 || rw_mode == 2;
+  t->rw = (rw_mode && big) ? rw_dispatch(p_c, p_f) : nullptr;
   t->J.assign(J, J + (p_f + 1) * (p_c + 1));
   *h = t;
   return SMG_OK;
@@ -563,6 +571,29 @@ int smg_prolongate_chain(const smg_transfer_t* const* tr, int K, const double* u
 int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* stream) {
   if (!h || !ff || !fc) { set_error("smg_restrict: bad argument"); return SMG_EINVAL; }
   return tr_run(h, ff, fc, 0, false, as_stream(stream));
+}
+
+size_t smg_transfer_ws_doubles(const smg_transfer_t* h) {
+  return (h && h->rw) ? (size_t)h->n_x * h->n_y * (2 * h->pc + 1) : 0;
+}
+
+int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, double* ws, void* stream) {
+  if (!h || !ff || !fc) { set_error("smg_restrict_ws: bad argument"); return SMG_EINVAL; }
+  if (!h->rw || !ws) return smg_restrict(h, ff, fc, stream);
+  TrArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.src = ff; A.dst = fc; A.n_x = h->n_x; A.n_y = h->n_y;
+  std::memcpy(A.J, h->J.data(), sizeof(double) * h->J.size());
+  return h->rw(A, ws, as_stream(stream));
+}
+
+int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,
+                             double* fc, double* work, double* ws, void* stream) {
+  if (!h || !h->rw || !ws) return smg_residual_restrict(h, op, u, f, fc, work, stream);
+  if (!op || !u || !f || !fc || !work) { set_error("smg_residual_restrict_ws: bad argument"); return SMG_EINVAL; }
+  int rc = smg_op_residual(op, u, f, work, stream);
+  if (rc) return rc;
+  return smg_restrict_ws(h, work, fc, ws, stream);
 }
 
 int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,

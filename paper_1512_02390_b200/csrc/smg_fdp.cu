@@ -12,6 +12,7 @@ const Cfg kCfgs[] = {
   {12, 2, 4, 4, &fdp_launch_k<12, 2, 4, 4>},
   {16, 1, 4, 4, &fdp_launch_k<16, 1, 4, 4>},
   {16, 1, 4, 2, &fdp_launch_k<16, 1, 4, 2>},
+  {16, 1, 2, 2, &fdp_launch_k<16, 1, 2, 2>},
   {16, 2, 4, 4, &fdp_launch_k<16, 2, 4, 4>},
   {16, 2, 4, 2, &fdp_launch_k<16, 2, 4, 2>},
   {24, 1, 4, 2, &fdp_launch_k<24, 1, 4, 2>},

@@ -17,4 +17,9 @@ using TrFn = int (*)(const TrArgs&, int n_x, int n_y, bool prolong, cudaStream_t
 // launcher for (p_c, p_f) on an n_x x n_y mesh (largest compiled tile that divides it)
 TrFn transfer_dispatch(int pc, int pf);
 
+// Halo-free restriction (smg_rw.cu): warp per fine element + ring workspace of
+// n_x n_y (2 p_c + 1) doubles + fixup launch; nullptr where it is not compiled.
+using RwFn = int (*)(const TrArgs&, double* ring, cudaStream_t);
+RwFn rw_dispatch(int pc, int pf);
+
 }  // namespace smg

@@ -102,6 +102,12 @@ class _Transfer:
         N.check(N.lib().smg_transfer_create(C.byref(raw), p_c, p_f, n_x, n_y, j[1]), "transfer_create")
         self.handle = N.Handle(raw, "smg_transfer_destroy")
         self.J = np.asarray(J)
+        # ring workspace of the halo-free restriction (caller-owned scratch, include/smg.h)
+        nws = int(N.lib().smg_transfer_ws_doubles(raw))
+        self.ws = torch.zeros(nws, dtype=torch.float64, device="cuda") if nws else None
+
+    def ws_ptr(self):
+        return N.ptr(self.ws) if self.ws is not None else None
 
 
 class _CoarsePinv:
@@ -227,7 +233,8 @@ def restrict_residual(h: MultigridHierarchy, l: int, fine) -> torch.Tensor:
     lv = h.levels[l]
     ff = to_device(fine, lv.op.layout.shape)
     out = torch.empty(h.levels[l - 1].op.layout.shape, dtype=torch.float64, device="cuda")
-    N.check(N.lib().smg_restrict(lv.transfer.handle.raw, N.ptr(ff), N.ptr(out), N.stream()), "restrict")
+    N.check(N.lib().smg_restrict_ws(lv.transfer.handle.raw, N.ptr(ff), N.ptr(out), lv.transfer.ws_ptr(), N.stream()),
+            "restrict")
     return out
 
 
@@ -344,10 +351,12 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
                 zero = False
             fc = h.levels[l - 1].f
             if zero:
-                N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.f), N.ptr(fc), st), "restrict")
+                N.check(lib.smg_restrict_ws(lv.transfer.handle.raw, N.ptr(lv.f), N.ptr(fc), lv.transfer.ws_ptr(), st),
+                        "restrict")
             else:
-                N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
-                                                  N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st), "residual_restrict")
+                N.check(lib.smg_residual_restrict_ws(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                     N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), lv.transfer.ws_ptr(),
+                                                     st), "residual_restrict")
     with _Range("coarse"):
         _coarse_into(h, h.levels[0].f, h.levels[0].u)
     K = _chain_levels(h)
