@@ -66,6 +66,14 @@ int smg_op_destroy(smg_op_t* h);
 /* out = f - A u   (f == NULL: out = A u).  out must not alias u. */
 int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out,
                     void* stream);
+/* Ring workspace of the halo-free operator kernel (doubles, device; 0 where the
+ * operator has none: 2 p per element for the tensor-core kernels, diffusion
+ * p = 24 and Poisson p = 32).  With it, smg_op_residual_ws runs the element
+ * kernel on its own (p+1)^2 window only and a fixup launch adds the neighbours'
+ * vertex terms in a fixed order; ring == NULL is smg_op_residual. */
+size_t smg_op_ring_doubles(const smg_op_t* h);
+int smg_op_residual_ws(const smg_op_t* h, const double* u, const double* f, double* out, double* ring,
+                       void* stream);
 /* Like smg_op_residual, and also *norm2_out (device double) = ||out||^2
  * summed deterministically; ws (device) must hold smg_op_ws_doubles(h)
  * doubles (the per-CTA partials) and must not overlap norm2_out. */
@@ -102,6 +110,9 @@ int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, doub
  * never read). */
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
                        double* work, double* ws, int n_it, int u_is_zero, void* stream);
+/* Same, with the operator's ring workspace (smg_op_ring_doubles; NULL allowed). */
+int smg_schwarz_smooth_ws(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
+                          double* work, double* ws, double* op_ring, int n_it, int u_is_zero, void* stream);
 /* FastDiagSolver.solve on nb independent (m,m) blocks: out = W*(S_y(S_y^T B S_x ./ L)S_x^T).
  * apply_weight=0 skips W (the multiplicative / kind=None solver). */
 int smg_fd_solve_blocks(const smg_schwarz_t* h, const double* blocks, double* out, int nb,
@@ -132,11 +143,13 @@ int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const dou
  * is compiled (p_f = 16, 24, 32: one warp per fine element, high-side
  * vertex rows handed over through the ring, a fixup launch adds them in a
  * fixed order) smg_transfer_ws_doubles(h) > 0 and the _ws calls use it; with
- * ws == NULL or 0 doubles they are smg_restrict / smg_residual_restrict. */
+ * ws == NULL or 0 doubles they are smg_restrict / smg_residual_restrict.
+ * op_ring: the operator's ring workspace (smg_op_ring_doubles) or NULL. */
 size_t smg_transfer_ws_doubles(const smg_transfer_t* h);
 int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, double* ws, void* stream);
 int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const double* u,
-                             const double* f, double* fc, double* work, double* ws, void* stream);
+                             const double* f, double* fc, double* work, double* ws, double* op_ring,
+                             void* stream);
 
 /* ---- p=1 coarse problem (replaces multigrid.py:196-228 coarse CG)
  * Poisson: exact pseudo-inverse by global fast diagonalization (zero mode

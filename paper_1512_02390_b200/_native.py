@@ -54,7 +54,10 @@ SIGNATURES = {
     "smg_residual_restrict": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _vp]),
     "smg_transfer_ws_doubles": (C.c_size_t, [_vp]),
     "smg_restrict_ws": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
-    "smg_residual_restrict_ws": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _dp, _vp]),
+    "smg_residual_restrict_ws": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _dp, _dp, _vp]),
+    "smg_op_ring_doubles": (C.c_size_t, [_vp]),
+    "smg_op_residual_ws": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _vp]),
+    "smg_schwarz_smooth_ws": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_int, _vp]),
     "smg_coarse_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double]),
     "smg_coarse_destroy": (C.c_int, [_vp]),
     "smg_coarse_ws_doubles": (C.c_size_t, [_vp]),

@@ -280,10 +280,11 @@ int smg_op_destroy(smg_op_t* h) {
 }
 
 static int op_run(const smg_op_t* h, const double* u, const double* f, double* out, double* partials,
-                  cudaStream_t st) {
+                  cudaStream_t st, double* ring = nullptr) {
   const bool norm = partials != nullptr;
   OpLaunch L;
   L.u = u; L.f = f; L.out = out; L.nu = h->nu; L.partials = partials;
+  L.ring = ring;
   L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
@@ -298,6 +299,16 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
 int smg_op_residual(const smg_op_t* h, const double* u, const double* f, double* out, void* stream) {
   if (!h || !u || !out || u == out) { set_error("smg_op_residual: bad argument"); return SMG_EINVAL; }
   return op_run(h, u, f, out, nullptr, as_stream(stream));
+}
+
+size_t smg_op_ring_doubles(const smg_op_t* h) {
+  return (h && h->dfrag && opd_applies(h->p, h->kind != 0)) ? (size_t)h->n_x * h->n_y * 2 * h->p : 0;
+}
+
+int smg_op_residual_ws(const smg_op_t* h, const double* u, const double* f, double* out, double* ring,
+                       void* stream) {
+  if (!h || !u || !out || u == out) { set_error("smg_op_residual_ws: bad argument"); return SMG_EINVAL; }
+  return op_run(h, u, f, out, nullptr, as_stream(stream), smg_op_ring_doubles(h) ? ring : nullptr);
 }
 
 int smg_sum_partials(const double* part, int nb, double* out, void* stream);
@@ -482,6 +493,11 @@ int smg_schwarz_correct(const smg_schwarz_t* h, const double* r, double* u, doub
 
 int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
                        double* work, double* ws, int n_it, int u_is_zero, void* stream) {
+  return smg_schwarz_smooth_ws(h, op, u, f, work, ws, nullptr, n_it, u_is_zero, stream);
+}
+
+int smg_schwarz_smooth_ws(const smg_schwarz_t* h, const smg_op_t* op, double* u, const double* f,
+                          double* work, double* ws, double* op_ring, int n_it, int u_is_zero, void* stream) {
   if (!h || !op || !u || !f || !work || n_it < 0 || op->p != h->p || op->n_x != h->n_x || op->n_y != h->n_y ||
       (h->ws_doubles && !ws)) {
     set_error("smg_schwarz_smooth: bad argument");
@@ -490,7 +506,7 @@ int smg_schwarz_smooth(const smg_schwarz_t* h, const smg_op_t* op, double* u, co
   for (int it = 0; it < n_it; ++it) {
     const double* r = f;
     if (!(it == 0 && u_is_zero)) {
-      int rc = smg_op_residual(op, u, f, work, stream);
+      int rc = smg_op_residual_ws(op, u, f, work, op_ring, stream);
       if (rc) return rc;
       r = work;
     }
@@ -588,10 +604,11 @@ int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, doubl
 }
 
 int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,
-                             double* fc, double* work, double* ws, void* stream) {
-  if (!h || !h->rw || !ws) return smg_residual_restrict(h, op, u, f, fc, work, stream);
+                             double* fc, double* work, double* ws, double* op_ring, void* stream) {
+  const bool ring = op && op_ring && smg_op_ring_doubles(op) > 0;
+  if (!h || ((!h->rw || !ws) && !ring)) return smg_residual_restrict(h, op, u, f, fc, work, stream);
   if (!op || !u || !f || !fc || !work) { set_error("smg_residual_restrict_ws: bad argument"); return SMG_EINVAL; }
-  int rc = smg_op_residual(op, u, f, work, stream);
+  int rc = smg_op_residual_ws(op, u, f, work, op_ring, stream);
   if (rc) return rc;
   return smg_restrict_ws(h, work, fc, ws, stream);
 }

@@ -420,6 +420,7 @@ struct OpLaunch {
   const double* Mt;   // host (p+1)^2
   const double* w;    // host p+1
   const double* wasm; // host p
+  double* ring = nullptr;   // optional: 2 p doubles per element (halo-free opdh_kernel, smg_opd.cu)
 };
 
 // Host: operator constants of OpArgs (everything but the pointers / tiling).

@@ -191,6 +191,115 @@ template <int P>
 __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double* nv, const double* xf,
                                                   const double* nf, int st, const double* WT,
                                                   const double* __restrict__ frag, double& vlast,
+                                                  double (&Vb)[2][2], double (&Vm)[2][2]);
+
+// Two FULL batches in lockstep (the halo-free kernel: a warp's row batch, stride 1, and
+// its column batch, stride stc): the same interleaving of DMMA chains as
+// opd_batch_eo_pair, every fragment load feeds both.  Returns V[n] (Vb) and V[P-n] (Vm)
+// of both batches, n = 8j + 2t + e <= H.
+template <int P>
+__device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double* nr, const double* xc,
+                                                 const double* nc, int stc, const double* WT,
+                                                 const double* __restrict__ frag, double (&Vb)[2][2][2],
+                                                 double (&Vm)[2][2][2]) {
+  constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+  static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
+  const int lane = threadIdx.x & 31, t = lane & 3;
+  const double* BE = frag;
+  const double* BO = frag + KH * NH * 32;
+  const double* BE2 = frag + 2 * KH * NH * 32;
+  const double* BO2 = frag + 3 * KH * NH * 32;
+  double W[2][NH][2], U[2][NH][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j = 0; j < NH; ++j) W[s][j][0] = W[s][j][1] = U[s][j][0] = U[s][j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int k = 4 * q + t;
+    double a[2], d[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double* x0 = s ? xc : xr;
+      const int st = s ? stc : 1;
+      const double xa = k <= H ? x0[k * st] : 0.0;
+      const double xb = k < H ? x0[(P - k) * st] : 0.0;
+      a[s] = xa + xb;
+      d[s] = k < H ? xa - xb : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double be = __ldg(BE + (q * NH + j) * 32 + lane), bo = __ldg(BO + (q * NH + j) * 32 + lane);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        dmma(W[s][j][0], W[s][j][1], a[s], be);
+        dmma(U[s][j][0], U[s][j][1], d[s], bo);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const double* n0 = s ? nc : nr;
+    const int st = s ? stc : 1;
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 8 * j + 2 * t + e;
+        double ga = 0.0, gd = 0.0;
+        if (n <= H) {
+          const double gn = (U[s][j][e] + W[s][j][e]) * (n0[n * st] * WT[n]);
+          const double gm = (U[s][j][e] - W[s][j][e]) * (n0[(P - n) * st] * WT[P - n]);
+          ga = n < H ? gn + gm : gn;
+          gd = n < H ? gn - gm : 0.0;
+        }
+        W[s][j][e] = ga;
+        U[s][j][e] = gd;
+      }
+  }
+  double W2[2][NH][2], U2[2][NH][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j = 0; j < NH; ++j) W2[s][j][0] = W2[s][j][1] = U2[s][j][0] = U2[s][j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+    double a[2], d[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double a0 = __shfl_sync(0xffffffffu, W[s][q >> 1][0], src);
+      const double a1 = __shfl_sync(0xffffffffu, W[s][q >> 1][1], src);
+      const double d0 = __shfl_sync(0xffffffffu, U[s][q >> 1][0], src);
+      const double d1 = __shfl_sync(0xffffffffu, U[s][q >> 1][1], src);
+      a[s] = (t & 1) ? a1 : a0;
+      d[s] = (t & 1) ? d1 : d0;
+    }
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+      const double be = __ldg(BE2 + (q * NH + j) * 32 + lane), bo = __ldg(BO2 + (q * NH + j) * 32 + lane);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        dmma(W2[s][j][0], W2[s][j][1], a[s], be);
+        dmma(U2[s][j][0], U2[s][j][1], d[s], bo);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        Vb[s][j][e] = U2[s][j][e] + W2[s][j][e];
+        Vm[s][j][e] = U2[s][j][e] - W2[s][j][e];
+      }
+}
+
+template <int P>
+__device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double* nv, const double* xf,
+                                                  const double* nf, int st, const double* WT,
+                                                  const double* __restrict__ frag, double& vlast,
                                                   double (&Vb)[2][2], double (&Vm)[2][2]) {
   constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
   static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
@@ -473,6 +582,206 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
   }
 }
 
+// ---- halo-free variant ------------------------------------------------------
+// opd_kernel stages a (2P+1)^2 window (the element and its left / lower /
+// corner neighbours) and recomputes the neighbours' row and column lines for
+// their node-P vertex value: every u and nu value is read four times from L2
+// and the vertex batches cost 75 % of a full batch.  Here a CTA stages only
+// its own (P+1)^2 window, runs its P row lines and P column lines (a warp's
+// row batch and column batch in lockstep), and hands the node-P value of
+// every line to the right / upper neighbour through a ring workspace of 2P
+// doubles per element; opdh_fixup subtracts them (adds them for out = A u) at
+// the neighbours' low-side nodes with the weights the fused kernel applied,
+// in a fixed order (x term, then y term at the corner).
+template <int P, bool DIFF>
+struct OpdhGeom {
+  static constexpr int NP = P + 1;
+  static constexpr int DP = (NP + 2) & ~1;
+  static constexpr int WARPS = P / 8;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int WIN = ((DP * NP + 15) & ~15);          // one window (doubles), 128-byte multiple
+  static constexpr int NWIN = DIFF ? 2 : 1;                    // u (and nu)
+  // x-part buffer pitch = 2 (mod 8): the column-wise combine (fixed column, rows 2 t apart
+  // across the quad lanes) hits 16 distinct banks per half-warp (pitch P gave 4-way conflicts)
+  static constexpr int OXP = P + 2;
+  static constexpr size_t SMEM =
+      sizeof(double) * ((size_t)2 * NWIN * WIN + (size_t)P * OXP + (size_t)P + NP) + 32;
+  static_assert(P % 8 == 0, "lines must fill whole batches");
+};
+
+// Persistent: a CTA walks elements e = blockIdx.x, + gridDim.x, ... with the NEXT element's
+// window in flight (two window buffers, two mbarriers) while the current one is computed --
+// one element per CTA spent 35-45 % of its stall samples waiting for its own window.
+template <int P, bool DIFF>
+__global__ void __launch_bounds__(OpdhGeom<P, DIFF>::THREADS, DIFF ? 5 : 4)
+opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag, double* __restrict__ ring,
+            int n_el) {
+  SMG_PDL_TRIGGER();
+  using G = OpdhGeom<P, DIFF>;
+  constexpr int NP = G::NP, DP = G::DP, OX = P, OY = P, NT = G::THREADS, WIN = G::WIN, NWIN = G::NWIN, OXP = G::OXP;
+  extern __shared__ __align__(128) double smd[];
+  double* WB = smd;                          // [2][NWIN] windows: NP x DP of u (and nu), column shift sh
+  double* AX = WB + 2 * NWIN * WIN;          // OY x OXP x-parts, then x+y parts
+  double* WS = AX + OY * OXP;                // P assembled weights
+  double* WT = WS + P;                       // NP GLL weights
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WT + NP);   // [2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int N_x = A.N_x, N_y = A.N_y;
+
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  SMG_PDL_WAIT();
+  __syncthreads();
+  // window of element e into buffer b (warp 0 issues; the buffer's previous readers are past a barrier)
+  auto issue = [&](int e, int b) {
+    const int tx = e % A.tiles_x, ty = e / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    if (tid == 0) mbar_arrive_expect_tx(bar + b, (unsigned)NWIN * pwin_bytes(NP, NP, pwin_shift(X0, N_x)));
+    __syncwarp();
+    pwin_issue_warp(A.u, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN) * WIN, DP, bar + b);
+    if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN + 1) * WIN, DP, bar + b);
+  };
+  if (warp == 0 && (int)blockIdx.x < n_el) issue(blockIdx.x, 0);
+
+  int it = 0;
+  for (int el = blockIdx.x; el < n_el; el += gridDim.x, ++it) {
+    const int bsel = it & 1;
+    const int tx = el % A.tiles_x, ty = el / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    const int sh = pwin_shift(X0, N_x);
+    double* R = ring + (size_t)el * (2 * P);   // [0,P): node-P values of the row lines; [P,2P): column lines
+    if (warp == 0 && el + (int)gridDim.x < n_el) issue(el + gridDim.x, bsel ^ 1);
+    constexpr int KO = (OX * OY + NT - 1) / NT;
+    double fv[KO];
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = tid + k * NT;
+      fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
+    }
+    const double* U = WB + (bsel * NWIN) * WIN;
+    const double* NU = U + WIN;
+    mbar_wait(bar + bsel, (unsigned)(it >> 1) & 1u);
+
+    // warp w: row lines y = 8w..8w+7 and column lines x = 8w..8w+7 of the element
+    const int li = 8 * warp + g;          // this lane group's row AND column index
+    const double* ur = U + li * DP + sh;
+    const double* nr = NU + li * DP + sh;
+    const double* uc = U + sh + li;
+    const double* nc = NU + sh + li;
+    constexpr int NHO = (P / 2 + 8) / 8;
+    double Vb[2][NHO][2], Vm[2][NHO][2];   // [0]: row batch, [1]: column batch
+    if constexpr (DIFF) {
+      opd_batch_eo_two<P>(ur, nr, uc, nc, DP, WT, frag, Vb, Vm);
+    } else {
+      opd_batch_pe<P, false>(ur, 1, frag, Vb[0], Vm[0]);
+      opd_batch_pe<P, false>(uc, DP, frag, Vb[1], Vm[1]);
+    }
+    // x-parts of the own nodes; the node-P value of the row line goes to the ring
+#pragma unroll
+    for (int j = 0; j < NHO; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = 8 * j + 2 * t + e;
+        if (b <= P / 2) {
+          AX[li * OXP + b] = Vb[0][j][e];
+          if (b == 0) R[li] = Vm[0][j][e];
+          else if (b < P / 2) AX[li * OXP + (P - b)] = Vm[0][j][e];
+        }
+      }
+    __syncthreads();   // also: every thread is done with this element's window
+    // combine with the y-parts (column li); the node-P value of the column line goes to the ring
+    {
+      const double wyb = A.cy * WS[li];
+      auto put = [&](int a, double v) {
+        if (a < P) AX[a * OXP + li] = fma(A.cx * WS[a], AX[a * OXP + li], wyb * v);
+        else R[P + li] = v;
+      };
+#pragma unroll
+      for (int j = 0; j < NHO; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int a = 8 * j + 2 * t + e;
+          if (a <= P / 2) {
+            put(a, Vb[1][j][e]);
+            if (a < P / 2) put(P - a, Vm[1][j][e]);
+          }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < OX * OY) {
+        const int y = idx / OX, x = idx - y * OX;
+        const double val = AX[y * OXP + x];
+        A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = A.f != nullptr ? fv[k] - val : val;
+      }
+    }
+    __syncthreads();   // AX is rewritten by the next element
+  }
+}
+
+// One thread per low-side node of an element: (a, 0) for k = a < P takes the left
+// element's row-line value (and, at the corner a = 0, the lower element's column-line
+// value after it); (0, b) for k = P + b, b >= 1, the lower element's.
+template <int P>
+__global__ void __launch_bounds__(256) opdh_fixup(double* __restrict__ out, const double* __restrict__ ring, int n_x,
+                                                  int n_y, double cx, double cy, double sign,
+                                                  const __grid_constant__ OpArgs<P> A) {
+  SMG_PDL_ENTRY();
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)n_x * n_y * 2 * P) return;
+  const int e = (int)(gid / (2 * P)), k = (int)(gid - (long)e * (2 * P));
+  if (k == P) return;   // the corner is handled by k = 0
+  const int ey = e / n_x, ex = e - ey * n_x;
+  const int el = ey * n_x + wrapi(ex - 1, n_x), ed = wrapi(ey - 1, n_y) * n_x + ex;
+  const int a = k < P ? k : 0, b = k < P ? 0 : k - P;
+  double* o = out + (size_t)(ey * P + a) * ((size_t)n_x * P) + ex * P + b;
+  double v = *o;
+  if (k < P) v = fma(sign * cx * A.wasm[a], ring[(size_t)el * (2 * P) + a], v);
+  if (k != 0 && k > P) v = fma(sign * cy * A.wasm[b], ring[(size_t)ed * (2 * P) + P + b], v);
+  if (k == 0) v = fma(sign * cy * A.wasm[0], ring[(size_t)ed * (2 * P) + P], v);
+  *o = v;
+}
+
+template <int P, bool DIFF>
+static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cudaStream_t st) {
+  using G = OpdhGeom<P, DIFF>;
+  OpArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
+  op_fill_consts<P>(A, L, DIFF);
+  A.tiles_x = L.n_x;
+  A.bulk = 1;
+  static DeviceFlag attr;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(opdh_kernel<P, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "opdh_kernel smem attribute");
+    attr = true;
+  }
+  static DeviceInt grid_cap;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opdh_kernel<P, DIFF>, G::THREADS, G::SMEM);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int n_el = L.n_x * L.n_y;
+  launch(opdh_kernel<P, DIFF>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring,
+         n_el);
+  int rc = check_launch("opdh_kernel");
+  if (rc) return rc;
+  const long nb = (long)L.n_x * L.n_y * 2 * P;
+  launch(opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
+         L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
+  return check_launch("opdh_fixup");
+}
+
 // Lane-ordered B fragments of D^T and D for opd_kernel (host): value for
 // (k-tile q, n-tile j, lane (g, t)) = B[4q + t][8j + g].
 void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out) {
@@ -569,6 +878,10 @@ int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
     return 1;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if ((L.n_x * L.p) % 2 != 0 || !al16(L.u) || (L.diffusion && !al16(L.nu))) return 1;
+  // halo-free kernel + fixup when the caller passes a ring workspace (SMG_OPDH=0 keeps the fused kernel)
+  static const bool hf = env_int("SMG_OPDH", 1) != 0;
+  if (L.ring != nullptr && hf)
+    return L.diffusion ? opdh_launch_t<24, true>(L, frag, L.ring, st) : opdh_launch_t<32, false>(L, frag, L.ring, st);
   return L.diffusion ? opd_launch_t<24, true>(L, frag, st) : opd_launch_t<32, false>(L, frag, st);
 }
 

@@ -345,9 +345,9 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
                         lv.u.zero_()
                     lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_pre)
                 else:
-                    N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                                   N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_pre, int(zero), st),
-                            "smooth")
+                    N.check(lib.smg_schwarz_smooth_ws(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                      N.ptr(lv.f), N.ptr(lv.work), N.ptr(lv.smoother.ring),
+                                                      lv.op.ring_ptr(), lv.n_pre, int(zero), st), "smooth")
                 zero = False
             fc = h.levels[l - 1].f
             if zero:
@@ -356,7 +356,7 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
             else:
                 N.check(lib.smg_residual_restrict_ws(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
                                                      N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), lv.transfer.ws_ptr(),
-                                                     st), "residual_restrict")
+                                                     lv.op.ring_ptr(), st), "residual_restrict")
     with _Range("coarse"):
         _coarse_into(h, h.levels[0].f, h.levels[0].u)
     K = _chain_levels(h)
@@ -375,9 +375,9 @@ def _v_cycle(h: MultigridHierarchy, u: torch.Tensor, f: torch.Tensor, u_zero: bo
                 if isinstance(lv.smoother, MultiplicativeSchwarz):
                     lv.smoother.smooth(lv.op, lv.u, lv.f, lv.n_post)
                 else:
-                    N.check(lib.smg_schwarz_smooth(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f),
-                                                   N.ptr(lv.work), N.ptr(lv.smoother.ring), lv.n_post, 0, st),
-                            "smooth")
+                    N.check(lib.smg_schwarz_smooth_ws(lv.smoother._h.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                      N.ptr(lv.f), N.ptr(lv.work), N.ptr(lv.smoother.ring),
+                                                      lv.op.ring_ptr(), lv.n_post, 0, st), "smooth")
     return u
 
 

@@ -55,20 +55,28 @@ class _DeviceOperator:
         self._norm_buf = None
         # per-CTA norm partials (caller-owned scratch of smg_op_residual_norm2)
         self.partials = torch.empty(max(1, int(lib.smg_op_ws_doubles(raw))), dtype=torch.float64, device="cuda")
+        # ring workspace of the halo-free element kernel (caller-owned scratch, include/smg.h)
+        nring = int(lib.smg_op_ring_doubles(raw))
+        self.ring = torch.zeros(nring, dtype=torch.float64, device="cuda") if nring else None
+
+    def ring_ptr(self):
+        return N.ptr(self.ring) if self.ring is not None else None
 
     def apply(self, u) -> torch.Tensor:
         """A u as a new device field (operators.py:49-54 / 86-92)."""
         _check_layout(self.layout, u)
         u = to_device(u)
         out = torch.empty_like(u)
-        N.check(N.lib().smg_op_residual(self._handle.raw, N.ptr(u), None, N.ptr(out), N.stream()), "apply")
+        N.check(N.lib().smg_op_residual_ws(self._handle.raw, N.ptr(u), None, N.ptr(out), self.ring_ptr(), N.stream()),
+                "apply")
         return out
 
     def residual_into(self, u, f, out, norm2=None):
         """out = f - A u (f may be None: out = A u); optional device ||out||^2."""
         lib = N.lib()
         if norm2 is None:
-            N.check(lib.smg_op_residual(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.stream()), "residual")
+            N.check(lib.smg_op_residual_ws(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), self.ring_ptr(),
+                                           N.stream()), "residual")
         else:
             N.check(lib.smg_op_residual_norm2(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.ptr(norm2),
                                               N.ptr(self.partials), N.stream()), "residual")

@@ -300,10 +300,11 @@ class AdditiveSchwarz:
         if not isinstance(u, torch.Tensor) or not u.is_cuda:
             raise TypeError("AdditiveSchwarz.smooth mutates u in place: pass a CUDA float64 tensor")
         f = _as_device(f)
-        N.check(N.lib().smg_schwarz_smooth(self._h.raw, op._handle.raw, N.ptr(u), N.ptr(f),
-                                           N.ptr(self._workspace()), N.ptr(self.ring), int(n_it),
-                                           int(bool(u_is_zero)),
-                                           N.stream()), "schwarz_smooth")
+        ring = op.ring_ptr() if hasattr(op, "ring_ptr") else None
+        N.check(N.lib().smg_schwarz_smooth_ws(self._h.raw, op._handle.raw, N.ptr(u), N.ptr(f),
+                                              N.ptr(self._workspace()), N.ptr(self.ring), ring, int(n_it),
+                                              int(bool(u_is_zero)),
+                                              N.stream()), "schwarz_smooth")
         return u
 
 

@@ -49,12 +49,13 @@ for l in range(h.depth, 0, -1):
     lv.f.normal_()
     fc = h.levels[l - 1].f
     uc = h.levels[l - 1].u
-    t_res = timeit(lambda: N.check(lib.smg_op_residual(lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f), N.ptr(lv.work), st)))
+    t_res = timeit(lambda: N.check(lib.smg_op_residual_ws(lv.op._handle.raw, N.ptr(lv.u), N.ptr(lv.f), N.ptr(lv.work), lv.op.ring_ptr(), st)))
     t_fd = timeit(lambda: N.check(lib.smg_schwarz_correct(lv.smoother._h.raw, N.ptr(lv.work), N.ptr(lv.u), N.ptr(lv.smoother.ring), st)))
-    t_rs = timeit(lambda: N.check(lib.smg_restrict(lv.transfer.handle.raw, N.ptr(lv.work), N.ptr(fc), st)))
+    t_rs = timeit(lambda: N.check(lib.smg_restrict_ws(lv.transfer.handle.raw, N.ptr(lv.work), N.ptr(fc), lv.transfer.ws_ptr(), st)))
     t_pr = timeit(lambda: N.check(lib.smg_prolongate(lv.transfer.handle.raw, N.ptr(uc), N.ptr(lv.u), 1, st)))
-    t_rr = timeit(lambda: N.check(lib.smg_residual_restrict(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
-                                                           N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work), st)))
+    t_rr = timeit(lambda: N.check(lib.smg_residual_restrict_ws(lv.transfer.handle.raw, lv.op._handle.raw, N.ptr(lv.u),
+                                                              N.ptr(lv.f), N.ptr(fc), N.ptr(lv.work),
+                                                              lv.transfer.ws_ptr(), lv.op.ring_ptr(), st)))
     rows.append((lv.basis.p, lv.op.layout.size, t_res, t_fd, t_rs, t_pr, t_rr))
     tot += t_res + t_fd + t_rr + t_pr
 f0, u0 = h.levels[0].f, h.levels[0].u
