@@ -639,13 +639,17 @@ def main():
     def tb(*names):
         v = [tr_all[n]["bytes_per_launch"] for n in names if n in tr_all]
         return float(sum(v)) if len(v) == len(names) else None
+    eng, tile_x, tile_y = top.smoother.kernel_info()
+    schwarz_kernel = "fdp_kernel" if eng == "pair" else "fdt_kernel"
+    schwarz_label = (f"{schwarz_kernel}<{c['p']},{rule.layers(c['p'])},{tile_x},{tile_y}> + fdt_fixup "
+                     f"(one Schwarz correction; engine {eng})")
     kern = {
         "residual": roofline_entry("opw_kernel<16,2,2> (r = f - A u, warp per element)", t_call["residual"],
                                    n_el * (4 * npp ** 3 + 3 * npp ** 2) + ndof, 24.0 * ndof, p64, bw * 1e9,
                                    tb("opw_kernel")),
-        "schwarz": roofline_entry("fdt_kernel<16,1,4,2> + fdt_fixup (one Schwarz correction)", t_call["schwarz"],
+        "schwarz": roofline_entry(schwarz_label, t_call["schwarz"],
                                   n_el * fd_eo_flops_per_element(m), 24.0 * ndof, p64, bw * 1e9,
-                                  tb("fdt_kernel", "fdt_fixup"),
+                                  tb(schwarz_kernel, "fdt_fixup"),
                                   note="even/odd flop count (SURVEY 8(d)); dense-FD equivalent "
                                        f"{n_el * fd_flops_per_element(m) / t_call['schwarz'] / 1e12:.2f} TF"),
         "restrict": roofline_entry("restrict_blk_kernel<8,16>", t_call["restrict"], f_tr, 8.0 * ndof + 8.0 * ndof_c,
@@ -657,9 +661,13 @@ def main():
         kern[nm]["us_per_call_flushed"] = 1e6 * t_call_flushed[nm]
         kern[nm]["timing"] = (f"{nset} distinct buffer sets (>= 320 MB, > L2) launched back to back x 4, "
                               "mean per launch; us_per_call_flushed: single launch after a 256 MiB L2 flush")
+    # `roofline` is the kernel the north star names -- the fused Schwarz correction -- whether
+    # or not it still has the largest share of the step (the residual runs twice per cycle;
+    # every top-level kernel is listed under top_level_kernels with its own fraction)
     dom = max(calls, key=lambda k: calls[k][1] * t_call[k])
-    roofline = dict(kern[dom])
-    roofline["share_of_step"] = calls[dom][1] * t_call[dom] / (ms_per_step / 1e3)
+    roofline = dict(kern["schwarz"])
+    roofline["share_of_step"] = calls["schwarz"][1] * t_call["schwarz"] / (ms_per_step / 1e3)
+    roofline["largest_share_of_step"] = {"kernel": dom, "share": calls[dom][1] * t_call[dom] / (ms_per_step / 1e3)}
     roofline["peak_source"] = (f"HBM {bw} GB/s ({bw_src}); FP64 {FP64_PEAK_TFLOPS} TF = measured DMMA "
                                "peak (tools/peaks/fp64_peaks.cu; MEASURED_PEAKS.json has no FP64 entry)")
     # ---- end to end through the public API with host buffers.  Every step

@@ -21,7 +21,7 @@ out = torch.empty_like(r)
 fc = h.levels[-2].f
 uc = torch.randn(fc.shape, dtype=torch.float64, device="cuda")
 for _ in range(int(os.environ.get("REPS", "1"))):
-    NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(u), NV.ptr(r), NV.ptr(out), NV.ptr(top.smoother.ring), st))
+    NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(u), NV.ptr(r), NV.ptr(out), st))
     NV.check(lib.smg_schwarz_correct(top.smoother._h.raw, NV.ptr(r), NV.ptr(out), NV.ptr(top.smoother.ring), st))
     NV.check(lib.smg_restrict(top.transfer.handle.raw, NV.ptr(r), NV.ptr(fc), st))
     NV.check(lib.smg_prolongate(top.transfer.handle.raw, NV.ptr(uc), NV.ptr(out), 1, st))
