@@ -116,9 +116,10 @@ __device__ __forceinline__ void opd_batch(const double* x0, const double* n0, in
 // ONLY_LAST: only the n-tile holding n = 0 (V[P] = Vm[0][0] at t = 0).
 template <int P, bool ONLY_LAST>
 __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0, int st, const double* WT,
-                                             const double* __restrict__ frag, double (&Vb)[2][2], double (&Vm)[2][2]) {
+                                             const double* __restrict__ frag, double (&Vb)[(P / 2 + 8) / 8][2],
+                                             double (&Vm)[(P / 2 + 8) / 8][2]) {
   constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
-  static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
+  static_assert(P % 2 == 0, "even order");
   const int lane = threadIdx.x & 31, t = lane & 3;
   const double* BE = frag;
   const double* BO = frag + KH * NH * 32;
@@ -726,6 +727,108 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   }
 }
 
+// Halo-free diffusion kernel for orders whose 2P lines fill whole 8-line batches but whose
+// rows alone do not (p = 12: rows 0-7 | rows 8-11 + columns 0-3 | columns 4-11): one batch
+// per warp, a lane group's line is a row (stride 1) or a column (stride DP); the x-parts and
+// y-parts meet in the final loop.  Same ring layout and fixup as opdh_kernel.
+template <int P>
+struct OpdqGeom {
+  static constexpr int NP = P + 1;
+  static constexpr int DP = (NP + 2) & ~1;
+  static constexpr int WARPS = 2 * P / 8;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int WIN = ((DP * NP + 15) & ~15);
+  static constexpr int OXP = P + 2;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)4 * WIN + (size_t)2 * P * OXP + (size_t)P + NP) + 32;
+  static_assert((2 * P) % 8 == 0, "lines must fill whole batches");
+};
+
+template <int P>
+__global__ void __launch_bounds__(OpdqGeom<P>::THREADS, 8)
+opdq_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag, double* __restrict__ ring,
+            int n_el) {
+  SMG_PDL_TRIGGER();
+  using G = OpdqGeom<P>;
+  constexpr int NP = G::NP, DP = G::DP, OX = P, OY = P, NT = G::THREADS, WIN = G::WIN, OXP = G::OXP;
+  extern __shared__ __align__(128) double smd[];
+  double* WB = smd;                    // [2][2] windows: NP x DP of u and nu, column shift sh
+  double* AX = WB + 4 * WIN;           // OY x OXP x-parts
+  double* AY = AX + OY * OXP;          // OY x OXP y-parts
+  double* WS = AY + OY * OXP;          // P assembled weights
+  double* WT = WS + P;                 // NP GLL weights
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WT + NP);   // [2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int N_x = A.N_x, N_y = A.N_y;
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  SMG_PDL_WAIT();
+  __syncthreads();
+  auto issue = [&](int e, int b) {
+    const int tx = e % A.tiles_x, ty = e / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    if (tid == 0) mbar_arrive_expect_tx(bar + b, 2u * pwin_bytes(NP, NP, pwin_shift(X0, N_x)));
+    __syncwarp();
+    pwin_issue_warp(A.u, N_x, N_y, X0, Y0, NP, NP, WB + (2 * b) * WIN, DP, bar + b);
+    pwin_issue_warp(A.nu, N_x, N_y, X0, Y0, NP, NP, WB + (2 * b + 1) * WIN, DP, bar + b);
+  };
+  if (warp == 0 && (int)blockIdx.x < n_el) issue(blockIdx.x, 0);
+  const int line = 8 * warp + g;            // [0,P): row lines, [P,2P): column lines
+  const bool isrow = line < P;
+  const int li = isrow ? line : line - P;
+  int it = 0;
+  for (int el = blockIdx.x; el < n_el; el += gridDim.x, ++it) {
+    const int bsel = it & 1;
+    const int tx = el % A.tiles_x, ty = el / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    const int sh = pwin_shift(X0, N_x);
+    double* R = ring + (size_t)el * (2 * P);
+    if (warp == 0 && el + (int)gridDim.x < n_el) issue(el + gridDim.x, bsel ^ 1);
+    constexpr int KO = (OX * OY + NT - 1) / NT;
+    double fv[KO];
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = tid + k * NT;
+      fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
+    }
+    const double* U = WB + (2 * bsel) * WIN;
+    const double* NU = U + WIN;
+    mbar_wait(bar + bsel, (unsigned)(it >> 1) & 1u);
+    constexpr int NHO = (P / 2 + 8) / 8;
+    double Vb[NHO][2], Vm[NHO][2];
+    const int off = isrow ? li * DP + sh : sh + li;
+    opd_batch_eo<P, false>(U + off, NU + off, isrow ? 1 : DP, WT, frag, Vb, Vm);
+#pragma unroll
+    for (int j = 0; j < NHO; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = 8 * j + 2 * t + e;
+        if (b <= P / 2) {
+          double* dst = isrow ? AX + li * OXP : AY + li;
+          const int sb = isrow ? 1 : OXP;
+          dst[b * sb] = Vb[j][e];
+          if (b == 0) R[line] = Vm[j][e];
+          else if (b < P / 2) dst[(P - b) * sb] = Vm[j][e];
+        }
+      }
+    __syncthreads();   // parts complete; every thread is done with this element's window
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < OX * OY) {
+        const int y = idx / OX, x = idx - y * OX;
+        const double val = fma(A.cx * WS[y], AX[y * OXP + x], (A.cy * WS[x]) * AY[y * OXP + x]);
+        A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = A.f != nullptr ? fv[k] - val : val;
+      }
+    }
+    __syncthreads();   // the parts are rewritten by the next element
+  }
+}
+
 // One thread per low-side node of an element: (a, 0) for k = a < P takes the left
 // element's row-line value (and, at the corner a = 0, the lower element's column-line
 // value after it); (0, b) for k = P + b, b >= 1, the lower element's.
@@ -777,6 +880,34 @@ static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cu
   int rc = check_launch("opdh_kernel");
   if (rc) return rc;
   const long nb = (long)L.n_x * L.n_y * 2 * P;
+  launch(opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
+         L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
+  return check_launch("opdh_fixup");
+}
+
+template <int P>
+static int opdq_launch_t(const OpLaunch& L, const double* frag, double* ring, cudaStream_t st) {
+  using G = OpdqGeom<P>;
+  OpArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
+  op_fill_consts<P>(A, L, true);
+  A.tiles_x = L.n_x;
+  A.bulk = 1;
+  static DeviceInt grid_cap;
+  if (grid_cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(opdq_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "opdq_kernel smem attribute");
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opdq_kernel<P>, G::THREADS, G::SMEM);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int n_el = L.n_x * L.n_y;
+  launch(opdq_kernel<P>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring, n_el);
+  int rc = check_launch("opdq_kernel");
+  if (rc) return rc;
+  const long nb = (long)n_el * 2 * P;
   launch(opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
          L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
   return check_launch("opdh_fixup");
@@ -864,7 +995,8 @@ static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) 
 
 // (a p = 12 diffusion variant -- 3 warps, full and vertex lines mixed per
 // batch -- measured 1016 us vs 839 us for op_kernel<12,2,2> at C5's level 3)
-bool opd_applies(int p, bool diffusion) { return diffusion ? p == 24 : p == 32; }
+// p = 12 diffusion only has the halo-free kernel (opdq_kernel): it needs the caller's ring
+bool opd_applies(int p, bool diffusion) { return diffusion ? (p == 24 || p == 12) : p == 32; }
 
 // 1 = not applicable (caller uses op_kernel / opw_kernel)
 // SMG_OPD=0 disables the tensor-core operator path (read once).
@@ -880,6 +1012,10 @@ int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
   if ((L.n_x * L.p) % 2 != 0 || !al16(L.u) || (L.diffusion && !al16(L.nu))) return 1;
   // halo-free kernel + fixup when the caller passes a ring workspace (SMG_OPDH=0 keeps the fused kernel)
   static const bool hf = env_int("SMG_OPDH", 1) != 0;
+  if (L.p == 12) {
+    static const bool q12 = env_int("SMG_OPDQ", 1) != 0;
+    return (L.ring != nullptr && hf && q12) ? opdq_launch_t<12>(L, frag, L.ring, st) : 1;
+  }
   if (L.ring != nullptr && hf)
     return L.diffusion ? opdh_launch_t<24, true>(L, frag, L.ring, st) : opdh_launch_t<32, false>(L, frag, L.ring, st);
   return L.diffusion ? opd_launch_t<24, true>(L, frag, st) : opd_launch_t<32, false>(L, frag, st);

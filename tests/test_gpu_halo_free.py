@@ -9,7 +9,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind,p,nx,ny,lx,ly", [("diffusion", 24, 4, 3, 1.0, 1.0), ("diffusion", 24, 6, 8, 2.0, 1.0),
+@pytest.mark.parametrize("kind,p,nx,ny,lx,ly", [("diffusion", 12, 5, 3, 1.0, 1.0), ("diffusion", 12, 16, 8, 1.0, 4.0),
+                                                ("diffusion", 24, 4, 3, 1.0, 1.0), ("diffusion", 24, 6, 8, 2.0, 1.0),
                                                 ("poisson", 32, 3, 4, 1.0, 1.3), ("poisson", 32, 6, 6, 8.0, 1.0)])
 def test_operator_ring_path(kind, p, nx, ny, lx, ly):
     import paper_1512_02390_b200 as P
