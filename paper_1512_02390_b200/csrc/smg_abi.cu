@@ -861,8 +861,12 @@ int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0,
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_pcg");
   if (hs[0] == 0.0) { *iters_out = 0; return SMG_OK; }
   int it = 0;
-  const int chunk = 16;
+  // iterations between two host reads of the convergence flag: the iterations enqueued
+  // after convergence still run (C5: 11-14 needed; with one read per 16 iterations 2-5 of
+  // 16 were wasted, ~80 us each), so after the first 8 the flag is read every 3
+  static const int chunk0 = env_int("SMG_PCG_CHUNK0", 8), chunk1 = env_int("SMG_PCG_CHUNK", 3);
   while (it < max_iter) {
+    const int chunk = it == 0 ? chunk0 : chunk1;
     const int stop = it + chunk < max_iter ? it + chunk : max_iter;
     for (; it < stop; ++it) {
       const int ro = 2 + (it & 1), rn = 3 - (it & 1);
