@@ -684,7 +684,8 @@ class GpuEngine:
 
     def restrict(self, l, fine, out):
         N = self.N
-        N.check(N.lib().smg_restrict(self.h.levels[l].transfer.handle.raw, N.ptr(fine), N.ptr(out), N.stream()),
+        tr = self.h.levels[l].transfer
+        N.check(N.lib().smg_restrict_ws(tr.handle.raw, N.ptr(fine), N.ptr(out), tr.ws_ptr(), N.stream()),
                 "strip restrict")
 
     def prolong_add(self, l, coarse, fine):
