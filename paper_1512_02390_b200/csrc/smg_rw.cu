@@ -46,17 +46,25 @@ __global__ void __launch_bounds__(32 * kRwWarps) restrict_warp_kernel(const __gr
     double t[NC];
 #pragma unroll
     for (int ay = 0; ay < NC; ++ay) t[ay] = 0.0;
+    // chunks of CH rows, the next chunk's loads issued before this chunk's FMAs (ncu: 63 %
+    // of the stall samples sat on the first FMA of a chunk waiting for its loads)
     constexpr int CH = 8;
     static_assert(PF % CH == 0, "row chunks");
+    double f[CH], g[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) f[q] = col[(size_t)q * Nxf];
 #pragma unroll
     for (int a0 = 0; a0 < PF; a0 += CH) {
-      double f[CH];
+      if (a0 + CH < PF) {
 #pragma unroll
-      for (int q = 0; q < CH; ++q) f[q] = col[(size_t)(a0 + q) * Nxf];
+        for (int q = 0; q < CH; ++q) g[q] = col[(size_t)(a0 + CH + q) * Nxf];
+      }
 #pragma unroll
       for (int q = 0; q < CH; ++q)
 #pragma unroll
         for (int ay = 0; ay < NC; ++ay) t[ay] = fma(A.J[(a0 + q) * NC + ay], f[q], t[ay]);
+#pragma unroll
+      for (int q = 0; q < CH; ++q) f[q] = g[q];
     }
 #pragma unroll
     for (int ay = 0; ay < NC; ++ay) T[ay * TP + lane] = t[ay];
