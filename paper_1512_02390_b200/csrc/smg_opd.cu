@@ -614,7 +614,7 @@ struct OpdhGeom {
 // window in flight (two window buffers, two mbarriers) while the current one is computed --
 // one element per CTA spent 35-45 % of its stall samples waiting for its own window.
 template <int P, bool DIFF>
-__global__ void __launch_bounds__(OpdhGeom<P, DIFF>::THREADS, DIFF ? 5 : 4)
+__global__ void __launch_bounds__(OpdhGeom<P, DIFF>::THREADS, DIFF ? 6 : 4)
 opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag, double* __restrict__ ring,
             int n_el) {
   SMG_PDL_TRIGGER();
