@@ -4,7 +4,7 @@ namespace smg {
 namespace {
 struct Cfg { int p, n_o, tx, ty; FDTLaunchFn fn; };
 // per order: largest tile first (B200, 256^2 elements, us per correction: p = 16 4x4 175.0 /
-// 4x2 205.7; p = 24 4x2 441.4 / 2x2 509.0; p = 32 4x2 871.3 / 2x2 1055.8)
+// 4x2 205.7; p = 24 4x4 429 / 4x2 437 / 2x2 509 (512^2: 1624 / 1693); p = 32 4x2 871.3 / 2x2 1055.8)
 const Cfg kCfgs[] = {
   {6, 1, 4, 4, &fdp_launch_k<6, 1, 4, 4>},
   {8, 1, 4, 4, &fdp_launch_k<8, 1, 4, 4>},
@@ -15,6 +15,7 @@ const Cfg kCfgs[] = {
   {16, 1, 2, 2, &fdp_launch_k<16, 1, 2, 2>},
   {16, 2, 4, 4, &fdp_launch_k<16, 2, 4, 4>},
   {16, 2, 4, 2, &fdp_launch_k<16, 2, 4, 2>},
+  {24, 1, 4, 4, &fdp_launch_k<24, 1, 4, 4>},
   {24, 1, 4, 2, &fdp_launch_k<24, 1, 4, 2>},
   {24, 1, 2, 2, &fdp_launch_k<24, 1, 2, 2>},
   {24, 3, 4, 2, &fdp_launch_k<24, 3, 4, 2>},

@@ -85,7 +85,8 @@ struct FDPK {
   static constexpr size_t SMEM = sizeof(double) * ((size_t)USZ + MM) + 16;
   static constexpr int by_smem = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int REGS = 4 * HE + 24 < 64 ? 64 : ((4 * HE + 24 + 7) / 8) * 8;   // two lines of HE accumulators + addressing
-  static constexpr int by_regs = 65536 / (NT * REGS);
+  // (two CTAs of 14 full warps at p = 24, 4x4 elements, need 72 registers: allow the cap)
+  static constexpr int by_regs = (65536 / (NT * REGS) < 2 && 65536 / (NT * 72) >= 2) ? 2 : 65536 / (NT * REGS);
 #ifdef SMG_FDP_MINB
   static constexpr int MINB = SMG_FDP_MINB;   // tuning aid
 #else
