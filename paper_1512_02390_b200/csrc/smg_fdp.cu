@@ -6,6 +6,9 @@ struct Cfg { int p, n_o, tx, ty; FDTLaunchFn fn; };
 // per order: largest tile first (B200, 256^2 elements, us per correction: p = 16 4x4 175.0 /
 // 4x2 205.7; p = 24 4x4 429 / 4x2 437 / 2x2 509 (512^2: 1624 / 1693); p = 32 4x2 871.3 / 2x2 1055.8)
 const Cfg kCfgs[] = {
+  {2, 1, 8, 8, &fdp_launch_k<2, 1, 8, 8>},
+  {4, 1, 8, 4, &fdp_launch_k<4, 1, 8, 4>},
+  {4, 1, 4, 4, &fdp_launch_k<4, 1, 4, 4>},
   {6, 1, 4, 4, &fdp_launch_k<6, 1, 4, 4>},
   {8, 1, 4, 4, &fdp_launch_k<8, 1, 4, 4>},
   {12, 1, 4, 4, &fdp_launch_k<12, 1, 4, 4>},
@@ -40,6 +43,9 @@ FDTLaunchFn fdp_dispatch(int p, int n_o, int n_x, int n_y, int* TX, int* TY) {
     if (tiles > best_tiles) { best = &c; best_tiles = tiles; }
   }
   if (!best) return nullptr;
+  // p <= 4 (measured: 256^2 elements p = 4 38.0 -> 31.7 us, p = 2 25.8 -> 23.6; equal on
+  // small meshes): only where every SM gets a tile, else fdt_kernel's smaller tiles
+  if (p <= 4 && (long)(n_x / best->tx) * (n_y / best->ty) < min_tiles) return nullptr;
   *TX = best->tx;
   *TY = best->ty;
   return best->fn;
