@@ -76,10 +76,17 @@ int smg_op_residual_ws(const smg_op_t* h, const double* u, const double* f, doub
                        void* stream);
 /* Like smg_op_residual, and also *norm2_out (device double) = ||out||^2
  * summed deterministically; ws (device) must hold smg_op_ws_doubles(h)
- * doubles (the per-CTA partials) and must not overlap norm2_out. */
+ * doubles (the per-CTA partials and the reduction workspace of the _ws
+ * variant; no initialisation needed) and must not overlap norm2_out. */
 size_t smg_op_ws_doubles(const smg_op_t* h);
 int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
                           double* norm2_out, double* ws, void* stream);
+/* Same with the operator's ring workspace (NULL allowed): where a specialised residual
+ * kernel exists (tensor-core / warp-per-element) the residual runs on it and ||out||^2 comes
+ * from a deterministic dot pass over out (8 B/DOF) instead of the generic kernel's fused
+ * partials -- C3: 301 -> ~165 us per residual + norm. */
+int smg_op_residual_norm2_ws(const smg_op_t* h, const double* u, const double* f, double* out,
+                             double* norm2_out, double* ws, double* ring, void* stream);
 
 /* ---- additive Schwarz (replaces schwarz.py:215-222 FastDiagSolver.solve,
  *      :268-275 AdditiveSchwarz.smooth with mesh.py:124-150 gather/scatter)

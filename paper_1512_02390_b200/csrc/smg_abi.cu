@@ -313,7 +313,10 @@ int smg_op_residual_ws(const smg_op_t* h, const double* u, const double* f, doub
 
 int smg_sum_partials(const double* part, int nb, double* out, void* stream);
 
-size_t smg_op_ws_doubles(const smg_op_t* h) { return h ? (size_t)h->n_ctas : 0; }
+size_t smg_op_ws_doubles(const smg_op_t* h) {
+  // per-CTA norm partials of the generic kernel, then the reduction workspace of the dot pass
+  return h ? (size_t)h->n_ctas + smg_reduce_ws_doubles() : 0;
+}
 
 int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, double* out,
                           double* norm2_out, double* ws, void* stream) {
@@ -324,6 +327,30 @@ int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, d
   int rc = op_run(h, u, f, out, ws, as_stream(stream));
   if (rc) return rc;
   return smg_sum_partials(ws, h->n_ctas, norm2_out, stream);
+}
+
+int smg_op_residual_norm2_ws(const smg_op_t* h, const double* u, const double* f, double* out,
+                             double* norm2_out, double* ws, double* ring, void* stream) {
+  if (!h || !u || !out || u == out || !norm2_out || !ws) {
+    set_error("smg_op_residual_norm2_ws: bad argument");
+    return SMG_EINVAL;
+  }
+  // specialised residual kernel + dot pass where that is the faster pair (B200: C3 p = 32
+  // 301 -> 165 us, C4 p = 16 160 -> 123 us; equal at C2, which keeps the fused partials)
+  const long ndof = (long)h->n_x * h->n_y * h->p * h->p;
+  const bool tensor = ring != nullptr && smg_op_ring_doubles(h) > 0;
+  const bool warp = h->kind == 0 && (h->p == 8 || h->p == 16) && ndof >= (1L << 22);
+  static const int mode = env_int("SMG_NORM_DOT", 1);
+  if (!mode || !(tensor || warp)) return smg_op_residual_norm2(h, u, f, out, norm2_out, ws, stream);
+  int rc = op_run(h, u, f, out, nullptr, as_stream(stream), ring);
+  if (rc) return rc;
+  // the dot's reduction workspace sits behind the generic kernel's partials; its arrival
+  // counter must start at zero (the kernel resets it after use): cleared here, so the
+  // caller's buffer needs no initialisation
+  double* red = ws + h->n_ctas;
+  cudaError_t e = cudaMemsetAsync(red, 0, sizeof(double) * smg_reduce_ws_doubles(), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "smg_op_residual_norm2_ws");
+  return smg_dot(out, out, (int64_t)ndof, norm2_out, red, stream);
 }
 
 // ---- additive Schwarz ---------------------------------------------------------

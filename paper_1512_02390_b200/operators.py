@@ -78,8 +78,8 @@ class _DeviceOperator:
             N.check(lib.smg_op_residual_ws(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), self.ring_ptr(),
                                            N.stream()), "residual")
         else:
-            N.check(lib.smg_op_residual_norm2(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.ptr(norm2),
-                                              N.ptr(self.partials), N.stream()), "residual")
+            N.check(lib.smg_op_residual_norm2_ws(self._handle.raw, N.ptr(u), N.ptr(f), N.ptr(out), N.ptr(norm2),
+                                                 N.ptr(self.partials), self.ring_ptr(), N.stream()), "residual")
         return out
 
 
