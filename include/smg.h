@@ -88,6 +88,13 @@ int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, d
 int smg_op_residual_norm2_ws(const smg_op_t* h, const double* u, const double* f, double* out,
                              double* norm2_out, double* ws, double* ring, void* stream);
 
+/* out = A u and *dot_out (device double) = u . out, deterministic: MGCG's q = A p, p . q
+ * (krylov.py:91-94).  The warp-per-element Poisson kernel (p = 8, 16) forms the product
+ * from its staged window (p and q are not read again); elsewhere the apply is followed by
+ * a dot pass.  ws: smg_op_ws_doubles(h) doubles; ring: smg_op_ring_doubles(h) or NULL. */
+int smg_op_apply_dot(const smg_op_t* h, const double* u, double* out, double* dot_out, double* ws,
+                     double* ring, void* stream);
+
 /* ---- additive Schwarz (replaces schwarz.py:215-222 FastDiagSolver.solve,
  *      :268-275 AdditiveSchwarz.smooth with mesh.py:124-150 gather/scatter)
  * S_x, S_y: m x m row-major generalized eigenvectors (reference S_x, S_y);

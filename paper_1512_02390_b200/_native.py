@@ -56,6 +56,7 @@ SIGNATURES = {
     "smg_restrict_ws": (C.c_int, [_vp, _dp, _dp, _dp, _vp]),
     "smg_residual_restrict_ws": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _dp, _dp, _vp]),
     "smg_op_residual_norm2_ws": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, _vp]),
+    "smg_op_apply_dot": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _vp]),
     "smg_op_ring_doubles": (C.c_size_t, [_vp]),
     "smg_op_residual_ws": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _vp]),
     "smg_schwarz_smooth_ws": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_int, _vp]),

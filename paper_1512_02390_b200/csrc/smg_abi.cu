@@ -329,6 +329,34 @@ int smg_op_residual_norm2(const smg_op_t* h, const double* u, const double* f, d
   return smg_sum_partials(ws, h->n_ctas, norm2_out, stream);
 }
 
+int smg_op_apply_dot(const smg_op_t* h, const double* u, double* out, double* dot_out, double* ws, double* ring,
+                     void* stream) {
+  if (!h || !u || !out || u == out || !dot_out || !ws) {
+    set_error("smg_op_apply_dot: bad argument");
+    return SMG_EINVAL;
+  }
+  const long ndof = (long)h->n_x * h->n_y * h->p * h->p;
+  static const int fused = env_int("SMG_APPLY_DOT", 1);
+  if (fused && h->kind == 0 && (h->p == 8 || h->p == 16) && h->n_x % 2 == 0 && h->n_y % 2 == 0 &&
+      (long)(h->n_x / 2) * (h->n_y / 2) <= (long)h->n_ctas + (long)smg_reduce_ws_doubles()) {
+    OpLaunch L;
+    L.u = u; L.f = nullptr; L.out = out; L.nu = h->nu; L.partials = nullptr;
+    L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
+    L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
+    L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
+    int nct = 0;
+    const int rc = opw_apply_dot(L, ws, &nct, as_stream(stream));
+    if (rc == 0) return smg_sum_partials(ws, nct, dot_out, stream);
+    if (rc != 1) return rc;
+  }
+  int rc = op_run(h, u, nullptr, out, nullptr, as_stream(stream), smg_op_ring_doubles(h) ? ring : nullptr);
+  if (rc) return rc;
+  double* red = ws + h->n_ctas;
+  cudaError_t e = cudaMemsetAsync(red, 0, sizeof(double) * smg_reduce_ws_doubles(), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "smg_op_apply_dot");
+  return smg_dot(u, out, (int64_t)ndof, dot_out, red, stream);
+}
+
 int smg_op_residual_norm2_ws(const smg_op_t* h, const double* u, const double* f, double* out,
                              double* norm2_out, double* ws, double* ring, void* stream) {
   if (!h || !u || !out || u == out || !norm2_out || !ws) {

@@ -24,6 +24,7 @@ struct OpwArgs {
   const double* __restrict__ u;
   const double* __restrict__ f;
   double* __restrict__ out;
+  double* __restrict__ dotp;   // DOT kernels: per-CTA partials of sum(u * out)
   int N_x, N_y, tiles_x;
   double cx, cy;
   double Le[((P + 1) / 2 + 1) * ((P + 1) / 2 + 1)];
@@ -86,7 +87,9 @@ struct OpwGeom {
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY + (size_t)NW * P * LDA) + 16;
 };
 
-template <int P, int TX, int TY>
+// DOT: also the per-CTA partial of sum(u * out) over the CTA's nodes (MGCG's p . A p without
+// re-reading p and q: the node's u is in the staged window); fixed shuffle / warp order.
+template <int P, int TX, int TY, bool DOT = false>
 __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   SMG_PDL_TRIGGER();
   using G = OpwGeom<P, TX, TY>;
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
   __syncwarp();
   // the column lane b keeps the y-part of its column in registers and writes
   // the column's outputs (each row of r coalesced across the half-warp)
+  [[maybe_unused]] double dacc = 0.0;
   if (col && lact) {
     const int b = li;
     const double wyb = A.cy * A.wasm[b];
@@ -153,22 +157,40 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
         const int a = a0 + i;
         double val = fma(A.cx * A.wasm[a], AX[a * LDA + b], wyb * v[a]);
         if (a == 0) val = fma(wyb, vv[P], val);
-        A.out[g0 + (size_t)a * N_x] = A.f != nullptr ? fv[i] - val : val;
+        const double o = A.f != nullptr ? fv[i] - val : val;
+        A.out[g0 + (size_t)a * N_x] = o;
+        if constexpr (DOT) dacc = fma(U[(ur0 + a) * DP + uc0 + b], o, dacc);
       }
+    }
+  }
+  if constexpr (DOT) {
+    // the column lanes hold their columns' sums, every other lane an exact zero: fixed
+    // xor tree over the whole warp (outside the divergent branches), then the warps in order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    if (lane == 0) AX[0] = dacc;   // the warp's x-part buffer is consumed
+  }
+  if constexpr (DOT) {
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += AXb[w * P * LDA];
+      A.dotp[blockIdx.x] = s;
     }
   }
 }
 
 // Host: 1 = not applicable (caller uses op_kernel).
 template <int P, int TX, int TY>
-int opw_launch_t(const OpLaunch& L, cudaStream_t st) {
+int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr) {
   using G = OpwGeom<P, TX, TY>;
   if (L.diffusion || L.partials != nullptr || L.n_x % TX || L.n_y % TY) return 1;
   const int N_x = L.n_x * P;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (N_x % 2 || !al16(L.u)) return 1;
   OpwArgs<P> A;
-  A.u = L.u; A.f = L.f; A.out = L.out;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.dotp = dotp;
   A.N_x = N_x; A.N_y = L.n_y * P; A.tiles_x = L.n_x / TX;
   A.cx = L.cx; A.cy = L.cy;
   {
@@ -198,8 +220,29 @@ int opw_launch_t(const OpLaunch& L, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "opw_kernel smem attribute");
     attr = true;
   }
+  if (dotp != nullptr) {
+    static DeviceFlag attr2;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(opw_kernel<P, TX, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)G::SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "opw_kernel smem attribute");
+      attr2 = true;
+    }
+    launch(opw_kernel<P, TX, TY, true>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(32 * G::NW), G::SMEM, st, A);
+    return check_launch("opw_kernel");
+  }
   launch(opw_kernel<P, TX, TY>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(32 * G::NW), G::SMEM, st, A);
   return check_launch("opw_kernel");
+}
+
+// out = A u and per-CTA partials of u . out (n_ctas of them); 1 = not applicable.
+int opw_apply_dot(const OpLaunch& L, double* partials, int* n_ctas, cudaStream_t st) {
+  static const int on = env_int("SMG_OP_WARP", 1);
+  if (!on || L.f != nullptr || partials == nullptr) return 1;
+  *n_ctas = (L.n_x / 2) * (L.n_y / 2);
+  if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, partials);
+  if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, partials);
+  return 1;
 }
 
 int opw_launch(const OpLaunch& L, cudaStream_t st) {

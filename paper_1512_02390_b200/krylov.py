@@ -199,8 +199,9 @@ def solve_mgcg(h: MultigridHierarchy, f, cfg: SolveConfig, u0=None):
             # krylov.py:91-103: q = A p, alpha = delta / p.q, u += alpha p, rb = ra - alpha q
             def run():
                 st = N.stream()
-                op.residual_into(p, None, q)
-                N.check(lib.smg_dot(N.ptr(p), N.ptr(q), n, N.ptr(s.dev[1:2]), N.ptr(ws), st), "dot")
+                # q = A p and p . q in one call (fused in the warp-per-element Poisson kernel)
+                N.check(lib.smg_op_apply_dot(op._handle.raw, N.ptr(p), N.ptr(q), N.ptr(s.dev[1:2]),
+                                             N.ptr(op.partials), op.ring_ptr(), st), "apply_dot")
                 N.check(lib.smg_cg_update2(N.ptr(u), N.ptr(ra), N.ptr(rb), N.ptr(p), N.ptr(q), n,
                                            N.ptr(s.dev), N.ptr(s.flag), N.ptr(ws), st), "cg_update")
             return run

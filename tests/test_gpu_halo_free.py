@@ -69,3 +69,28 @@ def test_restriction_ring_path(p, orders, nx, ny):
     lhs, rhs = (got * c).sum().item(), (r * pcf).sum().item()
     assert abs(lhs - rhs) < 1e-11 * max(abs(lhs), abs(rhs), 1.0)
     assert torch.equal(P.restrict_residual(h, h.depth, r), got)
+
+
+@pytest.mark.parametrize("kind,p,nx,ny", [("poisson", 16, 8, 6), ("poisson", 8, 4, 4), ("poisson", 32, 4, 3),
+                                          ("poisson", 4, 8, 8), ("diffusion", 24, 4, 4), ("diffusion", 6, 8, 8)])
+def test_apply_dot(kind, p, nx, ny):
+    """smg_op_apply_dot: q = A p and p . q (fused in the warp-per-element kernel at p = 8, 16,
+    apply + dot pass elsewhere) against apply() and a float64 dot; uninitialised workspace."""
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200 import _native as N
+    mesh = P.MeshConfig(nx, ny, 1.0, 2.0)
+    b = P.gll_basis(p)
+    rng = np.random.default_rng(3)
+    lay = P.layout_for(mesh, p)
+    op = P.PoissonOperator(b, mesh) if kind == "poisson" else P.DiffusionOperator(b, mesh, 0.3 + rng.random(lay.shape))
+    u = torch.from_numpy(rng.standard_normal(lay.shape)).cuda()
+    want_q = op.apply(u)
+    want = float((u * want_q).sum().item())
+    q = torch.empty_like(u)
+    d = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda")
+    op.partials.fill_(float("nan"))   # the call must not depend on the workspace contents
+    for _ in range(2):
+        N.check(N.lib().smg_op_apply_dot(op._handle.raw, N.ptr(u), N.ptr(q), N.ptr(d), N.ptr(op.partials),
+                                         op.ring_ptr(), N.stream()), "apply_dot")
+        assert torch.equal(q, want_q)
+        assert abs(d.item() - want) <= 1e-12 * float((u.abs() * want_q.abs()).sum().item())
