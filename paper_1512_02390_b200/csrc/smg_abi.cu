@@ -115,6 +115,7 @@ struct smg_transfer {
   std::vector<double> J;
   smg::TrFn fn;
   smg::RwFn rw;   // halo-free restriction (smg_rw.cu) or nullptr
+  smg::PrwFn prw; // warp-per-fine-element prolongation (smg_rw.cu) or nullptr
 };
 
 struct smg_coarse {
@@ -599,6 +600,11 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   // dependent chain than the kernel gains (C2 V-cycle 105.2 -> 107.8 us with it)
   const bool big = p_f >= 24 || (long)n_x * n_y >= 16384 || rw_mode == 2;
   t->rw = (rw_mode && big) ? rw_dispatch(p_c, p_f) : nullptr;
+  // SMG_PRW: 0 never, 1 where measured faster, 2 wherever compiled (B200, tools/time_prolong.py,
+  // us tiled -> warp per fine element: C3 p_f = 32 95.3 -> 79.9; 256^2 p_f = 24 156.7 -> 162.9,
+  // p_f = 16 76.9 -> 80.0; bitwise-equal results)
+  const int prw_mode = env_int("SMG_PRW", 1);
+  t->prw = (prw_mode == 2 || (prw_mode == 1 && p_f == 32)) ? prw_dispatch(p_c, p_f) : nullptr;
   t->J.assign(J, J + (p_f + 1) * (p_c + 1));
   *h = t;
   return SMG_OK;
@@ -611,6 +617,7 @@ static int tr_run(const smg_transfer_t* h, const double* src, double* dst, int a
   std::memset(&A, 0, sizeof(A));
   A.src = src; A.dst = dst; A.n_x = h->n_x; A.n_y = h->n_y; A.accumulate = acc;
   std::memcpy(A.J, h->J.data(), sizeof(double) * h->J.size());
+  if (prolong && h->prw) return h->prw(A, st);
   return h->fn(A, h->n_x, h->n_y, prolong, st);
 }
 

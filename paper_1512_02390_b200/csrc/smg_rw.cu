@@ -129,6 +129,93 @@ int rw_launch(const TrArgs& A, double* ring, cudaStream_t st) {
   return check_launch("restrict_fixup");
 }
 
+// Prolongation, one warp per fine element (multigrid.py:180-185; same passes as the
+// restriction above, transposed): the element's (p_c+1)^2 coarse values land in a per-warp
+// buffer; x pass: lane ay = coarse row, T[ay][b] = sum_ax J[b][ax] C[ay][ax] for the p_f
+// owned fine columns (J as uniform operands, 4 columns in flight); y pass: lane b = fine
+// column, out[a][b] (+)= sum_ay J[a][ay] T[ay][b], 8 rows in flight, rows written coalesced.
+// No halo beyond the element's own high-side coarse nodes, no ring.
+template <int PC, int PF>
+__global__ void __launch_bounds__(32 * kRwWarps) prolong_rw_kernel(const __grid_constant__ TrArgs A) {
+  SMG_PDL_ENTRY();
+  constexpr int NC = PC + 1, TP = PF | 1, CP = NC | 1;
+  static_assert(PF <= 32 && NC <= 32, "one lane per fine column / coarse row");
+  __shared__ double Ts[kRwWarps][NC * TP];
+  __shared__ double Cs[kRwWarps][NC * CP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * kRwWarps + warp;
+  const int n_el = A.n_x * A.n_y;
+  if (e >= n_el) return;
+  const int ey = e / A.n_x, ex = e - ey * A.n_x;
+  const int Nxf = A.n_x * PF, Nxc = A.n_x * PC, Nyc = A.n_y * PC;
+  double* T = Ts[warp];
+  double* C = Cs[warp];
+  for (int i = lane; i < NC * NC; i += 32) {
+    const int ay = i / NC, ax = i - ay * NC;
+    C[ay * CP + ax] = A.src[(size_t)wrapi(ey * PC + ay, Nyc) * Nxc + wrapi(ex * PC + ax, Nxc)];
+  }
+  __syncwarp();
+  // ---- x pass (lane = coarse row ay)
+  if (lane < NC) {
+    double c[NC];
+#pragma unroll
+    for (int ax = 0; ax < NC; ++ax) c[ax] = C[lane * CP + ax];
+    constexpr int BB = 4;
+    static_assert(PF % BB == 0, "fine columns in flight");
+#pragma unroll
+    for (int b0 = 0; b0 < PF; b0 += BB) {
+      double t[BB];
+#pragma unroll
+      for (int q = 0; q < BB; ++q) t[q] = 0.0;
+#pragma unroll
+      for (int ax = 0; ax < NC; ++ax)
+#pragma unroll
+        for (int q = 0; q < BB; ++q) t[q] = fma(A.J[(b0 + q) * NC + ax], c[ax], t[q]);
+#pragma unroll
+      for (int q = 0; q < BB; ++q) T[lane * TP + b0 + q] = t[q];
+    }
+  }
+  __syncwarp();
+  // ---- y pass (lane = fine column b)
+  if (lane < PF) {
+    double t[NC];
+#pragma unroll
+    for (int ay = 0; ay < NC; ++ay) t[ay] = T[ay * TP + lane];
+    double* out = A.dst + (size_t)(ey * PF) * Nxf + ex * PF + lane;
+    constexpr int CH = 8;
+    static_assert(PF % CH == 0, "row chunks");
+#pragma unroll
+    for (int a0 = 0; a0 < PF; a0 += CH) {
+      double o[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) o[q] = A.accumulate ? out[(size_t)(a0 + q) * Nxf] : 0.0;
+      double s[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) s[q] = 0.0;
+#pragma unroll
+      for (int ay = 0; ay < NC; ++ay)
+#pragma unroll
+        for (int q = 0; q < CH; ++q) s[q] = fma(A.J[(a0 + q) * NC + ay], t[ay], s[q]);
+#pragma unroll
+      for (int q = 0; q < CH; ++q) out[(size_t)(a0 + q) * Nxf] = A.accumulate ? o[q] + s[q] : s[q];
+    }
+  }
+}
+
+template <int PC, int PF>
+int prw_launch(const TrArgs& A, cudaStream_t st) {
+  const int n_el = A.n_x * A.n_y;
+  launch(prolong_rw_kernel<PC, PF>, dim3((n_el + kRwWarps - 1) / kRwWarps), dim3(32 * kRwWarps), 0, st, A);
+  return check_launch("prolong_rw_kernel");
+}
+
+PrwFn prw_dispatch(int pc, int pf) {
+  if (pc == 16 && pf == 32) return &prw_launch<16, 32>;
+  if (pc == 12 && pf == 24) return &prw_launch<12, 24>;
+  if (pc == 8 && pf == 16) return &prw_launch<8, 16>;
+  return nullptr;
+}
+
 RwFn rw_dispatch(int pc, int pf) {
   if (pc == 16 && pf == 32) return &rw_launch<16, 32>;
   if (pc == 12 && pf == 24) return &rw_launch<12, 24>;
