@@ -290,7 +290,8 @@ static int op_run(const smg_op_t* h, const double* u, const double* f, double* o
   L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
   L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
   if (!norm) {
-    int rc = opd_launch(L, h->dfrag, st);
+    int rc = (h->kind == 0 && ring != nullptr) ? opl_launch(L, st) : 1;
+    if (rc == 1) rc = opd_launch(L, h->dfrag, st);
     if (rc == 1 && h->kind == 0) rc = opw_launch(L, st);
     if (rc != 1) return rc;
   }

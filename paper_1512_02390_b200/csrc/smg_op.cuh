@@ -485,6 +485,8 @@ using OpLaunchFn = int (*)(const OpLaunch&, cudaStream_t);
 // Warp-per-element Poisson residual (smg_opw.cu) for p = 8, 16 without norm
 // partials; returns 1 when not applicable.
 int opw_launch(const OpLaunch& L, cudaStream_t st);
+// Poisson p = 32, row warp + column warp per element, halo-free with L.ring (smg_opw.cu)
+int opl_launch(const OpLaunch& L, cudaStream_t st);
 // out = A u with per-CTA partials of u . out (smg_opw.cu); 1 = not applicable
 int opw_apply_dot(const OpLaunch& L, double* partials, int* n_ctas, cudaStream_t st);
 // Launcher for order p and mesh n_x x n_y (largest compiled tile dividing the

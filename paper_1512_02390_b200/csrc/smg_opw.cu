@@ -13,6 +13,8 @@
 //   * x- and y-parts meet in two per-warp 16 x 17 shared buffers; each lane
 //     then writes p/2 outputs of its column: coalesced rows of r.
 // Deterministic: every output node has one writer, fixed summation order.
+#include <cstring>
+
 #include "smg_common.cuh"
 #include "smg_op.cuh"
 #include "smg_tma.cuh"
@@ -30,6 +32,11 @@ struct OpwArgs {
   double Le[((P + 1) / 2 + 1) * ((P + 1) / 2 + 1)];
   double Lo[((P + 1) / 2) * ((P + 1) / 2) + 1];
   double wasm[P];
+  // opl_kernel: the same halves transposed ([k][b], rows padded to an even length and 16-byte
+  // aligned) so that the b loop at a fixed k reads consecutive entries (128-bit uniform loads)
+  static constexpr int kH = (P + 1) / 2, kHC = kH + ((P + 1) & 1), kHCP = (kHC + 1) & ~1, kHP = (kH + 1) & ~1;
+  alignas(16) double LeT[(kH + 1) * kHCP];
+  alignas(16) double LoT[(kH > 0 ? kH : 1) * kHP];
 };
 
 // Even/odd 1D line: v[b] = sum_k L[k][b] x[k st] (L centro-symmetric); with
@@ -243,6 +250,224 @@ int opw_apply_dot(const OpLaunch& L, double* partials, int* n_ctas, cudaStream_t
   if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, partials);
   if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, partials);
   return 1;
+}
+
+// ---- p = 32: one element per CTA, a row warp and a column warp, halo-free -----------
+// The tensor-core kernel (opdh_kernel, smg_opd.cu) pads the even/odd halves of L-hat
+// (17 x 17, 16 x 16) to 20 x 24 DMMA slots -- 57 % useful -- and the DMMA and DFMA pipes
+// are one datapath (profiles/r2_fp64_mixed_pipes.txt), so at p = 32 the exact DFMA form is
+// the cheaper one per line (34 vs 60 pipe cycles).  A CTA stages its element's own
+// (p+1)^2 window (odd pitch: rows and columns are both conflict-free); warp 0 runs the p
+// row lines (lane = row a, k-streamed even/odd line, L-hat entries as uniform operands),
+// warp 1 the p column lines; the x-parts meet warp 1 in shared memory, which writes the
+// coalesced rows of r.  Node-p values go to the ring of opdh_kernel's layout ([0,p) rows,
+// [p,2p) columns per element); opl_fixup applies them.
+template <int P>
+__device__ __forceinline__ void opl_line(const OpwArgs<P>& A, const double* x, int st, double (&v)[P + 1]) {
+  constexpr int NP = P + 1, H = NP / 2;
+  constexpr bool MID = (NP & 1) != 0;
+  constexpr int HC = H + (MID ? 1 : 0);
+  constexpr int HCP = OpwArgs<P>::kHCP, HP = OpwArgs<P>::kHP;
+  double e[HC], o[H];
+  {
+    const double c = MID ? x[H * st] : 0.0;
+    const double2* __restrict__ Lc = reinterpret_cast<const double2*>(A.LeT + H * HCP);
+#pragma unroll
+    for (int b = 0; b < HC; b += 2) {
+      const double2 l2 = Lc[b / 2];
+      e[b] = MID ? l2.x * c : 0.0;
+      if (b + 1 < HC) e[b + 1] = MID ? l2.y * c : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < H; ++b) o[b] = 0.0;
+  }
+  // the inputs of the next PF steps are requested before this step's FMAs
+  constexpr int PF = 4;
+  double xk[PF], xm[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    xk[q] = q < H ? x[q * st] : 0.0;
+    xm[q] = q < H ? x[(P - q) * st] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const double a = xk[k % PF] + xm[k % PF], d = xk[k % PF] - xm[k % PF];
+    if (k + PF < H) {
+      xk[k % PF] = x[(k + PF) * st];
+      xm[k % PF] = x[(P - k - PF) * st];
+    }
+    const double2* __restrict__ Le2 = reinterpret_cast<const double2*>(A.LeT + k * HCP);
+    const double2* __restrict__ Lo2 = reinterpret_cast<const double2*>(A.LoT + k * HP);
+#pragma unroll
+    for (int b = 0; b < HC; b += 2) {
+      const double2 l2 = Le2[b / 2];
+      e[b] = fma(l2.x, a, e[b]);
+      if (b + 1 < HC) e[b + 1] = fma(l2.y, a, e[b + 1]);
+    }
+#pragma unroll
+    for (int b = 0; b < H; b += 2) {
+      const double2 l2 = Lo2[b / 2];
+      o[b] = fma(l2.x, d, o[b]);
+      if (b + 1 < H) o[b + 1] = fma(l2.y, d, o[b + 1]);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < H; ++b) {
+    v[b] = e[b] + o[b];
+    v[P - b] = e[b] - o[b];
+  }
+  if (MID) v[H] = e[H];
+}
+
+template <int P>
+struct OplGeom {
+  static constexpr int NP = P + 1, DPW = NP | 1, LDA = P | 1;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)NP * DPW + (size_t)P * LDA);
+};
+
+template <int P>
+__global__ void __launch_bounds__(64, 10) opl_kernel(const __grid_constant__ OpwArgs<P> A, double* __restrict__ ring) {
+  SMG_PDL_ENTRY();
+  using G = OplGeom<P>;
+  constexpr int NP = G::NP, DPW = G::DPW, LDA = G::LDA;
+  static_assert(P <= 32, "one lane per line");
+  extern __shared__ __align__(16) double smw[];
+  double* U = smw;                 // NP x DPW window of u, origin (Y0, X0)
+  double* AX = U + NP * DPW;       // P x LDA x-parts [a][b]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int el = blockIdx.x;
+  const int ex = el % A.tiles_x, ey = el / A.tiles_x;
+  const int X0 = ex * P, Y0 = ey * P;
+  const int N_x = A.N_x, N_y = A.N_y;
+  // window rows: coalesced row segments, periodic wrap on the high side
+  // (8-byte cp.async: every value in flight at once, no register round trip; the odd
+  // pitch rules out 16-byte bulk rows)
+  {
+    const int xw = X0 + P == N_x ? 0 : X0 + P;     // the high-side column (periodic)
+    for (int i = tid; i < NP * NP; i += 64) {
+      const int y = i / NP, x = i - y * NP;
+      const int gy = Y0 + y == N_y ? 0 : Y0 + y;
+      const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(U + y * DPW + x));
+      const double* g = A.u + (size_t)gy * N_x + (x == P ? xw : X0 + x);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+  __syncthreads();
+  double* R = ring + (size_t)el * (2 * P);
+  double v[P + 1];
+  if (lane < P) {
+    if (warp == 0) {
+      opl_line<P>(A, U + lane * DPW, 1, v);          // row a = lane
+#pragma unroll
+      for (int b = 0; b < P; ++b) AX[lane * LDA + b] = v[b];
+      R[lane] = v[P];
+    } else {
+      opl_line<P>(A, U + lane, DPW, v);              // column b = lane
+      R[P + lane] = v[P];
+    }
+  }
+  __syncthreads();
+  if (warp == 1 && lane < P) {
+    const int b = lane;
+    const double wyb = A.cy * A.wasm[b];
+    const size_t g0 = (size_t)Y0 * N_x + (X0 + b);
+    constexpr int CH = 8;
+#pragma unroll
+    for (int a0 = 0; a0 < P; a0 += CH) {
+      double fv[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) fv[i] = A.f != nullptr ? __ldg(A.f + g0 + (size_t)(a0 + i) * N_x) : 0.0;
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int a = a0 + i;
+        const double val = fma(A.cx * A.wasm[a], AX[a * LDA + b], wyb * v[a]);
+        A.out[g0 + (size_t)a * N_x] = A.f != nullptr ? fv[i] - val : val;
+      }
+    }
+  }
+}
+
+// One thread per low-side node of an element (as opdh_fixup, smg_opd.cu): (a, 0) takes the
+// left element's row-line value, then at the corner the lower element's column-line value;
+// (0, b), b >= 1, the lower element's.
+template <int P>
+__global__ void __launch_bounds__(256) opl_fixup(double* __restrict__ out, const double* __restrict__ ring, int n_x,
+                                                 int n_y, double sign, const __grid_constant__ OpwArgs<P> A) {
+  SMG_PDL_ENTRY();
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)n_x * n_y * 2 * P) return;
+  const int e = (int)(gid / (2 * P)), k = (int)(gid - (long)e * (2 * P));
+  if (k == P) return;
+  const int ey = e / n_x, ex = e - ey * n_x;
+  const int el = ey * n_x + wrapi(ex - 1, n_x), ed = wrapi(ey - 1, n_y) * n_x + ex;
+  const int a = k < P ? k : 0, b = k < P ? 0 : k - P;
+  double* o = out + (size_t)(ey * P + a) * ((size_t)n_x * P) + ex * P + b;
+  double v = *o;
+  if (k < P) v = fma(sign * A.cx * A.wasm[a], ring[(size_t)el * (2 * P) + a], v);
+  if (k > P) v = fma(sign * A.cy * A.wasm[b], ring[(size_t)ed * (2 * P) + P + b], v);
+  if (k == 0) v = fma(sign * A.cy * A.wasm[0], ring[(size_t)ed * (2 * P) + P], v);
+  *o = v;
+}
+
+// Host: 1 = not applicable.
+template <int P>
+int opl_launch_t(const OpLaunch& L, double* ring, cudaStream_t st) {
+  using G = OplGeom<P>;
+  if (L.diffusion || L.partials != nullptr || ring == nullptr) return 1;
+  OpwArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.dotp = nullptr;
+  A.N_x = L.n_x * P; A.N_y = L.n_y * P; A.tiles_x = L.n_x;
+  A.cx = L.cx; A.cy = L.cy;
+  {
+    constexpr int NP = P + 1, H = NP / 2, HC = H + (NP & 1);
+    auto Lbk = [&](int bb, int k) { return L.Mt[k * NP + bb]; };
+    double asym = 0.0, mx = 0.0;
+    for (int bb = 0; bb < NP; ++bb)
+      for (int k = 0; k < NP; ++k) {
+        asym = std::fmax(asym, std::fabs(Lbk(bb, k) - Lbk(P - bb, P - k)));
+        mx = std::fmax(mx, std::fabs(Lbk(bb, k)));
+      }
+    if (asym > 1e-14 * mx) return 1;
+    for (int bb = 0; bb < HC; ++bb) {
+      for (int k = 0; k < H; ++k) A.Le[bb * HC + k] = 0.5 * (Lbk(bb, k) + Lbk(bb, P - k));
+      if (NP & 1) A.Le[bb * HC + H] = Lbk(bb, H);
+    }
+    for (int bb = 0; bb < H; ++bb)
+      for (int k = 0; k < H; ++k) A.Lo[bb * H + k] = 0.5 * (Lbk(bb, k) - Lbk(bb, P - k));
+    A.Lo[H * H] = 0.0;
+    constexpr int HCP = OpwArgs<P>::kHCP, HP = OpwArgs<P>::kHP;
+    std::memset(A.LeT, 0, sizeof(A.LeT));
+    std::memset(A.LoT, 0, sizeof(A.LoT));
+    for (int bb = 0; bb < HC; ++bb)
+      for (int k = 0; k < HC; ++k) A.LeT[k * HCP + bb] = A.Le[bb * HC + k];
+    for (int bb = 0; bb < H; ++bb)
+      for (int k = 0; k < H; ++k) A.LoT[k * HP + bb] = A.Lo[bb * H + k];
+  }
+  for (int i = 0; i < P; ++i) A.wasm[i] = L.wasm[i];
+  static DeviceFlag attr;
+  if (!attr) {
+    if (G::SMEM > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(opl_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "opl_kernel smem attribute");
+    }
+    attr = true;
+  }
+  const int n_el = L.n_x * L.n_y;
+  launch(opl_kernel<P>, dim3(n_el), dim3(64), G::SMEM, st, A, ring);
+  int rc = check_launch("opl_kernel");
+  if (rc) return rc;
+  const long nb = (long)n_el * 2 * P;
+  launch(opl_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
+         L.f != nullptr ? -1.0 : 1.0, A);
+  return check_launch("opl_fixup");
+}
+
+// Poisson p = 32 with a ring workspace; 1 = not applicable (SMG_OPL=0 keeps opdh_kernel)
+int opl_launch(const OpLaunch& L, cudaStream_t st) {
+  static const int on = env_int("SMG_OPL", 1);
+  if (!on || L.p != 32) return 1;
+  return opl_launch_t<32>(L, L.ring, st);
 }
 
 int opw_launch(const OpLaunch& L, cudaStream_t st) {
