@@ -261,10 +261,14 @@ int smg_op_create(smg_op_t** h, int kind, int p, int n_x, int n_y, double dx, do
         dev = std::fmax(dev, std::fabs(kind == 1 ? a + b : a - b));
       }
     sym_ok = dev <= 1e-14 * (mmax > 0.0 ? mmax : 1.0);
+    // the diffusion fragments carry w[n] for both G[n] and G[P-n]
+    if (kind == 1)
+      for (int i = 0; i < NP; ++i)
+        if (std::fabs(weights[i] - weights[p - i]) > 1e-14 * std::fabs(weights[i])) sym_ok = false;
   }
   if (sym_ok && opd_applies(p, kind == 1)) {
     std::vector<double> fr;
-    opd_fragments(p, kind == 1, mat, fr);
+    opd_fragments(p, kind == 1, mat, weights, fr);
     e = cudaMalloc(&o->dfrag, sizeof(double) * fr.size());
     if (e == cudaSuccess) e = cudaMemcpy(o->dfrag, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { delete o; return cuda_fail(e, "smg_op_create"); }

@@ -479,7 +479,7 @@ int op_launch_t(const OpLaunch& L, cudaStream_t st) {
 // by opd_fragments.
 int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st);
 bool opd_applies(int p, bool diffusion);
-void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out);
+void opd_fragments(int p, bool diffusion, const double* D, const double* w, std::vector<double>& out);
 
 using OpLaunchFn = int (*)(const OpLaunch&, cudaStream_t);
 // Warp-per-element Poisson residual (smg_opw.cu) for p = 8, 16 without norm

@@ -124,7 +124,7 @@ __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0,
   const double* BE = frag;
   const double* BO = frag + KH * NH * 32;
   const double* BE2 = frag + 2 * KH * NH * 32;
-  const double* BO2 = frag + 3 * KH * NH * 32;
+  const double* BO2 = BE2 + 2 * NH * NH * 32;
   double W[NH][2], U[NH][2];
 #pragma unroll
   for (int j = 0; j < NH; ++j) W[j][0] = W[j][1] = U[j][0] = U[j][1] = 0.0;
@@ -148,8 +148,9 @@ __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0,
       const int n = 8 * j + 2 * t + e;
       double ga = 0.0, gd = 0.0;
       if (n <= H) {
-        const double gn = (U[j][e] + W[j][e]) * (n0[n * st] * WT[n]);
-        const double gm = (U[j][e] - W[j][e]) * (n0[(P - n) * st] * WT[P - n]);
+        // the GLL weight w[n] = w[P-n] is folded into column n of the first tables
+        const double gn = (U[j][e] + W[j][e]) * n0[n * st];
+        const double gm = (U[j][e] - W[j][e]) * n0[(P - n) * st];
         ga = n < H ? gn + gm : gn;
         gd = n < H ? gn - gm : 0.0;
       }
@@ -160,14 +161,12 @@ __device__ __forceinline__ void opd_batch_eo(const double* x0, const double* n0,
   double W2[NH][2], U2[NH][2];
 #pragma unroll
   for (int j = J0; j < J1; ++j) W2[j][0] = W2[j][1] = U2[j][0] = U2[j][1] = 0.0;
+  // k-step q = (n-tile q / 2, slot q % 2): lane t feeds ITS accumulator (node 8 (q/2) + 2t + q%2)
+  // as the A operand -- the sum over k is order-free, so the second product's fragment
+  // tables are stored in this node order (opd_fragments) and no quad shuffle is needed
 #pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
-    const double a0 = __shfl_sync(0xffffffffu, W[q >> 1][0], src);
-    const double a1 = __shfl_sync(0xffffffffu, W[q >> 1][1], src);
-    const double d0 = __shfl_sync(0xffffffffu, U[q >> 1][0], src);
-    const double d1 = __shfl_sync(0xffffffffu, U[q >> 1][1], src);
-    const double a = (t & 1) ? a1 : a0, d = (t & 1) ? d1 : d0;
+  for (int q = 0; q < 2 * NH; ++q) {
+    const double a = W[q >> 1][q & 1], d = U[q >> 1][q & 1];
 #pragma unroll
     for (int j = J0; j < J1; ++j) {
       dmma(W2[j][0], W2[j][1], a, __ldg(BE2 + (q * NH + j) * 32 + lane));
@@ -209,7 +208,7 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
   const double* BE = frag;
   const double* BO = frag + KH * NH * 32;
   const double* BE2 = frag + 2 * KH * NH * 32;
-  const double* BO2 = frag + 3 * KH * NH * 32;
+  const double* BO2 = BE2 + 2 * NH * NH * 32;
   double W[2][NH][2], U[2][NH][2];
 #pragma unroll
   for (int s = 0; s < 2; ++s)
@@ -249,8 +248,8 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
         const int n = 8 * j + 2 * t + e;
         double ga = 0.0, gd = 0.0;
         if (n <= H) {
-          const double gn = (U[s][j][e] + W[s][j][e]) * (n0[n * st] * WT[n]);
-          const double gm = (U[s][j][e] - W[s][j][e]) * (n0[(P - n) * st] * WT[P - n]);
+          const double gn = (U[s][j][e] + W[s][j][e]) * n0[n * st];
+          const double gm = (U[s][j][e] - W[s][j][e]) * n0[(P - n) * st];
           ga = n < H ? gn + gm : gn;
           gd = n < H ? gn - gm : 0.0;
         }
@@ -264,17 +263,12 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
 #pragma unroll
     for (int j = 0; j < NH; ++j) W2[s][j][0] = W2[s][j][1] = U2[s][j][0] = U2[s][j][1] = 0.0;
 #pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+  for (int q = 0; q < 2 * NH; ++q) {   // node-ordered k-steps (see opd_batch_eo): no quad shuffle
     double a[2], d[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const double a0 = __shfl_sync(0xffffffffu, W[s][q >> 1][0], src);
-      const double a1 = __shfl_sync(0xffffffffu, W[s][q >> 1][1], src);
-      const double d0 = __shfl_sync(0xffffffffu, U[s][q >> 1][0], src);
-      const double d1 = __shfl_sync(0xffffffffu, U[s][q >> 1][1], src);
-      a[s] = (t & 1) ? a1 : a0;
-      d[s] = (t & 1) ? d1 : d0;
+      a[s] = W[s][q >> 1][q & 1];
+      d[s] = U[s][q >> 1][q & 1];
     }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
@@ -308,7 +302,7 @@ __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double
   const double* BE = frag;
   const double* BO = frag + KH * NH * 32;
   const double* BE2 = frag + 2 * KH * NH * 32;
-  const double* BO2 = frag + 3 * KH * NH * 32;
+  const double* BO2 = BE2 + 2 * NH * NH * 32;
   double W[2][NH][2], U[2][NH][2];
 #pragma unroll
   for (int s = 0; s < 2; ++s)
@@ -346,8 +340,8 @@ __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double
         const int n = 8 * j + 2 * t + e;
         double ga = 0.0, gd = 0.0;
         if (n <= H) {
-          const double gn = (U[s][j][e] + W[s][j][e]) * (n0[n * st] * WT[n]);
-          const double gm = (U[s][j][e] - W[s][j][e]) * (n0[(P - n) * st] * WT[P - n]);
+          const double gn = (U[s][j][e] + W[s][j][e]) * n0[n * st];
+          const double gm = (U[s][j][e] - W[s][j][e]) * n0[(P - n) * st];
           ga = n < H ? gn + gm : gn;
           gd = n < H ? gn - gm : 0.0;
         }
@@ -361,17 +355,12 @@ __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double
 #pragma unroll
     for (int j = 0; j < NH; ++j) W2[s][j][0] = W2[s][j][1] = U2[s][j][0] = U2[s][j][1] = 0.0;
 #pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int src = (lane & ~3) | (2 * (q & 1) + (t >> 1));
+  for (int q = 0; q < 2 * NH; ++q) {   // node-ordered k-steps (see opd_batch_eo): no quad shuffle
     double a[2], d[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const double a0 = __shfl_sync(0xffffffffu, W[s][q >> 1][0], src);
-      const double a1 = __shfl_sync(0xffffffffu, W[s][q >> 1][1], src);
-      const double d0 = __shfl_sync(0xffffffffu, U[s][q >> 1][0], src);
-      const double d1 = __shfl_sync(0xffffffffu, U[s][q >> 1][1], src);
-      a[s] = (t & 1) ? a1 : a0;
-      d[s] = (t & 1) ? d1 : d0;
+      a[s] = W[s][q >> 1][q & 1];
+      d[s] = U[s][q >> 1][q & 1];
     }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
@@ -915,7 +904,7 @@ static int opdq_launch_t(const OpLaunch& L, const double* frag, double* ring, cu
 
 // Lane-ordered B fragments of D^T and D for opd_kernel (host): value for
 // (k-tile q, n-tile j, lane (g, t)) = B[4q + t][8j + g].
-void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& out) {
+void opd_fragments(int p, bool diffusion, const double* D, const double* w, std::vector<double>& out) {
   const int NP = p + 1, KT = (NP + 3) / 4, NTL = (NP + 7) / 8;
   if (diffusion) {
     // even/odd halves (opd_batch_eo): B[k][n] for k, n <= H
@@ -925,20 +914,27 @@ void opd_fragments(int p, bool diffusion, const double* D, std::vector<double>& 
     //   O2[k][n] = (D[k][n] - D[P-k][n]) / 2 (k < H)
     const int H = p / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
     auto d = [&](int i, int j) { return D[i * NP + j]; };
-    out.assign((size_t)4 * KH * NH * 32, 0.0);
+    // first product: k-step q holds k = 4q + t; second product: k-step q holds the node
+    // k = 8 (q / 2) + 2t + q % 2 that lane t's accumulator of the first product carries
+    const int K2 = 2 * NH;
+    out.assign((size_t)2 * (KH + K2) * NH * 32, 0.0);
     for (int m = 0; m < 4; ++m)
-      for (int q = 0; q < KH; ++q)
+      for (int q = 0; q < (m < 2 ? KH : K2); ++q)
         for (int j = 0; j < NH; ++j)
           for (int lane = 0; lane < 32; ++lane) {
-            const int k = 4 * q + (lane & 3), n = 8 * j + (lane >> 2);
+            const int k = m < 2 ? 4 * q + (lane & 3) : 8 * (q >> 1) + 2 * (lane & 3) + (q & 1);
+            const int n = 8 * j + (lane >> 2);
             double v = 0.0;
             if (k <= H && n <= H) {
               if (m == 0) v = k < H ? 0.5 * (d(n, k) + d(n, p - k)) : d(n, H);
               else if (m == 1) v = k < H ? 0.5 * (d(n, k) - d(n, p - k)) : 0.0;
+              // G[n] and G[P-n] are scaled by nu w at their nodes: the (mirror-symmetric) weight goes here
+              if (m < 2) v *= 0.5 * (w[n] + w[p - n]);
               else if (m == 2) v = k < H ? 0.5 * (d(k, n) + d(p - k, n)) : d(H, n);
               else v = k < H ? 0.5 * (d(k, n) - d(p - k, n)) : 0.0;
             }
-            out[((size_t)(m * KH + q) * NH + j) * 32 + lane] = v;
+            const size_t base = m < 2 ? (size_t)m * KH : (size_t)2 * KH + (size_t)(m - 2) * K2;
+            out[((base + q) * NH + j) * 32 + lane] = v;
           }
     return;
   }
