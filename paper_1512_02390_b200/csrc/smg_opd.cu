@@ -200,7 +200,7 @@ __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double
 template <int P>
 __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double* nr, const double* xc,
                                                  const double* nc, int stc, const double* WT,
-                                                 const double* __restrict__ frag, double (&Vb)[2][2][2],
+                                                 const double* frag, double (&Vb)[2][2][2],
                                                  double (&Vm)[2][2][2]) {
   constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
   static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
@@ -229,7 +229,7 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
     }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const double be = __ldg(BE + (q * NH + j) * 32 + lane), bo = __ldg(BO + (q * NH + j) * 32 + lane);
+      const double be = BE[(q * NH + j) * 32 + lane], bo = BO[(q * NH + j) * 32 + lane];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         dmma(W[s][j][0], W[s][j][1], a[s], be);
@@ -272,7 +272,7 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
     }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-      const double be = __ldg(BE2 + (q * NH + j) * 32 + lane), bo = __ldg(BO2 + (q * NH + j) * 32 + lane);
+      const double be = BE2[(q * NH + j) * 32 + lane], bo = BO2[(q * NH + j) * 32 + lane];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         dmma(W2[s][j][0], W2[s][j][1], a[s], be);
@@ -594,8 +594,12 @@ struct OpdhGeom {
   // x-part buffer pitch = 2 (mod 8): the column-wise combine (fixed column, rows 2 t apart
   // across the quad lanes) hits 16 distinct banks per half-warp (pitch P gave 4-way conflicts)
   static constexpr int OXP = P + 2;
+  // diffusion: the four fragment tables staged in shared memory (the persistent CTA reads
+  // them once per element; as L1-cached global loads they shared the LSU with everything else)
+  static constexpr int HH = P / 2, KHH = (HH + 1 + 3) / 4, NHH = (HH + 1 + 7) / 8;
+  static constexpr int NFR = DIFF ? 2 * (KHH + 2 * NHH) * NHH * 32 : 0;
   static constexpr size_t SMEM =
-      sizeof(double) * ((size_t)2 * NWIN * WIN + (size_t)P * OXP + (size_t)P + NP) + 32;
+      sizeof(double) * ((size_t)2 * NWIN * WIN + (size_t)P * OXP + (size_t)P + NP + NFR) + 32;
   static_assert(P % 8 == 0, "lines must fill whole batches");
 };
 
@@ -614,10 +618,12 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   double* AX = WB + 2 * NWIN * WIN;          // OY x OXP x-parts, then x+y parts
   double* WS = AX + OY * OXP;                // P assembled weights
   double* WT = WS + P;                       // NP GLL weights
-  uint64_t* bar = reinterpret_cast<uint64_t*>(WT + NP);   // [2]
+  double* FR = WT + NP;                      // NFR fragment doubles (diffusion)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(FR + G::NFR);   // [2]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int N_x = A.N_x, N_y = A.N_y;
 
+  for (int i = tid; i < G::NFR; i += NT) FR[i] = frag[i];
   for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
   for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
   if (tid == 0) {
@@ -666,7 +672,7 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
     constexpr int NHO = (P / 2 + 8) / 8;
     double Vb[2][NHO][2], Vm[2][NHO][2];   // [0]: row batch, [1]: column batch
     if constexpr (DIFF) {
-      opd_batch_eo_two<P>(ur, nr, uc, nc, DP, WT, frag, Vb, Vm);
+      opd_batch_eo_two<P>(ur, nr, uc, nc, DP, WT, FR, Vb, Vm);
     } else {
       opd_batch_pe<P, false>(ur, 1, frag, Vb[0], Vm[0]);
       opd_batch_pe<P, false>(uc, DP, frag, Vb[1], Vm[1]);
