@@ -19,6 +19,7 @@
 // (the parity tests pin 1e-12 against the reference).  The row/column line
 // batches of a pass are split over three warps so that each warp holds one
 // batch of full lines and one batch of vertex-only lines.
+#include <cstdlib>
 #include <vector>
 
 #include "smg_common.cuh"
@@ -193,39 +194,57 @@ __device__ __forceinline__ void opd_batch_eo_pair(const double* xv, const double
                                                   const double* __restrict__ frag, double& vlast,
                                                   double (&Vb)[2][2], double (&Vm)[2][2]);
 
+// Compact tables of the halo-free p = 24 kernel (H = P/2 = 12 = 3 x 4): doubles in the
+// fragment buffer before them (the opd_batch_eo tables) and their own size.
+constexpr int opd_two_offset(int p) {
+  const int H = p / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
+  return 2 * (KH + 2 * NH) * NH * 32;
+}
+constexpr int opd_two_doubles(int p) { return 4 * ((p / 2) / 4) * 2 * 32 + 32; }
+
 // Two FULL batches in lockstep (the halo-free kernel: a warp's row batch, stride 1, and
-// its column batch, stride stc): the same interleaving of DMMA chains as
-// opd_batch_eo_pair, every fragment load feeds both.  Returns V[n] (Vb) and V[P-n] (Vm)
-// of both batches, n = 8j + 2t + e <= H.
+// its column batch, stride stc), every fragment load feeds both.  Returns V[n] (Vb) and
+// V[P-n] (Vm) of both batches, n = 8j + 2t + e <= H.
+//
+// The four half products are 13 x 12 / 12 x 13 (the even halves have the centre as a 13th
+// input and no centre output, D[H][H] = 0 and E[.][H] = 0; the odd halves the reverse).
+// Padding k to 16 wasted a quarter of the DMMA slots, so here every product runs H / 4 = 3
+// k-steps over k < H and the centre input enters as a rank-1 DFMA update.  The first
+// product's outputs are placed (by the column order of its tables) where the second
+// product wants its k operand: n-tile 0 holds nodes 2t + e, n-tile 1 holds node 8 + t in
+// its even columns and the centre output (odd half only) in column 1 -- k-steps
+// (0,0), (0,1), (1,0) of the second product are then exactly the nodes < H, no shuffle;
+// the centre g_H is broadcast in the quad for the second rank-1 update.
+// fr: BE | BO | BE2 | BO2 (3 x 2 x 32 each) | CE1[16] | CE2[16]  (opd_fragments).
 template <int P>
 __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double* nr, const double* xc,
-                                                 const double* nc, int stc, const double* WT,
-                                                 const double* frag, double (&Vb)[2][2][2],
-                                                 double (&Vm)[2][2][2]) {
-  constexpr int H = P / 2, KH = (H + 1 + 3) / 4, NH = (H + 1 + 7) / 8;
-  static_assert(NH == 2 && P % 2 == 0, "p = 24 layout");
+                                                 const double* nc, int stc, const double* fr,
+                                                 double (&Vb)[2][2][2], double (&Vm)[2][2][2]) {
+  constexpr int H = P / 2, KQ = H / 4, NH = 2;
+  static_assert(H % 4 == 0 && H + 1 > 8 && H + 1 <= 16, "p = 24 layout");
   const int lane = threadIdx.x & 31, t = lane & 3;
-  const double* BE = frag;
-  const double* BO = frag + KH * NH * 32;
-  const double* BE2 = frag + 2 * KH * NH * 32;
-  const double* BO2 = BE2 + 2 * NH * NH * 32;
+  const double* BE = fr;
+  const double* BO = BE + KQ * NH * 32;
+  const double* BE2 = BO + KQ * NH * 32;
+  const double* BO2 = BE2 + KQ * NH * 32;
+  const double* CE1 = BO2 + KQ * NH * 32;
+  const double* CE2 = CE1 + 16;
   double W[2][NH][2], U[2][NH][2];
 #pragma unroll
   for (int s = 0; s < 2; ++s)
 #pragma unroll
     for (int j = 0; j < NH; ++j) W[s][j][0] = W[s][j][1] = U[s][j][0] = U[s][j][1] = 0.0;
 #pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int k = 4 * q + t;
+  for (int q = 0; q < KQ; ++q) {
+    const int k = 4 * q + t;   // < H
     double a[2], d[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const double* x0 = s ? xc : xr;
       const int st = s ? stc : 1;
-      const double xa = k <= H ? x0[k * st] : 0.0;
-      const double xb = k < H ? x0[(P - k) * st] : 0.0;
+      const double xa = x0[k * st], xb = x0[(P - k) * st];
       a[s] = xa + xb;
-      d[s] = k < H ? xa - xb : 0.0;
+      d[s] = xa - xb;
     }
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
@@ -237,25 +256,30 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
       }
     }
   }
+  // centre input x_H into the even half (slot (1,1) has no even output)
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const double c = (s ? xc : xr)[H * (s ? stc : 1)];
+    W[s][0][0] = fma(c, CE1[t], W[s][0][0]);
+    W[s][0][1] = fma(c, CE1[4 + t], W[s][0][1]);
+    W[s][1][0] = fma(c, CE1[8 + t], W[s][1][0]);
+  }
+  // g = G nu (w is in the tables) at nodes n and P - n -> a', d'; the centre g_H from slot (1,1) of lane t = 0
+  double cp[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const double* n0 = s ? nc : nr;
     const int st = s ? stc : 1;
 #pragma unroll
-    for (int j = 0; j < NH; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = 8 * j + 2 * t + e;
-        double ga = 0.0, gd = 0.0;
-        if (n <= H) {
-          const double gn = (U[s][j][e] + W[s][j][e]) * n0[n * st];
-          const double gm = (U[s][j][e] - W[s][j][e]) * n0[(P - n) * st];
-          ga = n < H ? gn + gm : gn;
-          gd = n < H ? gn - gm : 0.0;
-        }
-        W[s][j][e] = ga;
-        U[s][j][e] = gd;
-      }
+    for (int q = 0; q < 3; ++q) {
+      const int j = q >> 1, e = q & 1;
+      const int n = j == 0 ? 2 * t + e : 8 + t;
+      const double gn = (U[s][j][e] + W[s][j][e]) * n0[n * st];
+      const double gm = (U[s][j][e] - W[s][j][e]) * n0[(P - n) * st];
+      W[s][j][e] = gn + gm;
+      U[s][j][e] = gn - gm;
+    }
+    cp[s] = __shfl_sync(0xffffffffu, U[s][1][1] * n0[H * st], lane & ~3);
   }
   double W2[2][NH][2], U2[2][NH][2];
 #pragma unroll
@@ -263,32 +287,29 @@ __device__ __forceinline__ void opd_batch_eo_two(const double* xr, const double*
 #pragma unroll
     for (int j = 0; j < NH; ++j) W2[s][j][0] = W2[s][j][1] = U2[s][j][0] = U2[s][j][1] = 0.0;
 #pragma unroll
-  for (int q = 0; q < 2 * NH; ++q) {   // node-ordered k-steps (see opd_batch_eo): no quad shuffle
-    double a[2], d[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      a[s] = W[s][q >> 1][q & 1];
-      d[s] = U[s][q >> 1][q & 1];
-    }
+  for (int q = 0; q < KQ; ++q) {   // k-step q: the nodes of slot (q / 2, q % 2)
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       const double be = BE2[(q * NH + j) * 32 + lane], bo = BO2[(q * NH + j) * 32 + lane];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        dmma(W2[s][j][0], W2[s][j][1], a[s], be);
-        dmma(U2[s][j][0], U2[s][j][1], d[s], bo);
+        dmma(W2[s][j][0], W2[s][j][1], W[s][q >> 1][q & 1], be);
+        dmma(U2[s][j][0], U2[s][j][1], U[s][q >> 1][q & 1], bo);
       }
     }
   }
 #pragma unroll
-  for (int s = 0; s < 2; ++s)
+  for (int j = 0; j < NH; ++j)
 #pragma unroll
-    for (int j = 0; j < NH; ++j)
+    for (int e = 0; e < 2; ++e) {
+      const double c2 = CE2[(2 * j + e) * 4 + t];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        Vb[s][j][e] = U2[s][j][e] + W2[s][j][e];
-        Vm[s][j][e] = U2[s][j][e] - W2[s][j][e];
+      for (int s = 0; s < 2; ++s) {
+        const double w2 = fma(cp[s], c2, W2[s][j][e]);
+        Vb[s][j][e] = U2[s][j][e] + w2;
+        Vm[s][j][e] = U2[s][j][e] - w2;
       }
+    }
 }
 
 template <int P>
@@ -596,8 +617,7 @@ struct OpdhGeom {
   static constexpr int OXP = P + 2;
   // diffusion: the four fragment tables staged in shared memory (the persistent CTA reads
   // them once per element; as L1-cached global loads they shared the LSU with everything else)
-  static constexpr int HH = P / 2, KHH = (HH + 1 + 3) / 4, NHH = (HH + 1 + 7) / 8;
-  static constexpr int NFR = DIFF ? 2 * (KHH + 2 * NHH) * NHH * 32 : 0;
+  static constexpr int NFR = DIFF ? opd_two_doubles(P) : 0;
   static constexpr size_t SMEM =
       sizeof(double) * ((size_t)2 * NWIN * WIN + (size_t)P * OXP + (size_t)P + NP + NFR) + 32;
   static_assert(P % 8 == 0, "lines must fill whole batches");
@@ -623,7 +643,7 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int N_x = A.N_x, N_y = A.N_y;
 
-  for (int i = tid; i < G::NFR; i += NT) FR[i] = frag[i];
+  for (int i = tid; i < G::NFR; i += NT) FR[i] = frag[opd_two_offset(P) + i];
   for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
   for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
   if (tid == 0) {
@@ -672,7 +692,7 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
     constexpr int NHO = (P / 2 + 8) / 8;
     double Vb[2][NHO][2], Vm[2][NHO][2];   // [0]: row batch, [1]: column batch
     if constexpr (DIFF) {
-      opd_batch_eo_two<P>(ur, nr, uc, nc, DP, WT, FR, Vb, Vm);
+      opd_batch_eo_two<P>(ur, nr, uc, nc, DP, FR, Vb, Vm);
     } else {
       opd_batch_pe<P, false>(ur, 1, frag, Vb[0], Vm[0]);
       opd_batch_pe<P, false>(uc, DP, frag, Vb[1], Vm[1]);
@@ -942,6 +962,45 @@ void opd_fragments(int p, bool diffusion, const double* D, const double* w, std:
             const size_t base = m < 2 ? (size_t)m * KH : (size_t)2 * KH + (size_t)(m - 2) * K2;
             out[((base + q) * NH + j) * 32 + lane] = v;
           }
+    if (H % 4 == 0 && NH == 2) {
+      // compact tables of opd_batch_eo_two: H / 4 k-steps over k < H; first-product columns in
+      // slot order (n-tile 0: node g; n-tile 1: node 8 + g/2 in the even columns, the centre
+      // output in column 1 of the odd half), second-product k rows in the same slot order;
+      // then the rank-1 centre vectors CE1 (slot-indexed, weight folded) and CE2
+      const int KQ = H / 4;
+      const size_t off = out.size();
+      if ((int)off != opd_two_offset(p)) std::abort();
+      out.resize(off + (size_t)opd_two_doubles(p), 0.0);
+      auto node1 = [&](int j, int c) { return j == 0 ? c : (c % 2 == 0 ? 8 + c / 2 : (c == 1 ? H : -1)); };
+      auto wsym = [&](int n) { return 0.5 * (w[n] + w[p - n]); };
+      for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < KQ; ++q)
+          for (int j = 0; j < NH; ++j)
+            for (int lane = 0; lane < 32; ++lane) {
+              const int t = lane & 3, g = lane >> 2;
+              double v = 0.0;
+              if (m < 2) {
+                const int k = 4 * q + t, n = node1(j, g);
+                if (n >= 0 && n <= H && !(m == 0 && n == H))
+                  v = 0.5 * (m == 0 ? d(n, k) + d(n, p - k) : d(n, k) - d(n, p - k)) * wsym(n);
+              } else {
+                const int k = q == 0 ? 2 * t : (q == 1 ? 2 * t + 1 : 8 + t), n = 8 * j + g;
+                if (n <= H && !(m == 2 && n == H))
+                  v = 0.5 * (m == 2 ? d(k, n) + d(p - k, n) : d(k, n) - d(p - k, n));
+              }
+              out[off + ((size_t)(m * KQ + q) * NH + j) * 32 + lane] = v;
+            }
+      double* ce1 = out.data() + off + (size_t)4 * KQ * NH * 32;
+      double* ce2 = ce1 + 16;
+      for (int j = 0; j < 2; ++j)
+        for (int e = 0; e < 2; ++e)
+          for (int t = 0; t < 4; ++t) {
+            const int n1 = (j == 0) ? 2 * t + e : (e == 0 ? 8 + t : -1);
+            ce1[(2 * j + e) * 4 + t] = (n1 >= 0 && n1 < H) ? d(n1, H) * wsym(n1) : 0.0;
+            const int n2 = 8 * j + 2 * t + e;
+            ce2[(2 * j + e) * 4 + t] = n2 < H ? d(H, n2) : 0.0;
+          }
+    }
     return;
   }
   {
