@@ -653,16 +653,17 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   }
   SMG_PDL_WAIT();
   __syncthreads();
-  // window of element e into buffer b (warp 0 issues; the buffer's previous readers are past a barrier)
+  // window of element e into buffer b: warp 0 posts the byte count and issues the rows of u,
+  // warp 1 those of nu (a copy may complete before the count is posted: the phase cannot end
+  // before thread 0's arrival); the buffer's previous readers are past a barrier
   auto issue = [&](int e, int b) {
     const int tx = e % A.tiles_x, ty = e / A.tiles_x;
     const int X0 = tx * OX, Y0 = ty * OY;
     if (tid == 0) mbar_arrive_expect_tx(bar + b, (unsigned)NWIN * pwin_bytes(NP, NP, pwin_shift(X0, N_x)));
-    __syncwarp();
-    pwin_issue_warp(A.u, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN) * WIN, DP, bar + b);
-    if (DIFF) pwin_issue_warp(A.nu, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN + 1) * WIN, DP, bar + b);
+    if (warp == 0) pwin_issue_warp(A.u, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN) * WIN, DP, bar + b);
+    if (DIFF && warp == 1) pwin_issue_warp(A.nu, N_x, N_y, X0, Y0, NP, NP, WB + (b * NWIN + 1) * WIN, DP, bar + b);
   };
-  if (warp == 0 && (int)blockIdx.x < n_el) issue(blockIdx.x, 0);
+  if (warp < 2 && (int)blockIdx.x < n_el) issue(blockIdx.x, 0);
 
   int it = 0;
   for (int el = blockIdx.x; el < n_el; el += gridDim.x, ++it) {
@@ -671,7 +672,7 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
     const int X0 = tx * OX, Y0 = ty * OY;
     const int sh = pwin_shift(X0, N_x);
     double* R = ring + (size_t)el * (2 * P);   // [0,P): node-P values of the row lines; [P,2P): column lines
-    if (warp == 0 && el + (int)gridDim.x < n_el) issue(el + gridDim.x, bsel ^ 1);
+    if (warp < 2 && el + (int)gridDim.x < n_el) issue(el + gridDim.x, bsel ^ 1);
     constexpr int KO = (OX * OY + NT - 1) / NT;
     double fv[KO];
 #pragma unroll
