@@ -64,6 +64,9 @@ int ccg_dot(const double* x, const double* y, int64_t n, double* out, const doub
 int pcg_update(double* x, double* r, const double* p, const double* q, int64_t n, double* S, int ro, double tol,
                int it, double* ws, cudaStream_t st);
 int pcg_scale(double* z, int64_t n, double scale, const double* S, cudaStream_t st);
+int pcg_coop(int nx, int ny, double dx, double dy, const double* tab, const double* nu, double* x, double* r,
+             double* p0, double* p1, double* z, double* W, double* part, double* S, double tol, int max_iter,
+             cudaStream_t st);
 int pcg_dscale(const double* in, double* out, const double* nu, int64_t n, const double* S, cudaStream_t st);
 int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, double* ws, const double* tab,
              cudaStream_t st);
@@ -928,6 +931,20 @@ int smg_coarse_pcg(const smg_op_t* op, const smg_coarse_t* pc, const double* f0,
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_pcg");
   if (hs[0] == 0.0) { *iters_out = 0; return SMG_OK; }
   int it = 0;
+  // the whole iteration loop as one cooperative kernel (smg_fft.cu pcg_coop_kernel) where it
+  // applies: diagonally scaled FFT preconditioner, power-of-two mesh of 128..512 nodes a side.
+  // b and q are free by now: the per-CTA partial sums and the second p buffer
+  if (dsc) {
+    rc = pcg_coop(pc->n_x, pc->n_y, pc->dx, pc->dy, pc->fft, op->nu, u0, r, p, q, z, pws, b, S, tol, max_iter, st);
+    if (rc != 1) {
+      if (rc) return rc;
+      if ((e = cudaMemcpyAsync(hs, S, sizeof(double) * 8, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "smg_coarse_pcg");
+      if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "smg_coarse_pcg");
+      const bool okc = hs[4] != 0.0;
+      *iters_out = okc ? (int)hs[5] : -max_iter;
+      return smg_project_mean(u0, n, red, stream);
+    }
+  }
   // iterations between two host reads of the convergence flag: the iterations enqueued
   // after convergence still run (C5: 11-14 needed; with one read per 16 iterations 2-5 of
   // 16 were wasted, ~80 us each), so after the first 8 the flag is read every 3

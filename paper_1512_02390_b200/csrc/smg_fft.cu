@@ -15,8 +15,11 @@
 //                         complex workspace of n_x n_y entries (the coarse ws)
 //   up to 64 x 64       : the dense two-launch path is faster; a one-CTA FFT
 //                         kernel is kept behind SMG_PINV_FFT=2.
+#include <algorithm>
 #include <cmath>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "smg_common.cuh"
 
@@ -320,6 +323,260 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
   if (rc) return rc;
   launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, tab, static_cast<const double*>(nullptr), W, u, 1, lr);
   return check_launch("fft_rows_kernel");
+}
+
+
+// ---- coarse PCG iterations as ONE cooperative kernel ------------------------------
+// The p = 1 diffusion PCG (smg_coarse_pcg: preconditioner D^-1/2 A_P^+ D^-1/2, A_P^+ by
+// 2D FFT) ran ten launches per iteration on vectors of n_x n_y <= 512^2 doubles: ~110 us
+// per iteration at C5 for ~10 MB of traffic, all launch latency and serial last-block
+// reductions, plus iterations wasted between two host reads of the convergence flag.
+// Here G CTAs (one per SM, co-resident) each own n_y / G node rows (and n_x / G spectrum
+// columns) and run the whole loop with four grid barriers per iteration:
+//   EA  p <- z + beta p on the own rows and one halo row each side (p ping-pongs between
+//       two buffers), q = A_0 p on the own rows (A_0 at p = 1 is the 5-point stencil with
+//       edge coefficients c (nu_a + nu_b) / 2), partial p.q                   | barrier
+//   B   alpha; x += alpha p, r -= alpha q (own rows), partial r.r;
+//       rows of r / sqrt(nu) -> forward FFT along x -> W                        | barrier
+//   C   convergence test on r.r (same bits in every CTA: a uniform exit);
+//       own columns of W: FFT along y, / lambda, inverse FFT along y           | barrier
+//   D   own rows of W: inverse FFT along x, z = Re / sqrt(nu); partial r.z     | barrier
+// Sums are per-CTA tree reductions followed by a fixed-order sum of the G partials
+// that every warp repeats for itself: deterministic, no atomics, no host reads.
+// Everything another CTA wrote is read with ld.cg (L1 is not coherent across SMs).
+namespace cgx = cooperative_groups;
+
+struct PcgCoop {
+  int nx, ny, lx, ly, Lr, Lc, max_iter;
+  double cx, cy, tol;
+  const double* tab;   // fft_table
+  const double* nu;    // nodal diffusivity (n_y x n_x)
+  double* x;
+  double* r;
+  double* P0;          // p on entry
+  double* P1;
+  double* z;
+  double2* W;
+  double* part;        // 3 * G partial sums
+  double* S;           // S[0] = ||b||^2, S[2] = r.z on entry; S[4] = converged, S[5] = iterations, S[6] = ||r||^2
+};
+
+__device__ __forceinline__ double pcgc_block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();   // red is free
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  return s;
+}
+
+// fixed-order total of G per-CTA partials (every warp for itself; G <= 128)
+__device__ __forceinline__ double pcgc_total(const double* part, int G) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int i = lane; i < G; i += 32) v += __ldcg(part + i);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
+  cgx::grid_group grid = cgx::this_grid();
+  extern __shared__ __align__(16) double2 zs[];
+  const int nx = A.nx, ny = A.ny, Lr = A.Lr, Lc = A.Lc, G = gridDim.x;
+  const int lsx = fpad(nx), lsy = fpad(ny);
+  const int nz = max(Lr * lsx, 2 * Lc * lsy);
+  double2* SX = zs + nz;                       // n_x - 1 stage twiddles
+  double2* SY = SX + nx;                       // n_y - 1
+  double* MX = reinterpret_cast<double*>(SY + ny);   // mu_x (n_x), mu_y (n_y)
+  double* MY = MX + nx;
+  double* NU = MY + ny;                        // (Lr + 2) x n_x: rows r0 - 1 .. r0 + Lr of nu
+  double* ISN = NU + (Lr + 2) * nx;            // Lr x n_x: 1 / sqrt(nu) on the own rows
+  double* PS = ISN + Lr * nx;                  // (Lr + 2) x n_x: p on the own rows and the halo rows
+  double* QS = PS + (Lr + 2) * nx;             // Lr x n_x: q on the own rows
+  double* red = QS + Lr * nx;                  // 32
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int r0 = blockIdx.x * Lr, c0 = blockIdx.x * Lc;
+  const int own = Lr * nx;
+
+  fft_load_sw(A.tab, nx, SX);
+  fft_load_sw(A.tab + 2 * (nx - 1), ny, SY);
+  {
+    const double* mu = A.tab + 2 * (nx - 1) + 2 * (ny - 1);
+    for (int i = tid; i < nx; i += NT) MX[i] = __ldg(mu + i);
+    for (int i = tid; i < ny; i += NT) MY[i] = __ldg(mu + nx + i);
+  }
+  for (int i = tid; i < (Lr + 2) * nx; i += NT) {
+    const int l = i / nx, xx = i - l * nx;
+    const int gy = (r0 - 1 + l + ny) & (ny - 1);
+    NU[i] = __ldg(A.nu + (size_t)gy * nx + xx);
+  }
+  __syncthreads();
+  for (int i = tid; i < own; i += NT) ISN[i] = 1.0 / sqrt(NU[nx + i]);
+  const double bb = A.S[0];
+  double rz_old = A.S[2];
+  const double sc = 1.0 / ((double)nx * ny);
+  double* part_pq = A.part;
+  double* part_rr = A.part + G;
+  double* part_rz = A.part + 2 * G;
+  int done_it = 0;
+  double rr_last = 0.0;
+  __syncthreads();
+
+  for (int it = 0; it < A.max_iter; ++it) {
+    const double* Pold = (it & 1) ? A.P1 : A.P0;
+    double* Pnew = (it & 1) ? A.P0 : A.P1;
+    // ---- EA
+    double beta = 0.0;
+    if (it > 0) {
+      const double rz_new = pcgc_total(part_rz, G);
+      beta = rz_new / rz_old;
+      rz_old = rz_new;
+    }
+    for (int i = tid; i < (Lr + 2) * nx; i += NT) {
+      const int l = i / nx, xx = i - l * nx;
+      const size_t g = (size_t)((r0 - 1 + l + ny) & (ny - 1)) * nx + xx;
+      const double po = __ldcg(Pold + g);
+      const double pn = it > 0 ? __dadd_rn(__ldcg(A.z + g), __dmul_rn(beta, po)) : po;
+      PS[i] = pn;
+      if (l >= 1 && l <= Lr) Pnew[g] = pn;
+    }
+    __syncthreads();
+    double acc = 0.0;
+    for (int i = tid; i < own; i += NT) {
+      const int l = i / nx + 1, xx = i & (nx - 1);
+      const int xe = (xx + 1) & (nx - 1), xw = (xx - 1 + nx) & (nx - 1);
+      const double u = PS[l * nx + xx], v = NU[l * nx + xx];
+      const double kE = 0.5 * A.cx * (v + NU[l * nx + xe]), kW = 0.5 * A.cx * (v + NU[l * nx + xw]);
+      const double kN = 0.5 * A.cy * (v + NU[(l + 1) * nx + xx]), kS = 0.5 * A.cy * (v + NU[(l - 1) * nx + xx]);
+      const double q = kE * (u - PS[l * nx + xe]) + kW * (u - PS[l * nx + xw]) + kN * (u - PS[(l + 1) * nx + xx]) +
+                       kS * (u - PS[(l - 1) * nx + xx]);
+      QS[i] = q;
+      acc = fma(u, q, acc);
+    }
+    {
+      const double s = pcgc_block_sum(acc, red);
+      if (tid == 0) part_pq[blockIdx.x] = s;
+    }
+    grid.sync();
+    // ---- B
+    const double alpha = rz_old / pcgc_total(part_pq, G);
+    acc = 0.0;
+    for (int i = tid; i < own; i += NT) {
+      const int l = i / nx, xx = i - l * nx;
+      const size_t g = (size_t)(r0 + l) * nx + xx;
+      A.x[g] = __dadd_rn(A.x[g], __dmul_rn(alpha, PS[nx + i]));
+      const double ri = __dsub_rn(A.r[g], __dmul_rn(alpha, QS[i]));
+      A.r[g] = ri;
+      acc = fma(ri, ri, acc);
+      zs[l * lsx + fpad(brev(xx, A.lx))] = make_double2(ri * ISN[i], 0.0);
+    }
+    {
+      const double s = pcgc_block_sum(acc, red);   // its barriers also publish zs
+      if (tid == 0) part_rr[blockIdx.x] = s;
+    }
+    fft_lines_p(zs, nx, A.lx, Lr, lsx, SX, false);
+    for (int i = tid; i < own; i += NT) {
+      const int l = i / nx, xx = i - l * nx;
+      A.W[(size_t)(r0 + l) * nx + xx] = zs[l * lsx + fpad(xx)];
+    }
+    grid.sync();
+    // ---- C
+    rr_last = pcgc_total(part_rr, G);
+    if (sqrt(rr_last) <= A.tol * sqrt(bb)) {
+      done_it = it + 1;
+      break;
+    }
+    {
+      double2* Z2 = zs + Lc * lsy;
+      for (int i = tid; i < Lc * ny; i += NT) {
+        const int y = i / Lc, l = i - y * Lc;
+        zs[l * lsy + fpad(brev(y, A.ly))] = __ldcg(A.W + (size_t)y * nx + c0 + l);
+      }
+      __syncthreads();
+      fft_lines_p(zs, ny, A.ly, Lc, lsy, SY, false);
+      for (int i = tid; i < Lc * ny; i += NT) {
+        const int l = i / ny, ky = i - l * ny, kx = c0 + l;
+        const double lam = A.cx * MX[kx] + A.cy * MY[ky];
+        const double s = (ky == 0 && kx == 0) ? 0.0 : 1.0 / lam;
+        const double2 zz = zs[l * lsy + fpad(ky)];
+        Z2[l * lsy + fpad(brev(ky, A.ly))] = make_double2(zz.x * s, zz.y * s);
+      }
+      __syncthreads();
+      fft_lines_p(Z2, ny, A.ly, Lc, lsy, SY, true);
+      for (int i = tid; i < Lc * ny; i += NT) {
+        const int y = i / Lc, l = i - y * Lc;
+        A.W[(size_t)y * nx + c0 + l] = Z2[l * lsy + fpad(y)];
+      }
+    }
+    grid.sync();
+    // ---- D
+    for (int i = tid; i < own; i += NT) {
+      const int l = i / nx, xx = i - l * nx;
+      zs[l * lsx + fpad(brev(xx, A.lx))] = __ldcg(A.W + (size_t)(r0 + l) * nx + xx);
+    }
+    __syncthreads();
+    fft_lines_p(zs, nx, A.lx, Lr, lsx, SX, true);
+    acc = 0.0;
+    for (int i = tid; i < own; i += NT) {
+      const int l = i / nx, xx = i - l * nx;
+      const size_t g = (size_t)(r0 + l) * nx + xx;
+      const double zv = zs[l * lsx + fpad(xx)].x * sc * ISN[i];
+      A.z[g] = zv;
+      acc = fma(A.r[g], zv, acc);
+    }
+    {
+      const double s = pcgc_block_sum(acc, red);
+      if (tid == 0) part_rz[blockIdx.x] = s;
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    A.S[6] = rr_last;
+    if (done_it) { A.S[4] = 1.0; A.S[5] = (double)done_it; }
+  }
+}
+
+// 1 = not applicable (the caller keeps its launch-per-step loop)
+int pcg_coop(int nx, int ny, double dx, double dy, const double* tab, const double* nu, double* x, double* r,
+             double* p0, double* p1, double* z, double* W, double* part, double* S, double tol, int max_iter,
+             cudaStream_t st) {
+  int lx = 0, ly = 0;
+  static const int on = env_int("SMG_PCG_COOP", 1);
+  if (!on || tab == nullptr || !pow2(nx, &lx) || !pow2(ny, &ly) || nx > 512 || ny > 512 || nx < 128 || ny < 128) return 1;
+  int dev = 0, sms = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return 1;
+  int G = 128;
+  while (G > sms || G > nx || G > ny) G >>= 1;
+  if (G < 32) return 1;
+  PcgCoop A;
+  A.nx = nx; A.ny = ny; A.lx = lx; A.ly = ly; A.Lr = ny / G; A.Lc = nx / G; A.max_iter = max_iter;
+  A.cx = dy / dx; A.cy = dx / dy; A.tol = tol;
+  A.tab = tab; A.nu = nu; A.x = x; A.r = r; A.P0 = p0; A.P1 = p1; A.z = z;
+  A.W = reinterpret_cast<double2*>(W); A.part = part; A.S = S;
+  const int lsx = nx + nx / 16, lsy = ny + ny / 16;
+  const int nz = std::max(A.Lr * lsx, 2 * A.Lc * lsy);
+  const size_t smem = sizeof(double2) * ((size_t)nz + nx + ny) +
+                      sizeof(double) * ((size_t)nx + ny + (size_t)(A.Lr + 2) * nx * 2 + (size_t)A.Lr * nx * 2 + 32);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(pcg_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "pcg_coop_kernel smem attribute");
+    attr = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_coop_kernel, 512, smem);
+  if (per_sm < 1) return 1;
+  void* args[] = {&A};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)pcg_coop_kernel, dim3(G), dim3(512), args, smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "pcg_coop_kernel");
+  return SMG_OK;
 }
 
 }  // namespace smg
