@@ -373,14 +373,21 @@ __device__ __forceinline__ double pcgc_block_sum(double v, double* red) {
   return s;
 }
 
-// fixed-order total of G per-CTA partials (every warp for itself; G <= 128)
-__device__ __forceinline__ double pcgc_total(const double* part, int G) {
+// fixed-order total of G per-CTA partials (G <= 128): warp 0 reads them (every warp of every
+// CTA reading the same 1 KB was 21 % of the kernel's stall samples), the CTA shares the sum
+__device__ __forceinline__ double pcgc_total(const double* part, int G, double* red) {
   const int lane = threadIdx.x & 31;
-  double v = 0.0;
-  for (int i = lane; i < G; i += 32) v += __ldcg(part + i);
+  if (threadIdx.x < 32) {
+    double v[4];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+    for (int k = 0; k < 4; ++k) v[k] = lane + 32 * k < G ? __ldcg(part + lane + 32 * k) : 0.0;
+    double t = (v[0] + v[1]) + (v[2] + v[3]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
 }
 
 __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
   double* ISN = NU + (Lr + 2) * nx;            // Lr x n_x: 1 / sqrt(nu) on the own rows
   double* PS = ISN + Lr * nx;                  // (Lr + 2) x n_x: p on the own rows and the halo rows
   double* QS = PS + (Lr + 2) * nx;             // Lr x n_x: q on the own rows
-  double* red = QS + Lr * nx;                  // 32
+  double* red = QS + Lr * nx;                  // 64: warp sums, then the grid total
   const int tid = threadIdx.x, NT = blockDim.x;
   const int r0 = blockIdx.x * Lr, c0 = blockIdx.x * Lc;
   const int own = Lr * nx;
@@ -424,6 +431,19 @@ __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
   double* part_rz = A.part + 2 * G;
   int done_it = 0;
   double rr_last = 0.0;
+  // a thread's elements are fixed: i = tid + k NT of the own rows (k < KO) and of the own +
+  // halo rows (k < KH); x and r of the own rows stay in registers for the whole solve, and
+  // every loop that reads global memory issues all of its loads before using any (the
+  // phases are latency-bound: one round trip to L2 each instead of one per element)
+  constexpr int KO = 4, KH = 6;   // n_x <= 512, L_r <= 4, 512 threads
+  const int nhalo = (Lr + 2) * nx;
+  double xr[KO], rv[KO];
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int i = tid + k * NT;
+    xr[k] = i < own ? A.x[(size_t)r0 * nx + i] : 0.0;
+    rv[k] = i < own ? A.r[(size_t)r0 * nx + i] : 0.0;
+  }
   __syncthreads();
 
   for (int it = 0; it < A.max_iter; ++it) {
@@ -432,30 +452,51 @@ __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
     // ---- EA
     double beta = 0.0;
     if (it > 0) {
-      const double rz_new = pcgc_total(part_rz, G);
+      const double rz_new = pcgc_total(part_rz, G, red);
       beta = rz_new / rz_old;
       rz_old = rz_new;
     }
-    for (int i = tid; i < (Lr + 2) * nx; i += NT) {
-      const int l = i / nx, xx = i - l * nx;
-      const size_t g = (size_t)((r0 - 1 + l + ny) & (ny - 1)) * nx + xx;
-      const double po = __ldcg(Pold + g);
-      const double pn = it > 0 ? __dadd_rn(__ldcg(A.z + g), __dmul_rn(beta, po)) : po;
-      PS[i] = pn;
-      if (l >= 1 && l <= Lr) Pnew[g] = pn;
+    {
+      double po[KH], zv[KH];
+#pragma unroll
+      for (int k = 0; k < KH; ++k) {
+        const int i = tid + k * NT;
+        po[k] = zv[k] = 0.0;
+        if (i < nhalo) {
+          const int l = i / nx, xx = i - l * nx;
+          const size_t g = (size_t)((r0 - 1 + l + ny) & (ny - 1)) * nx + xx;
+          po[k] = __ldcg(Pold + g);
+          if (it > 0) zv[k] = __ldcg(A.z + g);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KH; ++k) {
+        const int i = tid + k * NT;
+        if (i < nhalo) {
+          const int l = i / nx, xx = i - l * nx;
+          const double pn = it > 0 ? __dadd_rn(zv[k], __dmul_rn(beta, po[k])) : po[k];
+          PS[i] = pn;
+          if (l >= 1 && l <= Lr) Pnew[(size_t)(r0 - 1 + l) * nx + xx] = pn;
+        }
+      }
     }
     __syncthreads();
     double acc = 0.0;
-    for (int i = tid; i < own; i += NT) {
-      const int l = i / nx + 1, xx = i & (nx - 1);
-      const int xe = (xx + 1) & (nx - 1), xw = (xx - 1 + nx) & (nx - 1);
-      const double u = PS[l * nx + xx], v = NU[l * nx + xx];
-      const double kE = 0.5 * A.cx * (v + NU[l * nx + xe]), kW = 0.5 * A.cx * (v + NU[l * nx + xw]);
-      const double kN = 0.5 * A.cy * (v + NU[(l + 1) * nx + xx]), kS = 0.5 * A.cy * (v + NU[(l - 1) * nx + xx]);
-      const double q = kE * (u - PS[l * nx + xe]) + kW * (u - PS[l * nx + xw]) + kN * (u - PS[(l + 1) * nx + xx]) +
-                       kS * (u - PS[(l - 1) * nx + xx]);
-      QS[i] = q;
-      acc = fma(u, q, acc);
+    double qv[KO];
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int i = tid + k * NT;
+      qv[k] = 0.0;
+      if (i < own) {
+        const int l = i / nx + 1, xx = i & (nx - 1);
+        const int xe = (xx + 1) & (nx - 1), xw = (xx - 1 + nx) & (nx - 1);
+        const double u = PS[l * nx + xx], v = NU[l * nx + xx];
+        const double kE = 0.5 * A.cx * (v + NU[l * nx + xe]), kW = 0.5 * A.cx * (v + NU[l * nx + xw]);
+        const double kN = 0.5 * A.cy * (v + NU[(l + 1) * nx + xx]), kS = 0.5 * A.cy * (v + NU[(l - 1) * nx + xx]);
+        qv[k] = kE * (u - PS[l * nx + xe]) + kW * (u - PS[l * nx + xw]) + kN * (u - PS[(l + 1) * nx + xx]) +
+                kS * (u - PS[(l - 1) * nx + xx]);
+        acc = fma(u, qv[k], acc);
+      }
     }
     {
       const double s = pcgc_block_sum(acc, red);
@@ -463,38 +504,57 @@ __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
     }
     grid.sync();
     // ---- B
-    const double alpha = rz_old / pcgc_total(part_pq, G);
+    const double alpha = rz_old / pcgc_total(part_pq, G, red);
     acc = 0.0;
-    for (int i = tid; i < own; i += NT) {
-      const int l = i / nx, xx = i - l * nx;
-      const size_t g = (size_t)(r0 + l) * nx + xx;
-      A.x[g] = __dadd_rn(A.x[g], __dmul_rn(alpha, PS[nx + i]));
-      const double ri = __dsub_rn(A.r[g], __dmul_rn(alpha, QS[i]));
-      A.r[g] = ri;
-      acc = fma(ri, ri, acc);
-      zs[l * lsx + fpad(brev(xx, A.lx))] = make_double2(ri * ISN[i], 0.0);
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int i = tid + k * NT;
+      if (i < own) {
+        const int l = i / nx, xx = i - l * nx;
+        xr[k] = __dadd_rn(xr[k], __dmul_rn(alpha, PS[nx + i]));
+        rv[k] = __dsub_rn(rv[k], __dmul_rn(alpha, qv[k]));
+        acc = fma(rv[k], rv[k], acc);
+        zs[l * lsx + fpad(brev(xx, A.lx))] = make_double2(rv[k] * ISN[i], 0.0);
+      }
     }
     {
       const double s = pcgc_block_sum(acc, red);   // its barriers also publish zs
       if (tid == 0) part_rr[blockIdx.x] = s;
     }
     fft_lines_p(zs, nx, A.lx, Lr, lsx, SX, false);
-    for (int i = tid; i < own; i += NT) {
-      const int l = i / nx, xx = i - l * nx;
-      A.W[(size_t)(r0 + l) * nx + xx] = zs[l * lsx + fpad(xx)];
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int i = tid + k * NT;
+      if (i < own) {
+        const int l = i / nx, xx = i - l * nx;
+        A.W[(size_t)(r0 + l) * nx + xx] = zs[l * lsx + fpad(xx)];
+      }
     }
     grid.sync();
     // ---- C
-    rr_last = pcgc_total(part_rr, G);
+    rr_last = pcgc_total(part_rr, G, red);
     if (sqrt(rr_last) <= A.tol * sqrt(bb)) {
       done_it = it + 1;
       break;
     }
     {
       double2* Z2 = zs + Lc * lsy;
-      for (int i = tid; i < Lc * ny; i += NT) {
-        const int y = i / Lc, l = i - y * Lc;
-        zs[l * lsy + fpad(brev(y, A.ly))] = __ldcg(A.W + (size_t)y * nx + c0 + l);
+      double2 wv[KO];
+#pragma unroll
+      for (int k = 0; k < KO; ++k) {
+        const int i = tid + k * NT;
+        if (i < Lc * ny) {
+          const int y = i / Lc, l = i - y * Lc;
+          wv[k] = __ldcg(A.W + (size_t)y * nx + c0 + l);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KO; ++k) {
+        const int i = tid + k * NT;
+        if (i < Lc * ny) {
+          const int y = i / Lc, l = i - y * Lc;
+          zs[l * lsy + fpad(brev(y, A.ly))] = wv[k];
+        }
       }
       __syncthreads();
       fft_lines_p(zs, ny, A.ly, Lc, lsy, SY, false);
@@ -514,25 +574,48 @@ __global__ void __launch_bounds__(512) pcg_coop_kernel(const PcgCoop A) {
     }
     grid.sync();
     // ---- D
-    for (int i = tid; i < own; i += NT) {
-      const int l = i / nx, xx = i - l * nx;
-      zs[l * lsx + fpad(brev(xx, A.lx))] = __ldcg(A.W + (size_t)(r0 + l) * nx + xx);
+    {
+      double2 wv[KO];
+#pragma unroll
+      for (int k = 0; k < KO; ++k) {
+        const int i = tid + k * NT;
+        if (i < own) wv[k] = __ldcg(A.W + (size_t)r0 * nx + i);
+      }
+#pragma unroll
+      for (int k = 0; k < KO; ++k) {
+        const int i = tid + k * NT;
+        if (i < own) {
+          const int l = i / nx, xx = i - l * nx;
+          zs[l * lsx + fpad(brev(xx, A.lx))] = wv[k];
+        }
+      }
     }
     __syncthreads();
     fft_lines_p(zs, nx, A.lx, Lr, lsx, SX, true);
     acc = 0.0;
-    for (int i = tid; i < own; i += NT) {
-      const int l = i / nx, xx = i - l * nx;
-      const size_t g = (size_t)(r0 + l) * nx + xx;
-      const double zv = zs[l * lsx + fpad(xx)].x * sc * ISN[i];
-      A.z[g] = zv;
-      acc = fma(A.r[g], zv, acc);
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int i = tid + k * NT;
+      if (i < own) {
+        const int l = i / nx, xx = i - l * nx;
+        const double zv = zs[l * lsx + fpad(xx)].x * sc * ISN[i];
+        A.z[(size_t)r0 * nx + i] = zv;
+        acc = fma(rv[k], zv, acc);
+      }
     }
     {
       const double s = pcgc_block_sum(acc, red);
       if (tid == 0) part_rz[blockIdx.x] = s;
     }
     grid.sync();
+  }
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int i = tid + k * NT;
+    if (i < own) {
+      A.x[(size_t)r0 * nx + i] = xr[k];
+      A.r[(size_t)r0 * nx + i] = rv[k];
+    }
   }
   if (blockIdx.x == 0 && tid == 0) {
     A.S[6] = rr_last;
@@ -563,7 +646,7 @@ int pcg_coop(int nx, int ny, double dx, double dy, const double* tab, const doub
   const int lsx = nx + nx / 16, lsy = ny + ny / 16;
   const int nz = std::max(A.Lr * lsx, 2 * A.Lc * lsy);
   const size_t smem = sizeof(double2) * ((size_t)nz + nx + ny) +
-                      sizeof(double) * ((size_t)nx + ny + (size_t)(A.Lr + 2) * nx * 2 + (size_t)A.Lr * nx * 2 + 32);
+                      sizeof(double) * ((size_t)nx + ny + (size_t)(A.Lr + 2) * nx * 2 + (size_t)A.Lr * nx * 2 + 64);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(pcg_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
