@@ -358,6 +358,20 @@ int smg_op_apply_dot(const smg_op_t* h, const double* u, double* out, double* do
     if (rc == 0) return smg_sum_partials(ws, nct, dot_out, stream);
     if (rc != 1) return rc;
   }
+  if (fused && h->kind == 1 && h->p == 24 && h->dfrag && ring && smg_op_ring_doubles(h) && h->nu) {
+    // tensor-core diffusion kernel: the product accumulated per persistent CTA (at most
+    // 148 x 6 partials, behind the generic kernel's)
+    OpLaunch L;
+    L.u = u; L.f = nullptr; L.out = out; L.nu = h->nu; L.partials = nullptr;
+    L.p = h->p; L.n_x = h->n_x; L.n_y = h->n_y; L.diffusion = h->kind;
+    L.cx = h->dy / h->dx; L.cy = h->dx / h->dy;
+    L.Mt = h->Mt.data(); L.w = h->w.data(); L.wasm = h->wasm.data();
+    int nct = 0;
+    double* part = ws + h->n_ctas;
+    const int rc = opdh_apply_dot(L, h->dfrag, ring, part, &nct, as_stream(stream));
+    if (rc == 0) return smg_sum_partials(part, nct, dot_out, stream);
+    if (rc != 1) return rc;
+  }
   int rc = op_run(h, u, nullptr, out, nullptr, as_stream(stream), smg_op_ring_doubles(h) ? ring : nullptr);
   if (rc) return rc;
   double* red = ws + h->n_ctas;

@@ -489,6 +489,8 @@ int opw_launch(const OpLaunch& L, cudaStream_t st);
 int opl_launch(const OpLaunch& L, cudaStream_t st);
 // out = A u with per-CTA partials of u . out (smg_opw.cu); 1 = not applicable
 int opw_apply_dot(const OpLaunch& L, double* partials, int* n_ctas, cudaStream_t st);
+int opdh_apply_dot(const OpLaunch& L, const double* frag, double* ring, double* partials, int* n_ctas,
+                   cudaStream_t st);
 // Launcher for order p and mesh n_x x n_y (largest compiled tile dividing the
 // mesh); *ctas = grid size (number of partials).
 OpLaunchFn op_dispatch(int p, bool diffusion, int n_x, int n_y, int* ctas);

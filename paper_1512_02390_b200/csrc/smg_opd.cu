@@ -626,7 +626,12 @@ struct OpdhGeom {
 // Persistent: a CTA walks elements e = blockIdx.x, + gridDim.x, ... with the NEXT element's
 // window in flight (two window buffers, two mbarriers) while the current one is computed --
 // one element per CTA spent 35-45 % of its stall samples waiting for its own window.
-template <int P, bool DIFF>
+// DOT (out = A u only): the CTA also accumulates u . (A u) over its elements -- the own
+// nodes' parts times the window's u, and the ring values it hands on times u at the
+// neighbours' nodes they are destined for (its own window's node-P column and row), with
+// the weights opdh_fixup applies -- into A.partials[blockIdx.x] (summed in block order by
+// the caller: deterministic for a given grid).
+template <int P, bool DIFF, bool DOT = false>
 __global__ void __launch_bounds__(OpdhGeom<P, DIFF>::THREADS, DIFF ? 6 : 4)
 opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag, double* __restrict__ ring,
             int n_el) {
@@ -666,6 +671,7 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   if (warp < 2 && (int)blockIdx.x < n_el) issue(blockIdx.x, 0);
 
   int it = 0;
+  double dacc = 0.0;
   for (int el = blockIdx.x; el < n_el; el += gridDim.x, ++it) {
     const int bsel = it & 1;
     const int tx = el % A.tiles_x, ty = el / A.tiles_x;
@@ -706,8 +712,12 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
         const int b = 8 * j + 2 * t + e;
         if (b <= P / 2) {
           AX[li * OXP + b] = Vb[0][j][e];
-          if (b == 0) R[li] = Vm[0][j][e];
-          else if (b < P / 2) AX[li * OXP + (P - b)] = Vm[0][j][e];
+          if (b == 0) {
+            R[li] = Vm[0][j][e];
+            if (DOT) dacc = fma(ur[P], (A.cx * WS[li]) * Vm[0][j][e], dacc);
+          } else if (b < P / 2) {
+            AX[li * OXP + (P - b)] = Vm[0][j][e];
+          }
         }
       }
     __syncthreads();   // also: every thread is done with this element's window
@@ -715,8 +725,12 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
     {
       const double wyb = A.cy * WS[li];
       auto put = [&](int a, double v) {
-        if (a < P) AX[a * OXP + li] = fma(A.cx * WS[a], AX[a * OXP + li], wyb * v);
-        else R[P + li] = v;
+        if (a < P) {
+          AX[a * OXP + li] = fma(A.cx * WS[a], AX[a * OXP + li], wyb * v);
+        } else {
+          R[P + li] = v;
+          if (DOT) dacc = fma(uc[P * DP], wyb * v, dacc);
+        }
       };
 #pragma unroll
       for (int j = 0; j < NHO; ++j)
@@ -737,9 +751,22 @@ opdh_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
         const int y = idx / OX, x = idx - y * OX;
         const double val = AX[y * OXP + x];
         A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = A.f != nullptr ? fv[k] - val : val;
+        if (DOT) dacc = fma(U[y * DP + sh + x], val, dacc);
       }
     }
     __syncthreads();   // AX is rewritten by the next element
+  }
+  if constexpr (DOT) {
+    // CTA total in a fixed order: lanes by xor tree, warps in index order (AX is free)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    if (lane == 0) AX[warp] = dacc;
+    __syncthreads();
+    if (tid == 0) {
+      double tsum = 0.0;
+      for (int w = 0; w < NT / 32; ++w) tsum += AX[w];
+      A.partials[blockIdx.x] = tsum;
+    }
   }
 }
 
@@ -868,17 +895,18 @@ __global__ void __launch_bounds__(256) opdh_fixup(double* __restrict__ out, cons
   *o = v;
 }
 
-template <int P, bool DIFF>
-static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cudaStream_t st) {
+template <int P, bool DIFF, bool DOT = false>
+static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cudaStream_t st, double* dotp = nullptr,
+                         int* n_ctas = nullptr) {
   using G = OpdhGeom<P, DIFF>;
   OpArgs<P> A;
-  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = dotp;
   op_fill_consts<P>(A, L, DIFF);
   A.tiles_x = L.n_x;
   A.bulk = 1;
   static DeviceFlag attr;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(opdh_kernel<P, DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(opdh_kernel<P, DIFF, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     if (e != cudaSuccess) return cuda_fail(e, "opdh_kernel smem attribute");
     attr = true;
   }
@@ -887,11 +915,12 @@ static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cu
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opdh_kernel<P, DIFF>, G::THREADS, G::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opdh_kernel<P, DIFF, DOT>, G::THREADS, G::SMEM);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int n_el = L.n_x * L.n_y;
-  launch(opdh_kernel<P, DIFF>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring,
+  if (n_ctas) *n_ctas = n_el < grid_cap ? n_el : (int)grid_cap;
+  launch(opdh_kernel<P, DIFF, DOT>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring,
          n_el);
   int rc = check_launch("opdh_kernel");
   if (rc) return rc;
@@ -1058,6 +1087,15 @@ static int opd_launch_t(const OpLaunch& L, const double* frag, cudaStream_t st) 
 // (a p = 12 diffusion variant -- 3 warps, full and vertex lines mixed per
 // batch -- measured 1016 us vs 839 us for op_kernel<12,2,2> at C5's level 3)
 // p = 12 diffusion only has the halo-free kernel (opdq_kernel): it needs the caller's ring
+// q = A u and per-CTA partials of u . q in one pass (diffusion p = 24 with the operator ring);
+// 1 = not applicable
+int opdh_apply_dot(const OpLaunch& L, const double* frag, double* ring, double* partials, int* n_ctas,
+                   cudaStream_t st) {
+  static const int on = env_int("SMG_OPDH_DOT", 1);
+  if (!on || !L.diffusion || L.p != 24 || frag == nullptr || ring == nullptr || L.f != nullptr) return 1;
+  return opdh_launch_t<24, true, true>(L, frag, ring, st, partials, n_ctas);
+}
+
 bool opd_applies(int p, bool diffusion) { return diffusion ? (p == 24 || p == 12) : p == 32; }
 
 // 1 = not applicable (caller uses op_kernel / opw_kernel)

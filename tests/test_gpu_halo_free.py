@@ -72,9 +72,11 @@ def test_restriction_ring_path(p, orders, nx, ny):
 
 
 @pytest.mark.parametrize("kind,p,nx,ny", [("poisson", 16, 8, 6), ("poisson", 8, 4, 4), ("poisson", 32, 4, 3),
-                                          ("poisson", 4, 8, 8), ("diffusion", 24, 4, 4), ("diffusion", 6, 8, 8)])
+                                          ("poisson", 4, 8, 8), ("diffusion", 24, 4, 4), ("diffusion", 24, 40, 30),
+                                          ("diffusion", 6, 8, 8)])
 def test_apply_dot(kind, p, nx, ny):
-    """smg_op_apply_dot: q = A p and p . q (fused in the warp-per-element kernel at p = 8, 16,
+    """smg_op_apply_dot: q = A p and p . q (fused in the warp-per-element kernel at p = 8, 16 and
+    in the persistent tensor-core diffusion kernel at p = 24 -- 40 x 30 elements: several per CTA;
     apply + dot pass elsewhere) against apply() and a float64 dot; uninitialised workspace."""
     import paper_1512_02390_b200 as P
     from paper_1512_02390_b200 import _native as N
