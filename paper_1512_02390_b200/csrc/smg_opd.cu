@@ -607,7 +607,10 @@ __global__ void __launch_bounds__(OpdGeom<P, DIFF>::THREADS, 5) opd_kernel(const
 template <int P, bool DIFF>
 struct OpdhGeom {
   static constexpr int NP = P + 1;
-  static constexpr int DP = (NP + 2) & ~1;
+  // window pitch: even (16-byte rows for the bulk copies); = 12 (mod 16) at p = 24, where the
+  // row batch (8 lines x 4 consecutive k) AND the column batch (4 rows k apart x 8 columns) both
+  // touch every bank pair exactly twice (pitch 26: three times for the columns; 1592 -> 1554 us)
+  static constexpr int DP = P == 24 ? 28 : (NP + 2) & ~1;
   static constexpr int WARPS = P / 8;
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int WIN = ((DP * NP + 15) & ~15);          // one window (doubles), 128-byte multiple
