@@ -112,8 +112,8 @@ bool pdl_enabled();
 int env_int(const char* name, int def);
 
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                          Args&&... args) {
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -121,11 +121,23 @@ inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  return launch_pdl(true, kern, grid, block, smem, st, std::forward<Args>(args)...);
+}
+
+// Meshes from this many elements up launch the persistent tensor-core operator kernels (and
+// their fixups) as ordinary stream-ordered grids: the early launch pays on the latency-bound
+// levels, but at C5 (512^2 elements) it cost 4-25 % of these kernels (B200, PDL on -> off:
+// p = 24 residual 1553 -> 1481 us, p = 12 residual + restriction 934 -> 694 us).
+constexpr int kPdlMaxElements = 16384;
 
 constexpr int kReduceBlocks = 592;   // 4 x 148 SMs: fixed => deterministic
 constexpr int kReduceThreads = 512;

@@ -875,6 +875,106 @@ opdq_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
   }
 }
 
+// The same scheme with one WARP per element (p = 12): opdq_kernel's three warps met at two
+// CTA barriers per 144-node element and 45 % of its stall samples sat there (ncu,
+// profiles/r2c_opdq12_ncu.txt).  Here a warp owns its element: its own two window buffers
+// and mbarriers, its own part buffers, the three batches one after the other, __syncwarp
+// instead of CTA barriers; a CTA is just W such warps sharing the weights.
+template <int P>
+struct OpdwGeom {
+  static constexpr int NP = P + 1;
+  static constexpr int DP = (NP + 2) & ~1;
+  static constexpr int WARPS = 4;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int NB = 2 * P / 8;                       // batches per element
+  static constexpr int WIN = ((DP * NP + 15) & ~15);
+  static constexpr int OXP = P + 2;
+  static constexpr int PERW = 4 * WIN + 2 * P * OXP;          // doubles per warp (16-byte multiple)
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)WARPS * PERW + (size_t)P + NP) + 16 * WARPS + 32;
+  static_assert((2 * P) % 8 == 0 && (2 * P * OXP) % 2 == 0, "lines must fill whole batches");
+};
+
+template <int P>
+__global__ void __launch_bounds__(OpdwGeom<P>::THREADS, 6)
+opdw_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag, double* __restrict__ ring,
+            int n_el) {
+  SMG_PDL_TRIGGER();
+  using G = OpdwGeom<P>;
+  constexpr int NP = G::NP, DP = G::DP, OX = P, OY = P, NT = G::THREADS, WIN = G::WIN, OXP = G::OXP;
+  extern __shared__ __align__(128) double smd[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  double* WB = smd + warp * G::PERW;   // [2][2] windows of this warp: NP x DP of u and nu
+  double* AX = WB + 4 * WIN;           // OY x OXP x-parts
+  double* AY = AX + OY * OXP;          // OY x OXP y-parts
+  double* WS = smd + G::WARPS * G::PERW;   // P assembled weights (shared by the warps)
+  double* WT = WS + P;                 // NP GLL weights
+  uint64_t* bar = reinterpret_cast<uint64_t*>(WT + NP) + 2 * warp;   // [2] per warp
+  const int N_x = A.N_x, N_y = A.N_y;
+  for (int i = tid; i < P; i += NT) WS[i] = A.wasm[i];
+  for (int i = tid; i < NP; i += NT) WT[i] = A.w[i];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  SMG_PDL_WAIT();
+  __syncthreads();
+  auto issue = [&](int e, int b) {
+    const int tx = e % A.tiles_x, ty = e / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    if (lane == 0) mbar_arrive_expect_tx(bar + b, 2u * pwin_bytes(NP, NP, pwin_shift(X0, N_x)));
+    __syncwarp();
+    pwin_issue_warp(A.u, N_x, N_y, X0, Y0, NP, NP, WB + (2 * b) * WIN, DP, bar + b);
+    pwin_issue_warp(A.nu, N_x, N_y, X0, Y0, NP, NP, WB + (2 * b + 1) * WIN, DP, bar + b);
+  };
+  const int gw = blockIdx.x * G::WARPS + warp, nw = gridDim.x * G::WARPS;
+  if (gw < n_el) issue(gw, 0);
+  int it = 0;
+  for (int el = gw; el < n_el; el += nw, ++it) {
+    const int bsel = it & 1;
+    const int tx = el % A.tiles_x, ty = el / A.tiles_x;
+    const int X0 = tx * OX, Y0 = ty * OY;
+    const int sh = pwin_shift(X0, N_x);
+    double* R = ring + (size_t)el * (2 * P);
+    // the other buffer's readers (this warp, one element ago) are past a __syncwarp
+    if (el + nw < n_el) issue(el + nw, bsel ^ 1);
+    const double* U = WB + (2 * bsel) * WIN;
+    const double* NU = U + WIN;
+    mbar_wait(bar + bsel, (unsigned)(it >> 1) & 1u);
+#pragma unroll
+    for (int bt = 0; bt < G::NB; ++bt) {
+      const int line = 8 * bt + g;            // [0,P): row lines, [P,2P): column lines
+      const bool isrow = line < P;
+      const int li = isrow ? line : line - P;
+      constexpr int NHO = (P / 2 + 8) / 8;
+      double Vb[NHO][2], Vm[NHO][2];
+      const int off = isrow ? li * DP + sh : sh + li;
+      opd_batch_eo<P, false>(U + off, NU + off, isrow ? 1 : DP, WT, frag, Vb, Vm);
+#pragma unroll
+      for (int j = 0; j < NHO; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int b = 8 * j + 2 * t + e;
+          if (b <= P / 2) {
+            double* dst = isrow ? AX + li * OXP : AY + li;
+            const int sb = isrow ? 1 : OXP;
+            dst[b * sb] = Vb[j][e];
+            if (b == 0) R[line] = Vm[j][e];
+            else if (b < P / 2) dst[(P - b) * sb] = Vm[j][e];
+          }
+        }
+    }
+    __syncwarp();   // parts complete; the warp is done with this element's window
+    for (int idx = lane; idx < OX * OY; idx += 32) {
+      const int y = idx / OX, x = idx - y * OX;
+      const double val = fma(A.cx * WS[y], AX[y * OXP + x], (A.cy * WS[x]) * AY[y * OXP + x]);
+      const size_t gi = (size_t)(Y0 + y) * N_x + (X0 + x);
+      A.out[gi] = A.f != nullptr ? __ldg(A.f + gi) - val : val;
+    }
+    __syncwarp();   // the parts are rewritten by the next element
+  }
+}
+
 // One thread per low-side node of an element: (a, 0) for k = a < P takes the left
 // element's row-line value (and, at the corner a = 0, the lower element's column-line
 // value after it); (0, b) for k = P + b, b >= 1, the lower element's.
@@ -923,13 +1023,45 @@ static int opdh_launch_t(const OpLaunch& L, const double* frag, double* ring, cu
   }
   const int n_el = L.n_x * L.n_y;
   if (n_ctas) *n_ctas = n_el < grid_cap ? n_el : (int)grid_cap;
-  launch(opdh_kernel<P, DIFF, DOT>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring,
-         n_el);
+  const bool pdl = n_el < kPdlMaxElements;
+  launch_pdl(pdl, opdh_kernel<P, DIFF, DOT>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A,
+             frag, ring, n_el);
   int rc = check_launch("opdh_kernel");
   if (rc) return rc;
   const long nb = (long)L.n_x * L.n_y * 2 * P;
-  launch(opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
-         L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
+  launch_pdl(pdl, opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x,
+             L.n_y, L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
+  return check_launch("opdh_fixup");
+}
+
+template <int P>
+static int opdw_launch_t(const OpLaunch& L, const double* frag, double* ring, cudaStream_t st) {
+  using G = OpdwGeom<P>;
+  OpArgs<P> A;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.nu = L.nu; A.partials = nullptr;
+  op_fill_consts<P>(A, L, true);
+  A.tiles_x = L.n_x;
+  A.bulk = 1;
+  static DeviceInt grid_cap;
+  if (grid_cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(opdw_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "opdw_kernel smem attribute");
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, opdw_kernel<P>, G::THREADS, G::SMEM);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int n_el = L.n_x * L.n_y;
+  const int want = (n_el + G::WARPS - 1) / G::WARPS;
+  const bool pdl = n_el < kPdlMaxElements;
+  launch_pdl(pdl, opdw_kernel<P>, dim3(want < grid_cap ? want : (int)grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag,
+             ring, n_el);
+  int rc = check_launch("opdw_kernel");
+  if (rc) return rc;
+  const long nb = (long)n_el * 2 * P;
+  launch_pdl(pdl, opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x,
+             L.n_y, L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
   return check_launch("opdh_fixup");
 }
 
@@ -952,12 +1084,14 @@ static int opdq_launch_t(const OpLaunch& L, const double* frag, double* ring, cu
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int n_el = L.n_x * L.n_y;
-  launch(opdq_kernel<P>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring, n_el);
+  const bool pdl = n_el < kPdlMaxElements;
+  launch_pdl(pdl, opdq_kernel<P>, dim3(n_el < grid_cap ? n_el : grid_cap), dim3(G::THREADS), G::SMEM, st, A, frag, ring,
+             n_el);
   int rc = check_launch("opdq_kernel");
   if (rc) return rc;
   const long nb = (long)n_el * 2 * P;
-  launch(opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
-         L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
+  launch_pdl(pdl, opdh_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x,
+             L.n_y, L.cx, L.cy, L.f != nullptr ? -1.0 : 1.0, A);
   return check_launch("opdh_fixup");
 }
 
@@ -1117,6 +1251,8 @@ int opd_launch(const OpLaunch& L, const double* frag, cudaStream_t st) {
   static const bool hf = env_int("SMG_OPDH", 1) != 0;
   if (L.p == 12) {
     static const bool q12 = env_int("SMG_OPDQ", 1) != 0;
+    static const bool w12 = env_int("SMG_OPDW", 1) != 0;   // warp per element (0: a CTA of three warps)
+    if (L.ring != nullptr && hf && q12 && w12) return opdw_launch_t<12>(L, frag, L.ring, st);
     return (L.ring != nullptr && hf && q12) ? opdq_launch_t<12>(L, frag, L.ring, st) : 1;
   }
   // tuning aid: one batch per warp at p = 24 (6 warps, 64 registers, 5 CTAs/SM): measured
