@@ -454,12 +454,14 @@ int opl_launch_t(const OpLaunch& L, double* ring, cudaStream_t st) {
     attr = true;
   }
   const int n_el = L.n_x * L.n_y;
-  launch(opl_kernel<P>, dim3(n_el), dim3(64), G::SMEM, st, A, ring);
+  static const int pdl_big = env_int("SMG_OPL_PDL", 0);
+  const bool pdl = n_el < kPdlMaxElements || pdl_big;
+  launch_pdl(pdl, opl_kernel<P>, dim3(n_el), dim3(64), G::SMEM, st, A, ring);
   int rc = check_launch("opl_kernel");
   if (rc) return rc;
   const long nb = (long)n_el * 2 * P;
-  launch(opl_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x, L.n_y,
-         L.f != nullptr ? -1.0 : 1.0, A);
+  launch_pdl(pdl, opl_fixup<P>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, L.out, (const double*)ring, L.n_x,
+             L.n_y, L.f != nullptr ? -1.0 : 1.0, A);
   return check_launch("opl_fixup");
 }
 
