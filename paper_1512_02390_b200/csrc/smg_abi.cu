@@ -118,6 +118,7 @@ struct smg_transfer {
   std::vector<double> J;
   smg::TrFn fn;
   smg::RwFn rw;   // halo-free restriction (smg_rw.cu) or nullptr
+  bool rr_opw = false;   // (8, 16): residual + restriction in the warp-per-element operator kernel needs the ring too
   smg::PrwFn prw; // warp-per-fine-element prolongation (smg_rw.cu) or nullptr
 };
 
@@ -622,6 +623,12 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   // dependent chain than the kernel gains (C2 V-cycle 105.2 -> 107.8 us with it)
   const bool big = p_f >= 24 || (long)n_x * n_y >= 16384 || rw_mode == 2;
   t->rw = (rw_mode && big) ? rw_dispatch(p_c, p_f) : nullptr;
+  // (8, 16): residual + restriction inside the warp-per-element operator kernel (smg_opw.cu) where
+  // it pays -- C4 (256^2 elements) 159 -> 135 us per pair, V-cycle 772 -> 753 us; inside C2's
+  // graph-replayed chain it measured even (104.5 vs 103.7 us), so small meshes keep the two
+  // kernels; SMG_RR_OPW = 0 never, 2 on every mesh
+  const int rr_mode = env_int("SMG_RR_OPW", 1);
+  t->rr_opw = p_c == 8 && p_f == 16 && (rr_mode == 2 || (rr_mode == 1 && (long)n_x * n_y >= 16384));
   // SMG_PRW: 0 never, 1 where measured faster, 2 wherever compiled (B200, tools/time_prolong.py,
   // us tiled -> warp per fine element: C3 p_f = 32 95.3 -> 79.9; 256^2 p_f = 24 156.7 -> 162.9,
   // p_f = 16 76.9 -> 80.0; bitwise-equal results)
@@ -674,7 +681,7 @@ int smg_restrict(const smg_transfer_t* h, const double* ff, double* fc, void* st
 }
 
 size_t smg_transfer_ws_doubles(const smg_transfer_t* h) {
-  return (h && h->rw) ? (size_t)h->n_x * h->n_y * (2 * h->pc + 1) : 0;
+  return (h && (h->rw || h->rr_opw)) ? (size_t)h->n_x * h->n_y * (2 * h->pc + 1) : 0;
 }
 
 int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, double* ws, void* stream) {
@@ -690,6 +697,19 @@ int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, doubl
 int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const double* u, const double* f,
                              double* fc, double* work, double* ws, double* op_ring, void* stream) {
   const bool ring = op && op_ring && smg_op_ring_doubles(op) > 0;
+  // Poisson p_f = 16: the warp-per-element residual kernel restricts its element in place
+  // (r is neither written nor re-read) and hands the high-side coarse nodes to the ring
+  if (h && h->rr_opw && ws && op && u && f && fc && op->kind == 0 && op->p == 16 && h->pf == 16 && h->pc == 8 &&
+      op->n_x == h->n_x && op->n_y == h->n_y && h->n_x % 2 == 0 && h->n_y % 2 == 0) {
+    OpLaunch L;
+    L.u = u; L.f = f; L.out = work; L.nu = op->nu; L.partials = nullptr;
+    L.p = op->p; L.n_x = op->n_x; L.n_y = op->n_y; L.diffusion = op->kind;
+    L.cx = op->dy / op->dx; L.cy = op->dx / op->dy;
+    L.Mt = op->Mt.data(); L.w = op->w.data(); L.wasm = op->wasm.data();
+    const int rc = opw_residual_restrict(L, h->J.data(), fc, ws, as_stream(stream));
+    if (rc == 0) return rw_fixup(h->pc, fc, ws, h->n_x, h->n_y, as_stream(stream));
+    if (rc != 1) return rc;
+  }
   if (!h || ((!h->rw || !ws) && !ring)) return smg_residual_restrict(h, op, u, f, fc, work, stream);
   if (!op || !u || !f || !fc || !work) { set_error("smg_residual_restrict_ws: bad argument"); return SMG_EINVAL; }
   int rc = smg_op_residual_ws(op, u, f, work, op_ring, stream);

@@ -489,6 +489,7 @@ int opw_launch(const OpLaunch& L, cudaStream_t st);
 int opl_launch(const OpLaunch& L, cudaStream_t st);
 // out = A u with per-CTA partials of u . out (smg_opw.cu); 1 = not applicable
 int opw_apply_dot(const OpLaunch& L, double* partials, int* n_ctas, cudaStream_t st);
+int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double* rring, cudaStream_t st);
 int opdh_apply_dot(const OpLaunch& L, const double* frag, double* ring, double* partials, int* n_ctas,
                    cudaStream_t st);
 // Launcher for order p and mesh n_x x n_y (largest compiled tile dividing the

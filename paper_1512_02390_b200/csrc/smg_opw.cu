@@ -27,6 +27,8 @@ struct OpwArgs {
   const double* __restrict__ f;
   double* __restrict__ out;
   double* __restrict__ dotp;   // DOT kernels: per-CTA partials of sum(u * out)
+  double* __restrict__ fc;     // RESTR kernels: the coarse field and the restriction ring (smg_rw.cu layout)
+  double* __restrict__ rring;
   int N_x, N_y, tiles_x;
   double cx, cy;
   double Le[((P + 1) / 2 + 1) * ((P + 1) / 2 + 1)];
@@ -37,6 +39,7 @@ struct OpwArgs {
   static constexpr int kH = (P + 1) / 2, kHC = kH + ((P + 1) & 1), kHCP = (kHC + 1) & ~1, kHP = (kH + 1) & ~1;
   alignas(16) double LeT[(kH + 1) * kHCP];
   alignas(16) double LoT[(kH > 0 ? kH : 1) * kHP];
+  double J[P * (P / 2 + 1)];   // RESTR: interpolation rows a < P (p_c = P/2), J[a * (p_c + 1) + ac]
 };
 
 // Even/odd 1D line: v[b] = sum_k L[k][b] x[k st] (L centro-symmetric); with
@@ -96,8 +99,14 @@ struct OpwGeom {
 
 // DOT: also the per-CTA partial of sum(u * out) over the CTA's nodes (MGCG's p . A p without
 // re-reading p and q: the node's u is in the staged window); fixed shuffle / warp order.
-template <int P, int TX, int TY, bool DOT = false>
-__global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel(const __grid_constant__ OpwArgs<P> A) {
+// RESTR (with f: r = f - A u): r is not written; the column lanes restrict their column of the
+// element's own nodes in registers (y pass), the row lanes finish the x pass from the warp's
+// buffer, own coarse nodes are written and the high-side coarse row / column go to the
+// restriction ring -- restrict_warp_kernel's passes and summation order (smg_rw.cu), fed from
+// registers instead of from a stored residual; restrict_fixup follows.
+template <int P, int TX, int TY, bool DOT = false, bool RESTR = false>
+__global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? (RESTR ? 6 : 7) : 1)
+opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   SMG_PDL_TRIGGER();
   using G = OpwGeom<P, TX, TY>;
   constexpr int NW = G::NW, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, DP = G::DP, LDA = G::LDA;
@@ -154,6 +163,12 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
     const double wyb = A.cy * A.wasm[b];
     const size_t g0 = (size_t)(Y0 + eyl * P) * N_x + (X0 + exl * P + b);
     constexpr int CH = P / 2;          // f loads in flight per chunk
+    constexpr int PCr = P / 2, NCr = PCr + 1;
+    [[maybe_unused]] double tr[NCr];
+    if constexpr (RESTR) {
+#pragma unroll
+      for (int ay = 0; ay < NCr; ++ay) tr[ay] = 0.0;
+    }
 #pragma unroll
     for (int a0 = 0; a0 < P; a0 += CH) {
       double fv[CH];
@@ -165,8 +180,45 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
         double val = fma(A.cx * A.wasm[a], AX[a * LDA + b], wyb * v[a]);
         if (a == 0) val = fma(wyb, vv[P], val);
         const double o = A.f != nullptr ? fv[i] - val : val;
-        A.out[g0 + (size_t)a * N_x] = o;
+        if constexpr (RESTR) {
+#pragma unroll
+          for (int ay = 0; ay < NCr; ++ay) tr[ay] = fma(A.J[a * NCr + ay], o, tr[ay]);
+        } else {
+          A.out[g0 + (size_t)a * N_x] = o;
+        }
         if constexpr (DOT) dacc = fma(U[(ur0 + a) * DP + uc0 + b], o, dacc);
+      }
+    }
+    if constexpr (RESTR) {
+      // T[ay][b] over the x-parts of this column (no other lane reads column b)
+#pragma unroll
+      for (int ay = 0; ay < NCr; ++ay) AX[ay * LDA + b] = tr[ay];
+    }
+  }
+  if constexpr (RESTR) {
+    constexpr int PCr = P / 2, NCr = PCr + 1;
+    __syncwarp();
+    if (lane < NCr) {
+      const double* trow = AX + lane * LDA;
+      double c[NCr];
+#pragma unroll
+      for (int ax = 0; ax < NCr; ++ax) c[ax] = 0.0;
+#pragma unroll
+      for (int b = 0; b < P; ++b) {
+        const double tb = trow[b];
+#pragma unroll
+        for (int ax = 0; ax < NCr; ++ax) c[ax] = fma(A.J[b * NCr + ax], tb, c[ax]);
+      }
+      const int ex = tx * TX + exl, ey = ty * TY + eyl, n_x = A.tiles_x * TX;
+      double* R = A.rring + (size_t)(ey * n_x + ex) * (2 * PCr + 1);
+      if (lane < PCr) {
+        double* d = A.fc + (size_t)(ey * PCr + lane) * ((size_t)n_x * PCr) + ex * PCr;
+#pragma unroll
+        for (int ax = 0; ax < PCr; ++ax) d[ax] = c[ax];
+        R[PCr + 1 + lane] = c[PCr];          // right column
+      } else {
+#pragma unroll
+        for (int ax = 0; ax < NCr; ++ax) R[ax] = c[ax];   // top row, corner last
       }
     }
   }
@@ -190,14 +242,16 @@ __global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? 7 : 1) opw_kernel
 
 // Host: 1 = not applicable (caller uses op_kernel).
 template <int P, int TX, int TY>
-int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr) {
+int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr, const double* J = nullptr,
+                 double* fc = nullptr, double* rring = nullptr) {
   using G = OpwGeom<P, TX, TY>;
   if (L.diffusion || L.partials != nullptr || L.n_x % TX || L.n_y % TY) return 1;
   const int N_x = L.n_x * P;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (N_x % 2 || !al16(L.u)) return 1;
   OpwArgs<P> A;
-  A.u = L.u; A.f = L.f; A.out = L.out; A.dotp = dotp;
+  A.u = L.u; A.f = L.f; A.out = L.out; A.dotp = dotp; A.fc = fc; A.rring = rring;
+  if (J != nullptr) std::memcpy(A.J, J, sizeof(A.J));
   A.N_x = N_x; A.N_y = L.n_y * P; A.tiles_x = L.n_x / TX;
   A.cx = L.cx; A.cy = L.cy;
   {
@@ -238,8 +292,27 @@ int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr) {
     launch(opw_kernel<P, TX, TY, true>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(32 * G::NW), G::SMEM, st, A);
     return check_launch("opw_kernel");
   }
+  if (J != nullptr) {
+    static DeviceFlag attr3;
+    if (!attr3) {
+      cudaError_t e = cudaFuncSetAttribute(opw_kernel<P, TX, TY, false, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "opw_kernel smem attribute");
+      attr3 = true;
+    }
+    launch(opw_kernel<P, TX, TY, false, true>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(32 * G::NW), G::SMEM, st, A);
+    return check_launch("opw_kernel");
+  }
   launch(opw_kernel<P, TX, TY>, dim3((L.n_x / TX) * (L.n_y / TY)), dim3(32 * G::NW), G::SMEM, st, A);
   return check_launch("opw_kernel");
+}
+
+// fc (+ ring) = restriction of r = f - A u to p_c = p / 2 without storing r (p = 16; J: rows a < p of
+// the (p+1) x (p_c+1) interpolation matrix); the caller runs restrict_fixup next.  1 = not applicable.
+int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double* rring, cudaStream_t st) {
+  static const int on = env_int("SMG_RR_OPW", 1);
+  if (!on || L.f == nullptr || J == nullptr || fc == nullptr || rring == nullptr || L.p != 16) return 1;
+  return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
 }
 
 // out = A u and per-CTA partials of u . out (n_ctas of them); 1 = not applicable.

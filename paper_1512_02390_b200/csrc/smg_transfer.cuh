@@ -21,6 +21,7 @@ TrFn transfer_dispatch(int pc, int pf);
 // n_x n_y (2 p_c + 1) doubles + fixup launch; nullptr where it is not compiled.
 using RwFn = int (*)(const TrArgs&, double* ring, cudaStream_t);
 RwFn rw_dispatch(int pc, int pf);
+int rw_fixup(int pc, double* dst, const double* ring, int n_x, int n_y, cudaStream_t st);
 // Warp-per-fine-element prolongation (smg_rw.cu); nullptr where it is not compiled.
 using PrwFn = int (*)(const TrArgs&, cudaStream_t);
 PrwFn prw_dispatch(int pc, int pf);

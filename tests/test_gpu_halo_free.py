@@ -96,3 +96,34 @@ def test_apply_dot(kind, p, nx, ny):
                                          op.ring_ptr(), N.stream()), "apply_dot")
         assert torch.equal(q, want_q)
         assert abs(d.item() - want) <= 1e-12 * float((u.abs() * want_q.abs()).sum().item())
+
+
+@pytest.mark.parametrize("nx,ny,lx,ly", [(6, 4, 1.0, 1.0), (64, 64, 1.0, 1.0), (8, 10, 2.0, 1.0), (128, 128, 1.0, 1.0)])
+def test_fused_residual_restriction_p16(nx, ny, lx, ly, monkeypatch):
+    """smg_residual_restrict_ws at p_f = 16 (Poisson): the warp-per-element residual kernel restricts
+    its element in place (r is never stored) + restrict_fixup, against residual then restriction
+    (multigrid.py:247-248), twice into a dirty workspace; bitwise reproducible."""
+    import paper_1512_02390_b200 as P
+    from paper_1512_02390_b200 import _native as N
+    if nx * ny < 16384:
+        monkeypatch.setenv("SMG_RR_OPW", "2")   # default only from 16384 elements up; read at create time
+    mesh = P.MeshConfig(nx, ny, lx, ly)
+    h = P.build_hierarchy(mesh, 16, P.OverlapRule("fixed", 1))
+    lv = h.top
+    tr = lv.transfer
+    assert tr.ws is not None and tr.ws.numel() == nx * ny * 17, "no ring: the fused path is not engaged"
+    torch.manual_seed(11)
+    u = torch.randn(lv.op.layout.shape, dtype=torch.float64, device="cuda")
+    f = torch.randn(lv.op.layout.shape, dtype=torch.float64, device="cuda")
+    r = torch.empty_like(u)
+    N.check(N.lib().smg_op_residual(lv.op._handle.raw, N.ptr(u), N.ptr(f), N.ptr(r), N.stream()), "residual")
+    want = torch.empty(h.levels[-2].op.layout.shape, dtype=torch.float64, device="cuda")
+    N.check(N.lib().smg_restrict(tr.handle.raw, N.ptr(r), N.ptr(want), N.stream()), "restrict")
+    tr.ws.fill_(float("nan"))
+    work = torch.full_like(u, float("nan"))
+    got = [torch.full_like(want, float("nan")) for _ in range(2)]
+    for g in got:
+        N.check(N.lib().smg_residual_restrict_ws(tr.handle.raw, lv.op._handle.raw, N.ptr(u), N.ptr(f), N.ptr(g),
+                                                 N.ptr(work), tr.ws_ptr(), lv.op.ring_ptr(), N.stream()), "rr")
+    assert torch.equal(got[0], got[1])
+    assert (got[0] - want).abs().max().item() <= 1e-13 * want.abs().max().item()
