@@ -628,7 +628,8 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   // graph-replayed chain it measured even (104.5 vs 103.7 us), so small meshes keep the two
   // kernels; SMG_RR_OPW = 0 never, 2 on every mesh
   const int rr_mode = env_int("SMG_RR_OPW", 1);
-  t->rr_opw = p_c == 8 && p_f == 16 && (rr_mode == 2 || (rr_mode == 1 && (long)n_x * n_y >= 16384));
+  t->rr_opw = ((p_c == 8 && p_f == 16) || (p_c == 4 && p_f == 8)) &&
+              (rr_mode == 2 || (rr_mode == 1 && (long)n_x * n_y >= 16384));
   // SMG_PRW: 0 never, 1 where measured faster, 2 wherever compiled (B200, tools/time_prolong.py,
   // us tiled -> warp per fine element: C3 p_f = 32 95.3 -> 79.9; 256^2 p_f = 24 156.7 -> 162.9,
   // p_f = 16 76.9 -> 80.0; bitwise-equal results)
@@ -699,7 +700,7 @@ int smg_residual_restrict_ws(const smg_transfer_t* h, const smg_op_t* op, const 
   const bool ring = op && op_ring && smg_op_ring_doubles(op) > 0;
   // Poisson p_f = 16: the warp-per-element residual kernel restricts its element in place
   // (r is neither written nor re-read) and hands the high-side coarse nodes to the ring
-  if (h && h->rr_opw && ws && op && u && f && fc && op->kind == 0 && op->p == 16 && h->pf == 16 && h->pc == 8 &&
+  if (h && h->rr_opw && ws && op && u && f && fc && op->kind == 0 && op->p == h->pf && 2 * h->pc == h->pf &&
       op->n_x == h->n_x && op->n_y == h->n_y && h->n_x % 2 == 0 && h->n_y % 2 == 0) {
     OpLaunch L;
     L.u = u; L.f = f; L.out = work; L.nu = op->nu; L.partials = nullptr;

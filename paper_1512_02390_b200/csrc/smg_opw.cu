@@ -307,12 +307,14 @@ int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr, con
   return check_launch("opw_kernel");
 }
 
-// fc (+ ring) = restriction of r = f - A u to p_c = p / 2 without storing r (p = 16; J: rows a < p of
+// fc (+ ring) = restriction of r = f - A u to p_c = p / 2 without storing r (p = 8, 16; J: rows a < p of
 // the (p+1) x (p_c+1) interpolation matrix); the caller runs restrict_fixup next.  1 = not applicable.
 int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double* rring, cudaStream_t st) {
   static const int on = env_int("SMG_RR_OPW", 1);
-  if (!on || L.f == nullptr || J == nullptr || fc == nullptr || rring == nullptr || L.p != 16) return 1;
-  return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
+  if (!on || L.f == nullptr || J == nullptr || fc == nullptr || rring == nullptr) return 1;
+  if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
+  if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, nullptr, J, fc, rring);
+  return 1;
 }
 
 // out = A u and per-CTA partials of u . out (n_ctas of them); 1 = not applicable.

@@ -98,9 +98,10 @@ def test_apply_dot(kind, p, nx, ny):
         assert abs(d.item() - want) <= 1e-12 * float((u.abs() * want_q.abs()).sum().item())
 
 
+@pytest.mark.parametrize("p", [16, 8])
 @pytest.mark.parametrize("nx,ny,lx,ly", [(6, 4, 1.0, 1.0), (64, 64, 1.0, 1.0), (8, 10, 2.0, 1.0), (128, 128, 1.0, 1.0)])
-def test_fused_residual_restriction_p16(nx, ny, lx, ly, monkeypatch):
-    """smg_residual_restrict_ws at p_f = 16 (Poisson): the warp-per-element residual kernel restricts
+def test_fused_residual_restriction_p16(nx, ny, lx, ly, p, monkeypatch):
+    """smg_residual_restrict_ws at p_f = 16, 8 (Poisson): the warp-per-element residual kernel restricts
     its element in place (r is never stored) + restrict_fixup, against residual then restriction
     (multigrid.py:247-248), twice into a dirty workspace; bitwise reproducible."""
     import paper_1512_02390_b200 as P
@@ -108,10 +109,10 @@ def test_fused_residual_restriction_p16(nx, ny, lx, ly, monkeypatch):
     if nx * ny < 16384:
         monkeypatch.setenv("SMG_RR_OPW", "2")   # default only from 16384 elements up; read at create time
     mesh = P.MeshConfig(nx, ny, lx, ly)
-    h = P.build_hierarchy(mesh, 16, P.OverlapRule("fixed", 1))
+    h = P.build_hierarchy(mesh, p, P.OverlapRule("fixed", 1))
     lv = h.top
     tr = lv.transfer
-    assert tr.ws is not None and tr.ws.numel() == nx * ny * 17, "no ring: the fused path is not engaged"
+    assert tr.ws is not None and tr.ws.numel() == nx * ny * (p + 1), "no ring: the fused path is not engaged"
     torch.manual_seed(11)
     u = torch.randn(lv.op.layout.shape, dtype=torch.float64, device="cuda")
     f = torch.randn(lv.op.layout.shape, dtype=torch.float64, device="cuda")
