@@ -89,12 +89,17 @@ __device__ __forceinline__ void opw_line(const OpwArgs<P>& A, const double* x, i
 
 template <int P, int TX, int TY>
 struct OpwGeom {
-  static constexpr int NW = TX * TY;
+  // elements per warp: the row lines of an element take P of a half-warp's 16 lanes, so at
+  // p = 8 a warp carries two elements (one per 8-lane group of each half) -- 8 idle lanes of
+  // 16 made the p = 8 residual latency-bound at twice the warps (C4 level 8: 51 us for 4.2 M DOF)
+  static constexpr int EW = P <= 8 ? 16 / P : 1;
+  static_assert((TX * TY) % EW == 0, "whole warps");
+  static constexpr int NW = TX * TY / EW;
   static constexpr int OX = TX * P, OY = TY * P;
   static constexpr int HX = OX + P + 1, HY = OY + P + 1;
   static constexpr int DP = (HX + 2) & ~1;
   static constexpr int LDA = P + 1;   // per-warp AX row stride
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY + (size_t)NW * P * LDA) + 16;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)DP * HY + (size_t)TX * TY * P * LDA) + 16;
 };
 
 // DOT: also the per-CTA partial of sum(u * out) over the CTA's nodes (MGCG's p . A p without
@@ -105,16 +110,17 @@ struct OpwGeom {
 // restriction ring -- restrict_warp_kernel's passes and summation order (smg_rw.cu), fed from
 // registers instead of from a stored residual; restrict_fixup follows.
 template <int P, int TX, int TY, bool DOT = false, bool RESTR = false>
-__global__ void __launch_bounds__(32 * TX * TY, TX * TY == 4 ? (RESTR ? 6 : 7) : 1)
+__global__ void __launch_bounds__(32 * OpwGeom<P, TX, TY>::NW,
+                                  OpwGeom<P, TX, TY>::NW == 4 ? (RESTR ? 6 : 7) : (OpwGeom<P, TX, TY>::NW == 2 ? 12 : 1))
 opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   SMG_PDL_TRIGGER();
   using G = OpwGeom<P, TX, TY>;
-  constexpr int NW = G::NW, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, DP = G::DP, LDA = G::LDA;
+  constexpr int NW = G::NW, EW = G::EW, OX = G::OX, OY = G::OY, HX = G::HX, HY = G::HY, DP = G::DP, LDA = G::LDA;
   static_assert(2 * P <= 32, "row and column lines share one warp");
   extern __shared__ __align__(16) double smw[];
   double* U = smw;                          // HY x DP, origin (Y0-P, X0-P) at column sh
-  double* AXb = U + DP * HY;                // NW x P x LDA: x-part [a][b]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(AXb + NW * P * LDA);
+  double* AXb = U + DP * HY;                // (TX TY) x P x LDA: x-part [a][b] per element
+  uint64_t* bar = reinterpret_cast<uint64_t*>(AXb + TX * TY * P * LDA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tx = blockIdx.x % A.tiles_x, ty = blockIdx.x / A.tiles_x;
   const int X0 = tx * OX, Y0 = ty * OY;
@@ -128,15 +134,17 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   SMG_PDL_WAIT();   // barrier set up while the preceding grid drains; u after it
   __syncthreads();
   if (warp == 0) pwin_issue_warp(A.u, N_x, N_y, X0 - P, Y0 - P, HX, HY, U, DP, bar);
-  // this warp's element
-  const int exl = warp % TX, eyl = warp / TX;
+  // this lane's element: lane group (lane & 15) / P of the warp's EW elements
+  const int sub = (lane & 15) / P;
+  const bool lact = sub < EW;
+  const int eidx = warp * EW + (lact ? sub : 0);
+  const int exl = eidx % TX, eyl = eidx / TX;
   mbar_wait(bar, 0);
   // element origin in U
   const int ur0 = P + eyl * P, uc0 = sh + P + exl * P;
-  double* AX = AXb + warp * P * LDA;
-  // lanes 0..P-1: row a = lane (stride 1); lanes 16..16+P-1: column b (stride DP)
-  const int li = lane & 15;
-  const bool lact = li < P;
+  double* AX = AXb + eidx * P * LDA;
+  // lanes [0,16): row a = li (stride 1); lanes [16,32): column b = li (stride DP)
+  const int li = (lane & 15) % P;
   const bool col = lane >= 16;
   const int st = col ? DP : 1;
   const double* xl = col ? U + ur0 * DP + uc0 + li : U + (ur0 + li) * DP + uc0;
@@ -198,8 +206,8 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   if constexpr (RESTR) {
     constexpr int PCr = P / 2, NCr = PCr + 1;
     __syncwarp();
-    if (lane < NCr) {
-      const double* trow = AX + lane * LDA;
+    if (!col && lact && li < NCr) {
+      const double* trow = AX + li * LDA;
       double c[NCr];
 #pragma unroll
       for (int ax = 0; ax < NCr; ++ax) c[ax] = 0.0;
@@ -211,11 +219,11 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
       }
       const int ex = tx * TX + exl, ey = ty * TY + eyl, n_x = A.tiles_x * TX;
       double* R = A.rring + (size_t)(ey * n_x + ex) * (2 * PCr + 1);
-      if (lane < PCr) {
-        double* d = A.fc + (size_t)(ey * PCr + lane) * ((size_t)n_x * PCr) + ex * PCr;
+      if (li < PCr) {
+        double* d = A.fc + (size_t)(ey * PCr + li) * ((size_t)n_x * PCr) + ex * PCr;
 #pragma unroll
         for (int ax = 0; ax < PCr; ++ax) d[ax] = c[ax];
-        R[PCr + 1 + lane] = c[PCr];          // right column
+        R[PCr + 1 + li] = c[PCr];            // right column
       } else {
 #pragma unroll
         for (int ax = 0; ax < NCr; ++ax) R[ax] = c[ax];   // top row, corner last
@@ -227,14 +235,14 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
     // xor tree over the whole warp (outside the divergent branches), then the warps in order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
-    if (lane == 0) AX[0] = dacc;   // the warp's x-part buffer is consumed
+    if (lane == 0) AX[0] = dacc;   // the x-part buffer of the warp's first element is consumed
   }
   if constexpr (DOT) {
     __syncthreads();
     if (tid == 0) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += AXb[w * P * LDA];
+      for (int w = 0; w < NW; ++w) s += AXb[w * EW * P * LDA];
       A.dotp[blockIdx.x] = s;
     }
   }
