@@ -623,13 +623,11 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   // dependent chain than the kernel gains (C2 V-cycle 105.2 -> 107.8 us with it)
   const bool big = p_f >= 24 || (long)n_x * n_y >= 16384 || rw_mode == 2;
   t->rw = (rw_mode && big) ? rw_dispatch(p_c, p_f) : nullptr;
-  // (8, 16): residual + restriction inside the warp-per-element operator kernel (smg_opw.cu) where
-  // it pays -- C4 (256^2 elements) 159 -> 135 us per pair, V-cycle 772 -> 753 us; inside C2's
-  // graph-replayed chain it measured even (104.5 vs 103.7 us), so small meshes keep the two
-  // kernels; SMG_RR_OPW = 0 never, 2 on every mesh
-  const int rr_mode = env_int("SMG_RR_OPW", 1);
-  t->rr_opw = ((p_c == 8 && p_f == 16) || (p_c == 4 && p_f == 8)) &&
-              (rr_mode == 2 || (rr_mode == 1 && (long)n_x * n_y >= 16384));
+  // (8, 16) and (4, 8): residual + restriction inside the warp-per-element operator kernel
+  // (smg_opw.cu; the ring below is its workspace) -- C4 (256^2 elements) pair 159 -> 135 us at
+  // p_f = 16, 74 -> 36 us at p_f = 8; C2 (64^2) V-cycle in the replayed graph 103.6 -> 100.3 us
+  // with both.  SMG_RR_OPW = 0: residual kernel + restriction kernel (or rr_kernel at p_f <= 8)
+  t->rr_opw = ((p_c == 8 && p_f == 16) || (p_c == 4 && p_f == 8)) && env_int("SMG_RR_OPW", 1) != 0;
   // SMG_PRW: 0 never, 1 where measured faster, 2 wherever compiled (B200, tools/time_prolong.py,
   // us tiled -> warp per fine element: C3 p_f = 32 95.3 -> 79.9; 256^2 p_f = 24 156.7 -> 162.9,
   // p_f = 16 76.9 -> 80.0; bitwise-equal results)
