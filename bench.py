@@ -593,13 +593,21 @@ def main():
         return torch.randn(sh, dtype=torch.float64, device=dev)
     sets = [dict(r=rnd(shape), u=rnd(shape), o=rnd(shape), fc=torch.empty(fshape, dtype=torch.float64, device=dev),
                  uc=rnd(fshape)) for _ in range(nset)]
+    # per V-cycle (1 pre-smoothing sweep, u != 0): r = f - A u, the Schwarz correction, the
+    # residual restricted in place (r = f - A u is not stored: smg_residual_restrict_ws), the
+    # prolongation; the stand-alone restriction is listed for reference (0 calls per cycle when
+    # the fused residual + restriction is engaged)
+    fused_rr = top.transfer.ws is not None
     calls = {
         "residual": (lambda S: NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(S["u"]), NV.ptr(S["r"]),
-                                                            NV.ptr(S["o"]), st)), 2),
+                                                            NV.ptr(S["o"]), st)), 1 if fused_rr else 2),
         "schwarz": (lambda S: NV.check(lib.smg_schwarz_correct(top.smoother._h.raw, NV.ptr(S["r"]), NV.ptr(S["o"]),
                                                               NV.ptr(top.smoother.ring), st)), 1),
+        "residual_restrict": (lambda S: NV.check(lib.smg_residual_restrict_ws(
+            top.transfer.handle.raw, top.op._handle.raw, NV.ptr(S["u"]), NV.ptr(S["r"]), NV.ptr(S["fc"]),
+            NV.ptr(S["o"]), top.transfer.ws_ptr(), top.op.ring_ptr(), st)), 1 if fused_rr else 0),
         "restrict": (lambda S: NV.check(lib.smg_restrict(top.transfer.handle.raw, NV.ptr(S["r"]), NV.ptr(S["fc"]),
-                                                         st)), 1),
+                                                         st)), 0 if fused_rr else 1),
         "prolong": (lambda S: NV.check(lib.smg_prolongate(top.transfer.handle.raw, NV.ptr(S["uc"]), NV.ptr(S["o"]), 1,
                                                           st)), 1),
     }
@@ -652,8 +660,13 @@ def main():
                                   tb(schwarz_kernel, "fdt_fixup"),
                                   note="even/odd flop count (SURVEY 8(d)); dense-FD equivalent "
                                        f"{n_el * fd_flops_per_element(m) / t_call['schwarz'] / 1e12:.2f} TF"),
-        "restrict": roofline_entry("restrict_blk_kernel<8,16>", t_call["restrict"], f_tr, 8.0 * ndof + 8.0 * ndof_c,
-                                   p64, bw * 1e9, tb("restrict_blk_kernel")),
+        "residual_restrict": roofline_entry(
+            "opw_kernel<16,2,2,RESTR> + restrict_fixup<8> (f_c = R (f - A u), r not stored)"
+            if fused_rr else "opw_kernel<16,2,2> + restrict_blk_kernel<8,16>", t_call["residual_restrict"],
+            n_el * (4 * npp ** 3 + 3 * npp ** 2) + ndof + f_tr, 16.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9,
+            tb("opw_kernel_restr", "restrict_fixup")),
+        "restrict": roofline_entry("restrict_blk_kernel<8,16> (stand-alone restriction)", t_call["restrict"], f_tr,
+                                   8.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9, tb("restrict_blk_kernel")),
         "prolong": roofline_entry("prolong_warp_kernel<8,16> (u_f += P u_c)", t_call["prolong"], f_tr,
                                   16.0 * ndof + 8.0 * ndof_c, p64, bw * 1e9, tb("prolong_warp_kernel")),
     }

@@ -27,6 +27,8 @@ res = {}
 for row in rows[2:]:
     name = row[h.index("Kernel Name")]
     key = name.split("<")[0].split("(")[0].replace("void ", "").replace("smg::", "").strip()
+    if key == "opw_kernel" and name.split("(")[0].rstrip(">").rstrip().endswith("1"):
+        key = "opw_kernel_restr"   # opw_kernel<P, TX, TY, DOT, RESTR = 1>: residual restricted in place
     tr = val(row, "dram__bytes_read.sum") + val(row, "dram__bytes_write.sum")
     res.setdefault(key, {"bytes_per_launch": tr, "kernel": name[:90], "report": rep.split("/")[-1]})
 json.dump(res, open(out, "w"), indent=1)

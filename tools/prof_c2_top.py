@@ -1,5 +1,5 @@
-"""Run each C2 top-level kernel call once (residual, Schwarz correction,
-restriction, prolongation) -- the launches bench.py times -- for ncu."""
+"""Run each C2 top-level kernel call once (residual, Schwarz correction, residual restricted
+in place, stand-alone restriction, prolongation) -- the launches bench.py times -- for ncu."""
 import os
 import sys
 
@@ -23,6 +23,8 @@ uc = torch.randn(fc.shape, dtype=torch.float64, device="cuda")
 for _ in range(int(os.environ.get("REPS", "1"))):
     NV.check(lib.smg_op_residual(top.op._handle.raw, NV.ptr(u), NV.ptr(r), NV.ptr(out), st))
     NV.check(lib.smg_schwarz_correct(top.smoother._h.raw, NV.ptr(r), NV.ptr(out), NV.ptr(top.smoother.ring), st))
+    NV.check(lib.smg_residual_restrict_ws(top.transfer.handle.raw, top.op._handle.raw, NV.ptr(u), NV.ptr(r), NV.ptr(fc),
+                                          NV.ptr(out), top.transfer.ws_ptr(), top.op.ring_ptr(), st))
     NV.check(lib.smg_restrict(top.transfer.handle.raw, NV.ptr(r), NV.ptr(fc), st))
     NV.check(lib.smg_prolongate(top.transfer.handle.raw, NV.ptr(uc), NV.ptr(out), 1, st))
 torch.cuda.synchronize()
