@@ -659,7 +659,7 @@ int pcg_coop(int nx, int ny, double dx, double dy, const double* tab, const doub
   void* args[] = {&A};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)pcg_coop_kernel, dim3(G), dim3(512), args, smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "pcg_coop_kernel");
-  return SMG_OK;
+  return check_launch("pcg_coop_kernel");
 }
 
 }  // namespace smg
