@@ -322,6 +322,10 @@ int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double
   if (!on || L.f == nullptr || J == nullptr || fc == nullptr || rring == nullptr) return 1;
   if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
   if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, nullptr, J, fc, rring);
+  if (L.p == 4) {   // four elements per warp; 4 x 4-element tiles where the mesh allows
+    if (L.n_x % 4 == 0 && L.n_y % 4 == 0) return opw_launch_t<4, 4, 4>(L, st, nullptr, J, fc, rring);
+    return opw_launch_t<4, 2, 2>(L, st, nullptr, J, fc, rring);
+  }
   return 1;
 }
 

@@ -211,10 +211,11 @@ int prw_launch(const TrArgs& A, cudaStream_t st) {
 
 // restrict_fixup alone (the fused residual + restriction of smg_opw.cu filled dst and the ring)
 int rw_fixup(int pc, double* dst, const double* ring, int n_x, int n_y, cudaStream_t st) {
-  if (pc != 8 && pc != 4) return 1;
+  if (pc != 8 && pc != 4 && pc != 2) return 1;
   const long nb = (long)n_x * n_y * (2 * pc - 1);
   if (pc == 8) launch(restrict_fixup<8>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, dst, ring, n_x, n_y);
-  else launch(restrict_fixup<4>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, dst, ring, n_x, n_y);
+  else if (pc == 4) launch(restrict_fixup<4>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, dst, ring, n_x, n_y);
+  else launch(restrict_fixup<2>, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, st, dst, ring, n_x, n_y);
   return check_launch("restrict_fixup");
 }
 
