@@ -254,6 +254,8 @@ int opw_launch_t(const OpLaunch& L, cudaStream_t st, double* dotp = nullptr, con
                  double* fc = nullptr, double* rring = nullptr) {
   using G = OpwGeom<P, TX, TY>;
   if (L.diffusion || L.partials != nullptr || L.n_x % TX || L.n_y % TY) return 1;
+  // the periodic window loader wraps once: the staged window must not exceed the mesh
+  if (L.n_x * P < G::HX || L.n_y * P < G::HY) return 1;
   const int N_x = L.n_x * P;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (N_x % 2 || !al16(L.u)) return 1;
@@ -323,8 +325,8 @@ int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double
   if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
   if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, nullptr, J, fc, rring);
   if (L.p == 4) {   // four elements per warp; 4 x 4-element tiles where the mesh allows
-    if (L.n_x % 4 == 0 && L.n_y % 4 == 0) return opw_launch_t<4, 4, 4>(L, st, nullptr, J, fc, rring);
-    return opw_launch_t<4, 2, 2>(L, st, nullptr, J, fc, rring);
+    const int rc = opw_launch_t<4, 4, 4>(L, st, nullptr, J, fc, rring);
+    return rc != 1 ? rc : opw_launch_t<4, 2, 2>(L, st, nullptr, J, fc, rring);
   }
   return 1;
 }

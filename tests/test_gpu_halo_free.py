@@ -99,7 +99,8 @@ def test_apply_dot(kind, p, nx, ny):
 
 
 @pytest.mark.parametrize("p", [16, 8, 4])
-@pytest.mark.parametrize("nx,ny,lx,ly", [(6, 4, 1.0, 1.0), (64, 64, 1.0, 1.0), (8, 10, 2.0, 1.0), (128, 128, 1.0, 1.0)])
+@pytest.mark.parametrize("nx,ny,lx,ly", [(6, 4, 1.0, 1.0), (4, 4, 1.0, 1.0), (64, 64, 1.0, 1.0), (8, 10, 2.0, 1.0),
+                                         (128, 128, 1.0, 1.0)])
 def test_fused_residual_restriction_p16(nx, ny, lx, ly, p, monkeypatch):
     """smg_residual_restrict_ws at p_f = 16, 8, 4 (Poisson): the warp-per-element residual kernel restricts
     its element in place (r is never stored) + restrict_fixup, against residual then restriction
