@@ -323,7 +323,10 @@ int opw_residual_restrict(const OpLaunch& L, const double* J, double* fc, double
   static const int on = env_int("SMG_RR_OPW", 1);
   if (!on || L.f == nullptr || J == nullptr || fc == nullptr || rring == nullptr) return 1;
   if (L.p == 16) return opw_launch_t<16, 2, 2>(L, st, nullptr, J, fc, rring);
-  if (L.p == 8) return opw_launch_t<8, 2, 2>(L, st, nullptr, J, fc, rring);
+  if (L.p == 8) {   // 4x2-element tiles (four warps) where they fit: C4 level-8 pair 35.8 -> 33.1 us
+    const int rc = opw_launch_t<8, 4, 2>(L, st, nullptr, J, fc, rring);
+    return rc != 1 ? rc : opw_launch_t<8, 2, 2>(L, st, nullptr, J, fc, rring);
+  }
   if (L.p == 4) {   // four elements per warp; 4 x 4-element tiles where the mesh allows
     const int rc = opw_launch_t<4, 4, 4>(L, st, nullptr, J, fc, rring);
     return rc != 1 ? rc : opw_launch_t<4, 2, 2>(L, st, nullptr, J, fc, rring);
