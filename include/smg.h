@@ -158,6 +158,10 @@ int smg_residual_restrict(const smg_transfer_t* h, const smg_op_t* op, const dou
  * vertex rows handed over through the ring, a fixup launch adds them in a
  * fixed order) smg_transfer_ws_doubles(h) > 0 and the _ws calls use it; with
  * ws == NULL or 0 doubles they are smg_restrict / smg_residual_restrict.
+ * The same ring serves smg_residual_restrict_ws for the Poisson operator at
+ * p_f = 4, 8, 16 (p_c = p_f / 2): the warp-per-element residual kernel
+ * restricts its element in place -- r = f - A u is NOT stored, `work` is left
+ * untouched -- and hands the high-side coarse nodes over through the ring.
  * op_ring: the operator's ring workspace (smg_op_ring_doubles) or NULL. */
 size_t smg_transfer_ws_doubles(const smg_transfer_t* h);
 int smg_restrict_ws(const smg_transfer_t* h, const double* ff, double* fc, double* ws, void* stream);
