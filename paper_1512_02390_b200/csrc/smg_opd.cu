@@ -940,6 +940,15 @@ opdw_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
     if (el + nw < n_el) issue(el + nw, bsel ^ 1);
     const double* U = WB + (2 * bsel) * WIN;
     const double* NU = U + WIN;
+    // f at this lane's output nodes, requested before the products (loaded at the store they
+    // were 60 % of the kernel's stall samples: five dependent global loads per element)
+    constexpr int KO = (OX * OY + 31) / 32;
+    double fv[KO];
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = lane + 32 * k;
+      fv[k] = (A.f != nullptr && idx < OX * OY) ? __ldg(A.f + (size_t)(Y0 + idx / OX) * N_x + (X0 + idx % OX)) : 0.0;
+    }
     mbar_wait(bar + bsel, (unsigned)(it >> 1) & 1u);
 #pragma unroll
     for (int bt = 0; bt < G::NB; ++bt) {
@@ -965,11 +974,14 @@ opdw_kernel(const __grid_constant__ OpArgs<P> A, const double* __restrict__ frag
         }
     }
     __syncwarp();   // parts complete; the warp is done with this element's window
-    for (int idx = lane; idx < OX * OY; idx += 32) {
-      const int y = idx / OX, x = idx - y * OX;
-      const double val = fma(A.cx * WS[y], AX[y * OXP + x], (A.cy * WS[x]) * AY[y * OXP + x]);
-      const size_t gi = (size_t)(Y0 + y) * N_x + (X0 + x);
-      A.out[gi] = A.f != nullptr ? __ldg(A.f + gi) - val : val;
+#pragma unroll
+    for (int k = 0; k < KO; ++k) {
+      const int idx = lane + 32 * k;
+      if (idx < OX * OY) {
+        const int y = idx / OX, x = idx - y * OX;
+        const double val = fma(A.cx * WS[y], AX[y * OXP + x], (A.cy * WS[x]) * AY[y * OXP + x]);
+        A.out[(size_t)(Y0 + y) * N_x + (X0 + x)] = A.f != nullptr ? fv[k] - val : val;
+      }
     }
     __syncwarp();   // the parts are rewritten by the next element
   }
