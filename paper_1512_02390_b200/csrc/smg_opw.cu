@@ -139,6 +139,17 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
   const bool lact = sub < EW;
   const int eidx = warp * EW + (lact ? sub : 0);
   const int exl = eidx % TX, eyl = eidx / TX;
+  // the first chunk of f rows of the column lanes, requested while the window is in flight
+  // (ncu: 16 % of the stall samples sat on the first use of f after the lines)
+  // (RESTR only: the plain and DOT variants at p = 16 spill with eight more live doubles)
+  constexpr int CHF = P / 2;
+  [[maybe_unused]] double f0[CHF];
+  if constexpr (RESTR) {
+    const bool cl = lane >= 16 && lact && A.f != nullptr;
+    const size_t gf = (size_t)(Y0 + eyl * P) * N_x + (X0 + exl * P + (lane & 15) % P);
+#pragma unroll
+    for (int i = 0; i < CHF; ++i) f0[i] = cl ? __ldg(A.f + gf + (size_t)i * N_x) : 0.0;
+  }
   mbar_wait(bar, 0);
   // element origin in U
   const int ur0 = P + eyl * P, uc0 = sh + P + exl * P;
@@ -181,7 +192,8 @@ opw_kernel(const __grid_constant__ OpwArgs<P> A) {
     for (int a0 = 0; a0 < P; a0 += CH) {
       double fv[CH];
 #pragma unroll
-      for (int i = 0; i < CH; ++i) fv[i] = A.f != nullptr ? __ldg(A.f + g0 + (size_t)(a0 + i) * N_x) : 0.0;
+      for (int i = 0; i < CH; ++i)
+        fv[i] = (RESTR && a0 == 0) ? f0[i] : (A.f != nullptr ? __ldg(A.f + g0 + (size_t)(a0 + i) * N_x) : 0.0);
 #pragma unroll
       for (int i = 0; i < CH; ++i) {
         const int a = a0 + i;
