@@ -582,8 +582,8 @@ def main():
     # launch streams its inputs from HBM -- the per-launch duration the
     # roofline uses; (2) "flushed": one launch after a 256 MiB L2 flush, event
     # to event (includes the launch latency and the flush's dirty write-back).
-    # The dominant kernel (largest share of a V-cycle: the residual runs twice
-    # per cycle) is reported as `roofline`.
+    # `roofline` is the kernel the north star names, the fused Schwarz correction;
+    # `largest_share_of_step` names whichever call has the largest share of a V-cycle.
     top = h.top
     st = NV.stream()
     fshape = h.levels[-2].f.shape
@@ -675,8 +675,9 @@ def main():
         kern[nm]["timing"] = (f"{nset} distinct buffer sets (>= 320 MB, > L2) launched back to back x 4, "
                               "mean per launch; us_per_call_flushed: single launch after a 256 MiB L2 flush")
     # `roofline` is the kernel the north star names -- the fused Schwarz correction -- whether
-    # or not it still has the largest share of the step (the residual runs twice per cycle;
-    # every top-level kernel is listed under top_level_kernels with its own fraction)
+    # or not it still has the largest share of the step (the operator is applied twice per
+    # cycle, once as the plain residual and once inside the restricted residual; every
+    # top-level kernel is listed under top_level_kernels with its own fraction)
     dom = max(calls, key=lambda k: calls[k][1] * t_call[k])
     roofline = dict(kern["schwarz"])
     roofline["share_of_step"] = calls["schwarz"][1] * t_call["schwarz"] / (ms_per_step / 1e3)
