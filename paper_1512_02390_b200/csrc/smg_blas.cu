@@ -727,11 +727,11 @@ int pinv_cluster(int nx, int ny, const double* Qx, const double* QxT, const doub
   const int rb = (ny + kCl - 1) / kCl;
   if (((size_t)rb * nx) % 2) return 1;  // keep every row block 16-byte aligned
   const size_t smem = sizeof(double) * (2 * (size_t)ny * nx + (size_t)ny * ny + 2 * (size_t)nx * nx + 2 * (size_t)rb * nx) + 16;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static DeviceInt attr;   // largest size set so far, per device
+  if ((int)smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(pinv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "pinv_cluster_kernel smem attribute");
-    attr = smem;
+    attr = (int)smem;
   }
   launch(pinv_cluster_kernel, dim3(kCl), dim3(kClThreads), smem, st, nx, ny, Qx, QxT, Qy, Lp, f, u);
   return check_launch("pinv_cluster_kernel");

@@ -303,16 +303,16 @@ int pinv_fft(int nx, int ny, double dx, double dy, const double* f, double* u, d
   const int lr = pick(ny, nx, &tr), lc = pick(nx, ny, &tc);
   const size_t smr = sizeof(double2) * ((size_t)lr * (nx + nx / 16) + nx);
   const size_t smc = sizeof(double2) * (2 * (size_t)lc * (ny + ny / 16) + ny) + sizeof(double) * ny;
-  static size_t attr_r = 0, attr_c = 0;
-  if (smr > attr_r) {
+  static DeviceInt attr_r, attr_c;   // largest dynamic shared-memory size set so far, per device
+  if ((int)smr > attr_r) {
     cudaError_t e = cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
     if (e != cudaSuccess) return cuda_fail(e, "fft_rows_kernel smem attribute");
-    attr_r = smr;
+    attr_r = (int)smr;
   }
-  if (smc > attr_c) {
+  if ((int)smc > attr_c) {
     cudaError_t e = cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
     if (e != cudaSuccess) return cuda_fail(e, "fft_cols_kernel smem attribute");
-    attr_c = smc;
+    attr_c = (int)smc;
   }
   const int gr = (ny + lr - 1) / lr, gc = (nx + lc - 1) / lc;
   launch(fft_rows_kernel, dim3(gr), dim3(tr), smr, st, nx, ny, lx, tab, f, W, static_cast<double*>(nullptr), 0, lr);
@@ -647,11 +647,11 @@ int pcg_coop(int nx, int ny, double dx, double dy, const double* tab, const doub
   const int nz = std::max(A.Lr * lsx, 2 * A.Lc * lsy);
   const size_t smem = sizeof(double2) * ((size_t)nz + nx + ny) +
                       sizeof(double) * ((size_t)nx + ny + (size_t)(A.Lr + 2) * nx * 2 + (size_t)A.Lr * nx * 2 + 64);
-  static size_t attr = 0;
-  if (smem > attr) {
+  static DeviceInt attr;   // per device
+  if ((int)smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(pcg_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "pcg_coop_kernel smem attribute");
-    attr = smem;
+    attr = (int)smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_coop_kernel, 512, smem);
