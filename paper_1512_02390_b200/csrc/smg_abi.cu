@@ -627,10 +627,10 @@ int smg_transfer_create(smg_transfer_t** h, int p_c, int p_f, int n_x, int n_y, 
   // (smg_opw.cu; the ring below is its workspace) -- C4 (256^2 elements) pair 159 -> 135 us at
   // p_f = 16, 74 -> 36 us at p_f = 8; C2 (64^2) V-cycle in the replayed graph 103.6 -> 100.3 us
   // with both.  SMG_RR_OPW = 0: residual kernel + restriction kernel (or rr_kernel at p_f <= 8)
-  // (2, 4): only where the mesh is large (one launch of rr_kernel wins inside C2's chain); 2 = every mesh
-  const int rr_mode = env_int("SMG_RR_OPW", 1);
-  t->rr_opw = rr_mode != 0 && ((p_c == 8 && p_f == 16) || (p_c == 4 && p_f == 8) ||
-                               (p_c == 2 && p_f == 4 && (rr_mode == 2 || (long)n_x * n_y >= 16384)));
+  // (2, 4) as well: four elements per warp (C4 level-4 pair 21.5 -> 12.5 us; C2's replayed
+  // V-cycle 99.87 -> 99.67 us, i.e. even)
+  t->rr_opw = env_int("SMG_RR_OPW", 1) != 0 &&
+              ((p_c == 8 && p_f == 16) || (p_c == 4 && p_f == 8) || (p_c == 2 && p_f == 4));
   // SMG_PRW: 0 never, 1 where measured faster, 2 wherever compiled (B200, tools/time_prolong.py,
   // us tiled -> warp per fine element: C3 p_f = 32 95.3 -> 79.9; 256^2 p_f = 24 156.7 -> 162.9,
   // p_f = 16 76.9 -> 80.0; bitwise-equal results)

@@ -101,14 +101,12 @@ def test_apply_dot(kind, p, nx, ny):
 @pytest.mark.parametrize("p", [16, 8, 4])
 @pytest.mark.parametrize("nx,ny,lx,ly", [(6, 4, 1.0, 1.0), (4, 4, 1.0, 1.0), (64, 64, 1.0, 1.0), (8, 10, 2.0, 1.0),
                                          (128, 128, 1.0, 1.0)])
-def test_fused_residual_restriction_p16(nx, ny, lx, ly, p, monkeypatch):
+def test_fused_residual_restriction_p16(nx, ny, lx, ly, p):
     """smg_residual_restrict_ws at p_f = 16, 8, 4 (Poisson): the warp-per-element residual kernel restricts
     its element in place (r is never stored) + restrict_fixup, against residual then restriction
     (multigrid.py:247-248), twice into a dirty workspace; bitwise reproducible."""
     import paper_1512_02390_b200 as P
     from paper_1512_02390_b200 import _native as N
-    if p == 4:
-        monkeypatch.setenv("SMG_RR_OPW", "2")   # p_f = 4: default only from 16384 elements up (read at create time)
     mesh = P.MeshConfig(nx, ny, lx, ly)
     h = P.build_hierarchy(mesh, p, P.OverlapRule("fixed", 1))
     lv = h.top
